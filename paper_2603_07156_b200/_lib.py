@@ -1,0 +1,122 @@
+"""ctypes binding of libotb.so (include/otb.h).
+
+The library is the product: there is no CPU fallback.  Importing this
+module on a machine where ``libotb.so`` is missing raises immediately, and
+every entry point checks its status code and raises the exception class the
+reference raises at the corresponding site (errors.STATUS_TO_ERROR).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import glob
+import os
+from pathlib import Path
+
+from . import errors
+
+LIB_PATH = Path(__file__).resolve().parent / "libotb.so"
+
+i64 = C.c_int64
+dbl = C.c_double
+vp = C.c_void_p
+
+
+class EvalOut(C.Structure):
+    _fields_ = [("value", dbl), ("grad_norm", dbl)]
+
+
+class CgOut(C.Structure):
+    _fields_ = [("iters", i64), ("residual", dbl), ("status", C.c_int), ("pad", C.c_int)]
+
+
+class NewtonParams(C.Structure):
+    _fields_ = [("sigma", dbl), ("beta", dbl), ("cg_rel_tol", dbl), ("cg_max_iters", i64),
+                ("rho_override", dbl)]
+
+
+class NewtonOut(C.Structure):
+    _fields_ = [("t", dbl), ("slope", dbl), ("rho", dbl), ("value_before", dbl),
+                ("value_after", dbl), ("grad_norm_before", dbl), ("grad_norm_after", dbl),
+                ("cg_iters", i64), ("nnz", i64), ("trials", i64), ("cg_residual", dbl)]
+
+
+class TestOut(C.Structure):
+    _fields_ = [("bregman", dbl), ("objective", dbl), ("delta_p", dbl), ("delta_d", dbl),
+                ("delta_c", dbl), ("delta_kkt", dbl), ("sum_x", dbl), ("deficit", dbl)]
+
+    __test__ = False
+
+
+class WarmOut(C.Structure):
+    _fields_ = [("sweeps", i64), ("err", dbl)]
+
+
+# name -> (restype, argtypes); the export list of include/otb.h
+SIGNATURES = {
+    "otb_abi_version": (C.c_int, []),
+    "otb_last_error": (C.c_char_p, []),
+    "otb_create": (C.c_int, [C.POINTER(vp), i64, i64, i64, i64, i64, C.c_int, vp]),
+    "otb_destroy": (C.c_int, [vp]),
+    "otb_set_stream": (C.c_int, [vp, vp]),
+    "otb_nccl_get_unique_id": (C.c_int, [C.c_char_p, vp]),
+    "otb_attach_nccl": (C.c_int, [vp, C.c_char_p, vp, C.c_int, C.c_int]),
+    "otb_bind": (C.c_int, [vp, vp, vp, vp, vp, vp, dbl, i64, dbl, dbl, dbl]),
+    "otb_eval": (C.c_int, [vp, vp, vp, vp, vp, C.POINTER(EvalOut)]),
+    "otb_sparsify": (C.c_int, [vp, vp, vp, dbl, C.POINTER(i64)]),
+    "otb_csr_export": (C.c_int, [vp, vp, vp, vp, vp]),
+    "otb_hess_apply": (C.c_int, [vp, vp, dbl, vp]),
+    "otb_cg": (C.c_int, [vp, dbl, vp, dbl, i64, vp, C.POINTER(CgOut)]),
+    "otb_newton_step": (C.c_int, [vp, vp, vp, vp, C.POINTER(NewtonParams), C.POINTER(NewtonOut)]),
+    "otb_recover_round": (C.c_int, [vp, vp, vp, vp, C.c_int, C.c_int, C.POINTER(TestOut)]),
+    "otb_materialize_rounded": (C.c_int, [vp, vp, i64]),
+    "otb_warm_start": (C.c_int, [vp, vp, vp, vp, dbl, i64, C.POINTER(WarmOut)]),
+    "otb_zeta_from_lse": (C.c_int, [vp, vp]),
+    "otb_init_plan": (C.c_int, [vp, vp]),
+    "otb_materialize_p": (C.c_int, [vp, vp, vp, vp, i64]),
+    "otb_info": (C.c_int, [vp, C.POINTER(i64)]),
+    "otb_prof_enable": (C.c_int, [vp, C.c_int]),
+    "otb_prof_read": (C.c_int, [vp, C.POINTER(dbl), C.POINTER(i64), C.POINTER(dbl), C.c_int]),
+}
+
+
+def _load() -> C.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is not built; run `python -m paper_2603_07156_b200.build` "
+            "(there is no CPU fallback for the solver path)"
+        )
+    lib = C.CDLL(str(LIB_PATH))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if lib.otb_abi_version() != 1:
+        raise ImportError("libotb ABI version mismatch")
+    return lib
+
+
+lib = _load()
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = lib.otb_last_error().decode(errors="replace")
+        raise errors.STATUS_TO_ERROR.get(status, errors.DeviceError)(msg)
+
+
+def nccl_path() -> str:
+    """The torch-bundled libnccl.so.2 (one NCCL per process)."""
+    env = os.environ.get("OTB_NCCL_PATH")
+    if env:
+        return env
+    try:
+        import nvidia.nccl  # type: ignore
+
+        for base in nvidia.nccl.__path__:
+            hits = glob.glob(os.path.join(base, "lib", "libnccl.so*"))
+            if hits:
+                return sorted(hits)[0]
+    except Exception:  # pragma: no cover - layout differs
+        pass
+    return "libnccl.so.2"

@@ -1,0 +1,786 @@
+// Dense passes over (C, log X): each kernel streams every local row once
+// through the TMA ring of rowpipe.cuh.  Reference sites are cited per kernel.
+#pragma once
+
+#include "rowpipe.cuh"
+
+namespace otb {
+
+constexpr int kMaxThreads = 544;   // 512 consumers + 1 producer warp
+constexpr int kTabInts = 2 * kMaxNS * 32;
+
+// ---------------------------------------------------------------- eval (K1)
+// semidual.py:51-100: logits = logX + (gamma - C)/eta, row max, shifted
+// exponentials, row sums, lse = max + log(sum); column sums of a_i P_ij
+// (gradient before -b) and a.lse (objective) are reduced without
+// materialising P.  Per-row max / sum are kept for the sparsify pass.
+struct EvalIO {
+  const double* gamma;
+  const double* a;      // global-row indexed
+  double eta;
+  double* rowM;
+  double* rowS;
+  double* lse;
+  double* colpart;      // [ncl][n]
+  double* vpart;        // [ncl][2]: a.lse, count of non-finite rows
+};
+
+template <int NS>
+__global__ void __launch_bounds__(kMaxThreads, 1) k_eval(Geom geo, EvalIO io) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  Dense<2> D;
+  D.setup(geo, smem);
+  if (D.producer) {
+    D.produce();
+    D.finish();
+    return;
+  }
+  const double eta = io.eta;
+  double alse = 0.0, nbad = 0.0;
+  for (int r = D.r0; r < D.r1; ++r) {
+    double z[2 * NS];
+    double mx = -INFINITY;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      z[2 * s] = -INFINITY;
+      z[2 * s + 1] = -INFINITY;
+      if (s < D.nsl) {
+        double2 c, x;
+        D.fetch(c, x);
+        const int j = D.col(s, 0);
+        const double2 gm = load_pair(io.gamma, j, D.c1);
+        if (j < D.c1) z[2 * s] = x.x + div_rn(gm.x - c.x, eta);
+        if (j + 1 < D.c1) z[2 * s + 1] = x.y + div_rn(gm.y - c.y, eta);
+        mx = fmax(mx, fmax(z[2 * s], z[2 * s + 1]));
+      }
+    }
+    double t[1] = {mx};
+    D.reduce<1, kMax>(t);
+    double M = t[0];
+    double se = 0.0;
+#pragma unroll
+    for (int k = 0; k < 2 * NS; ++k) {
+      z[k] = exp(z[k] - M);
+      se += z[k];
+    }
+    t[0] = se;
+    D.reduce<1, kSum>(t);
+    double S = t[0];
+    double scale = 1.0;
+    if (D.g.cl > 1) {
+      double v2[2] = {M, S};
+      double all[kMaxCluster * 4];
+      D.exchange<2>(v2, all);
+      double Mg = all[0];
+      for (int q = 1; q < D.g.cl; ++q) Mg = fmax(Mg, all[q * 4]);
+      double Sg = 0.0;
+      for (int q = 0; q < D.g.cl; ++q) Sg += all[q * 4 + 1] * exp(all[q * 4] - Mg);
+      scale = exp(M - Mg);
+      M = Mg;
+      S = Sg;
+    }
+    const double l = M + log(S);
+    const double ai = __ldg(io.a + D.g.row0 + r);
+    const double w = (ai / S) * scale;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      if (s < D.nsl) {
+        double2* a2 = D.acc2(0, s);
+        double2 v = *a2;
+        v.x = fma(w, z[2 * s], v.x);
+        v.y = fma(w, z[2 * s + 1], v.y);
+        *a2 = v;
+      }
+    }
+    if (D.tid == 0 && D.cr == 0) {
+      io.rowM[r] = M;
+      io.rowS[r] = S;
+      io.lse[r] = l;
+      alse = fma(ai, l, alse);
+      if (!isfinite(l) || !isfinite(S)) nbad += 1.0;
+    }
+  }
+  bar_sync(1, D.g.nt);
+  D.store_acc(0, io.colpart + (size_t)D.cid * D.g.n);
+  if (D.tid == 0 && D.cr == 0) {
+    io.vpart[2 * D.cid] = alse;
+    io.vpart[2 * D.cid + 1] = nbad;
+  }
+  D.finish();
+}
+
+// ------------------------------------------------------------ sparsify (K2/K3)
+// sparsify.py:90-127 + 143-145: keep P >= rho and P > 0 off the anchor row,
+// empty rows keep their first argmax with value 1, kept values divided by
+// the kept sum, anchor row stored unnormalised and dense.  Rows are written
+// as contiguous runs (ascending columns) into chunks obtained with one
+// atomicAdd per chunk; d = P_rho^T a is accumulated on the fly.
+struct SparsifyIO {
+  const double* gamma;
+  const double* a;
+  double eta;
+  double rho;
+  int64_t anchor_local;   // local row of the anchor, -1 if not on this rank
+  const double* rowM;
+  const double* rowS;
+  uint16_t* cols;
+  double* vals;
+  int64_t cap;
+  int64_t* row_start;     // [m_loc]
+  int* row_len;           // [m_loc]
+  unsigned long long* alloc;
+  int64_t chunk;
+  double* colpart;        // [ncl][n] partial of d
+  int* flags;             // bit 1: capacity overflow
+};
+
+template <int NS>
+__global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyIO io) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  Dense<2> D;
+  D.setup(geo, smem);
+  if (D.producer) {
+    D.produce();
+    D.finish();
+    return;
+  }
+  __shared__ int tab[kTabInts];
+  __shared__ unsigned long long chunk_base;
+  const double eta = io.eta, rho = io.rho;
+  const int nw = D.g.nt >> 5;
+  const unsigned lt = (1u << D.lane) - 1u;
+  unsigned long long cur = 0, end = 0;
+  int rowpar = 0;
+  for (int r = D.r0; r < D.r1; ++r) {
+    const bool anc = (r == io.anchor_local);
+    const double M = io.rowM[r], S = io.rowS[r];
+    double P[2 * NS];
+    unsigned keep = 0;
+    double ks = 0.0;
+    int* tb = tab + rowpar * kMaxNS * 32;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      P[2 * s] = -1.0;
+      P[2 * s + 1] = -1.0;
+      if (s < D.nsl) {
+        double2 c, x;
+        D.fetch(c, x);
+        const int j = D.col(s, 0);
+        const double2 gm = load_pair(io.gamma, j, D.c1);
+        if (j < D.c1) P[2 * s] = div_rn(exp((x.x + div_rn(gm.x - c.x, eta)) - M), S);
+        if (j + 1 < D.c1) P[2 * s + 1] = div_rn(exp((x.y + div_rn(gm.y - c.y, eta)) - M), S);
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double p = P[2 * s + e];
+        const bool k = (p >= 0.0) && (anc || (p >= rho && p > 0.0));
+        if (k) {
+          keep |= 1u << (2 * s + e);
+          ks += p;
+        }
+      }
+      if (s < D.nsl) {
+        const unsigned b0 = __ballot_sync(0xffffffffu, (keep >> (2 * s)) & 1u);
+        const unsigned b1 = __ballot_sync(0xffffffffu, (keep >> (2 * s + 1)) & 1u);
+        if (D.lane == 0) tb[s * 32 + D.warp] = __popc(b0) + __popc(b1);
+      }
+    }
+    double t[1] = {ks};
+    D.reduce<1, kSum>(t);   // barrier also publishes tb
+    double ksum = t[0];
+    // per-slice totals (lane s holds slice s), exclusive scan over slices
+    int tot = 0;
+    if (D.lane < D.nsl)
+      for (int w = 0; w < nw; ++w) tot += tb[D.lane * 32 + w];
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (D.lane >= o) incl += v;
+    }
+    const int excl = incl - tot;
+    int need = __shfl_sync(0xffffffffu, incl, 31);   // kept in this CTA's window
+    int cnt = need;                                    // kept in the whole row
+    int myoff = 0;                                     // offset of this window in the row
+    if (D.g.cl > 1) {
+      double v2[2] = {(double)need, ksum};
+      double all[kMaxCluster * 4];
+      D.exchange<2>(v2, all);
+      double cs = 0.0, kss = 0.0;
+      for (int q = 0; q < D.g.cl; ++q) {
+        if (q < D.cr) myoff += (int)all[q * 4];
+        cs += all[q * 4];
+        kss += all[q * 4 + 1];
+      }
+      cnt = (int)cs;
+      ksum = kss;
+    }
+    bool fallback = false;
+    int jbest = -1;
+    if (!anc && cnt == 0) {
+      // sparsify.py:103-107: keep the first argmax of the row with value 1.
+      fallback = true;
+      double pm = -1.0;
+#pragma unroll
+      for (int k = 0; k < 2 * NS; ++k) pm = fmax(pm, P[k]);
+      double u[1] = {pm};
+      D.reduce<1, kMax>(u);
+      double pmax = u[0];
+      double jm = 1e300;
+#pragma unroll
+      for (int k = 0; k < 2 * NS; ++k)
+        if (P[k] >= 0.0 && P[k] == pmax) jm = fmin(jm, (double)D.col(k >> 1, k & 1));
+      u[0] = jm;
+      D.reduce<1, kMin>(u);
+      jm = u[0];
+      if (D.g.cl > 1) {
+        double v2[2] = {pmax, jm};
+        double all[kMaxCluster * 4];
+        D.exchange<2>(v2, all);
+        double bp = all[0], bj = all[1];
+        for (int q = 1; q < D.g.cl; ++q) {
+          if (all[q * 4] > bp || (all[q * 4] == bp && all[q * 4 + 1] < bj)) {
+            bp = all[q * 4];
+            bj = all[q * 4 + 1];
+          }
+        }
+        jm = bj;
+      }
+      jbest = (int)jm;
+      need = (jbest >= D.c0 && jbest < D.c1) ? 1 : 0;
+      cnt = 1;
+      myoff = 0;
+    }
+    // Contiguous row run: cluster rank 0 bump-allocates from its current
+    // chunk (state replicated in all of its consumer threads) and shares
+    // the start with the other ranks of the cluster.
+    unsigned long long start = 0;
+    if (D.cr == 0) {
+      if (cur + (unsigned long long)cnt > end) {
+        const unsigned long long want = (unsigned long long)max((int64_t)cnt, io.chunk);
+        if (D.tid == 0) chunk_base = atomicAdd(io.alloc, want);
+        bar_sync(1, D.g.nt);
+        cur = chunk_base;
+        end = cur + want;
+        bar_sync(1, D.g.nt);   // chunk_base may be rewritten next time
+      }
+      start = cur;
+      cur += (unsigned long long)cnt;
+    }
+    if (D.g.cl > 1) {
+      double v1[1] = {(double)start};
+      double all[kMaxCluster * 4];
+      D.exchange<1>(v1, all);
+      start = (unsigned long long)all[0];
+    }
+    const bool ovf = (int64_t)(start + cnt) > io.cap;
+    if (ovf && D.tid == 0 && D.cr == 0) atomicOr(io.flags, 2);
+    const double ai = __ldg(io.a + D.g.row0 + r);
+    const unsigned long long wbase = start + myoff;
+    if (!ovf) {
+      if (fallback) {
+#pragma unroll
+        for (int k = 0; k < 2 * NS; ++k) {
+          if (D.col(k >> 1, k & 1) == jbest && P[k] >= 0.0) {
+            io.cols[wbase] = (uint16_t)jbest;
+            io.vals[wbase] = 1.0;
+            double2* a2 = D.acc2(0, k >> 1);
+            if (k & 1) a2->y += ai * 1.0;
+            else a2->x += ai * 1.0;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+          if (s < D.nsl) {
+            const unsigned k0 = (keep >> (2 * s)) & 1u, k1 = (keep >> (2 * s + 1)) & 1u;
+            const unsigned b0 = __ballot_sync(0xffffffffu, k0);
+            const unsigned b1 = __ballot_sync(0xffffffffu, k1);
+            int base = __shfl_sync(0xffffffffu, excl, s);
+            for (int w = 0; w < D.warp; ++w) base += tb[s * 32 + w];
+            const int off = base + __popc(b0 & lt) + __popc(b1 & lt);
+            const int j = D.col(s, 0);
+            double2* a2 = D.acc2(0, s);
+            if (k0) {
+              const double v = anc ? P[2 * s] : div_rn(P[2 * s], ksum);
+              io.cols[wbase + off] = (uint16_t)j;
+              io.vals[wbase + off] = v;
+              a2->x += ai * v;
+            }
+            if (k1) {
+              const double v = anc ? P[2 * s + 1] : div_rn(P[2 * s + 1], ksum);
+              io.cols[wbase + off + k0] = (uint16_t)(j + 1);
+              io.vals[wbase + off + k0] = v;
+              a2->y += ai * v;
+            }
+          }
+        }
+      }
+    }
+    if (D.tid == 0 && D.cr == 0) {
+      io.row_start[r] = (int64_t)start;
+      io.row_len[r] = ovf ? 0 : cnt;
+    }
+    rowpar ^= 1;
+  }
+  bar_sync(1, D.g.nt);
+  D.store_acc(0, io.colpart + (size_t)D.cid * D.g.n);
+  D.finish();
+}
+
+// ------------------------------------------------- inexact test, pass A (K7/K8)
+// inner_newton.py:160-167 + core.py:141-145 (candidate log plan, NaN/+inf
+// check, floor clamp) fused with feasibility.py:56-60 (row sums, z, column
+// sums of F = X diag-scaled).  Writes the candidate into Xout.
+struct TestAIO {
+  const double* gamma;
+  const double* a;
+  const double* log_a;
+  const double* lse;
+  double eta;
+  double* Xout;
+  double* zrow;
+  double* colpart;   // [ncl][n]
+  double* spart;     // [gridDim][2]: sum of exp(candidate), count of NaN/+inf
+  int recover;       // 0: round the given log plan as is (no candidate write)
+};
+
+template <int NS>
+__global__ void __launch_bounds__(kMaxThreads, 1) k_test_a(Geom geo, TestAIO io) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  Dense<2> D;
+  D.setup(geo, smem);
+  if (D.producer) {
+    D.produce();
+    D.finish();
+    return;
+  }
+  const double eta = io.eta;
+  double sumx = 0.0;
+  int bad = 0;
+  for (int r = D.r0; r < D.r1; ++r) {
+    const int64_t gi = D.g.row0 + r;
+    const double la = io.recover ? __ldg(io.log_a + gi) : 0.0;
+    const double l = io.recover ? io.lse[r] : 0.0;
+    double xv[2 * NS];
+    double rs = 0.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      xv[2 * s] = 0.0;
+      xv[2 * s + 1] = 0.0;
+      if (s < D.nsl) {
+        double2 c, x;
+        D.fetch(c, x);
+        const int j = D.col(s, 0);
+        const double2 gm = load_pair(io.gamma, j, D.c1);
+        double* dst = io.Xout + (size_t)r * D.g.ld + j;
+        if (io.recover) {
+          if (j < D.c1) {
+            const double raw = ((la + x.x) + div_rn(gm.x - c.x, eta)) - l;
+            bad |= (isnan(raw) || raw == INFINITY);
+            const double xl = fmax(raw, kLogFloor);
+            dst[0] = xl;
+            xv[2 * s] = exp(xl);
+          }
+          if (j + 1 < D.c1) {
+            const double raw = ((la + x.y) + div_rn(gm.y - c.y, eta)) - l;
+            bad |= (isnan(raw) || raw == INFINITY);
+            const double xl = fmax(raw, kLogFloor);
+            dst[1] = xl;
+            xv[2 * s + 1] = exp(xl);
+          }
+        } else {
+          if (j < D.c1) xv[2 * s] = exp(x.x);
+          if (j + 1 < D.c1) xv[2 * s + 1] = exp(x.y);
+        }
+        rs += xv[2 * s] + xv[2 * s + 1];
+      }
+    }
+    const double rsum = D.row_sum(rs);
+    const double ai = __ldg(io.a + gi);
+    const double z = (rsum > 0.0) ? fmin(div_rn(ai, rsum), 1.0) : 1.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      if (s < D.nsl) {
+        double2* a2 = D.acc2(0, s);
+        double2 v = *a2;
+        v.x = v.x + xv[2 * s] * z;
+        v.y = v.y + xv[2 * s + 1] * z;
+        *a2 = v;
+      }
+    }
+    if (D.tid == 0 && D.cr == 0) {
+      io.zrow[r] = z;
+      sumx += rsum;
+    }
+  }
+  double bv[1] = {(double)bad};
+  D.reduce<1, kSum>(bv);
+  D.store_acc(0, io.colpart + (size_t)D.cid * D.g.n);
+  if (D.tid == 0) {
+    io.spart[2 * blockIdx.x] = (D.cr == 0) ? sumx : 0.0;
+    io.spart[2 * blockIdx.x + 1] = bv[0];
+  }
+  D.finish();
+}
+
+// ------------------------------------------------------ inexact test, pass B
+// feasibility.py:61-66: F = (X z) y; row sums -> e_r, column sums -> e_c.
+struct TestBIO {
+  const double* zrow;
+  const double* y;
+  double* rowpart;   // [m_loc * cl]
+  double* colpart;   // [ncl][n]
+};
+
+template <int NS>
+__global__ void __launch_bounds__(kMaxThreads, 1) k_test_b(Geom geo, TestBIO io) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  Dense<1> D;
+  D.setup(geo, smem);
+  if (D.producer) {
+    D.produce();
+    D.finish();
+    return;
+  }
+  for (int r = D.r0; r < D.r1; ++r) {
+    const double z = io.zrow[r];
+    double rs = 0.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      if (s < D.nsl) {
+        double2 x, unused;
+        D.fetch(x, unused);
+        const int j = D.col(s, 0);
+        const double2 yy = load_pair(io.y, j, D.c1);
+        double f0 = 0.0, f1 = 0.0;
+        if (j < D.c1) f0 = (exp(x.x) * z) * yy.x;
+        if (j + 1 < D.c1) f1 = (exp(x.y) * z) * yy.y;
+        rs += f0 + f1;
+        double2* a2 = D.acc2(0, s);
+        double2 v = *a2;
+        v.x += f0;
+        v.y += f1;
+        *a2 = v;
+      }
+    }
+    double t[1] = {rs};
+    D.reduce<1, kSum>(t);
+    if (D.tid == 0) io.rowpart[(size_t)r * D.g.cl + D.cr] = t[0];
+  }
+  bar_sync(1, D.g.nt);
+  D.store_acc(0, io.colpart + (size_t)D.cid * D.g.n);
+  D.finish();
+}
+
+// ------------------------------------------------------ inexact test, pass C
+// feasibility.py:67-68 (rank-one correction) + 80-85 (Bregman divergence)
+// and, with METRICS, bregman_outer.py:53 (objective) + feasibility.py:103-122
+// (c-transform, slack, KKT sums).  Scalar partials per CTA (8 slots):
+//   0 sum f(log f - logY) [f>0]  1 sum f  2 sum C f  3 sum f^2
+//   4 sum min(f,0)^2  5 sum min(slack,0)^2  6 sum f*slack
+struct TestCIO {
+  const double* zrow;
+  const double* y;
+  const double* er;
+  const double* ec;
+  const double* deficit;   // device scalar (feasibility.py:66)
+  const double* gamma;
+  double* rowpart;   // [m_loc * cl] row sums of the rounded plan
+  double* colpart;   // [ncl][n] column sums of the rounded plan
+  double* spart;     // [gridDim][8]
+};
+
+template <int NS, bool METRICS>
+__global__ void __launch_bounds__(kMaxThreads, 1) k_test_c(Geom geo, TestCIO io) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  Dense<METRICS ? 2 : 1> D;
+  D.setup(geo, smem);
+  if (D.producer) {
+    D.produce();
+    D.finish();
+    return;
+  }
+  const double deficit = *io.deficit;
+  double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int r = D.r0; r < D.r1; ++r) {
+    const double z = io.zrow[r];
+    const double e_r = io.er[r];
+    double f[2 * NS];
+    double sh[2 * NS];
+    double shmin = INFINITY;
+    double rs = 0.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      f[2 * s] = 0.0;
+      f[2 * s + 1] = 0.0;
+      sh[2 * s] = 0.0;
+      sh[2 * s + 1] = 0.0;
+      if (s < D.nsl) {
+        double2 x, c;
+        D.fetch(x, c);
+        const int j = D.col(s, 0);
+        const double2 yy = load_pair(io.y, j, D.c1);
+        const double2 ee = load_pair(io.ec, j, D.c1);
+        double2 gm = make_double2(0.0, 0.0);
+        if constexpr (METRICS) gm = load_pair(io.gamma, j, D.c1);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (j + e < D.c1) {
+            const double xl = e ? x.y : x.x;
+            double fv = (exp(xl) * z) * (e ? yy.y : yy.x);
+            if (deficit > 0.0) fv = fv + div_rn(e_r * (e ? ee.y : ee.x), deficit);
+            f[2 * s + e] = fv;
+            if (fv > 0.0) acc[0] += fv * (log(fv) - xl);
+            acc[1] += fv;
+            rs += fv;
+            if constexpr (METRICS) {
+              const double cv = e ? c.y : c.x;
+              acc[2] += cv * fv;
+              acc[3] += fv * fv;
+              const double fm = fmin(fv, 0.0);
+              acc[4] += fm * fm;
+              const double shv = cv - (e ? gm.y : gm.x);
+              sh[2 * s + e] = shv;
+              shmin = fmin(shmin, shv);
+            }
+          }
+        }
+        double2* a2 = D.acc2(0, s);
+        double2 v = *a2;
+        v.x += f[2 * s];
+        v.y += f[2 * s + 1];
+        *a2 = v;
+      }
+    }
+    if constexpr (METRICS) {
+      const double zeta = D.row_min(shmin);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        if (s < D.nsl) {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            if (D.col(s, e) < D.c1) {
+              const double sl = sh[2 * s + e] - zeta;
+              const double sm = fmin(sl, 0.0);
+              acc[5] += sm * sm;
+              acc[6] += f[2 * s + e] * sl;
+            }
+          }
+        }
+      }
+    }
+    double t[1] = {rs};
+    D.template reduce<1, kSum>(t);
+    if (D.tid == 0) io.rowpart[(size_t)r * D.g.cl + D.cr] = t[0];
+  }
+  // CTA-level scalar partials
+  double v4[4] = {acc[0], acc[1], acc[2], acc[3]};
+  D.template reduce<4, kSum>(v4);
+  double w3[3] = {acc[4], acc[5], acc[6]};
+  D.template reduce<3, kSum>(w3);
+  if (D.tid == 0) {
+    double* sp = io.spart + (size_t)blockIdx.x * 8;
+    sp[0] = v4[0];
+    sp[1] = v4[1];
+    sp[2] = v4[2];
+    sp[3] = v4[3];
+    sp[4] = w3[0];
+    sp[5] = w3[1];
+    sp[6] = w3[2];
+    sp[7] = 0.0;
+  }
+  bar_sync(1, D.g.nt);
+  D.store_acc(0, io.colpart + (size_t)D.cid * D.g.n);
+  D.finish();
+}
+
+// -------------------------------------------------------- warm start, zeta
+// sinkhorn.py:47-51 (zeta = eta (log a - LSE_row(logX + (gamma - C)/eta)))
+// fused with sinkhorn.py:61-65 (column sums of exp(logX + (zeta + gamma -
+// C)/eta), evaluated with the reference's own expression order).
+struct WarmZIO {
+  const double* gamma;
+  const double* log_a;
+  double eta;
+  double* zeta;      // local rows
+  double* colpart;   // [ncl][n]
+};
+
+template <int NS>
+__global__ void __launch_bounds__(kMaxThreads, 1) k_warm_zeta(Geom geo, WarmZIO io) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  Dense<2> D;
+  D.setup(geo, smem);
+  if (D.producer) {
+    D.produce();
+    D.finish();
+    return;
+  }
+  const double eta = io.eta;
+  for (int r = D.r0; r < D.r1; ++r) {
+    double xs[2 * NS], cs[2 * NS];
+    double mx = -INFINITY;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      xs[2 * s] = xs[2 * s + 1] = 0.0;
+      cs[2 * s] = cs[2 * s + 1] = 0.0;
+      if (s < D.nsl) {
+        double2 c, x;
+        D.fetch(c, x);
+        xs[2 * s] = x.x;
+        xs[2 * s + 1] = x.y;
+        cs[2 * s] = c.x;
+        cs[2 * s + 1] = c.y;
+        const int j = D.col(s, 0);
+        const double2 gm = load_pair(io.gamma, j, D.c1);
+        if (j < D.c1) mx = fmax(mx, x.x + div_rn(gm.x - c.x, eta));
+        if (j + 1 < D.c1) mx = fmax(mx, x.y + div_rn(gm.y - c.y, eta));
+      }
+    }
+    double t[1] = {mx};
+    D.reduce<1, kMax>(t);
+    double M = t[0];
+    double se = 0.0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      if (s < D.nsl) {
+        const int j = D.col(s, 0);
+        const double2 gm = load_pair(io.gamma, j, D.c1);
+        if (j < D.c1) se += exp((xs[2 * s] + div_rn(gm.x - cs[2 * s], eta)) - M);
+        if (j + 1 < D.c1) se += exp((xs[2 * s + 1] + div_rn(gm.y - cs[2 * s + 1], eta)) - M);
+      }
+    }
+    t[0] = se;
+    D.reduce<1, kSum>(t);
+    double S = t[0];
+    if (D.g.cl > 1) {
+      double v2[2] = {M, S};
+      double all[kMaxCluster * 4];
+      D.exchange<2>(v2, all);
+      double Mg = all[0];
+      for (int q = 1; q < D.g.cl; ++q) Mg = fmax(Mg, all[q * 4]);
+      double Sg = 0.0;
+      for (int q = 0; q < D.g.cl; ++q) Sg += all[q * 4 + 1] * exp(all[q * 4] - Mg);
+      M = Mg;
+      S = Sg;
+    }
+    const int64_t gi = D.g.row0 + r;
+    const double zeta = eta * (__ldg(io.log_a + gi) - (M + log(S)));
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      if (s < D.nsl) {
+        const int j = D.col(s, 0);
+        const double2 gm = load_pair(io.gamma, j, D.c1);
+        double e0 = 0.0, e1 = 0.0;
+        if (j < D.c1) e0 = exp(xs[2 * s] + div_rn((zeta + gm.x) - cs[2 * s], eta));
+        if (j + 1 < D.c1) e1 = exp(xs[2 * s + 1] + div_rn((zeta + gm.y) - cs[2 * s + 1], eta));
+        double2* a2 = D.acc2(0, s);
+        double2 v = *a2;
+        v.x += e0;
+        v.y += e1;
+        *a2 = v;
+      }
+    }
+    if (D.tid == 0 && D.cr == 0) io.zeta[r] = zeta;
+  }
+  bar_sync(1, D.g.nt);
+  D.store_acc(0, io.colpart + (size_t)D.cid * D.g.n);
+  D.finish();
+}
+
+// ------------------------------------------------------- warm start, gamma
+// sinkhorn.py:54-58: column log-sum-exp of logX + (zeta - C)/eta, as an
+// online (max, sum) pair per column; partial pairs per cluster.
+struct WarmGIO {
+  const double* zeta;
+  double eta;
+  double* colpart;   // [ncl][2][n]
+};
+
+template <int NS>
+__global__ void __launch_bounds__(kMaxThreads, 1) k_warm_gamma(Geom geo, WarmGIO io) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  Dense<2> D;
+  D.setup(geo, smem);
+  if (D.producer) {
+    D.produce();
+    D.finish();
+    return;
+  }
+  const double eta = io.eta;
+#pragma unroll
+  for (int s = 0; s < NS; ++s)
+    if (s < D.nsl) *D.acc2(0, s) = make_double2(-INFINITY, -INFINITY);
+  for (int r = D.r0; r < D.r1; ++r) {
+    const double zi = io.zeta[r];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      if (s < D.nsl) {
+        double2 c, x;
+        D.fetch(c, x);
+        const int j = D.col(s, 0);
+        double2* m2 = D.acc2(0, s);
+        double2* s2 = D.acc2(1, s);
+        double2 m = *m2, sm = *s2;
+        if (j < D.c1) {
+          const double tv = x.x + div_rn(zi - c.x, eta);
+          if (tv > m.x) {
+            sm.x = sm.x * exp(m.x - tv) + 1.0;
+            m.x = tv;
+          } else {
+            sm.x += exp(tv - m.x);
+          }
+        }
+        if (j + 1 < D.c1) {
+          const double tv = x.y + div_rn(zi - c.y, eta);
+          if (tv > m.y) {
+            sm.y = sm.y * exp(m.y - tv) + 1.0;
+            m.y = tv;
+          } else {
+            sm.y += exp(tv - m.y);
+          }
+        }
+        *m2 = m;
+        *s2 = sm;
+      }
+    }
+  }
+  bar_sync(1, D.g.nt);
+  D.store_acc(0, io.colpart + ((size_t)D.cid * 2 + 0) * D.g.n);
+  D.store_acc(1, io.colpart + ((size_t)D.cid * 2 + 1) * D.g.n);
+  D.finish();
+}
+
+// -------------------------------------------------------- test-only hook
+// Dense P = exp(logit - M_i) / S_i using the row statistics of the last
+// eval (semidual.py:82-83).  Used by RowSoftmaxCache.p in parity tests.
+__global__ void k_materialize_p(const double* C, const double* X, int64_t ld, int m_loc, int n,
+                                const double* gamma, double eta, const double* rowM, const double* rowS,
+                                double* P, int64_t ldp) {
+  const int64_t total = (int64_t)m_loc * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n), j = (int)(idx % n);
+    const double z = X[(size_t)r * ld + j] + div_rn(gamma[j] - C[(size_t)r * ld + j], eta);
+    P[(size_t)r * ldp + j] = div_rn(exp(z - rowM[r]), rowS[r]);
+  }
+}
+
+// Dense rounded plan F^ of the last test (feasibility.py:63-68), test /
+// result hook: ((exp(logX) z_i) y_j) + (e_r_i e_c_j) / deficit.
+__global__ void k_materialize_rounded(const double* X, int64_t ld, int m_loc, int n, const double* zrow,
+                                      const double* y, const double* er, const double* ec,
+                                      const double* deficit_ptr, double* out, int64_t ldo) {
+  const double deficit = *deficit_ptr;
+  const int64_t total = (int64_t)m_loc * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n), j = (int)(idx % n);
+    double f = (exp(X[(size_t)r * ld + j]) * zrow[r]) * y[j];
+    if (deficit > 0.0) f = f + div_rn(er[r] * ec[j], deficit);
+    out[(size_t)r * ldo + j] = f;
+  }
+}
+
+}  // namespace otb

@@ -1,0 +1,282 @@
+// Column-parallel "finish" kernels: reduce the per-cluster partial rows of a
+// dense pass in fixed order, apply the per-column post-operation, and fold
+// scalar partials with the last-block pattern (deterministic).  When the
+// rows are sharded over ranks, phase 1 (k_colreduce) fills a send buffer,
+// the host all-reduces it with NCCL, and phase 2 (the *_post kernels) runs
+// on the globally reduced vector.
+#pragma once
+
+#include "common.cuh"
+
+namespace otb {
+
+struct DevScalars {
+  double value, gnorm, alse, bgam;     // eval
+  double slope;                        // g . direction
+  double sumx, deficit;                // test pass A / B
+  double s8[8];                        // test pass C scalar totals
+  double row_sq, col_sq;               // KKT marginal residual sums of squares
+  double warm_err;
+  double drift;
+  double scratch[4];
+  unsigned long long alloc;            // CSR bump allocator
+  int flags;
+  int pad;
+  unsigned int cnt[16];                // last-block counters
+};
+
+enum CounterIdx {
+  CNT_COLRED = 0, CNT_EVALPOST = 1, CNT_DOT = 2, CNT_ROWS = 3, CNT_VECPOST = 4, CNT_SUM = 5, CNT_WARM = 6
+};
+
+// out[j] = sum_c part[c*n + j]; out[n + k] = sum_c spart[c*sstride + k].
+__global__ void __launch_bounds__(256) k_colreduce(const double* part, int nparts, int n, double* out,
+                                                   const double* spart, int nspart, int sstride, int nscal,
+                                                   unsigned int* counter) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < nparts; ++c) s += part[(size_t)c * n + j];
+    out[j] = s;
+  }
+  if (nscal > 0) {
+    if (last_block(counter)) {
+      if (threadIdx.x < 32) {
+        for (int k = 0; k < nscal; ++k) {
+          const double v = warp_fixed_sum(spart + k, nspart, sstride);
+          if (threadIdx.x == 0) out[n + k] = v;
+        }
+      }
+    }
+  }
+}
+
+// semidual.py:90-100 finish: g = (P^T a) - b, ||g||, L = -b.gamma + eta a.lse.
+// buf[0..n) = column sums of a_i P_ij, buf[n] = a.lse.
+__global__ void __launch_bounds__(256) k_eval_post(int n, const double* buf, const double* b, const double* gamma,
+                                                   double eta, double* g, DevScalars* ds, double* bpart) {
+  __shared__ double red[2][32 * 4];
+  double sq = 0.0, bg = 0.0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const double gj = buf[j] - b[j];
+    g[j] = gj;
+    sq = fma(gj, gj, sq);
+    bg += (-b[j]) * gamma[j];
+  }
+  int ph = 0;
+  double t[2] = {sq, bg};
+  block_reduce<2, kSum>(t, &red[0][0], ph, blockDim.x);
+  if (threadIdx.x == 0) {
+    bpart[2 * blockIdx.x] = t[0];
+    bpart[2 * blockIdx.x + 1] = t[1];
+  }
+  if (last_block(&ds->cnt[CNT_EVALPOST])) {
+    if (threadIdx.x < 32) {
+      const double s = warp_fixed_sum(bpart, gridDim.x, 2);
+      const double bgs = warp_fixed_sum(bpart + 1, gridDim.x, 2);
+      if (threadIdx.x == 0) {
+        const double alse = buf[n];
+        ds->scratch[0] = buf[n + 1];   // count of non-finite rows
+        ds->gnorm = sqrt(s);
+        ds->alse = alse;
+        ds->bgam = bgs;
+        ds->value = bgs + eta * alse;
+      }
+    }
+  }
+}
+
+// Dot product x.y into *out (fixed-order), e.g. slope = g.dir.
+__global__ void __launch_bounds__(256) k_dot(int n, const double* x, const double* y, DevScalars* ds,
+                                             double* bpart, double* out) {
+  __shared__ double red[2][32 * 4];
+  double s = 0.0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) s = fma(x[j], y[j], s);
+  int ph = 0;
+  double t[1] = {s};
+  block_reduce<1, kSum>(t, &red[0][0], ph, blockDim.x);
+  if (threadIdx.x == 0) bpart[blockIdx.x] = t[0];
+  if (last_block(&ds->cnt[CNT_DOT])) {
+    if (threadIdx.x < 32) {
+      const double v = warp_fixed_sum(bpart, gridDim.x, 1);
+      if (threadIdx.x == 0) *out = v;
+    }
+  }
+}
+
+// Sum of v into *out.
+__global__ void __launch_bounds__(256) k_sum(int n, const double* v, DevScalars* ds, double* bpart, double* out) {
+  __shared__ double red[2][32 * 4];
+  double s = 0.0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) s += v[j];
+  int ph = 0;
+  double t[1] = {s};
+  block_reduce<1, kSum>(t, &red[0][0], ph, blockDim.x);
+  if (threadIdx.x == 0) bpart[blockIdx.x] = t[0];
+  if (last_block(&ds->cnt[CNT_SUM])) {
+    if (threadIdx.x < 32) {
+      const double v2 = warp_fixed_sum(bpart, gridDim.x, 1);
+      if (threadIdx.x == 0) *out = v2;
+    }
+  }
+}
+
+// inner_newton.py:88: trial = gamma + t * direction.
+__global__ void k_trial(int n, const double* gamma, const double* dir, double t, double* out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    out[j] = gamma[j] + t * dir[j];
+}
+
+// out = -v
+__global__ void k_neg(int n, const double* v, double* out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) out[j] = -v[j];
+}
+
+// v +/- (*total) / divisor   (sinkhorn.py:102-103 recentring)
+__global__ void k_shift(int len, double* v, const double* total, double divisor, double sign) {
+  const double drift = *total / divisor;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < len; j += gridDim.x * blockDim.x)
+    v[j] = (sign > 0) ? v[j] + drift : v[j] - drift;
+}
+
+// Per-column post operations on a reduced vector buf (length n).
+enum VecPost { POST_COPY = 0, POST_Y = 1, POST_EC = 2, POST_COLRES = 3, POST_WARMERR = 4 };
+
+// POST_COPY:     out = buf
+// POST_Y:        out = buf > 0 ? min(b / buf, 1) : 1        (feasibility.py:62)
+// POST_EC:       out = b - buf                              (feasibility.py:65)
+// POST_COLRES:   *out_s = sum (buf - b)^2                   (feasibility.py:111)
+// POST_WARMERR:  *out_s = sum (buf - b)^2                   (sinkhorn.py:65)
+__global__ void __launch_bounds__(256) k_vec_post(int mode, int n, const double* buf, const double* b,
+                                                  double* out, DevScalars* ds, double* bpart, double* out_s) {
+  __shared__ double red[2][32 * 4];
+  double s = 0.0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const double v = buf[j];
+    if (mode == POST_COPY) out[j] = v;
+    else if (mode == POST_Y) out[j] = (v > 0.0) ? fmin(div_rn(b[j], v), 1.0) : 1.0;
+    else if (mode == POST_EC) out[j] = b[j] - v;
+    else {
+      const double e = v - b[j];
+      s = fma(e, e, s);
+    }
+  }
+  if (mode >= POST_COLRES) {
+    int ph = 0;
+    double t[1] = {s};
+    block_reduce<1, kSum>(t, &red[0][0], ph, blockDim.x);
+    if (threadIdx.x == 0) bpart[blockIdx.x] = t[0];
+    if (last_block(&ds->cnt[CNT_VECPOST])) {
+      if (threadIdx.x < 32) {
+        const double v2 = warp_fixed_sum(bpart, gridDim.x, 1);
+        if (threadIdx.x == 0) *out_s = v2;
+      }
+    }
+  }
+}
+
+// Row-side finishes over local rows (rowpart [m_loc][cl]):
+//   mode 0 (test pass B): er_i = a_i - rowsum_i, *out_s = sum |er_i|  (feasibility.py:64-66)
+//   mode 1 (test pass C): *out_s = sum (rowsum_i - a_i)^2            (feasibility.py:110)
+__global__ void __launch_bounds__(256) k_rows_post(int mode, int m_loc, int cl, const double* rowpart,
+                                                   const double* a, int64_t row0, double* er, DevScalars* ds,
+                                                   double* bpart, double* out_s) {
+  __shared__ double red[2][32 * 4];
+  double s = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m_loc; i += gridDim.x * blockDim.x) {
+    double rs = 0.0;
+    for (int q = 0; q < cl; ++q) rs += rowpart[(size_t)i * cl + q];
+    const double ai = a[row0 + i];
+    if (mode == 0) {
+      const double e = ai - rs;
+      er[i] = e;
+      s += fabs(e);
+    } else {
+      const double e = rs - ai;
+      s = fma(e, e, s);
+    }
+  }
+  int ph = 0;
+  double t[1] = {s};
+  block_reduce<1, kSum>(t, &red[0][0], ph, blockDim.x);
+  if (threadIdx.x == 0) bpart[blockIdx.x] = t[0];
+  if (last_block(&ds->cnt[CNT_ROWS])) {
+    if (threadIdx.x < 32) {
+      const double v = warp_fixed_sum(bpart, gridDim.x, 1);
+      if (threadIdx.x == 0) *out_s = v;
+    }
+  }
+}
+
+// Warm-start gamma finish (sinkhorn.py:36-39, 54-58): combine the per-cluster
+// (max, sum) pairs of each column.  mode 0: write M and S (multi-rank phase
+// 1); mode 1: write gamma_j = eta (log b_j - (M + log S)) directly.
+__global__ void __launch_bounds__(256) k_warm_gamma_combine(int mode, int n, const double* part, int nparts,
+                                                            double* outM, double* outS, const double* log_b,
+                                                            double eta, double* gamma) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    double M = -INFINITY;
+    for (int c = 0; c < nparts; ++c) M = fmax(M, part[((size_t)c * 2) * n + j]);
+    double S = 0.0;
+    for (int c = 0; c < nparts; ++c) {
+      const double mc = part[((size_t)c * 2) * n + j];
+      if (mc != -INFINITY) S += part[((size_t)c * 2 + 1) * n + j] * exp(mc - M);
+    }
+    if (mode == 0) {
+      outM[j] = M;
+      outS[j] = S;
+    } else {
+      gamma[j] = eta * (log_b[j] - (M + log(S)));
+    }
+  }
+}
+
+// Multi-rank: rescale the local S to the global max, before the sum reduce.
+__global__ void k_warm_rescale(int n, const double* Mloc, const double* Mglob, double* S) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const double ml = Mloc[j];
+    S[j] = (ml == -INFINITY) ? 0.0 : S[j] * exp(ml - Mglob[j]);
+  }
+}
+
+__global__ void k_warm_gamma_post(int n, const double* M, const double* S, const double* log_b, double eta,
+                                  double* gamma) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+    gamma[j] = eta * (log_b[j] - (M[j] + log(S[j])));
+}
+
+// zeta_i = eta (log a_i - lse_i): the row potential of the accepted dual
+// (bregman_outer.py:123-126 -> sinkhorn.py:47-51 on the cached lse).
+__global__ void k_zeta_from_lse(int m_loc, const double* log_a, int64_t row0, const double* lse, double eta,
+                                double* zeta) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m_loc; i += gridDim.x * blockDim.x)
+    zeta[i] = eta * (log_a[row0 + i] - lse[i]);
+}
+
+// Test hook: CSR rows gathered into local-row order (int32 columns).
+__global__ void k_csr_compact(int m_loc, const int64_t* row_start, const int* row_len, const int64_t* rowpre,
+                              const uint16_t* cols, const double* vals, int32_t* out_cols, double* out_vals) {
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int r = gw; r < m_loc; r += nw) {
+    const int64_t s = row_start[r], o = rowpre[r];
+    for (int k = lane; k < row_len[r]; k += 32) {
+      out_cols[o + k] = cols[s + k];
+      out_vals[o + k] = vals[s + k];
+    }
+  }
+}
+
+}  // namespace otb
+
+namespace otb {
+// X^0 = a b^T in the log domain, clamped (bregman_outer.py:91-93, core.py:141-145).
+__global__ void k_init_plan(double* X, int64_t ld, int m_loc, int n, const double* log_a, int64_t row0,
+                            const double* log_b) {
+  const int64_t total = (int64_t)m_loc * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n), j = (int)(idx % n);
+    X[(size_t)r * ld + j] = fmax(log_a[row0 + r] + log_b[j], kLogFloor);
+  }
+}
+}  // namespace otb

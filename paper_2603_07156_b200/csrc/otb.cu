@@ -1,0 +1,1061 @@
+// libotb host side: context, C ABI (include/otb.h) and the orchestration of
+// one IBSN inner iteration on the device.  The host only reads scalars back
+// (objective, gradient norm, CG status every kCgBatch iterations, slope,
+// test results); every vector stays in HBM.
+#include "otb.h"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dense.cuh"
+#include "finish.cuh"
+#include "sparse.cuh"
+
+using namespace otb;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess) return fail(OTB_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define TRY(expr)                  \
+  do {                             \
+    int s_ = (expr);               \
+    if (s_ != OTB_OK) return s_;   \
+  } while (0)
+
+#define LAUNCH_CHECK() CUDA_TRY(cudaGetLastError())
+
+// ------------------------------------------------------------------ NCCL
+struct NcclId {
+  char internal[128];
+};
+typedef void* NcclComm;
+struct Nccl {
+  void* h = nullptr;
+  int (*getUniqueId)(NcclId*) = nullptr;
+  int (*commInitRank)(NcclComm*, int, NcclId, int) = nullptr;
+  int (*allReduce)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+  int (*commDestroy)(NcclComm) = nullptr;
+  const char* (*getErrorString)(int) = nullptr;
+};
+constexpr int kNcclFloat64 = 8;
+constexpr int kNcclSum = 0;
+constexpr int kNcclMax = 2;
+
+int load_nccl(const char* path, Nccl& api) {
+  if (api.h) return OTB_OK;
+  void* h = dlopen(path && path[0] ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return fail(OTB_ERR_NCCL, std::string("dlopen nccl: ") + dlerror());
+  api.getUniqueId = (int (*)(NcclId*))dlsym(h, "ncclGetUniqueId");
+  api.commInitRank = (int (*)(NcclComm*, int, NcclId, int))dlsym(h, "ncclCommInitRank");
+  api.allReduce = (int (*)(const void*, void*, size_t, int, int, NcclComm, cudaStream_t))dlsym(h, "ncclAllReduce");
+  api.commDestroy = (int (*)(NcclComm))dlsym(h, "ncclCommDestroy");
+  api.getErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+  if (!api.getUniqueId || !api.commInitRank || !api.allReduce || !api.commDestroy)
+    return fail(OTB_ERR_NCCL, "nccl symbols missing");
+  api.h = h;
+  return OTB_OK;
+}
+
+// ------------------------------------------------------------- kernels
+enum DenseKind { DK_EVAL = 0, DK_SPARSIFY, DK_TESTA, DK_TESTB, DK_TESTC0, DK_TESTC1, DK_WARMZ, DK_WARMG, DK_COUNT };
+const int kNmat[DK_COUNT] = {2, 2, 2, 1, 1, 2, 2, 2};
+const int kNacc[DK_COUNT] = {1, 1, 1, 1, 1, 1, 1, 2};
+const int kStaticSmem[DK_COUNT] = {0, (int)(kTabInts * 4 + 16), 0, 0, 0, 0, 0, 0};
+
+#define NS_ROW(K) \
+  { nullptr, (const void*)K<1>, (const void*)K<2>, (const void*)K<3>, (const void*)K<4>, \
+    (const void*)K<5>, (const void*)K<6>, (const void*)K<7>, (const void*)K<8> }
+const void* const kDenseFn[DK_COUNT][kMaxNS + 1] = {
+    NS_ROW(k_eval), NS_ROW(k_sparsify), NS_ROW(k_test_a), NS_ROW(k_test_b),
+    {nullptr, (const void*)k_test_c<1, false>, (const void*)k_test_c<2, false>, (const void*)k_test_c<3, false>,
+     (const void*)k_test_c<4, false>, (const void*)k_test_c<5, false>, (const void*)k_test_c<6, false>,
+     (const void*)k_test_c<7, false>, (const void*)k_test_c<8, false>},
+    {nullptr, (const void*)k_test_c<1, true>, (const void*)k_test_c<2, true>, (const void*)k_test_c<3, true>,
+     (const void*)k_test_c<4, true>, (const void*)k_test_c<5, true>, (const void*)k_test_c<6, true>,
+     (const void*)k_test_c<7, true>, (const void*)k_test_c<8, true>},
+    NS_ROW(k_warm_zeta), NS_ROW(k_warm_gamma)};
+
+enum ProfClass { PC_EVAL = 0, PC_SPARSIFY, PC_HV, PC_CGVEC, PC_TESTA, PC_TESTB, PC_TESTC, PC_WARMZ, PC_WARMG, PC_N = 16 };
+
+constexpr int kCgBatch = 16;
+constexpr size_t kMaxDynSmem = 232448;  // 227 KB
+
+}  // namespace
+
+struct otb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int64_t m_glob = 0, n = 0, row0 = 0, row1 = 0, m_loc = 0, ld = 0;
+  int num_sms = 148;
+  // dense geometry
+  int nt = 0, ns = 0, cl = 1, colw = 0, ncl = 0, grid = 0;
+  int nstage[DK_COUNT] = {};
+  size_t smem[DK_COUNT] = {};
+  // hess_apply
+  int hv_mode = 0, hv_grid = 0;
+  size_t hv_smem = 0;
+  int colgrid = 0;
+  // problem
+  const double *C = nullptr, *a = nullptr, *b = nullptr, *log_a = nullptr, *log_b = nullptr;
+  double eta = 0.0, norm_c = 0.0, norm_a = 0.0, norm_b = 0.0;
+  int64_t anchor = -1;
+  bool bound = false;
+  // buffers
+  double *rowM = nullptr, *rowS = nullptr, *lse = nullptr, *zrow = nullptr, *er = nullptr, *rowpart = nullptr;
+  double *colpart = nullptr, *vpart = nullptr, *sendbuf = nullptr, *bpart = nullptr;
+  double *g = nullptr, *d = nullptr, *rhs = nullptr, *dir = nullptr, *cg_r = nullptr, *cg_p[2] = {nullptr, nullptr};
+  double *cg_ap = nullptr, *cg_y = nullptr, *gtrial = nullptr, *yv = nullptr, *ec = nullptr;
+  double *Mloc = nullptr, *Mglob = nullptr, *Sloc = nullptr;
+  int64_t *row_start = nullptr, *rowpre = nullptr;
+  int* row_len = nullptr;
+  uint16_t* cols = nullptr;
+  double* vals = nullptr;
+  int64_t cap = 0, chunk = 0, nnz = 0;
+  DevScalars* ds = nullptr;
+  DevScalars* hs = nullptr;   // pinned
+  CgState* cg = nullptr;
+  CgState* hcg = nullptr;     // pinned
+  double* hbuf = nullptr;     // pinned, 16 doubles
+  // state
+  double last_value = 0.0, last_gnorm = 0.0;
+  bool have_eval = false;
+  const double* round_src = nullptr;
+  // NCCL
+  Nccl nccl;
+  NcclComm comm = nullptr;
+  int nranks = 1, rank = 0;
+  // profiling
+  bool prof = false;
+  struct Rec {
+    int cls;
+    cudaEvent_t e0, e1;
+    double bytes;
+  };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  double prof_ms[PC_N] = {}, prof_bytes[PC_N] = {};
+  int64_t prof_cnt[PC_N] = {};
+};
+
+namespace {
+
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
+
+template <class T>
+int dalloc(T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc((void**)p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(OTB_ERR_NOMEM, std::string("cudaMalloc ") + std::to_string(count * sizeof(T)) + " bytes: " +
+                                   cudaGetErrorString(e));
+  }
+  return OTB_OK;
+}
+
+size_t dense_smem(const otb_ctx* c, int kind, int nstage) {
+  const size_t slice = 2 * (size_t)c->nt;
+  const size_t dbl = (size_t)nstage * kNmat[kind] * slice + (size_t)kNacc[kind] * c->ns * slice + 2 * 32 * 4 + 2 * 8 * 4;
+  return dbl * 8 + (2 * (size_t)nstage + 2) * 8 + 64 * 4;
+}
+
+Geom make_geom(const otb_ctx* c, int kind, const double* m0, const double* m1) {
+  Geom g;
+  g.mat0 = m0;
+  g.mat1 = m1;
+  g.ld = c->ld;
+  g.m_loc = (int)c->m_loc;
+  g.n = (int)c->n;
+  g.row0 = c->row0;
+  g.nt = c->nt;
+  g.ns = c->ns;
+  g.cl = c->cl;
+  g.colw = c->colw;
+  g.nstage = c->nstage[kind];
+  g.nacc = kNacc[kind];
+  return g;
+}
+
+// ---------------------------------------------------------- profiling
+int prof_begin(otb_ctx* c, cudaEvent_t* e0) {
+  if (!c->prof) return OTB_OK;
+  if (c->pool.empty()) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    c->pool.push_back(e);
+  }
+  *e0 = c->pool.back();
+  c->pool.pop_back();
+  CUDA_TRY(cudaEventRecord(*e0, c->stream));
+  return OTB_OK;
+}
+
+int prof_end(otb_ctx* c, int cls, cudaEvent_t e0, double bytes) {
+  if (!c->prof) return OTB_OK;
+  if (c->pool.empty()) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    c->pool.push_back(e);
+  }
+  cudaEvent_t e1 = c->pool.back();
+  c->pool.pop_back();
+  CUDA_TRY(cudaEventRecord(e1, c->stream));
+  c->recs.push_back({cls, e0, e1, bytes});
+  return OTB_OK;
+}
+
+int prof_collect(otb_ctx* c) {
+  if (c->recs.empty()) return OTB_OK;
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  for (auto& r : c->recs) {
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, r.e0, r.e1));
+    c->prof_ms[r.cls] += ms;
+    c->prof_bytes[r.cls] += r.bytes;
+    c->prof_cnt[r.cls] += 1;
+    c->pool.push_back(r.e0);
+    c->pool.push_back(r.e1);
+  }
+  c->recs.clear();
+  return OTB_OK;
+}
+
+// ------------------------------------------------------------- helpers
+int launch_dense(otb_ctx* c, int kind, Geom geo, void* io) {
+  const void* fn = kDenseFn[kind][geo.ns];
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)c->grid);
+  cfg.blockDim = dim3((unsigned)(geo.nt + 32));
+  cfg.dynamicSmemBytes = c->smem[kind];
+  cfg.stream = c->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)c->cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[2] = {&geo, io};
+  CUDA_TRY(cudaLaunchKernelExC(&cfg, fn, args));
+  return OTB_OK;
+}
+
+int allreduce(otb_ctx* c, double* buf, size_t count, int op) {
+  if (c->nranks <= 1) return OTB_OK;
+  const int r = c->nccl.allReduce(buf, buf, count, kNcclFloat64, op, c->comm, c->stream);
+  if (r != 0)
+    return fail(OTB_ERR_NCCL, std::string("ncclAllReduce: ") + (c->nccl.getErrorString ? c->nccl.getErrorString(r) : "?"));
+  return OTB_OK;
+}
+
+int sync_scalars(otb_ctx* c) {
+  CUDA_TRY(cudaMemcpyAsync(c->hs, c->ds, sizeof(DevScalars), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return OTB_OK;
+}
+
+int colreduce(otb_ctx* c, int nparts, const double* spart, int nspart, int sstride, int nscal) {
+  k_colreduce<<<c->colgrid, 256, 0, c->stream>>>(c->colpart, nparts, (int)c->n, c->sendbuf, spart, nspart, sstride,
+                                                 nscal, &c->ds->cnt[CNT_COLRED]);
+  LAUNCH_CHECK();
+  return OTB_OK;
+}
+
+int require_bound(const otb_ctx* c) {
+  if (!c) return fail(OTB_ERR_ARG, "null context");
+  if (!c->bound) return fail(OTB_ERR_ARG, "no problem bound (otb_bind)");
+  return OTB_OK;
+}
+
+// ------------------------------------------------------------- eval
+int do_eval(otb_ctx* c, const double* X, const double* gamma) {
+  const int n = (int)c->n;
+  Geom geo = make_geom(c, DK_EVAL, c->C, X);
+  EvalIO io{gamma, c->a, c->eta, c->rowM, c->rowS, c->lse, c->colpart, c->vpart};
+  cudaEvent_t e0 = nullptr;
+  TRY(prof_begin(c, &e0));
+  TRY(launch_dense(c, DK_EVAL, geo, &io));
+  TRY(prof_end(c, PC_EVAL, e0, 16.0 * c->m_loc * n + 24.0 * c->m_loc + 16.0 * n));
+  TRY(colreduce(c, c->ncl, c->vpart, c->ncl, 2, 2));
+  TRY(allreduce(c, c->sendbuf, (size_t)n + 2, kNcclSum));
+  k_eval_post<<<c->colgrid, 256, 0, c->stream>>>(n, c->sendbuf, c->b, gamma, c->eta, c->g, c->ds, c->bpart);
+  LAUNCH_CHECK();
+  TRY(sync_scalars(c));
+  if (c->hs->scratch[0] != 0.0) {
+    c->have_eval = false;
+    return fail(OTB_ERR_NONFINITE, "row softmax produced non-finite values after stabilization");
+  }
+  c->last_value = c->hs->value;
+  c->last_gnorm = c->hs->gnorm;
+  c->have_eval = true;
+  return OTB_OK;
+}
+
+// --------------------------------------------------------- sparsify
+int grow_csr(otb_ctx* c, int64_t want) {
+  if (want <= c->cap) return OTB_OK;
+  int64_t ncap = std::max<int64_t>(want, (int64_t)(c->cap * 1.5));
+  ncap = std::min<int64_t>(ncap, c->m_loc * c->n + (int64_t)c->ncl * c->chunk + c->n);
+  if (c->cols) cudaFree(c->cols);
+  if (c->vals) cudaFree(c->vals);
+  c->cols = nullptr;
+  c->vals = nullptr;
+  c->cap = 0;
+  TRY(dalloc(&c->cols, (size_t)ncap));
+  TRY(dalloc(&c->vals, (size_t)ncap));
+  c->cap = ncap;
+  return OTB_OK;
+}
+
+int do_sparsify(otb_ctx* c, const double* X, const double* gamma, double rho) {
+  const int n = (int)c->n;
+  const int64_t anchor_local = (c->anchor >= c->row0 && c->anchor < c->row1) ? c->anchor - c->row0 : -1;
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    CUDA_TRY(cudaMemsetAsync(&c->ds->alloc, 0, sizeof(unsigned long long), c->stream));
+    CUDA_TRY(cudaMemsetAsync(&c->ds->flags, 0, sizeof(int), c->stream));
+    Geom geo = make_geom(c, DK_SPARSIFY, c->C, X);
+    SparsifyIO io{gamma, c->a, c->eta, rho, anchor_local, c->rowM, c->rowS, c->cols, c->vals, c->cap,
+                  c->row_start, c->row_len, &c->ds->alloc, c->chunk, c->colpart, &c->ds->flags};
+    cudaEvent_t e0 = nullptr;
+    TRY(prof_begin(c, &e0));
+    TRY(launch_dense(c, DK_SPARSIFY, geo, &io));
+    k_row_prefix<<<1, 1024, 0, c->stream>>>(c->row_len, (int)c->m_loc, c->rowpre);
+    LAUNCH_CHECK();
+    CUDA_TRY(cudaMemcpyAsync(c->hbuf, c->rowpre + c->m_loc, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    TRY(sync_scalars(c));
+    int64_t nnz;
+    std::memcpy(&nnz, c->hbuf, sizeof(int64_t));
+    TRY(prof_end(c, PC_SPARSIFY, e0, 16.0 * c->m_loc * n + 10.0 * nnz + 12.0 * c->m_loc));
+    if (c->hs->flags & 2) {
+      const int64_t need = (int64_t)c->hs->alloc + (int64_t)c->ncl * c->chunk;
+      TRY(grow_csr(c, need + need / 8));
+      continue;
+    }
+    c->nnz = nnz;
+    TRY(colreduce(c, c->ncl, nullptr, 0, 0, 0));
+    TRY(allreduce(c, c->sendbuf, (size_t)n, kNcclSum));
+    k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_COPY, n, c->sendbuf, c->b, c->d, c->ds, c->bpart, nullptr);
+    LAUNCH_CHECK();
+    return OTB_OK;
+  }
+  return fail(OTB_ERR_NOMEM, "CSR capacity could not be grown");
+}
+
+Csr csr_view(const otb_ctx* c) {
+  Csr A;
+  A.row_start = c->row_start;
+  A.row_len = c->row_len;
+  A.rowpre = c->rowpre;
+  A.cols = c->cols;
+  A.vals = c->vals;
+  A.m_loc = (int)c->m_loc;
+  A.row0 = c->row0;
+  return A;
+}
+
+double hv_bytes(const otb_ctx* c) { return 10.0 * c->nnz + 12.0 * c->m_loc + 16.0 * c->n; }
+
+// y = P_rho^T (a * (P_rho v)) reduced to: (mode smem) colpart[hv_grid][n] or
+// sendbuf (multi-rank), (mode atomic) cg_y or sendbuf.  Returns via
+// ysum/colpart/yatomic the arguments for the column kernels.
+struct HvResult {
+  const double* colpart;
+  int nparts;
+  double* yatomic;
+  const double* ysum;
+};
+
+int run_hv(otb_ctx* c, const double* v_src, const double* r, const double* p_prev, double* p_cur, int update,
+           const CgState* st, HvResult* res) {
+  const int n = (int)c->n;
+  cudaEvent_t e0 = nullptr;
+  if (c->hv_mode == 0) {
+    HvArgs h{csr_view(c), c->a, n, v_src, r, p_prev, p_cur, update, st, c->colpart};
+    TRY(prof_begin(c, &e0));
+    k_hv_smem<<<c->hv_grid, 512, c->hv_smem, c->stream>>>(h);
+    LAUNCH_CHECK();
+    TRY(prof_end(c, PC_HV, e0, hv_bytes(c)));
+    if (c->nranks > 1) {
+      TRY(colreduce(c, c->hv_grid, nullptr, 0, 0, 0));
+      TRY(allreduce(c, c->sendbuf, (size_t)n, kNcclSum));
+      *res = {nullptr, 0, nullptr, c->sendbuf};
+    } else {
+      *res = {c->colpart, c->hv_grid, nullptr, nullptr};
+    }
+  } else {
+    const double* v = update ? p_cur : v_src;
+    if (update) {
+      k_cg_p<<<c->colgrid, 256, 0, c->stream>>>(n, r, p_prev, p_cur, st);
+      LAUNCH_CHECK();
+    }
+    HvAtomicArgs h{csr_view(c), c->a, v, c->cg_y, st};
+    TRY(prof_begin(c, &e0));
+    k_hv_atomic<<<c->hv_grid, 256, 0, c->stream>>>(h);
+    LAUNCH_CHECK();
+    TRY(prof_end(c, PC_HV, e0, hv_bytes(c)));
+    if (c->nranks > 1) {
+      CUDA_TRY(cudaMemcpyAsync(c->sendbuf, c->cg_y, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+      CUDA_TRY(cudaMemsetAsync(c->cg_y, 0, sizeof(double) * n, c->stream));
+      TRY(allreduce(c, c->sendbuf, (size_t)n, kNcclSum));
+      *res = {nullptr, 0, nullptr, c->sendbuf};
+    } else {
+      *res = {nullptr, 0, c->cg_y, nullptr};
+    }
+  }
+  return OTB_OK;
+}
+
+// ------------------------------------------------------------------ CG
+int cg_iteration(otb_ctx* c, int64_t k, double* x) {
+  const int n = (int)c->n;
+  double* pc = c->cg_p[k & 1];
+  double* pp = c->cg_p[(k + 1) & 1];
+  HvResult hr;
+  TRY(run_hv(c, pc, c->cg_r, pp, pc, k > 0 ? 1 : 0, c->cg, &hr));
+  cudaEvent_t e0 = nullptr;
+  TRY(prof_begin(c, &e0));
+  CgApArgs a{n, hr.colpart, hr.nparts, hr.yatomic, hr.ysum, c->d, pc, c->eta, c->cg_ap, c->cg, c->bpart};
+  k_cg_ap<<<c->colgrid, 256, 0, c->stream>>>(a);
+  LAUNCH_CHECK();
+  k_cg_update<<<c->colgrid, 256, 0, c->stream>>>(n, x, c->cg_r, pc, c->cg_ap, c->cg, c->bpart);
+  LAUNCH_CHECK();
+  TRY(prof_end(c, PC_CGVEC, e0, 8.0 * 9 * n));
+  return OTB_OK;
+}
+
+int do_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t max_iters, double* x, otb_cg_out* out) {
+  const int n = (int)c->n;
+  k_cg_init<<<c->colgrid, 256, 0, c->stream>>>(n, rhs, x, c->cg_r, c->cg_p[0], c->cg, c->bpart, shift, rel_tol,
+                                               (long long)max_iters);
+  LAUNCH_CHECK();
+  CUDA_TRY(cudaMemcpyAsync(c->hcg, c->cg, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (c->hcg->status == CG_INCONSISTENT)
+    return fail(OTB_ERR_INCONSISTENT, "unshifted system with right-hand side outside the range");
+  int64_t k = 0;
+  while (c->hcg->status == CG_RUN) {
+    for (int j = 0; j < kCgBatch; ++j, ++k) TRY(cg_iteration(c, k, x));
+    CUDA_TRY(cudaMemcpyAsync(c->hcg, c->cg, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
+  if (c->hcg->status == CG_NOTPD) {
+    char buf[96];
+    std::snprintf(buf, sizeof buf, "p^T A p = %.3g before convergence", c->hcg->curv);
+    return fail(OTB_ERR_NOT_PD, buf);
+  }
+  if (out) {
+    out->iters = c->hcg->iters;
+    out->residual = c->hcg->res;
+    out->status = c->hcg->status;
+  }
+  return OTB_OK;
+}
+
+// ------------------------------------------------------ inexact test
+int do_round(otb_ctx* c, const double* X, const double* gamma, double* Xout, int recover, int metrics,
+             otb_test_out* out) {
+  const int n = (int)c->n;
+  const double mn = (double)c->m_loc * n;
+  // pass A: candidate + row scaling + column sums
+  {
+    Geom geo = make_geom(c, DK_TESTA, c->C, X);
+    TestAIO io{gamma, c->a, c->log_a, c->lse, c->eta, Xout, c->zrow, c->colpart, c->vpart, recover};
+    cudaEvent_t e0 = nullptr;
+    TRY(prof_begin(c, &e0));
+    TRY(launch_dense(c, DK_TESTA, geo, &io));
+    TRY(prof_end(c, PC_TESTA, e0, recover ? 24.0 * mn : 16.0 * mn));
+    TRY(colreduce(c, c->ncl, c->vpart, c->grid, 2, 2));
+    TRY(allreduce(c, c->sendbuf, (size_t)n + 2, kNcclSum));
+    k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_Y, n, c->sendbuf, c->b, c->yv, c->ds, c->bpart, nullptr);
+    LAUNCH_CHECK();
+    CUDA_TRY(cudaMemcpyAsync(&c->ds->sumx, c->sendbuf + n, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(&c->ds->scratch[1], c->sendbuf + n + 1, sizeof(double), cudaMemcpyDeviceToDevice,
+                             c->stream));
+  }
+  const double* src = recover ? Xout : X;
+  // pass B: F = (X z) y, e_r, e_c, deficit
+  {
+    Geom geo = make_geom(c, DK_TESTB, src, nullptr);
+    TestBIO io{c->zrow, c->yv, c->rowpart, c->colpart};
+    cudaEvent_t e0 = nullptr;
+    TRY(prof_begin(c, &e0));
+    TRY(launch_dense(c, DK_TESTB, geo, &io));
+    TRY(prof_end(c, PC_TESTB, e0, 8.0 * mn));
+    k_rows_post<<<c->colgrid, 256, 0, c->stream>>>(0, (int)c->m_loc, c->cl, c->rowpart, c->a, c->row0, c->er, c->ds,
+                                                   c->bpart, &c->ds->scratch[2]);
+    LAUNCH_CHECK();
+    TRY(colreduce(c, c->ncl, &c->ds->scratch[2], 1, 1, 1));
+    TRY(allreduce(c, c->sendbuf, (size_t)n + 1, kNcclSum));
+    k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_EC, n, c->sendbuf, c->b, c->ec, c->ds, c->bpart, nullptr);
+    LAUNCH_CHECK();
+    CUDA_TRY(cudaMemcpyAsync(&c->ds->deficit, c->sendbuf + n, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  }
+  // pass C: rank-one correction, Bregman divergence, objective, KKT sums
+  {
+    const int kind = metrics ? DK_TESTC1 : DK_TESTC0;
+    Geom geo = make_geom(c, kind, src, metrics ? c->C : nullptr);
+    TestCIO io{c->zrow, c->yv, c->er, c->ec, &c->ds->deficit, gamma, c->rowpart, c->colpart, c->vpart};
+    cudaEvent_t e0 = nullptr;
+    TRY(prof_begin(c, &e0));
+    TRY(launch_dense(c, kind, geo, &io));
+    TRY(prof_end(c, PC_TESTC, e0, metrics ? 16.0 * mn : 8.0 * mn));
+    k_rows_post<<<c->colgrid, 256, 0, c->stream>>>(1, (int)c->m_loc, c->cl, c->rowpart, c->a, c->row0, nullptr,
+                                                   c->ds, c->bpart, c->vpart + 7);
+    LAUNCH_CHECK();
+    TRY(colreduce(c, c->ncl, c->vpart, c->grid, 8, 8));
+    TRY(allreduce(c, c->sendbuf, (size_t)n + 8, kNcclSum));
+    k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_COLRES, n, c->sendbuf, c->b, nullptr, c->ds, c->bpart,
+                                                  &c->ds->col_sq);
+    LAUNCH_CHECK();
+    CUDA_TRY(cudaMemcpyAsync(c->ds->s8, c->sendbuf + n, 8 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  }
+  TRY(sync_scalars(c));
+  c->round_src = src;
+  const DevScalars& h = *c->hs;
+  if (h.scratch[1] != 0.0) return fail(OTB_ERR_BAD_LOGPLAN, "log plan contains NaN or +inf entries");
+  if (out) {
+    out->sum_x = h.sumx;
+    out->deficit = h.deficit;
+    out->bregman = h.s8[0] - h.s8[1] + h.sumx;   // feasibility.py:85
+    out->objective = h.s8[2];
+    const double cscale = 1.0 + c->norm_c;
+    const double row_res = std::sqrt(h.s8[7]) / (1.0 + c->norm_a);
+    const double col_res = std::sqrt(h.col_sq) / (1.0 + c->norm_b);
+    const double neg = std::sqrt(h.s8[4]) / (1.0 + std::sqrt(h.s8[3]));
+    out->delta_p = std::max(std::max(row_res, col_res), neg);
+    out->delta_d = std::sqrt(h.s8[5]) / cscale;
+    out->delta_c = std::fabs(h.s8[6]) / cscale;
+    out->delta_kkt = std::max(std::max(out->delta_p, out->delta_d), out->delta_c);
+    if (metrics && !std::isfinite(out->objective)) {
+      char buf[64];
+      std::snprintf(buf, sizeof buf, "non-finite objective %g", out->objective);
+      return fail(OTB_ERR_OBJECTIVE, buf);
+    }
+  }
+  return OTB_OK;
+}
+
+}  // namespace
+
+// ======================================================================
+// C ABI
+// ======================================================================
+extern "C" {
+
+int otb_abi_version(void) { return OTB_ABI_VERSION; }
+
+const char* otb_last_error(void) { return g_err.c_str(); }
+
+int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, int64_t row_end, int64_t ld,
+               int device, void* stream) {
+  if (!out) return fail(OTB_ERR_ARG, "out is null");
+  *out = nullptr;
+  if (m_global <= 0 || n <= 0) return fail(OTB_ERR_ARG, "empty problem");
+  if (n > 65536) return fail(OTB_ERR_ARG, "n > 65536 is not supported (16-bit CSR column indices)");
+  if (row_begin < 0 || row_end > m_global || row_end <= row_begin) return fail(OTB_ERR_ARG, "bad row range");
+  if (ld < n || ld % 32 != 0) return fail(OTB_ERR_ARG, "ld must be >= n and a multiple of 32");
+  CUDA_TRY(cudaSetDevice(device));
+  otb_ctx* c = new otb_ctx();
+  c->device = device;
+  c->stream = (cudaStream_t)stream;
+  c->m_glob = m_global;
+  c->n = n;
+  c->row0 = row_begin;
+  c->row1 = row_end;
+  c->m_loc = row_end - row_begin;
+  c->ld = ld;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  c->num_sms = sms;
+  // dense geometry: cluster size, column window, slices, threads
+  int cl = 1;
+  while (cdiv(n, cl) > 2 * 512 * kMaxNS && cl < kMaxCluster) cl *= 2;
+  c->cl = cl;
+  c->colw = (int)rup(cdiv(n, cl), 2);
+  int ns = (int)std::min<int64_t>(kMaxNS, std::max<int64_t>(1, cdiv(c->colw, 1024)));
+  int nt = (int)rup(cdiv(c->colw, 2 * ns), 32);
+  const char* env_nt = std::getenv("OTB_DENSE_NT");
+  if (env_nt) {
+    const int want = std::atoi(env_nt);
+    if (want >= 32 && want <= 512 && want % 32 == 0) {
+      nt = want;
+      ns = (int)cdiv(c->colw, 2 * nt);
+      if (ns > kMaxNS) {
+        ns = kMaxNS;
+        nt = (int)rup(cdiv(c->colw, 2 * ns), 32);
+      }
+    }
+  }
+  c->ns = ns;
+  c->nt = std::max(nt, 32);
+  int per_sm = 1;
+  const char* env_cps = std::getenv("OTB_DENSE_CTAS_PER_SM");
+  if (env_cps) per_sm = std::max(1, std::min(4, std::atoi(env_cps)));
+  c->ncl = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)(sms * per_sm) / cl, c->m_loc));
+  c->grid = c->ncl * cl;
+  for (int k = 0; k < DK_COUNT; ++k) {
+    const size_t budget = kMaxDynSmem / per_sm - kStaticSmem[k] - 1024;
+    int st = 8;
+    while (st > 2 && dense_smem(c, k, st) > budget) --st;
+    c->nstage[k] = st;
+    c->smem[k] = dense_smem(c, k, st);
+    if (c->smem[k] > budget) {
+      delete c;
+      return fail(OTB_ERR_ARG, "dense geometry does not fit shared memory");
+    }
+    const void* fn = kDenseFn[k][c->ns];
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem[k]);
+    if (e != cudaSuccess) {
+      delete c;
+      return fail(OTB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    }
+  }
+  // hess_apply variant
+  const int64_t npad = rup(n, 2);
+  c->hv_smem = (size_t)(2 * npad + 2 * 32 * 4) * 8;
+  const char* env_hv = std::getenv("OTB_HV_MODE");
+  c->hv_mode = (c->hv_smem <= kMaxDynSmem - 1024) ? 0 : 1;
+  if (env_hv && std::atoi(env_hv) == 1) c->hv_mode = 1;
+  if (c->hv_mode == 0) {
+    c->hv_grid = sms;
+    cudaError_t e = cudaFuncSetAttribute((const void*)k_hv_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)c->hv_smem);
+    if (e != cudaSuccess) {
+      delete c;
+      return fail(OTB_ERR_CUDA, std::string("cudaFuncSetAttribute(hv): ") + cudaGetErrorString(e));
+    }
+  } else {
+    c->hv_grid = sms * 8;
+  }
+  c->colgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 2 * sms));
+  // buffers
+  const int64_t m_loc = c->m_loc;
+  const int64_t nv = npad + 16;
+  int st = OTB_OK;
+  auto A = [&](double** p, size_t cnt) {
+    if (st == OTB_OK) st = dalloc(p, cnt);
+  };
+  A(&c->rowM, m_loc);
+  A(&c->rowS, m_loc);
+  A(&c->lse, m_loc);
+  A(&c->zrow, m_loc);
+  A(&c->er, m_loc);
+  A(&c->rowpart, (size_t)m_loc * cl);
+  const int64_t parts = std::max<int64_t>(2 * c->ncl, c->hv_mode == 0 ? c->hv_grid : 1);
+  A(&c->colpart, (size_t)parts * n);
+  A(&c->vpart, (size_t)std::max(c->grid, c->ncl) * 8 + 8);
+  A(&c->sendbuf, nv);
+  A(&c->bpart, 4 * (size_t)c->colgrid + 64);
+  for (double** p : {&c->g, &c->d, &c->rhs, &c->dir, &c->cg_r, &c->cg_p[0], &c->cg_p[1], &c->cg_ap, &c->cg_y,
+                     &c->gtrial, &c->yv, &c->ec, &c->Mloc, &c->Mglob, &c->Sloc})
+    A(p, nv);
+  if (st == OTB_OK) st = dalloc(&c->row_start, m_loc);
+  if (st == OTB_OK) st = dalloc(&c->rowpre, m_loc + 1);
+  if (st == OTB_OK) st = dalloc(&c->row_len, m_loc);
+  if (st == OTB_OK) st = dalloc(&c->ds, 1);
+  if (st == OTB_OK) st = dalloc(&c->cg, 1);
+  if (st != OTB_OK) {
+    otb_destroy(c);
+    return st;
+  }
+  c->chunk = std::max<int64_t>(8192, 2 * n);
+  const int64_t init_cap = std::max<int64_t>((int64_t)1 << 20, m_loc * n / 4) + (int64_t)c->ncl * c->chunk;
+  st = grow_csr(c, init_cap);
+  if (st != OTB_OK) {
+    otb_destroy(c);
+    return st;
+  }
+  if (cudaMallocHost((void**)&c->hs, sizeof(DevScalars)) != cudaSuccess ||
+      cudaMallocHost((void**)&c->hcg, sizeof(CgState)) != cudaSuccess ||
+      cudaMallocHost((void**)&c->hbuf, 16 * sizeof(double)) != cudaSuccess) {
+    otb_destroy(c);
+    return fail(OTB_ERR_NOMEM, "cudaMallocHost failed");
+  }
+  cudaMemset(c->ds, 0, sizeof(DevScalars));
+  cudaMemset(c->cg, 0, sizeof(CgState));
+  cudaMemset(c->cg_y, 0, sizeof(double) * nv);
+  cudaMemset(c->row_len, 0, sizeof(int) * m_loc);
+  cudaMemset(c->rowpre, 0, sizeof(int64_t) * (m_loc + 1));
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    otb_destroy(c);
+    return fail(OTB_ERR_CUDA, std::string("init: ") + cudaGetErrorString(e));
+  }
+  *out = c;
+  return OTB_OK;
+}
+
+int otb_destroy(otb_ctx* c) {
+  if (!c) return OTB_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (void* p : {(void*)c->rowM, (void*)c->rowS, (void*)c->lse, (void*)c->zrow, (void*)c->er, (void*)c->rowpart,
+                  (void*)c->colpart, (void*)c->vpart, (void*)c->sendbuf, (void*)c->bpart, (void*)c->g, (void*)c->d,
+                  (void*)c->rhs, (void*)c->dir, (void*)c->cg_r, (void*)c->cg_p[0], (void*)c->cg_p[1],
+                  (void*)c->cg_ap, (void*)c->cg_y, (void*)c->gtrial, (void*)c->yv, (void*)c->ec, (void*)c->Mloc,
+                  (void*)c->Mglob, (void*)c->Sloc, (void*)c->row_start, (void*)c->rowpre, (void*)c->row_len,
+                  (void*)c->cols, (void*)c->vals, (void*)c->ds, (void*)c->cg})
+    if (p) cudaFree(p);
+  if (c->hs) cudaFreeHost(c->hs);
+  if (c->hcg) cudaFreeHost(c->hcg);
+  if (c->hbuf) cudaFreeHost(c->hbuf);
+  for (auto& r : c->recs) {
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+  for (auto e : c->pool) cudaEventDestroy(e);
+  if (c->comm && c->nccl.commDestroy) c->nccl.commDestroy(c->comm);
+  delete c;
+  return OTB_OK;
+}
+
+int otb_set_stream(otb_ctx* c, void* stream) {
+  if (!c) return fail(OTB_ERR_ARG, "null context");
+  c->stream = (cudaStream_t)stream;
+  return OTB_OK;
+}
+
+int otb_nccl_get_unique_id(const char* nccl_path, void* id128) {
+  static Nccl api;
+  TRY(load_nccl(nccl_path, api));
+  NcclId id;
+  const int r = api.getUniqueId(&id);
+  if (r != 0) return fail(OTB_ERR_NCCL, "ncclGetUniqueId failed");
+  std::memcpy(id128, &id, sizeof id);
+  return OTB_OK;
+}
+
+int otb_attach_nccl(otb_ctx* c, const char* nccl_path, const void* id128, int nranks, int rank) {
+  if (!c) return fail(OTB_ERR_ARG, "null context");
+  if (nranks <= 1) {
+    c->nranks = 1;
+    c->rank = 0;
+    return OTB_OK;
+  }
+  TRY(load_nccl(nccl_path, c->nccl));
+  NcclId id;
+  std::memcpy(&id, id128, sizeof id);
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int r = c->nccl.commInitRank(&c->comm, nranks, id, rank);
+  if (r != 0) return fail(OTB_ERR_NCCL, "ncclCommInitRank failed");
+  c->nranks = nranks;
+  c->rank = rank;
+  return OTB_OK;
+}
+
+int otb_bind(otb_ctx* c, const double* C, const double* a, const double* b, const double* log_a,
+             const double* log_b, double eta, int64_t anchor_global, double norm_c, double norm_a, double norm_b) {
+  if (!c) return fail(OTB_ERR_ARG, "null context");
+  if (!C || !a || !b || !log_a || !log_b) return fail(OTB_ERR_ARG, "null problem array");
+  if (!(eta > 0.0)) return fail(OTB_ERR_ARG, "eta must be positive");
+  if (anchor_global < 0 || anchor_global >= c->m_glob) return fail(OTB_ERR_ARG, "anchor out of range");
+  if (((uintptr_t)C) % 256 != 0) return fail(OTB_ERR_ARG, "C must be 256-byte aligned");
+  c->C = C;
+  c->a = a;
+  c->b = b;
+  c->log_a = log_a;
+  c->log_b = log_b;
+  c->eta = eta;
+  c->anchor = anchor_global;
+  c->norm_c = norm_c;
+  c->norm_a = norm_a;
+  c->norm_b = norm_b;
+  c->bound = true;
+  c->have_eval = false;
+  return OTB_OK;
+}
+
+int otb_eval(otb_ctx* c, const double* logX, const double* gamma, double* lse_out, double* grad_out,
+             otb_eval_out* out) {
+  TRY(require_bound(c));
+  if (((uintptr_t)logX) % 256 != 0) return fail(OTB_ERR_ARG, "logX must be 256-byte aligned");
+  TRY(do_eval(c, logX, gamma));
+  if (lse_out)
+    CUDA_TRY(cudaMemcpyAsync(lse_out, c->lse, sizeof(double) * c->m_loc, cudaMemcpyDeviceToDevice, c->stream));
+  if (grad_out)
+    CUDA_TRY(cudaMemcpyAsync(grad_out, c->g, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, c->stream));
+  if (lse_out || grad_out) CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (out) {
+    out->value = c->last_value;
+    out->grad_norm = c->last_gnorm;
+  }
+  return OTB_OK;
+}
+
+int otb_sparsify(otb_ctx* c, const double* logX, const double* gamma, double rho, int64_t* nnz_out) {
+  TRY(require_bound(c));
+  if (!c->have_eval) return fail(OTB_ERR_ARG, "otb_sparsify needs a preceding otb_eval at the same gamma");
+  TRY(do_sparsify(c, logX, gamma, rho));
+  if (nnz_out) *nnz_out = c->nnz;
+  return OTB_OK;
+}
+
+int otb_csr_export(otb_ctx* c, int64_t* row_ptr, int32_t* cols, double* vals, double* d) {
+  TRY(require_bound(c));
+  if (row_ptr)
+    CUDA_TRY(cudaMemcpyAsync(row_ptr, c->rowpre, sizeof(int64_t) * (c->m_loc + 1), cudaMemcpyDeviceToDevice,
+                             c->stream));
+  if (cols && vals) {
+    k_csr_compact<<<c->num_sms * 4, 256, 0, c->stream>>>((int)c->m_loc, c->row_start, c->row_len, c->rowpre, c->cols,
+                                                         c->vals, cols, vals);
+    LAUNCH_CHECK();
+  }
+  if (d) CUDA_TRY(cudaMemcpyAsync(d, c->d, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return OTB_OK;
+}
+
+int otb_hess_apply(otb_ctx* c, const double* v, double shift, double* out) {
+  TRY(require_bound(c));
+  const int n = (int)c->n;
+  if (c->hv_mode == 1) CUDA_TRY(cudaMemsetAsync(c->cg_y, 0, sizeof(double) * n, c->stream));
+  HvResult hr;
+  TRY(run_hv(c, v, nullptr, nullptr, nullptr, 0, nullptr, &hr));
+  const double* cp = hr.ysum ? hr.ysum : hr.colpart;
+  const int np = hr.ysum ? 1 : hr.nparts;
+  k_hv_out<<<c->colgrid, 256, 0, c->stream>>>(n, cp, np, hr.yatomic, c->d, v, c->eta, shift, out);
+  LAUNCH_CHECK();
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return OTB_OK;
+}
+
+int otb_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t max_iters, double* x_out,
+           otb_cg_out* out) {
+  TRY(require_bound(c));
+  if (max_iters < 0) max_iters = 2 * c->n;
+  return do_cg(c, shift, rhs, rel_tol, max_iters, x_out, out);
+}
+
+int otb_newton_step(otb_ctx* c, const double* logX, const double* gamma_in, double* gamma_out,
+                    const otb_newton_params* p, otb_newton_out* out) {
+  TRY(require_bound(c));
+  if (!p) return fail(OTB_ERR_ARG, "null params");
+  if (!c->have_eval) return fail(OTB_ERR_ARG, "otb_newton_step needs a preceding otb_eval at gamma_in");
+  const int n = (int)c->n;
+  const double v0 = c->last_value, g0 = c->last_gnorm;
+  // inner_newton.py:112-114
+  const double rho = (p->rho_override >= 0.0) ? p->rho_override : c->eta * g0 / ((double)c->m_glob * (double)c->n);
+  TRY(do_sparsify(c, logX, gamma_in, rho));
+  const int64_t nnz = c->nnz;
+  // inner_newton.py:117: (H_rho + ||g|| I) d = -g
+  k_neg<<<c->colgrid, 256, 0, c->stream>>>(n, c->g, c->rhs);
+  LAUNCH_CHECK();
+  otb_cg_out cgo;
+  const int64_t maxit = (p->cg_max_iters > 0) ? p->cg_max_iters : 2 * c->n;
+  TRY(do_cg(c, g0, c->rhs, p->cg_rel_tol, maxit, c->dir, &cgo));
+  // inner_newton.py:118: slope = g . d
+  k_dot<<<c->colgrid, 256, 0, c->stream>>>(n, c->g, c->dir, c->ds, c->bpart, &c->ds->slope);
+  LAUNCH_CHECK();
+  TRY(sync_scalars(c));
+  const double slope = c->hs->slope;
+  // inner_newton.py:74-94: Armijo backtracking
+  double t = 1.0;
+  int64_t trials = 0;
+  bool ok = false;
+  for (int k = 0; k < 200; ++k) {
+    k_trial<<<c->colgrid, 256, 0, c->stream>>>(n, gamma_in, c->dir, t, c->gtrial);
+    LAUNCH_CHECK();
+    TRY(do_eval(c, logX, c->gtrial));
+    ++trials;
+    if (c->last_value <= v0 + p->sigma * t * slope) {
+      ok = true;
+      break;
+    }
+    t *= p->beta;
+  }
+  if (!ok) {
+    c->have_eval = false;
+    return fail(OTB_ERR_LINESEARCH, "no Armijo step accepted after 200 trials");
+  }
+  CUDA_TRY(cudaMemcpyAsync(gamma_out, c->gtrial, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (out) {
+    out->t = t;
+    out->slope = slope;
+    out->rho = rho;
+    out->value_before = v0;
+    out->value_after = c->last_value;
+    out->grad_norm_before = g0;
+    out->grad_norm_after = c->last_gnorm;
+    out->cg_iters = cgo.iters;
+    out->nnz = nnz;
+    out->trials = trials;
+    out->cg_residual = cgo.residual;
+  }
+  return OTB_OK;
+}
+
+int otb_recover_round(otb_ctx* c, const double* logX, const double* gamma, double* logX_out, int recover,
+                      int metrics, otb_test_out* out) {
+  TRY(require_bound(c));
+  if (recover && !c->have_eval) return fail(OTB_ERR_ARG, "recovery needs a preceding otb_eval at gamma");
+  if (recover && (!logX_out || ((uintptr_t)logX_out) % 256 != 0))
+    return fail(OTB_ERR_ARG, "logX_out must be a 256-byte aligned buffer");
+  return do_round(c, logX, gamma, logX_out, recover, metrics, out);
+}
+
+int otb_materialize_rounded(otb_ctx* c, double* out, int64_t ldo) {
+  TRY(require_bound(c));
+  if (!c->round_src) return fail(OTB_ERR_ARG, "no rounding performed yet");
+  k_materialize_rounded<<<c->num_sms * 8, 256, 0, c->stream>>>(c->round_src, c->ld, (int)c->m_loc, (int)c->n,
+                                                               c->zrow, c->yv, c->er, c->ec, &c->ds->deficit, out,
+                                                               ldo);
+  LAUNCH_CHECK();
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return OTB_OK;
+}
+
+int otb_warm_start(otb_ctx* c, const double* logX, double* gamma, double* zeta, double warm_tol, int64_t max_sweeps,
+                   otb_warm_out* out) {
+  TRY(require_bound(c));
+  const int n = (int)c->n;
+  const double mn = (double)c->m_loc * n;
+  int64_t sweeps = 0;
+  double err = INFINITY;
+  bool done = false;
+  for (int64_t s = 0; s < max_sweeps; ++s) {
+    {
+      Geom geo = make_geom(c, DK_WARMZ, c->C, logX);
+      WarmZIO io{gamma, c->log_a, c->eta, zeta, c->colpart};
+      cudaEvent_t e0 = nullptr;
+      TRY(prof_begin(c, &e0));
+      TRY(launch_dense(c, DK_WARMZ, geo, &io));
+      TRY(prof_end(c, PC_WARMZ, e0, 16.0 * mn));
+      TRY(colreduce(c, c->ncl, nullptr, 0, 0, 0));
+      TRY(allreduce(c, c->sendbuf, (size_t)n, kNcclSum));
+      k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_WARMERR, n, c->sendbuf, c->b, nullptr, c->ds, c->bpart,
+                                                    &c->ds->warm_err);
+      LAUNCH_CHECK();
+      TRY(sync_scalars(c));
+      err = std::sqrt(c->hs->warm_err);
+      sweeps = s + 1;
+      if (err < warm_tol) {
+        done = true;
+        break;
+      }
+    }
+    {
+      Geom geo = make_geom(c, DK_WARMG, c->C, logX);
+      WarmGIO io{zeta, c->eta, c->colpart};
+      cudaEvent_t e0 = nullptr;
+      TRY(prof_begin(c, &e0));
+      TRY(launch_dense(c, DK_WARMG, geo, &io));
+      TRY(prof_end(c, PC_WARMG, e0, 16.0 * mn));
+      if (c->nranks == 1) {
+        k_warm_gamma_combine<<<c->colgrid, 256, 0, c->stream>>>(1, n, c->colpart, c->ncl, nullptr, nullptr, c->log_b,
+                                                                c->eta, gamma);
+        LAUNCH_CHECK();
+      } else {
+        k_warm_gamma_combine<<<c->colgrid, 256, 0, c->stream>>>(0, n, c->colpart, c->ncl, c->Mloc, c->Sloc, c->log_b,
+                                                                c->eta, gamma);
+        LAUNCH_CHECK();
+        CUDA_TRY(cudaMemcpyAsync(c->Mglob, c->Mloc, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+        TRY(allreduce(c, c->Mglob, (size_t)n, kNcclMax));
+        k_warm_rescale<<<c->colgrid, 256, 0, c->stream>>>(n, c->Mloc, c->Mglob, c->Sloc);
+        LAUNCH_CHECK();
+        TRY(allreduce(c, c->Sloc, (size_t)n, kNcclSum));
+        k_warm_gamma_post<<<c->colgrid, 256, 0, c->stream>>>(n, c->Mglob, c->Sloc, c->log_b, c->eta, gamma);
+        LAUNCH_CHECK();
+      }
+    }
+  }
+  if (!done) {
+    char buf[96];
+    std::snprintf(buf, sizeof buf, "warm start did not reach %g in %lld sweeps", warm_tol, (long long)max_sweeps);
+    return fail(OTB_ERR_WARMSTART, buf);
+  }
+  // sinkhorn.py:102-103: recentre gamma onto the zero-sum slice
+  k_sum<<<c->colgrid, 256, 0, c->stream>>>(n, gamma, c->ds, c->bpart, &c->ds->drift);
+  LAUNCH_CHECK();
+  k_shift<<<c->colgrid, 256, 0, c->stream>>>(n, gamma, &c->ds->drift, (double)n, -1.0);
+  LAUNCH_CHECK();
+  k_shift<<<c->colgrid, 256, 0, c->stream>>>((int)c->m_loc, zeta, &c->ds->drift, (double)n, 1.0);
+  LAUNCH_CHECK();
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->have_eval = false;
+  if (out) {
+    out->sweeps = sweeps;
+    out->err = err;
+  }
+  return OTB_OK;
+}
+
+int otb_zeta_from_lse(otb_ctx* c, double* zeta) {
+  TRY(require_bound(c));
+  if (!c->have_eval) return fail(OTB_ERR_ARG, "no eval cached");
+  k_zeta_from_lse<<<c->colgrid, 256, 0, c->stream>>>((int)c->m_loc, c->log_a, c->row0, c->lse, c->eta, zeta);
+  LAUNCH_CHECK();
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return OTB_OK;
+}
+
+int otb_init_plan(otb_ctx* c, double* logX) {
+  TRY(require_bound(c));
+  k_init_plan<<<c->num_sms * 8, 256, 0, c->stream>>>(logX, c->ld, (int)c->m_loc, (int)c->n, c->log_a, c->row0,
+                                                     c->log_b);
+  LAUNCH_CHECK();
+  return OTB_OK;
+}
+
+int otb_materialize_p(otb_ctx* c, const double* logX, const double* gamma, double* P, int64_t ldp) {
+  TRY(require_bound(c));
+  if (!c->have_eval) return fail(OTB_ERR_ARG, "no eval cached");
+  k_materialize_p<<<c->num_sms * 8, 256, 0, c->stream>>>(c->C, logX, c->ld, (int)c->m_loc, (int)c->n, gamma, c->eta,
+                                                         c->rowM, c->rowS, P, ldp);
+  LAUNCH_CHECK();
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return OTB_OK;
+}
+
+int otb_info(otb_ctx* c, int64_t* o) {
+  if (!c || !o) return fail(OTB_ERR_ARG, "null");
+  const int64_t v[16] = {c->nt,  c->ns,     c->cl,   c->colw, c->nstage[DK_EVAL], c->ncl, c->grid, c->hv_mode,
+                         c->hv_grid, c->nnz, c->cap, c->m_loc, c->n, c->ld, c->nranks, c->rank};
+  std::memcpy(o, v, sizeof v);
+  return OTB_OK;
+}
+
+int otb_prof_enable(otb_ctx* c, int on) {
+  if (!c) return fail(OTB_ERR_ARG, "null context");
+  TRY(prof_collect(c));
+  c->prof = on != 0;
+  return OTB_OK;
+}
+
+int otb_prof_read(otb_ctx* c, double* ms16, int64_t* launches16, double* bytes16, int reset) {
+  if (!c) return fail(OTB_ERR_ARG, "null context");
+  TRY(prof_collect(c));
+  for (int k = 0; k < PC_N; ++k) {
+    if (ms16) ms16[k] = c->prof_ms[k];
+    if (launches16) launches16[k] = c->prof_cnt[k];
+    if (bytes16) bytes16[k] = c->prof_bytes[k];
+  }
+  if (reset) {
+    std::fill(c->prof_ms, c->prof_ms + PC_N, 0.0);
+    std::fill(c->prof_bytes, c->prof_bytes + PC_N, 0.0);
+    std::fill(c->prof_cnt, c->prof_cnt + PC_N, (int64_t)0);
+  }
+  return OTB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,278 @@
+// Row-streaming machinery shared by the dense passes over C and log X.
+//
+// Layout and mapping:
+//   * a matrix is m_loc rows x ld doubles in HBM (ld = round_up(n, 32), so
+//     every row starts 256-byte aligned);
+//   * a cluster of `cl` CTAs owns a contiguous block of rows; CTA rank q of
+//     the cluster owns the column window [q*colw, min((q+1)*colw, n));
+//   * a CTA = `nt` consumer threads + one producer warp.  The producer's
+//     elected lane streams the window of each row, one "slice" of 2*nt
+//     columns at a time, into an `nstage`-deep shared-memory ring with 1-D
+//     TMA bulk copies (cp.async.bulk ... complete_tx on an mbarrier);
+//   * consumer thread t owns columns c0 + s*2*nt + 2t + {0,1} of every row
+//     (slice s < NS), reads them from the ring as one 16-byte vector, and
+//     keeps the row in registers until the per-row reductions are done;
+//   * per-column accumulators live in shared memory at the thread's own
+//     slots (conflict-free, no atomics), and are written once per CTA as a
+//     partial row that a column-parallel "finish" kernel reduces in fixed
+//     order (deterministic);
+//   * per-row reductions (max / sum / min) are warp shuffles + one named
+//     barrier; when cl > 1 the per-CTA results are exchanged through DSMEM
+//     (remote st.shared::cluster + remote mbarrier arrive).
+#pragma once
+
+#include "common.cuh"
+
+namespace otb {
+
+constexpr int kMaxCluster = 8;
+constexpr int kMaxNS = 8;
+
+struct Geom {
+  const double* mat0;   // first streamed matrix (row-major, ld)
+  const double* mat1;   // second streamed matrix or nullptr
+  int64_t ld;           // leading dimension (doubles)
+  int m_loc;            // local rows
+  int n;                // columns
+  int64_t row0;         // global index of local row 0
+  int nt;               // consumer threads per CTA
+  int ns;               // slices per row per CTA (<= NS template)
+  int cl;               // cluster size
+  int colw;             // columns per CTA window (even)
+  int nstage;           // ring depth
+  int nacc;             // accumulator vectors in smem (0..2)
+};
+
+// Shared-memory carve-up; identical for every dense kernel.
+struct SmemMap {
+  double* ring;      // nstage * nmat * 2nt
+  double* acc;       // nacc * ns * 2nt
+  double* slots;     // 2 * 32 * 4
+  double* xbuf;      // 2 * 8 * 4
+  uint64_t* full;    // nstage
+  uint64_t* empty;   // nstage
+  uint64_t* xbar;    // 2
+  int* misc;         // 64 ints
+};
+
+OTB_DEV size_t smem_bytes_for(const Geom& g, int nmat) {
+  size_t slice = 2 * (size_t)g.nt;
+  size_t d = (size_t)g.nstage * nmat * slice + (size_t)g.nacc * g.ns * slice + 2 * 32 * 4 + 2 * 8 * 4;
+  return d * 8 + (2 * (size_t)g.nstage + 2) * 8 + 64 * 4;
+}
+
+OTB_DEV SmemMap carve(const Geom& g, int nmat, unsigned char* base) {
+  SmemMap s;
+  const size_t slice = 2 * (size_t)g.nt;
+  double* p = reinterpret_cast<double*>(base);
+  s.ring = p;
+  p += (size_t)g.nstage * nmat * slice;
+  s.acc = p;
+  p += (size_t)g.nacc * g.ns * slice;
+  s.slots = p;
+  p += 2 * 32 * 4;
+  s.xbuf = p;
+  p += 2 * 8 * 4;
+  uint64_t* b = reinterpret_cast<uint64_t*>(p);
+  s.full = b;
+  s.empty = b + g.nstage;
+  s.xbar = b + 2 * g.nstage;
+  s.misc = reinterpret_cast<int*>(b + 2 * g.nstage + 2);
+  return s;
+}
+
+// Per-CTA context of a dense pass.
+template <int NMAT>
+struct Dense {
+  Geom g;
+  SmemMap sm;
+  int tid, lane, warp;
+  bool producer;
+  int cr;        // rank in cluster
+  int cid;       // cluster index
+  int ncl;       // number of clusters
+  int r0, r1;    // local rows of this cluster
+  int c0, c1;    // column window of this CTA
+  int nsl;       // slices actually used by this CTA
+  int slice;     // 2*nt
+  // pipeline state
+  int stage;
+  uint32_t phase;
+  int rphase;    // block-reduce slot parity
+  int xcount;    // DSMEM exchanges done
+
+  OTB_DEV void setup(const Geom& geo, unsigned char* smem) {
+    g = geo;
+    sm = carve(g, NMAT, smem);
+    tid = threadIdx.x;
+    lane = tid & 31;
+    warp = tid >> 5;
+    producer = tid >= g.nt;
+    cr = (g.cl > 1) ? (int)cluster_ctarank() : 0;
+    cid = blockIdx.x / g.cl;
+    ncl = gridDim.x / g.cl;
+    r0 = (int)(((int64_t)cid * g.m_loc) / ncl);
+    r1 = (int)(((int64_t)(cid + 1) * g.m_loc) / ncl);
+    c0 = cr * g.colw;
+    c1 = min(c0 + g.colw, g.n);
+    slice = 2 * g.nt;
+    nsl = (c1 > c0) ? (c1 - c0 + slice - 1) / slice : 0;
+    stage = 0;
+    phase = 0;
+    rphase = 0;
+    xcount = 0;
+    if (tid == 0) {
+      for (int s = 0; s < g.nstage; ++s) {
+        mbar_init(&sm.full[s], 1);
+        mbar_init(&sm.empty[s], g.nt / 32);
+      }
+      mbar_init(&sm.xbar[0], g.cl);
+      mbar_init(&sm.xbar[1], g.cl);
+      fence_mbar_init();
+    }
+    // zero accumulators (consumer-owned slots only, but any thread may do it)
+    const int na = g.nacc * g.ns * slice;
+    for (int i = tid; i < na; i += blockDim.x) sm.acc[i] = 0.0;
+    if (g.cl > 1) {
+      __syncwarp();
+      cluster_sync_all();
+    } else {
+      __syncthreads();
+    }
+  }
+
+  OTB_DEV double* stage_buf(int st, int mat) const { return sm.ring + ((size_t)st * NMAT + mat) * slice; }
+
+  OTB_DEV void advance() {
+    if (++stage == g.nstage) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
+
+  // Producer: stream every (row, slice) of this CTA's window.
+  OTB_DEV void produce() {
+    if (lane != 0) return;
+    for (int r = r0; r < r1; ++r) {
+      for (int s = 0; s < nsl; ++s) {
+        mbar_wait(&sm.empty[stage], phase ^ 1u);
+        int cols = min(slice, c1 - c0 - s * slice);
+        cols = (cols + 1) & ~1;
+        const uint32_t bytes = (uint32_t)cols * 8u;
+        mbar_arrive_expect_tx(&sm.full[stage], bytes * NMAT);
+        const size_t off = (size_t)r * g.ld + c0 + (size_t)s * slice;
+        bulk_g2s(stage_buf(stage, 0), g.mat0 + off, bytes, &sm.full[stage]);
+        if (NMAT > 1) bulk_g2s(stage_buf(stage, 1), g.mat1 + off, bytes, &sm.full[stage]);
+        advance();
+      }
+    }
+  }
+
+  // Consumer: column index of element e (0/1) of slice s for this thread.
+  OTB_DEV int col(int s, int e) const { return c0 + s * slice + 2 * tid + e; }
+  OTB_DEV bool valid(int s, int e) const { return col(s, e) < c1; }
+
+  // Wait for slice s of the current row; returns the thread's two values of
+  // each matrix (garbage where !valid).
+  OTB_DEV void fetch(double2& v0, double2& v1) {
+    mbar_wait(&sm.full[stage], phase);
+    const double2* b0 = reinterpret_cast<const double2*>(stage_buf(stage, 0));
+    v0 = b0[tid];
+    if (NMAT > 1) {
+      const double2* b1 = reinterpret_cast<const double2*>(stage_buf(stage, 1));
+      v1 = b1[tid];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[stage]);
+    advance();
+  }
+
+  // Accumulator slots of this thread for slice s (double2 at acc[k]).
+  OTB_DEV double2* acc2(int k, int s) const {
+    return reinterpret_cast<double2*>(sm.acc + (size_t)k * g.ns * slice + (size_t)s * slice) + tid;
+  }
+
+  template <int K, int OP>
+  OTB_DEV void reduce(double (&v)[K]) {
+    block_reduce<K, OP>(v, sm.slots, rphase, g.nt);
+  }
+
+  // Exchange K (<=4) values among the cl CTAs of the cluster; out[q*4+k] is
+  // CTA q's value k.  No-op copy when cl == 1.  Consumer threads only.
+  template <int K>
+  OTB_DEV void exchange(const double (&v)[K], double* out) {
+    if (g.cl == 1) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) out[k] = v[k];
+      return;
+    }
+    const int q = xcount & 1;
+    const uint32_t par = (uint32_t)((xcount >> 1) & 1);
+    double* mine = sm.xbuf + (q * kMaxCluster + cr) * 4;
+    if (tid == 0) {
+      for (int rk = 0; rk < g.cl; ++rk) {
+        const uint32_t dst = mapa(smem_u32(mine), (uint32_t)rk);
+#pragma unroll
+        for (int k = 0; k < K; ++k) st_cluster_f64(dst + 8u * k, v[k]);
+        mbar_arrive_remote(mapa(smem_u32(&sm.xbar[q]), (uint32_t)rk));
+      }
+      while (!mbar_try_wait_cluster(&sm.xbar[q], par)) {
+      }
+    }
+    bar_sync(1, g.nt);
+    const double* src = sm.xbuf + q * kMaxCluster * 4;
+    for (int rk = 0; rk < g.cl; ++rk)
+#pragma unroll
+      for (int k = 0; k < K; ++k) out[rk * 4 + k] = src[rk * 4 + k];
+    ++xcount;
+  }
+
+  // Row-wide (cluster-wide) sum of a per-thread value.
+  OTB_DEV double row_sum(double v) {
+    double t[1] = {v};
+    reduce<1, kSum>(t);
+    if (g.cl == 1) return t[0];
+    double all[kMaxCluster * 4];
+    exchange<1>(t, all);
+    double s = 0.0;
+    for (int q = 0; q < g.cl; ++q) s += all[q * 4];
+    return s;
+  }
+  OTB_DEV double row_min(double v) {
+    double t[1] = {v};
+    reduce<1, kMin>(t);
+    if (g.cl == 1) return t[0];
+    double all[kMaxCluster * 4];
+    exchange<1>(t, all);
+    double s = all[0];
+    for (int q = 1; q < g.cl; ++q) s = fmin(s, all[q * 4]);
+    return s;
+  }
+
+  // Writes accumulator k to the partial row `dst` (global columns).
+  OTB_DEV void store_acc(int k, double* dst) const {
+    for (int s = 0; s < nsl; ++s) {
+      const double2 a = *acc2(k, s);
+      const int j = col(s, 0);
+      if (j < c1) dst[j] = a.x;
+      if (j + 1 < c1) dst[j + 1] = a.y;
+    }
+  }
+
+  OTB_DEV void finish() {
+    if (g.cl > 1) {
+      __syncwarp();
+      cluster_sync_all();
+    }
+  }
+};
+
+// Loads gamma-like column vectors as pairs (bounds-checked at n).
+OTB_DEV double2 load_pair(const double* v, int j, int lim) {
+  double2 r;
+  r.x = (j < lim) ? __ldg(v + j) : 0.0;
+  r.y = (j + 1 < lim) ? __ldg(v + j + 1) : 0.0;
+  return r;
+}
+
+}  // namespace otb

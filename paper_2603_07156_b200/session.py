@@ -1,0 +1,279 @@
+"""Device binding of one transport problem: padded HBM copies of C and the
+marginals plus the libotb context that owns the scratch (CSR, CG vectors,
+partial sums).
+
+A ``Session`` is created on first use and cached on the ``OtProblem``
+object, so the reference-style free functions (``compute_p(logplan, gamma,
+problem, eta)`` ...) do not re-upload C per call.  With a row range (see
+``distributed.py``) the session holds only rows [row_begin, row_end) of C
+and attaches an NCCL communicator for the length-n all-reduces.
+
+HBM layout: C and every log plan are stored as
+(m_loc, ld) float64 row-major with ld = round_up(n, 32), so every row is
+256-byte aligned for the 1-D TMA bulk copies of the dense passes.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .core import OtProblem, _is_torch, host
+from .errors import ShapeMismatch
+
+_SESSION_ATTR = "_otb_sessions"
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2603_07156_b200 needs a CUDA device (sm_100a); there is no CPU path")
+    return torch
+
+
+def round_up(x: int, k: int) -> int:
+    return (x + k - 1) // k * k
+
+
+class Session:
+    """libotb context bound to (problem, eta) on the current CUDA device."""
+
+    def __init__(self, problem: OtProblem, eta: float, row_begin: int = 0, row_end: int | None = None,
+                 comm=None, device=None):
+        torch = _torch()
+        self.torch = torch
+        m, n = problem.shape
+        self.m, self.n = m, n
+        self.row_begin = row_begin
+        self.row_end = m if row_end is None else row_end
+        self.m_loc = self.row_end - self.row_begin
+        self.ld = round_up(n, 32)
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.eta = None
+        dev = self.device
+        f64 = torch.float64
+
+        cost = problem.cost
+        a_h = host(problem.source_marginal)
+        b_h = host(problem.target_marginal)
+        if a_h.shape[0] != m or b_h.shape[0] != n:
+            raise ShapeMismatch("marginal lengths do not match the cost matrix")
+        # padded local rows of C
+        self.C = torch.zeros((self.m_loc, self.ld), dtype=f64, device=dev)
+        rows = slice(self.row_begin, self.row_end)
+        if _is_torch(cost):
+            self.C[:, :n].copy_(cost[rows])
+            self.norm_c = float(torch.linalg.norm(cost))
+        else:
+            self.C[:, :n].copy_(torch.from_numpy(np.ascontiguousarray(cost[rows])))
+            self.norm_c = float(np.linalg.norm(cost))
+        # marginals and their logs (numpy on the host: the reference's bits)
+        self.a_host, self.b_host = a_h, b_h
+        self.a = torch.from_numpy(np.ascontiguousarray(a_h)).to(dev)
+        self.b = self._vec(b_h)
+        self.log_a = torch.from_numpy(np.log(a_h)).to(dev)
+        self.log_b = self._vec(np.log(b_h))
+        self.norm_a = float(np.linalg.norm(a_h))
+        self.norm_b = float(np.linalg.norm(b_h))
+        self.default_anchor = int(np.argmax(a_h))             # sparsify.py:25-27
+        self.anchor = None
+        self.ctx = C.c_void_p()
+        with torch.cuda.device(dev):
+            _lib.check(_lib.lib.otb_create(C.byref(self.ctx), m, n, self.row_begin, self.row_end, self.ld,
+                                           dev.index, C.c_void_p(self._stream())))
+        if comm is not None:
+            comm.attach(self)
+        self.bind(eta)
+
+    # ------------------------------------------------------------------
+    def _stream(self) -> int:
+        return self.torch.cuda.current_stream(self.device).cuda_stream
+
+    def sync_stream(self):
+        _lib.check(_lib.lib.otb_set_stream(self.ctx, C.c_void_p(self._stream())))
+
+    def _vec(self, v, length=None):
+        """Device float64 vector padded to an even length (+16)."""
+        torch = self.torch
+        length = self.n if length is None else length
+        out = torch.zeros(round_up(length, 2) + 16, dtype=torch.float64, device=self.device)
+        if _is_torch(v):
+            out[:length].copy_(v.reshape(-1)[:length])
+        else:
+            out[:length].copy_(torch.from_numpy(np.ascontiguousarray(np.asarray(v, dtype=np.float64))))
+        return out
+
+    def new_vec(self, length=None):
+        length = self.n if length is None else length
+        return self.torch.zeros(round_up(length, 2) + 16, dtype=self.torch.float64, device=self.device)
+
+    def new_plan(self):
+        return self.torch.empty((self.m_loc, self.ld), dtype=self.torch.float64, device=self.device)
+
+    def bind(self, eta: float, anchor: int | None = None):
+        eta = float(eta)
+        anchor = self.default_anchor if anchor is None else int(anchor)
+        if eta == self.eta and anchor == self.anchor:
+            return
+        _lib.check(_lib.lib.otb_bind(self.ctx, self.C.data_ptr(), self.a.data_ptr(), self.b.data_ptr(),
+                                     self.log_a.data_ptr(), self.log_b.data_ptr(), eta, anchor,
+                                     self.norm_c, self.norm_a, self.norm_b))
+        self.eta = eta
+        self.anchor = anchor
+
+    @property
+    def ops(self) -> "Ops":
+        return Ops(self)
+
+    def plan(self, logplan):
+        """Padded device tensor of the local rows of a LogPlan."""
+        t = logplan.device_padded(self.ld, self.device) if logplan.shape[0] == self.m_loc else None
+        if t is None:
+            raise ShapeMismatch("log plan rows do not match the session's row range")
+        return t
+
+    def info(self) -> dict:
+        out = (C.c_int64 * 16)()
+        _lib.check(_lib.lib.otb_info(self.ctx, out))
+        keys = ("nt", "ns", "cl", "colw", "nstage", "ncl", "grid", "hv_mode", "hv_grid", "nnz", "capacity",
+                "m_loc", "n", "ld", "nranks", "rank")
+        return dict(zip(keys, list(out)))
+
+    # ------------------------------------------------------------ profiling
+    def prof_enable(self, on: bool = True):
+        _lib.check(_lib.lib.otb_prof_enable(self.ctx, 1 if on else 0))
+
+    def prof_read(self, reset: bool = True) -> dict:
+        ms = (C.c_double * 16)()
+        cnt = (C.c_int64 * 16)()
+        by = (C.c_double * 16)()
+        _lib.check(_lib.lib.otb_prof_read(self.ctx, ms, cnt, by, 1 if reset else 0))
+        names = ("eval", "sparsify", "hess_apply", "cg_vector", "test_a", "test_b", "test_c",
+                 "warm_zeta", "warm_gamma")
+        return {nm: dict(ms=ms[k], launches=cnt[k], bytes=by[k]) for k, nm in enumerate(names)}
+
+    def close(self):
+        if self.ctx:
+            _lib.lib.otb_destroy(self.ctx)
+            self.ctx = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order varies
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def session_for(problem: OtProblem, eta: float, comm=None) -> Session:
+    """Cached Session of (problem, current device); rebinds eta if needed."""
+    torch = _torch()
+    cache = getattr(problem, _SESSION_ATTR, None)
+    if cache is None:
+        cache = {}
+        object.__setattr__(problem, _SESSION_ATTR, cache)
+    key = (torch.cuda.current_device(), None if comm is None else id(comm))
+    s = cache.get(key)
+    if s is None:
+        if comm is None:
+            s = Session(problem, eta)
+        else:
+            r0, r1 = comm.row_range(problem.shape[0])
+            s = Session(problem, eta, r0, r1, comm=comm)
+        cache[key] = s
+    s.bind(eta)
+    s.sync_stream()
+    return s
+
+
+# ---------------------------------------------------------------------------
+# thin wrappers over the C ABI (device tensors in, scalars out)
+# ---------------------------------------------------------------------------
+
+def _ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+class Ops:
+    """Entry points of libotb on a Session; every call is stream-ordered on
+    torch's current stream and returns host scalars only."""
+
+    def __init__(self, s: Session):
+        self.s = s
+
+    def eval(self, plan_t, gamma_t, lse_out=None, grad_out=None):
+        out = _lib.EvalOut()
+        _lib.check(_lib.lib.otb_eval(self.s.ctx, plan_t.data_ptr(), gamma_t.data_ptr(), _ptr(lse_out),
+                                     _ptr(grad_out), C.byref(out)))
+        return out.value, out.grad_norm
+
+    def sparsify(self, plan_t, gamma_t, rho: float) -> int:
+        nnz = C.c_int64()
+        _lib.check(_lib.lib.otb_sparsify(self.s.ctx, plan_t.data_ptr(), gamma_t.data_ptr(), float(rho),
+                                         C.byref(nnz)))
+        return int(nnz.value)
+
+    def csr_export(self, nnz: int):
+        torch = self.s.torch
+        dev = self.s.device
+        row_ptr = torch.empty(self.s.m_loc + 1, dtype=torch.int64, device=dev)
+        cols = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+        vals = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+        d = self.s.new_vec()
+        _lib.check(_lib.lib.otb_csr_export(self.s.ctx, row_ptr.data_ptr(), cols.data_ptr(), vals.data_ptr(),
+                                           d.data_ptr()))
+        return row_ptr, cols[:nnz], vals[:nnz], d[: self.s.n]
+
+    def hess_apply(self, v_t, shift: float = 0.0, out=None):
+        out = self.s.new_vec() if out is None else out
+        _lib.check(_lib.lib.otb_hess_apply(self.s.ctx, v_t.data_ptr(), float(shift), out.data_ptr()))
+        return out
+
+    def cg(self, shift, rhs_t, rel_tol, max_iters, x_out=None):
+        x_out = self.s.new_vec() if x_out is None else x_out
+        out = _lib.CgOut()
+        _lib.check(_lib.lib.otb_cg(self.s.ctx, float(shift), rhs_t.data_ptr(), float(rel_tol), int(max_iters),
+                                   x_out.data_ptr(), C.byref(out)))
+        return x_out, int(out.iters), float(out.residual)
+
+    def newton_step(self, plan_t, gamma_in, gamma_out, sigma, beta, cg_rel_tol, cg_max_iters, rho=None):
+        p = _lib.NewtonParams(float(sigma), float(beta), float(cg_rel_tol),
+                              0 if cg_max_iters is None else int(cg_max_iters),
+                              -1.0 if rho is None else float(rho))
+        out = _lib.NewtonOut()
+        _lib.check(_lib.lib.otb_newton_step(self.s.ctx, plan_t.data_ptr(), gamma_in.data_ptr(),
+                                            gamma_out.data_ptr(), C.byref(p), C.byref(out)))
+        return out
+
+    def recover_round(self, plan_t, gamma_t, out_plan=None, recover=True, metrics=True):
+        res = _lib.TestOut()
+        _lib.check(_lib.lib.otb_recover_round(self.s.ctx, plan_t.data_ptr(), gamma_t.data_ptr(), _ptr(out_plan),
+                                              1 if recover else 0, 1 if metrics else 0, C.byref(res)))
+        return res
+
+    def materialize_rounded(self):
+        out = self.s.torch.empty((self.s.m_loc, self.s.n), dtype=self.s.torch.float64, device=self.s.device)
+        _lib.check(_lib.lib.otb_materialize_rounded(self.s.ctx, out.data_ptr(), self.s.n))
+        return out
+
+    def materialize_p(self, plan_t, gamma_t):
+        out = self.s.torch.empty((self.s.m_loc, self.s.n), dtype=self.s.torch.float64, device=self.s.device)
+        _lib.check(_lib.lib.otb_materialize_p(self.s.ctx, plan_t.data_ptr(), gamma_t.data_ptr(), out.data_ptr(),
+                                              self.s.n))
+        return out
+
+    def warm_start(self, plan_t, gamma_t, zeta_t, warm_tol, max_sweeps):
+        out = _lib.WarmOut()
+        _lib.check(_lib.lib.otb_warm_start(self.s.ctx, plan_t.data_ptr(), gamma_t.data_ptr(), zeta_t.data_ptr(),
+                                           float(warm_tol), int(max_sweeps), C.byref(out)))
+        return int(out.sweeps), float(out.err)
+
+    def init_plan(self, plan_t):
+        _lib.check(_lib.lib.otb_init_plan(self.s.ctx, plan_t.data_ptr()))
+        return plan_t
+
+    def zeta_from_lse(self, zeta_t):
+        _lib.check(_lib.lib.otb_zeta_from_lse(self.s.ctx, zeta_t.data_ptr()))
+        return zeta_t
