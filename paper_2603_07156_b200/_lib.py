@@ -75,6 +75,7 @@ SIGNATURES = {
     "otb_init_plan": (C.c_int, [vp, vp]),
     "otb_materialize_p": (C.c_int, [vp, vp, vp, vp, i64]),
     "otb_info": (C.c_int, [vp, C.POINTER(i64)]),
+    "otb_launch_count": (C.c_int, [vp, C.POINTER(i64)]),
     "otb_prof_enable": (C.c_int, [vp, C.c_int]),
     "otb_prof_read": (C.c_int, [vp, C.POINTER(dbl), C.POINTER(i64), C.POINTER(dbl), C.c_int]),
 }

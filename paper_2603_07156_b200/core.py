@@ -117,11 +117,16 @@ class LogPlan:
 
     def __init__(self, log_entries):
         arr = _as_float_array(log_entries, 2)
-        if _is_torch(arr):
+        if _is_torch(arr) and not arr.is_cuda:
+            # host tensor (e.g. pinned): validated and clamped on the device
+            # right after its upload (device_padded), raising the same error
+            self._host = None
+            self._dev = ("host", arr)
+            self._shape = tuple(arr.shape)
+        elif _is_torch(arr):
             import torch
 
-            if bool(torch.isnan(arr).any()) or bool((arr == float("inf")).any()):
-                raise InvalidCost("log plan contains NaN or +inf entries")
+            _check_plan_tensor(arr)
             self._host = None
             self._dev = ("dense", torch.clamp_min(arr, LOG_FLOOR))
             self._shape = tuple(arr.shape)
@@ -150,6 +155,12 @@ class LogPlan:
     def log_entries(self) -> np.ndarray:
         if self._host is None:
             kind, t = self._dev
+            if kind == "host":
+                arr = t.numpy()
+                if np.isnan(arr).any() or (arr == np.inf).any():
+                    raise InvalidCost("log plan contains NaN or +inf entries")
+                self._host = np.maximum(arr, LOG_FLOOR)
+                return self._host
             t = t[:, : self._shape[1]] if kind == "padded" else t
             self._host = t.detach().cpu().numpy()
         return self._host
@@ -158,16 +169,23 @@ class LogPlan:
         """(m, ld) float64 CUDA tensor with the plan in columns [0, n)."""
         import torch
 
+        check = False
         if self._dev is not None:
             kind, t = self._dev
             if kind == "padded" and t.shape[1] == ld and t.device == device:
                 return t
             src = t[:, : self._shape[1]] if kind == "padded" else t
+            check = kind == "host"
         else:
             src = torch.from_numpy(self._host)
         m, n = self._shape
-        out = torch.zeros((m, ld), dtype=torch.float64, device=device)
-        out[:, :n].copy_(src, non_blocking=False)
+        out = torch.empty((m, ld), dtype=torch.float64, device=device)
+        out[:, :n].copy_(src, non_blocking=True)
+        if ld > n:
+            out[:, n:].zero_()
+        if check:
+            _check_plan_tensor(out[:, :n])
+            torch.clamp_min_(out[:, :n], LOG_FLOOR)
         self._dev = ("padded", out)
         return out
 
@@ -177,6 +195,14 @@ class LogPlan:
 
     def total_mass(self) -> float:
         return float(self.dense().sum())
+
+
+def _check_plan_tensor(t) -> None:
+    """core.py:143-144 on a tensor: NaN or +inf -> InvalidCost."""
+    import torch
+
+    if bool(torch.isnan(t).any()) or bool(torch.isposinf(t).any()):
+        raise InvalidCost("log plan contains NaN or +inf entries")
 
 
 def normalize_cost(raw_cost) -> np.ndarray:

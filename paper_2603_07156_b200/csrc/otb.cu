@@ -41,7 +41,11 @@ int fail(int code, const std::string& msg) {
     if (s_ != OTB_OK) return s_;   \
   } while (0)
 
-#define LAUNCH_CHECK() CUDA_TRY(cudaGetLastError())
+#define LAUNCH_CHECK()            \
+  do {                            \
+    ++c->launches;                \
+    CUDA_TRY(cudaGetLastError()); \
+  } while (0)
 
 // ------------------------------------------------------------------ NCCL
 struct NcclId {
@@ -143,6 +147,7 @@ struct otb_ctx {
   Nccl nccl;
   NcclComm comm = nullptr;
   int nranks = 1, rank = 0;
+  int64_t launches = 0;       // kernels launched by this context
   // profiling
   bool prof = false;
   struct Rec {
@@ -257,6 +262,7 @@ int launch_dense(otb_ctx* c, int kind, Geom geo, void* io) {
   cfg.numAttrs = 1;
   void* args[2] = {&geo, io};
   CUDA_TRY(cudaLaunchKernelExC(&cfg, fn, args));
+  ++c->launches;
   return OTB_OK;
 }
 
@@ -1032,6 +1038,12 @@ int otb_info(otb_ctx* c, int64_t* o) {
   const int64_t v[16] = {c->nt,  c->ns,     c->cl,   c->colw, c->nstage[DK_EVAL], c->ncl, c->grid, c->hv_mode,
                          c->hv_grid, c->nnz, c->cap, c->m_loc, c->n, c->ld, c->nranks, c->rank};
   std::memcpy(o, v, sizeof v);
+  return OTB_OK;
+}
+
+int otb_launch_count(otb_ctx* c, int64_t* out) {
+  if (!c || !out) return fail(OTB_ERR_ARG, "null");
+  *out = c->launches;
   return OTB_OK;
 }
 

@@ -85,7 +85,7 @@ def newton_step(logplan: LogPlan, gamma: DualState, problem: OtProblem, eta: flo
 
 
 def _is_device(x) -> bool:
-    return type(x).__module__.startswith("torch")
+    return type(x).__module__.startswith("torch") and x.is_cuda
 
 
 def plan_candidate_log(logplan: LogPlan, cache, gamma: DualState, problem: OtProblem, eta: float) -> LogPlan:

@@ -65,8 +65,13 @@ class Session:
         self.C = torch.zeros((self.m_loc, self.ld), dtype=f64, device=dev)
         rows = slice(self.row_begin, self.row_end)
         if _is_torch(cost):
-            self.C[:, :n].copy_(cost[rows])
-            self.norm_c = float(torch.linalg.norm(cost))
+            self.C[:, :n].copy_(cost[rows], non_blocking=True)
+            sq = torch.sum(self.C * self.C).reshape(1)        # ||C||_F^2 of the local rows
+            if comm is not None and comm.world > 1:
+                import torch.distributed as dist
+
+                dist.all_reduce(sq)
+            self.norm_c = float(torch.sqrt(sq))
         else:
             self.C[:, :n].copy_(torch.from_numpy(np.ascontiguousarray(cost[rows])))
             self.norm_c = float(np.linalg.norm(cost))
@@ -141,6 +146,11 @@ class Session:
         keys = ("nt", "ns", "cl", "colw", "nstage", "ncl", "grid", "hv_mode", "hv_grid", "nnz", "capacity",
                 "m_loc", "n", "ld", "nranks", "rank")
         return dict(zip(keys, list(out)))
+
+    def launches(self) -> int:
+        out = C.c_int64()
+        _lib.check(_lib.lib.otb_launch_count(self.ctx, C.byref(out)))
+        return int(out.value)
 
     # ------------------------------------------------------------ profiling
     def prof_enable(self, on: bool = True):

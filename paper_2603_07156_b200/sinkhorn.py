@@ -40,7 +40,7 @@ def warm_start(logplan: LogPlan, problem: OtProblem, eta: float, warm_tol: float
     s._last_warm = (sweeps, err)
     if session is not None:
         return DualState(gamma_buf, generation=generation), zeta_buf
-    device_in = gamma0 is not None and type(gamma0).__module__.startswith("torch")
+    device_in = gamma0 is not None and type(gamma0).__module__.startswith("torch") and gamma0.is_cuda
     if device_in:
         return DualState(gamma_buf[:n], generation=generation), zeta_buf[: s.m_loc]
     return DualState(gamma_buf[:n].cpu().numpy(), generation=generation), zeta_buf[: s.m_loc].cpu().numpy()
