@@ -162,7 +162,7 @@ class LogPlan:
                 self._host = np.maximum(arr, LOG_FLOOR)
                 return self._host
             t = t[:, : self._shape[1]] if kind == "padded" else t
-            self._host = t.detach().cpu().numpy()
+            self._host = _to_host(t)
         return self._host
 
     def device_padded(self, ld: int, device):
@@ -201,8 +201,19 @@ def _check_plan_tensor(t) -> None:
     """core.py:143-144 on a tensor: NaN or +inf -> InvalidCost."""
     import torch
 
-    if bool(torch.isnan(t).any()) or bool(torch.isposinf(t).any()):
+    if bool(torch.logical_or(t != t, t == float("inf")).any()):
         raise InvalidCost("log plan contains NaN or +inf entries")
+
+
+def _to_host(t) -> np.ndarray:
+    """Device -> host copy through (cached) pinned memory."""
+    import torch
+
+    if not t.is_cuda:
+        return t.detach().numpy()
+    out = torch.empty(tuple(t.shape), dtype=t.dtype, pin_memory=True)
+    out.copy_(t)
+    return out.numpy()
 
 
 def normalize_cost(raw_cost) -> np.ndarray:

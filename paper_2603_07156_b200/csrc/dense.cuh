@@ -255,9 +255,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
     // chunk (state replicated in all of its consumer threads) and shares
     // the start with the other ranks of the cluster.
     unsigned long long start = 0;
+    const int cnt_al = (cnt + 7) & ~7;   // runs start on 8-entry boundaries (vector loads in hess_apply)
     if (D.cr == 0) {
-      if (cur + (unsigned long long)cnt > end) {
-        const unsigned long long want = (unsigned long long)max((int64_t)cnt, io.chunk);
+      if (cur + (unsigned long long)cnt_al > end) {
+        const unsigned long long want = (unsigned long long)max((int64_t)cnt_al, io.chunk);
         if (D.tid == 0) chunk_base = atomicAdd(io.alloc, want);
         bar_sync(1, D.g.nt);
         cur = chunk_base;
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
         bar_sync(1, D.g.nt);   // chunk_base may be rewritten next time
       }
       start = cur;
-      cur += (unsigned long long)cnt;
+      cur += (unsigned long long)cnt_al;
     }
     if (D.g.cl > 1) {
       double v1[1] = {(double)start};
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
       D.exchange<1>(v1, all);
       start = (unsigned long long)all[0];
     }
-    const bool ovf = (int64_t)(start + cnt) > io.cap;
+    const bool ovf = (int64_t)(start + cnt_al) > io.cap;
     if (ovf && D.tid == 0 && D.cr == 0) atomicOr(io.flags, 2);
     const double ai = __ldg(io.a + D.g.row0 + r);
     const unsigned long long wbase = start + myoff;

@@ -30,14 +30,14 @@ enum CounterIdx {
 };
 
 // out[j] = sum_c part[c*n + j]; out[n + k] = sum_c spart[c*sstride + k].
+// One block = 32 columns; the 8 warps split the partial rows (fixed order).
 __global__ void __launch_bounds__(256) k_colreduce(const double* part, int nparts, int n, double* out,
                                                    const double* spart, int nspart, int sstride, int nscal,
                                                    unsigned int* counter) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < nparts; ++c) s += part[(size_t)c * n + j];
-    out[j] = s;
-  }
+  __shared__ double red[8 * 32];
+  const double s = reduce_partials32(part, nparts, n, blockIdx.x * 32, red);
+  const int j = blockIdx.x * 32 + threadIdx.x;
+  if (threadIdx.x < 32 && j < n) out[j] = s;
   if (nscal > 0) {
     if (last_block(counter)) {
       if (threadIdx.x < 32) {
@@ -210,22 +210,44 @@ __global__ void __launch_bounds__(256) k_rows_post(int mode, int m_loc, int cl, 
 // Warm-start gamma finish (sinkhorn.py:36-39, 54-58): combine the per-cluster
 // (max, sum) pairs of each column.  mode 0: write M and S (multi-rank phase
 // 1); mode 1: write gamma_j = eta (log b_j - (M + log S)) directly.
+// One block = 32 columns; warp w folds partials w, w+8, ... with the online
+// (max, sum) rule, then warp 0 folds the 8 warp results in order.
 __global__ void __launch_bounds__(256) k_warm_gamma_combine(int mode, int n, const double* part, int nparts,
                                                             double* outM, double* outS, const double* log_b,
                                                             double eta, double* gamma) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    double M = -INFINITY;
-    for (int c = 0; c < nparts; ++c) M = fmax(M, part[((size_t)c * 2) * n + j]);
-    double S = 0.0;
-    for (int c = 0; c < nparts; ++c) {
+  __shared__ double rm[8 * 32], rs[8 * 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int j = blockIdx.x * 32 + lane;
+  double M = -INFINITY, S = 0.0;
+  if (j < n) {
+    for (int c = warp; c < nparts; c += nw) {
       const double mc = part[((size_t)c * 2) * n + j];
-      if (mc != -INFINITY) S += part[((size_t)c * 2 + 1) * n + j] * exp(mc - M);
+      if (mc == -INFINITY) continue;
+      const double sc = part[((size_t)c * 2 + 1) * n + j];
+      if (mc > M) {
+        S = S * exp(M - mc) + sc;
+        M = mc;
+      } else {
+        S += sc * exp(mc - M);
+      }
+    }
+  }
+  rm[warp * 32 + lane] = M;
+  rs[warp * 32 + lane] = S;
+  __syncthreads();
+  if (warp == 0 && j < n) {
+    double Mg = -INFINITY;
+    for (int w = 0; w < nw; ++w) Mg = fmax(Mg, rm[w * 32 + lane]);
+    double Sg = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      const double mw = rm[w * 32 + lane];
+      if (mw != -INFINITY) Sg += rs[w * 32 + lane] * exp(mw - Mg);
     }
     if (mode == 0) {
-      outM[j] = M;
-      outS[j] = S;
+      outM[j] = Mg;
+      outS[j] = Sg;
     } else {
-      gamma[j] = eta * (log_b[j] - (M + log(S)));
+      gamma[j] = eta * (log_b[j] - (Mg + log(Sg)));
     }
   }
 }

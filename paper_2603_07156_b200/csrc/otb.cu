@@ -98,7 +98,9 @@ const void* const kDenseFn[DK_COUNT][kMaxNS + 1] = {
      (const void*)k_test_c<7, true>, (const void*)k_test_c<8, true>},
     NS_ROW(k_warm_zeta), NS_ROW(k_warm_gamma)};
 
-enum ProfClass { PC_EVAL = 0, PC_SPARSIFY, PC_HV, PC_CGVEC, PC_TESTA, PC_TESTB, PC_TESTC, PC_WARMZ, PC_WARMG, PC_N = 16 };
+enum ProfClass {
+  PC_EVAL = 0, PC_SPARSIFY, PC_HV, PC_CGVEC, PC_TESTA, PC_TESTB, PC_TESTC, PC_WARMZ, PC_WARMG, PC_CGFUSED, PC_N = 16
+};
 
 constexpr int kCgBatch = 16;
 constexpr size_t kMaxDynSmem = 232448;  // 227 KB
@@ -115,9 +117,11 @@ struct otb_ctx {
   int nstage[DK_COUNT] = {};
   size_t smem[DK_COUNT] = {};
   // hess_apply
-  int hv_mode = 0, hv_grid = 0;
+  int hv_mode = 0, hv_grid = 0, hv_ng = 1;
   size_t hv_smem = 0;
-  int colgrid = 0;
+  bool cg_fused = false;     // persistent cooperative CG available (1 rank, smem hv)
+  int colgrid = 0, col32 = 0;
+  double* scal = nullptr;    // [hv_grid][2] per-CTA scalars of the fused CG
   // problem
   const double *C = nullptr, *a = nullptr, *b = nullptr, *log_a = nullptr, *log_b = nullptr;
   double eta = 0.0, norm_c = 0.0, norm_a = 0.0, norm_b = 0.0;
@@ -176,6 +180,20 @@ int dalloc(T** p, size_t count) {
                                    cudaGetErrorString(e));
   }
   return OTB_OK;
+}
+
+// The dynamic shared-memory limit is a per-FUNCTION (process-wide)
+// attribute: raise it once to the device maximum instead of to this
+// context's need, so contexts of different shapes never lower it for each
+// other.
+cudaError_t allow_max_smem(const void* fn, int device) {
+  int optin = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
 }
 
 size_t dense_smem(const otb_ctx* c, int kind, int nstage) {
@@ -281,7 +299,7 @@ int sync_scalars(otb_ctx* c) {
 }
 
 int colreduce(otb_ctx* c, int nparts, const double* spart, int nspart, int sstride, int nscal) {
-  k_colreduce<<<c->colgrid, 256, 0, c->stream>>>(c->colpart, nparts, (int)c->n, c->sendbuf, spart, nspart, sstride,
+  k_colreduce<<<c->col32, 256, 0, c->stream>>>(c->colpart, nparts, (int)c->n, c->sendbuf, spart, nspart, sstride,
                                                  nscal, &c->ds->cnt[CNT_COLRED]);
   LAUNCH_CHECK();
   return OTB_OK;
@@ -321,7 +339,7 @@ int do_eval(otb_ctx* c, const double* X, const double* gamma) {
 int grow_csr(otb_ctx* c, int64_t want) {
   if (want <= c->cap) return OTB_OK;
   int64_t ncap = std::max<int64_t>(want, (int64_t)(c->cap * 1.5));
-  ncap = std::min<int64_t>(ncap, c->m_loc * c->n + (int64_t)c->ncl * c->chunk + c->n);
+  ncap = std::min<int64_t>(ncap, c->m_loc * rup(c->n, kCsrAlign) + (int64_t)c->ncl * c->chunk + c->n);
   if (c->cols) cudaFree(c->cols);
   if (c->vals) cudaFree(c->vals);
   c->cols = nullptr;
@@ -396,9 +414,9 @@ int run_hv(otb_ctx* c, const double* v_src, const double* r, const double* p_pre
   const int n = (int)c->n;
   cudaEvent_t e0 = nullptr;
   if (c->hv_mode == 0) {
-    HvArgs h{csr_view(c), c->a, n, v_src, r, p_prev, p_cur, update, st, c->colpart};
+    HvArgs h{csr_view(c), c->a, n, c->hv_ng, v_src, r, p_prev, p_cur, update, st, c->colpart};
     TRY(prof_begin(c, &e0));
-    k_hv_smem<<<c->hv_grid, 512, c->hv_smem, c->stream>>>(h);
+    k_hv_grp<<<c->hv_grid, 512, c->hv_smem, c->stream>>>(h);
     LAUNCH_CHECK();
     TRY(prof_end(c, PC_HV, e0, hv_bytes(c)));
     if (c->nranks > 1) {
@@ -441,7 +459,7 @@ int cg_iteration(otb_ctx* c, int64_t k, double* x) {
   cudaEvent_t e0 = nullptr;
   TRY(prof_begin(c, &e0));
   CgApArgs a{n, hr.colpart, hr.nparts, hr.yatomic, hr.ysum, c->d, pc, c->eta, c->cg_ap, c->cg, c->bpart};
-  k_cg_ap<<<c->colgrid, 256, 0, c->stream>>>(a);
+  k_cg_ap<<<c->col32, 256, 0, c->stream>>>(a);
   LAUNCH_CHECK();
   k_cg_update<<<c->colgrid, 256, 0, c->stream>>>(n, x, c->cg_r, pc, c->cg_ap, c->cg, c->bpart);
   LAUNCH_CHECK();
@@ -458,6 +476,22 @@ int do_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t m
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   if (c->hcg->status == CG_INCONSISTENT)
     return fail(OTB_ERR_INCONSISTENT, "unshifted system with right-hand side outside the range");
+  if (c->cg_fused && c->hcg->status == CG_RUN) {
+    // whole CG loop in one cooperative launch (k_cg_fused)
+    CgFusedArgs fa{csr_view(c), c->a, c->d, n, c->hv_ng, c->eta, x, c->cg_r, c->cg_p[0], c->cg_p[1], c->cg_ap,
+                   c->colpart, c->scal, c->cg};
+    void* args[1] = {&fa};
+    cudaEvent_t e0 = nullptr;
+    TRY(prof_begin(c, &e0));
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_cg_fused, dim3(c->hv_grid), dim3(512), args, c->hv_smem,
+                                         c->stream));
+    ++c->launches;
+    TRY(prof_end(c, PC_CGFUSED, e0, 0.0));
+    CUDA_TRY(cudaMemcpyAsync(c->hcg, c->cg, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (c->prof && !c->recs.empty())
+      c->recs.back().bytes = (double)c->hcg->iters * (hv_bytes(c) + 72.0 * n);
+  }
   int64_t k = 0;
   while (c->hcg->status == CG_RUN) {
     for (int j = 0; j < kCgBatch; ++j, ++k) TRY(cg_iteration(c, k, x));
@@ -629,31 +663,42 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
       delete c;
       return fail(OTB_ERR_ARG, "dense geometry does not fit shared memory");
     }
-    const void* fn = kDenseFn[k][c->ns];
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem[k]);
+    cudaError_t e = allow_max_smem(kDenseFn[k][c->ns], device);
     if (e != cudaSuccess) {
       delete c;
       return fail(OTB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     }
   }
-  // hess_apply variant
+  // hess_apply variant: shared-memory group accumulators (NG groups of
+  // 512/NG threads, as many as fit) or, for very wide n, global RED.
   const int64_t npad = rup(n, 2);
-  c->hv_smem = (size_t)(2 * npad + 2 * 32 * 4) * 8;
+  const size_t hv_budget = kMaxDynSmem - 8192;   // static smem of k_cg_fused
+  int ng = 8;
+  const char* env_ng = std::getenv("OTB_HV_GROUPS");
+  if (env_ng) ng = std::max(1, std::min(16, std::atoi(env_ng)));
+  while (ng > 1 && (size_t)((1 + ng) * npad + 16 * 64) * 8 > hv_budget) ng >>= 1;
+  c->hv_ng = ng;
+  c->hv_smem = (size_t)((1 + ng) * npad + 16 * 64) * 8;
   const char* env_hv = std::getenv("OTB_HV_MODE");
-  c->hv_mode = (c->hv_smem <= kMaxDynSmem - 1024) ? 0 : 1;
+  c->hv_mode = (c->hv_smem <= hv_budget) ? 0 : 1;
   if (env_hv && std::atoi(env_hv) == 1) c->hv_mode = 1;
   if (c->hv_mode == 0) {
     c->hv_grid = sms;
-    cudaError_t e = cudaFuncSetAttribute((const void*)k_hv_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)c->hv_smem);
+    cudaError_t e = allow_max_smem((const void*)k_hv_grp, device);
+    if (e == cudaSuccess) e = allow_max_smem((const void*)k_cg_fused, device);
     if (e != cudaSuccess) {
       delete c;
       return fail(OTB_ERR_CUDA, std::string("cudaFuncSetAttribute(hv): ") + cudaGetErrorString(e));
     }
+    int per_sm_fused = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fused, (const void*)k_cg_fused, 512, c->hv_smem);
+    const char* env_f = std::getenv("OTB_CG_FUSED");
+    c->cg_fused = per_sm_fused >= 1 && !(env_f && std::atoi(env_f) == 0);
   } else {
     c->hv_grid = sms * 8;
   }
   c->colgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 2 * sms));
+  c->col32 = (int)cdiv(n, 32);
   // buffers
   const int64_t m_loc = c->m_loc;
   const int64_t nv = npad + 16;
@@ -671,7 +716,8 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   A(&c->colpart, (size_t)parts * n);
   A(&c->vpart, (size_t)std::max(c->grid, c->ncl) * 8 + 8);
   A(&c->sendbuf, nv);
-  A(&c->bpart, 4 * (size_t)c->colgrid + 64);
+  A(&c->bpart, 4 * (size_t)std::max(c->colgrid, c->col32) + 64);
+  A(&c->scal, 2 * (size_t)c->hv_grid + 16);
   for (double** p : {&c->g, &c->d, &c->rhs, &c->dir, &c->cg_r, &c->cg_p[0], &c->cg_p[1], &c->cg_ap, &c->cg_y,
                      &c->gtrial, &c->yv, &c->ec, &c->Mloc, &c->Mglob, &c->Sloc})
     A(p, nv);
@@ -684,8 +730,10 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
     otb_destroy(c);
     return st;
   }
-  c->chunk = std::max<int64_t>(8192, 2 * n);
-  const int64_t init_cap = std::max<int64_t>((int64_t)1 << 20, m_loc * n / 4) + (int64_t)c->ncl * c->chunk;
+  c->chunk = rup(std::max<int64_t>(8192, 2 * n), kCsrAlign);
+  // first Newton steps keep 50-70% of P: start at 3/4
+  const int64_t init_cap =
+      std::max<int64_t>((int64_t)1 << 20, m_loc * (rup(n, kCsrAlign)) * 3 / 4) + (int64_t)c->ncl * c->chunk;
   st = grow_csr(c, init_cap);
   if (st != OTB_OK) {
     otb_destroy(c);
@@ -720,7 +768,7 @@ int otb_destroy(otb_ctx* c) {
                   (void*)c->rhs, (void*)c->dir, (void*)c->cg_r, (void*)c->cg_p[0], (void*)c->cg_p[1],
                   (void*)c->cg_ap, (void*)c->cg_y, (void*)c->gtrial, (void*)c->yv, (void*)c->ec, (void*)c->Mloc,
                   (void*)c->Mglob, (void*)c->Sloc, (void*)c->row_start, (void*)c->rowpre, (void*)c->row_len,
-                  (void*)c->cols, (void*)c->vals, (void*)c->ds, (void*)c->cg})
+                  (void*)c->cols, (void*)c->vals, (void*)c->ds, (void*)c->cg, (void*)c->scal})
     if (p) cudaFree(p);
   if (c->hs) cudaFreeHost(c->hs);
   if (c->hcg) cudaFreeHost(c->hcg);
@@ -839,7 +887,7 @@ int otb_hess_apply(otb_ctx* c, const double* v, double shift, double* out) {
   TRY(run_hv(c, v, nullptr, nullptr, nullptr, 0, nullptr, &hr));
   const double* cp = hr.ysum ? hr.ysum : hr.colpart;
   const int np = hr.ysum ? 1 : hr.nparts;
-  k_hv_out<<<c->colgrid, 256, 0, c->stream>>>(n, cp, np, hr.yatomic, c->d, v, c->eta, shift, out);
+  k_hv_out<<<c->col32, 256, 0, c->stream>>>(n, cp, np, hr.yatomic, c->d, v, c->eta, shift, out);
   LAUNCH_CHECK();
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   return OTB_OK;
@@ -968,11 +1016,11 @@ int otb_warm_start(otb_ctx* c, const double* logX, double* gamma, double* zeta, 
       TRY(launch_dense(c, DK_WARMG, geo, &io));
       TRY(prof_end(c, PC_WARMG, e0, 16.0 * mn));
       if (c->nranks == 1) {
-        k_warm_gamma_combine<<<c->colgrid, 256, 0, c->stream>>>(1, n, c->colpart, c->ncl, nullptr, nullptr, c->log_b,
+        k_warm_gamma_combine<<<c->col32, 256, 0, c->stream>>>(1, n, c->colpart, c->ncl, nullptr, nullptr, c->log_b,
                                                                 c->eta, gamma);
         LAUNCH_CHECK();
       } else {
-        k_warm_gamma_combine<<<c->colgrid, 256, 0, c->stream>>>(0, n, c->colpart, c->ncl, c->Mloc, c->Sloc, c->log_b,
+        k_warm_gamma_combine<<<c->col32, 256, 0, c->stream>>>(0, n, c->colpart, c->ncl, c->Mloc, c->Sloc, c->log_b,
                                                                 c->eta, gamma);
         LAUNCH_CHECK();
         CUDA_TRY(cudaMemcpyAsync(c->Mglob, c->Mloc, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
@@ -1035,8 +1083,9 @@ int otb_materialize_p(otb_ctx* c, const double* logX, const double* gamma, doubl
 
 int otb_info(otb_ctx* c, int64_t* o) {
   if (!c || !o) return fail(OTB_ERR_ARG, "null");
-  const int64_t v[16] = {c->nt,  c->ns,     c->cl,   c->colw, c->nstage[DK_EVAL], c->ncl, c->grid, c->hv_mode,
-                         c->hv_grid, c->nnz, c->cap, c->m_loc, c->n, c->ld, c->nranks, c->rank};
+  const int64_t v[20] = {c->nt,     c->ns,  c->cl,  c->colw,  c->nstage[DK_EVAL], c->ncl,    c->grid,
+                         c->hv_mode, c->hv_grid, c->nnz, c->cap, c->m_loc, c->n, c->ld, c->nranks, c->rank,
+                         c->hv_ng,   c->cg_fused ? 1 : 0, (int64_t)c->hv_smem, c->launches};
   std::memcpy(o, v, sizeof v);
   return OTB_OK;
 }

@@ -2,11 +2,25 @@
 //
 // CSR layout: every local row r owns one
 // contiguous run [row_start[r], row_start[r] + row_len[r]) of 16-bit column
-// indices and float64 values, ascending columns; the anchor row is stored
-// dense and unnormalised (sparsify.py:125).  Runs of different rows are not
-// in row order (chunked allocation), so a row prefix `rowpre` of lengths is
-// built once per Newton step for nnz-balanced scheduling.
+// indices and float64 values, ascending columns, starting on an 8-entry
+// boundary (so a thread can load 8 entries as one 16-byte vector of columns
+// and four 16-byte vectors of values); the anchor row is stored dense and
+// unnormalised (sparsify.py:125).  Runs are not in row order (chunked
+// allocation); `rowpre` (prefix of row lengths) drives nnz-balanced
+// scheduling.
+//
+// H v = (d * v - P^T (a * (P v))) / eta is applied in ONE pass over the
+// CSR: the CTA's warps are split into NG groups, each group walks its own
+// rows (s_r = P_r . v from a shared-memory copy of v, then a_r s_r P_rj
+// scattered into the group's private shared-memory column accumulator —
+// no atomics: within a group one row at a time, rows have distinct
+// columns).  The next row's first chunk is prefetched into registers while
+// the current row is reduced and scattered.  The group accumulators are
+// summed and written as one partial row per CTA; partial rows are reduced
+// in fixed order (deterministic).
 #pragma once
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 
@@ -30,6 +44,8 @@ struct CgState {
   int status, pad;
   unsigned int cnt[4];
 };
+
+constexpr int kCsrAlign = 8;   // row runs start on 8-entry boundaries
 
 // rowpre[r] = sum_{q<r} row_len[q]; single CTA (m_loc <= a few 1e5).
 __global__ void k_row_prefix(const int* row_len, int m_loc, int64_t* rowpre) {
@@ -79,19 +95,129 @@ OTB_DEV int lower_bound_i64(const int64_t* a, int n, int64_t key) {
   return lo;
 }
 
-// ---------------------------------------------------------------- hess_apply
-// sparsify.py:151-153 with SparseRowStochastic.matvec/rmatvec (64-78):
-// y = P_rho^T (a * (P_rho v)).  One pass over each row: s_r = P_r . v from a
-// shared-memory copy of v, then a_r s_r P_rj scattered into a shared-memory
-// column accumulator.  All threads of the CTA work on the same row between
-// two barriers, and a row has distinct columns, so the scatter needs no
-// atomics.  Each CTA writes its accumulator as one partial row.
-// With `update`, the CTA first forms v = r + beta p_prev (krylov.py:83) and
-// stores its slice of v into p_cur.
+// Rows of CTA `b` out of `nb`: [rb, re), balanced by nonzeros.
+OTB_DEV void cta_rows(const Csr& A, int b, int nb, int& rb, int& re) {
+  const int64_t total = A.rowpre[A.m_loc];
+  const int64_t lo = (total * b) / nb;
+  const int64_t hi = (total * (b + 1)) / nb;
+  rb = (b == 0) ? 0 : lower_bound_i64(A.rowpre, A.m_loc, lo);
+  re = (b + 1 == nb) ? A.m_loc : lower_bound_i64(A.rowpre, A.m_loc, hi);
+}
+
+// Sum over the threads of one warp group (TG threads, named barrier `bar`).
+OTB_DEV double group_sum(double v, double* slots, int& phase, int tg, int TG, int bar) {
+  v = warp_sum(v);
+  double* s = slots + phase * 32;
+  if ((tg & 31) == 0) s[tg >> 5] = v;
+  bar_sync(bar, TG);
+  double acc = s[0];
+  for (int w = 1; w < (TG >> 5); ++w) acc += s[w];
+  phase ^= 1;
+  return acc;
+}
+
+// A thread's share of one chunk of a row: entries base + i*stride, i < 8.
+// Consecutive threads hold consecutive entries, so for the dense-ish rows
+// of P_rho the 32 lanes of a warp touch ~consecutive columns: the
+// shared-memory gathers of v and the accumulator updates are (nearly)
+// bank-conflict free, and the global loads are fully coalesced.
+constexpr int kEA = 8;
+struct Chunk {
+  double v[kEA];
+  int c[kEA];
+};
+
+OTB_DEV void load_chunk(const Csr& A, int64_t st0, int base, int stride, int len, Chunk& ch) {
+#pragma unroll
+  for (int i = 0; i < kEA; ++i) {
+    const int k = base + i * stride;
+    if (k < len) {
+      ch.v[i] = A.vals[st0 + k];
+      ch.c[i] = A.cols[st0 + k];
+    } else {
+      ch.v[i] = 0.0;     // contributes 0 * v[0] to the dot product
+      ch.c[i] = 0;
+    }
+  }
+}
+
+OTB_DEV double chunk_dot(const Chunk& ch, const double* v) {
+  double d = 0.0;
+#pragma unroll
+  for (int i = 0; i < kEA; ++i) d = fma(ch.v[i], v[ch.c[i]], d);
+  return d;
+}
+
+// sparsify.py:78 product then sum: acc_j += val * (a_i s_i)
+OTB_DEV void chunk_scatter(const Chunk& ch, int base, int stride, int len, double* acc, double w) {
+#pragma unroll
+  for (int i = 0; i < kEA; ++i) {
+    if (base + i * stride < len) {
+      const int j = ch.c[i];
+      acc[j] = acc[j] + ch.v[i] * w;
+    }
+  }
+}
+
+// One CTA's share of y = P^T (a * (P v)): rows [rb, re) split round-robin
+// over NG warp groups; `acc` holds NG accumulators of `npad` doubles.
+OTB_DEV void hv_rows(const Csr& A, const double* a, const double* vsm, double* acc, int npad, int rb, int re,
+                     int NG, double* gslots) {
+  const int TG = blockDim.x / NG;
+  const int g = threadIdx.x / TG, tg = threadIdx.x % TG;
+  double* myacc = acc + (size_t)g * npad;
+  double* slots = gslots + g * 64;
+  const int bar = 1 + g;
+  const int span = kEA * TG;     // entries covered by one chunk of the group
+  int phase = 0;
+  Chunk nx;
+  int64_t nst = 0;
+  int nlen = 0;
+  int r = rb + g;
+  if (r < re) {
+    nst = A.row_start[r];
+    nlen = A.row_len[r];
+    load_chunk(A, nst, tg, TG, nlen, nx);
+  }
+  for (; r < re; r += NG) {
+    const int64_t st0 = nst;
+    const int len = nlen;
+    const Chunk c0 = nx;
+    Chunk c1;
+    const int b1 = tg + span;
+    load_chunk(A, st0, b1, TG, len, c1);
+    const int rn = r + NG;
+    if (rn < re) {                                   // prefetch the next row
+      nst = A.row_start[rn];
+      nlen = A.row_len[rn];
+      load_chunk(A, nst, tg, TG, nlen, nx);
+    }
+    double dot = chunk_dot(c0, vsm) + chunk_dot(c1, vsm);
+    for (int base = b1 + span; base < len + tg; base += span) {
+      Chunk ct;
+      load_chunk(A, st0, base, TG, len, ct);
+      dot += chunk_dot(ct, vsm);
+    }
+    const double s = group_sum(dot, slots, phase, tg, TG, bar);
+    const double w = __ldg(a + A.row0 + r) * s;       // sparsify.py:153: weights * pv
+    chunk_scatter(c0, tg, TG, len, myacc, w);
+    chunk_scatter(c1, b1, TG, len, myacc, w);
+    for (int base = b1 + span; base < len + tg; base += span) {
+      Chunk ct;
+      load_chunk(A, st0, base, TG, len, ct);
+      chunk_scatter(ct, base, TG, len, myacc, w);
+    }
+  }
+}
+
+// Shared-memory layout of the group hv: v[npad] | acc[NG][npad] | slots.
+OTB_DEV size_t hv_smem_doubles(int npad, int NG) { return (size_t)npad * (1 + NG) + 16 * 64; }
+
 struct HvArgs {
   Csr A;
   const double* a;
   int n;
+  int ng;
   const double* v_src;     // used when !update
   const double* r;
   const double* p_prev;
@@ -101,60 +227,43 @@ struct HvArgs {
   double* colpart;         // [gridDim][n]
 };
 
-__global__ void __launch_bounds__(512, 1) k_hv_smem(HvArgs h) {
+// Standalone hess_apply partials (multi-rank CG iterations, otb_hess_apply).
+__global__ void __launch_bounds__(512, 1) k_hv_grp(HvArgs h) {
   extern __shared__ __align__(16) double hsm[];
   if (h.st != nullptr && h.st->status != CG_RUN) return;
-  const int n = h.n;
-  const int npad = (n + 1) & ~1;
+  const int n = h.n, npad = (n + 1) & ~1, NG = h.ng;
   double* vsm = hsm;
   double* acc = hsm + npad;
-  double* slots = acc + npad;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  double* gslots = acc + (size_t)npad * NG;
   const double beta = h.update ? h.st->beta : 0.0;
   const int sl0 = (int)(((int64_t)blockIdx.x * n) / gridDim.x);
   const int sl1 = (int)(((int64_t)(blockIdx.x + 1) * n) / gridDim.x);
-  for (int j = tid; j < n; j += nt) {
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
     double v;
     if (h.update) {
-      v = h.r[j] + beta * h.p_prev[j];
+      v = h.r[j] + beta * h.p_prev[j];       // krylov.py:83
       if (j >= sl0 && j < sl1) h.p_cur[j] = v;
     } else {
       v = h.v_src[j];
     }
     vsm[j] = v;
-    acc[j] = 0.0;
   }
+  for (int j = threadIdx.x; j < npad * NG; j += blockDim.x) acc[j] = 0.0;
   __syncthreads();
-  const int64_t total = h.A.rowpre[h.A.m_loc];
-  const int64_t lo = (total * blockIdx.x) / gridDim.x;
-  const int64_t hi = (total * (blockIdx.x + 1)) / gridDim.x;
-  const int rb = (blockIdx.x == 0) ? 0 : lower_bound_i64(h.A.rowpre, h.A.m_loc, lo);
-  const int re = (blockIdx.x + 1 == gridDim.x) ? h.A.m_loc : lower_bound_i64(h.A.rowpre, h.A.m_loc, hi);
-  int rphase = 0;
-  for (int r = rb; r < re; ++r) {
-    const int len = h.A.row_len[r];
-    const int64_t st0 = h.A.row_start[r];
-    const double* vals = h.A.vals + st0;
-    const uint16_t* cols = h.A.cols + st0;
-    double dot = 0.0;
-#pragma unroll 4
-    for (int k = tid; k < len; k += nt) dot = fma(vals[k], vsm[cols[k]], dot);
-    double t[1] = {dot};
-    block_reduce<1, kSum>(t, slots, rphase, nt);
-    const double w = __ldg(h.a + h.A.row0 + r) * t[0];
-#pragma unroll 4
-    for (int k = tid; k < len; k += nt) {
-      const int j = cols[k];
-      acc[j] = acc[j] + vals[k] * w;
-    }
-  }
+  int rb, re;
+  cta_rows(h.A, blockIdx.x, gridDim.x, rb, re);
+  hv_rows(h.A, h.a, vsm, acc, npad, rb, re, NG, gslots);
   __syncthreads();
   double* dst = h.colpart + (size_t)blockIdx.x * n;
-  for (int j = tid; j < n; j += nt) dst[j] = acc[j];
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double t = acc[j];
+    for (int g = 1; g < NG; ++g) t += acc[(size_t)g * npad + j];
+    dst[j] = t;
+  }
 }
 
-// Warp-per-row variant for n too large for a shared accumulator: the
-// scatter goes to global memory with fp64 RED (non-deterministic order).
+// Warp-per-row variant for n too large for shared accumulators: the
+// scatter goes to global memory with fp64 RED (order not deterministic).
 struct HvAtomicArgs {
   Csr A;
   const double* a;
@@ -171,13 +280,22 @@ __global__ void __launch_bounds__(256) k_hv_atomic(HvAtomicArgs h) {
   for (int r = gw; r < h.A.m_loc; r += nw) {
     const int len = h.A.row_len[r];
     const int64_t st0 = h.A.row_start[r];
-    const double* vals = h.A.vals + st0;
-    const uint16_t* cols = h.A.cols + st0;
     double dot = 0.0;
-    for (int k = lane; k < len; k += 32) dot = fma(vals[k], __ldg(h.v + cols[k]), dot);
+    for (int base = lane; base < len; base += 32 * kEA) {
+      Chunk ch;
+      load_chunk(h.A, st0, base, 32, len, ch);
+#pragma unroll
+      for (int i = 0; i < kEA; ++i) dot = fma(ch.v[i], __ldg(h.v + ch.c[i]), dot);
+    }
     dot = warp_sum(dot);
     const double w = __ldg(h.a + h.A.row0 + r) * dot;
-    for (int k = lane; k < len; k += 32) atomicAdd(h.y + cols[k], vals[k] * w);
+    for (int base = lane; base < len; base += 32 * kEA) {
+      Chunk ch;
+      load_chunk(h.A, st0, base, 32, len, ch);
+#pragma unroll
+      for (int i = 0; i < kEA; ++i)
+        if (base + i * 32 < len) atomicAdd(h.y + ch.c[i], ch.v[i] * w);
+    }
   }
 }
 
@@ -189,21 +307,9 @@ __global__ void k_cg_p(int n, const double* r, const double* p_prev, double* p_c
     p_cur[j] = r[j] + beta * p_prev[j];
 }
 
-// Column sums of the hv partials (or the RED accumulator) into `out`.
-OTB_DEV double hv_column(int j, int n, const double* colpart, int nparts, double* yatomic) {
-  if (yatomic != nullptr) {
-    const double v = yatomic[j];
-    yatomic[j] = 0.0;
-    return v;
-  }
-  double s = 0.0;
-  for (int c = 0; c < nparts; ++c) s += colpart[(size_t)c * n + j];
-  return s;
-}
-
-// krylov.py:63-66 (ap = Hp + shift p; curvature = p.ap) and 70-75.
-// `ysum` != nullptr: column sums already reduced (multi-rank, after the
-// all-reduce); else reduce colpart / yatomic here.
+// krylov.py:63-75 for the multi-kernel path: ap = Hp + shift p, curvature.
+// Column sums come from colpart (reduced here), yatomic, or ysum
+// (multi-rank, after the all-reduce).  One block = 32 columns.
 struct CgApArgs {
   int n;
   const double* colpart;
@@ -220,19 +326,31 @@ struct CgApArgs {
 
 __global__ void __launch_bounds__(256) k_cg_ap(CgApArgs c) {
   if (c.st->status != CG_RUN) return;
-  __shared__ double red[2][32 * 4];
+  __shared__ double red[8 * 32];
+  __shared__ double red2[2][32 * 4];
   const double shift = c.st->shift;
+  const int j = blockIdx.x * 32 + (threadIdx.x & 31);
+  double y = 0.0;
+  if (c.colpart != nullptr) {
+    y = reduce_partials32(c.colpart, c.nparts, c.n, blockIdx.x * 32, red);
+  } else if (threadIdx.x < 32 && j < c.n) {
+    if (c.ysum) {
+      y = c.ysum[j];
+    } else {
+      y = c.yatomic[j];
+      c.yatomic[j] = 0.0;
+    }
+  }
   double part = 0.0;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < c.n; j += gridDim.x * blockDim.x) {
-    const double y = c.ysum ? c.ysum[j] : hv_column(j, c.n, c.colpart, c.nparts, c.yatomic);
+  if (threadIdx.x < 32 && j < c.n) {
     const double pj = c.p[j];
-    const double apj = div_rn(c.d[j] * pj - y, c.eta) + shift * pj;
+    const double apj = div_rn(c.d[j] * pj - y, c.eta) + shift * pj;   // sparsify.py:153 + krylov.py:65
     c.ap[j] = apj;
-    part = fma(pj, apj, part);
+    part = pj * apj;
   }
   int ph = 0;
   double t[1] = {part};
-  block_reduce<1, kSum>(t, &red[0][0], ph, blockDim.x);
+  block_reduce<1, kSum>(t, &red2[0][0], ph, blockDim.x);
   if (threadIdx.x == 0) c.bpart[blockIdx.x] = t[0];
   if (last_block(&c.st->cnt[0])) {
     if (threadIdx.x < 32) {
@@ -333,13 +451,172 @@ __global__ void __launch_bounds__(256) k_cg_init(int n, const double* rhs, doubl
   }
 }
 
-// Standalone H v (+ shift v) for parity tests: out_j = (d v - y)/eta + shift v.
-__global__ void k_hv_out(int n, const double* colpart, int nparts, double* yatomic, const double* d,
-                         const double* v, double eta, double shift, double* out) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const double y = hv_column(j, n, colpart, nparts, yatomic);
-    out[j] = div_rn(d[j] * v[j] - y, eta) + shift * v[j];
+// ---------------------------------------------------------------------------
+// Persistent single-GPU CG: the whole krylov.py:68-84 loop in ONE
+// cooperative launch (one CTA per SM), three grid barriers per iteration:
+//   phase 1  p = r + beta p_prev (every CTA, into shared memory; the CTA's
+//            column slice also to HBM), group hess_apply partial row
+//   --sync-- phase 2  column slice: y = sum of partial rows, ap = (d p - y)/eta
+//            + shift p, curvature partial
+//   --sync-- every CTA sums the curvature partials in the same order ->
+//            identical alpha everywhere; x += alpha p, r -= alpha ap on the
+//            slice, r.r partial
+//   --sync-- identical r.r -> stop test / beta in every CTA.
+// No host round trip; status, iteration count and residual end in *st.
+struct CgFusedArgs {
+  Csr A;
+  const double* a;
+  const double* d;
+  int n;
+  int ng;
+  double eta;
+  double* x;
+  double* r;
+  double* p0;
+  double* p1;
+  double* ap;
+  double* colpart;   // [gridDim][n]
+  double* scal;      // [gridDim][2]
+  CgState* st;
+};
+
+__global__ void __launch_bounds__(512, 1) k_cg_fused(CgFusedArgs c) {
+  namespace cgrp = cooperative_groups;
+  extern __shared__ __align__(16) double hsm[];
+  __shared__ double red[16 * 32];
+  __shared__ double red2[2][32 * 4];
+  __shared__ double bcast[2];
+  cgrp::grid_group grid = cgrp::this_grid();
+  if (c.st->status != CG_RUN) return;
+  const int n = c.n, npad = (n + 1) & ~1, NG = c.ng;
+  const int B = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  double* vsm = hsm;
+  double* acc = hsm + npad;
+  double* gslots = acc + (size_t)npad * NG;
+  const double eta = c.eta, shift = c.st->shift, target = c.st->target;
+  const long long max_iters = c.st->max_iters;
+  double rs = c.st->rs, beta = 0.0, alpha = 0.0, curv = 0.0;
+  long long it = 0;
+  int status = CG_RUN;
+  const int j0 = (int)(((int64_t)b * n) / B), j1 = (int)(((int64_t)(b + 1) * n) / B);
+  int rb, re;
+  cta_rows(c.A, b, B, rb, re);
+  for (;;) {
+    double* pc = (it & 1) ? c.p1 : c.p0;
+    const double* pp = (it & 1) ? c.p0 : c.p1;
+    // ---- phase 1: p and the hess_apply partial row
+    for (int j = tid; j < n; j += blockDim.x) {
+      double v;
+      if (it == 0) {
+        v = pc[j];
+      } else {
+        v = c.r[j] + beta * pp[j];
+        if (j >= j0 && j < j1) pc[j] = v;
+      }
+      vsm[j] = v;
+    }
+    for (int j = tid; j < npad * NG; j += blockDim.x) acc[j] = 0.0;
+    __syncthreads();
+    hv_rows(c.A, c.a, vsm, acc, npad, rb, re, NG, gslots);
+    __syncthreads();
+    double* dst = c.colpart + (size_t)b * n;
+    for (int j = tid; j < n; j += blockDim.x) {
+      double t = acc[j];
+      for (int g = 1; g < NG; ++g) t += acc[(size_t)g * npad + j];
+      dst[j] = t;
+    }
+    grid.sync();
+    // ---- phase 2: column slice of ap, curvature partial
+    double part = 0.0;
+    for (int jc = j0; jc < j1; jc += 32) {
+      const double y = reduce_partials32(c.colpart, B, n, jc, red);
+      const int j = jc + (tid & 31);
+      if (tid < 32 && j < j1) {
+        const double pj = vsm[j];
+        const double apj = div_rn(c.d[j] * pj - y, eta) + shift * pj;
+        c.ap[j] = apj;
+        part += pj * apj;
+      }
+    }
+    {
+      int ph = 0;
+      double t[1] = {part};
+      block_reduce<1, kSum>(t, &red2[0][0], ph, blockDim.x);
+      if (tid == 0) c.scal[2 * b] = t[0];
+    }
+    grid.sync();
+    if (tid < 32) {
+      const double v = warp_fixed_sum(c.scal, B, 2);
+      if (tid == 0) bcast[0] = v;
+    }
+    __syncthreads();
+    curv = bcast[0];
+    if (curv <= 0.0) {                                   // krylov.py:70-74
+      status = (sqrt(rs) <= target) ? CG_DONE : CG_NOTPD;
+      break;
+    }
+    alpha = rs / curv;
+    // ---- phase 3: x, r on the slice; r.r partial
+    part = 0.0;
+    for (int j = j0 + tid; j < j1; j += blockDim.x) {
+      const double pj = vsm[j];
+      c.x[j] = c.x[j] + alpha * pj;
+      const double rj = c.r[j] - alpha * c.ap[j];
+      c.r[j] = rj;
+      part = fma(rj, rj, part);
+    }
+    {
+      int ph = 0;
+      double t[1] = {part};
+      block_reduce<1, kSum>(t, &red2[0][0], ph, blockDim.x);
+      if (tid == 0) c.scal[2 * b + 1] = t[0];
+    }
+    grid.sync();
+    if (tid < 32) {
+      const double v = warp_fixed_sum(c.scal + 1, B, 2);
+      if (tid == 0) bcast[1] = v;
+    }
+    __syncthreads();
+    const double rsn = bcast[1];
+    ++it;
+    if (sqrt(rsn) <= target) {                           // krylov.py:79-82
+      rs = rsn;
+      status = CG_DONE;
+      break;
+    }
+    beta = rsn / rs;
+    rs = rsn;
+    if (it >= max_iters) {
+      status = CG_MAXIT;
+      break;
+    }
   }
+  if (b == 0 && tid == 0) {
+    CgState* s = c.st;
+    s->rs = rs;
+    s->curv = curv;
+    s->alpha = alpha;
+    s->beta = beta;
+    s->iters = it;
+    s->status = status;
+    s->res = sqrt(rs);
+  }
+}
+
+// Standalone H v (+ shift v) for parity tests: out_j = (d v - y)/eta + shift v.
+// One block = 32 columns.
+__global__ void __launch_bounds__(256) k_hv_out(int n, const double* colpart, int nparts, double* yatomic,
+                                                const double* d, const double* v, double eta, double shift,
+                                                double* out) {
+  __shared__ double red[8 * 32];
+  const int j = blockIdx.x * 32 + (threadIdx.x & 31);
+  double y = 0.0;
+  if (colpart != nullptr) {
+    y = reduce_partials32(colpart, nparts, n, blockIdx.x * 32, red);
+  } else if (threadIdx.x < 32 && j < n) {
+    y = yatomic[j];
+  }
+  if (threadIdx.x < 32 && j < n) out[j] = div_rn(d[j] * v[j] - y, eta) + shift * v[j];
 }
 
 }  // namespace otb

@@ -51,6 +51,7 @@ class InnerReport:
     nnz: list[int] = field(default_factory=list)
     cg_iters: list[int] = field(default_factory=list)
     values: list[float] = field(default_factory=list)
+    tests: list[tuple] = field(default_factory=list)   # (inner_v, grad_norm, D_phi) per inexact test
 
 
 @dataclass(frozen=True)
@@ -130,6 +131,7 @@ def inner_solve(logplan: LogPlan, gamma0: DualState, problem: OtProblem, config:
     cg_total = 0
     stop = StopReason.MAX_INNER
     tested = None
+    tests: list[tuple] = []
     for v in range(1, config.max_inner + 1):
         if grad_norm <= floor:
             stop = StopReason.GRAD_FLOOR
@@ -154,6 +156,7 @@ def inner_solve(logplan: LogPlan, gamma0: DualState, problem: OtProblem, config:
                                       value_before=value_before, value_after=value, slope=float(r.slope)))
         if grad_target is None and grad_norm < mu_k:
             res = s.ops.recover_round(plan_t, g_cur, cand_t, recover=True, metrics=True)
+            tests.append((v, grad_norm, float(res.bregman)))
             if res.bregman <= scale * mu_k:
                 stop = StopReason.INEXACT_CRITERION
                 tested = res
@@ -172,6 +175,7 @@ def inner_solve(logplan: LogPlan, gamma0: DualState, problem: OtProblem, config:
         nnz=nnzs,
         cg_iters=cgs,
         values=values,
+        tests=tests,
     )
     gamma_out = g_cur if (gamma_bufs is not None or _is_device(gamma0.gamma)) else g_cur[:n].cpu().numpy()
     if gamma_bufs is None and _is_device(gamma0.gamma):

@@ -24,6 +24,8 @@ from .core import OtProblem, _is_torch, host
 from .errors import ShapeMismatch
 
 _SESSION_ATTR = "_otb_sessions"
+_CTX_POOL: dict = {}      # (device, m, n, row_begin, row_end, ld) -> idle libotb contexts
+_POOL_DEPTH = 2
 
 
 def _torch():
@@ -62,11 +64,13 @@ class Session:
         if a_h.shape[0] != m or b_h.shape[0] != n:
             raise ShapeMismatch("marginal lengths do not match the cost matrix")
         # padded local rows of C
-        self.C = torch.zeros((self.m_loc, self.ld), dtype=f64, device=dev)
+        self.C = torch.empty((self.m_loc, self.ld), dtype=f64, device=dev)
+        if self.ld > n:
+            self.C[:, n:].zero_()
         rows = slice(self.row_begin, self.row_end)
         if _is_torch(cost):
             self.C[:, :n].copy_(cost[rows], non_blocking=True)
-            sq = torch.sum(self.C * self.C).reshape(1)        # ||C||_F^2 of the local rows
+            sq = torch.linalg.vector_norm(self.C).reshape(1) ** 2   # ||C||_F^2 of the local rows
             if comm is not None and comm.world > 1:
                 import torch.distributed as dist
 
@@ -86,9 +90,15 @@ class Session:
         self.default_anchor = int(np.argmax(a_h))             # sparsify.py:25-27
         self.anchor = None
         self.ctx = C.c_void_p()
-        with torch.cuda.device(dev):
-            _lib.check(_lib.lib.otb_create(C.byref(self.ctx), m, n, self.row_begin, self.row_end, self.ld,
-                                           dev.index, C.c_void_p(self._stream())))
+        self._pool_key = None if comm is not None else (dev.index, m, n, self.row_begin, self.row_end, self.ld)
+        pooled = _CTX_POOL.get(self._pool_key) if self._pool_key is not None else None
+        if pooled:
+            self.ctx = pooled.pop()
+            _lib.check(_lib.lib.otb_set_stream(self.ctx, C.c_void_p(self._stream())))
+        else:
+            with torch.cuda.device(dev):
+                _lib.check(_lib.lib.otb_create(C.byref(self.ctx), m, n, self.row_begin, self.row_end, self.ld,
+                                               dev.index, C.c_void_p(self._stream())))
         if comm is not None:
             comm.attach(self)
         self.bind(eta)
@@ -141,10 +151,10 @@ class Session:
         return t
 
     def info(self) -> dict:
-        out = (C.c_int64 * 16)()
+        out = (C.c_int64 * 20)()
         _lib.check(_lib.lib.otb_info(self.ctx, out))
         keys = ("nt", "ns", "cl", "colw", "nstage", "ncl", "grid", "hv_mode", "hv_grid", "nnz", "capacity",
-                "m_loc", "n", "ld", "nranks", "rank")
+                "m_loc", "n", "ld", "nranks", "rank", "hv_groups", "cg_fused", "hv_smem_bytes", "launches")
         return dict(zip(keys, list(out)))
 
     def launches(self) -> int:
@@ -162,12 +172,19 @@ class Session:
         by = (C.c_double * 16)()
         _lib.check(_lib.lib.otb_prof_read(self.ctx, ms, cnt, by, 1 if reset else 0))
         names = ("eval", "sparsify", "hess_apply", "cg_vector", "test_a", "test_b", "test_c",
-                 "warm_zeta", "warm_gamma")
+                 "warm_zeta", "warm_gamma", "cg_fused")
         return {nm: dict(ms=ms[k], launches=cnt[k], bytes=by[k]) for k, nm in enumerate(names)}
 
     def close(self):
+        """Return the libotb context to the pool (its scratch — CSR capacity,
+        CG vectors, partial rows — is reused by the next session of the same
+        shape); contexts with an NCCL communicator are destroyed."""
         if self.ctx:
-            _lib.lib.otb_destroy(self.ctx)
+            pool = _CTX_POOL.setdefault(self._pool_key, []) if self._pool_key is not None else None
+            if pool is not None and len(pool) < _POOL_DEPTH:
+                pool.append(self.ctx)
+            else:
+                _lib.lib.otb_destroy(self.ctx)
             self.ctx = C.c_void_p()
 
     def __del__(self):  # pragma: no cover - interpreter shutdown order varies
