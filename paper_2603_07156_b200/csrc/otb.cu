@@ -120,6 +120,9 @@ struct otb_ctx {
   int hv_mode = 0, hv_grid = 0, hv_ng = 1;
   size_t hv_smem = 0;
   bool cg_fused = false;     // persistent cooperative CG available (1 rank, smem hv)
+  int fused_ng = 1;
+  size_t fused_smem = 0;
+  int* cta_rb = nullptr;     // [hv_grid + 1] row bounds of the hess_apply CTAs
   int colgrid = 0, col32 = 0;
   double* scal = nullptr;    // [hv_grid][2] per-CTA scalars of the fused CG
   // problem
@@ -336,6 +339,8 @@ int do_eval(otb_ctx* c, const double* X, const double* gamma) {
 }
 
 // --------------------------------------------------------- sparsify
+Csr csr_view(const otb_ctx* c);
+
 int grow_csr(otb_ctx* c, int64_t want) {
   if (want <= c->cap) return OTB_OK;
   int64_t ncap = std::max<int64_t>(want, (int64_t)(c->cap * 1.5));
@@ -376,6 +381,13 @@ int do_sparsify(otb_ctx* c, const double* X, const double* gamma, double rho) {
       continue;
     }
     c->nnz = nnz;
+    {
+      // nnz-balanced row bounds of the hess_apply CTAs, once per sparsify
+      Csr A = csr_view(c);
+      A.cta_rb = nullptr;
+      k_cta_bounds<<<(int)cdiv(c->hv_grid + 1, 256), 256, 0, c->stream>>>(A, c->hv_grid, c->cta_rb);
+      LAUNCH_CHECK();
+    }
     TRY(colreduce(c, c->ncl, nullptr, 0, 0, 0));
     TRY(allreduce(c, c->sendbuf, (size_t)n, kNcclSum));
     k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_COPY, n, c->sendbuf, c->b, c->d, c->ds, c->bpart, nullptr);
@@ -390,6 +402,7 @@ Csr csr_view(const otb_ctx* c) {
   A.row_start = c->row_start;
   A.row_len = c->row_len;
   A.rowpre = c->rowpre;
+  A.cta_rb = c->cta_rb;
   A.cols = c->cols;
   A.vals = c->vals;
   A.m_loc = (int)c->m_loc;
@@ -478,12 +491,11 @@ int do_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t m
     return fail(OTB_ERR_INCONSISTENT, "unshifted system with right-hand side outside the range");
   if (c->cg_fused && c->hcg->status == CG_RUN) {
     // whole CG loop in one cooperative launch (k_cg_fused)
-    CgFusedArgs fa{csr_view(c), c->a, c->d, n, c->hv_ng, c->eta, x, c->cg_r, c->cg_p[0], c->cg_p[1], c->cg_ap,
-                   c->colpart, c->scal, c->cg};
+    CgFusedArgs fa{csr_view(c), c->a, c->d, n, c->fused_ng, c->eta, x, rhs, c->cg_ap, c->colpart, c->scal, c->cg};
     void* args[1] = {&fa};
     cudaEvent_t e0 = nullptr;
     TRY(prof_begin(c, &e0));
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_cg_fused, dim3(c->hv_grid), dim3(512), args, c->hv_smem,
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_cg_fused, dim3(c->hv_grid), dim3(512), args, c->fused_smem,
                                          c->stream));
     ++c->launches;
     TRY(prof_end(c, PC_CGFUSED, e0, 0.0));
@@ -690,8 +702,14 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
       delete c;
       return fail(OTB_ERR_CUDA, std::string("cudaFuncSetAttribute(hv): ") + cudaGetErrorString(e));
     }
+    // the persistent CG keeps p and r in shared memory as well: (2 + NG) rows
+    int fng = ng;
+    while (fng > 1 && (size_t)((2 + fng) * npad + 16 * 64) * 8 > hv_budget) fng >>= 1;
+    c->fused_ng = fng;
+    c->fused_smem = (size_t)((2 + fng) * npad + 16 * 64) * 8;
     int per_sm_fused = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fused, (const void*)k_cg_fused, 512, c->hv_smem);
+    if (c->fused_smem <= hv_budget)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fused, (const void*)k_cg_fused, 512, c->fused_smem);
     const char* env_f = std::getenv("OTB_CG_FUSED");
     c->cg_fused = per_sm_fused >= 1 && !(env_f && std::atoi(env_f) == 0);
   } else {
@@ -724,6 +742,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   if (st == OTB_OK) st = dalloc(&c->row_start, m_loc);
   if (st == OTB_OK) st = dalloc(&c->rowpre, m_loc + 1);
   if (st == OTB_OK) st = dalloc(&c->row_len, m_loc);
+  if (st == OTB_OK) st = dalloc(&c->cta_rb, (size_t)c->hv_grid + 2);
   if (st == OTB_OK) st = dalloc(&c->ds, 1);
   if (st == OTB_OK) st = dalloc(&c->cg, 1);
   if (st != OTB_OK) {
@@ -768,7 +787,7 @@ int otb_destroy(otb_ctx* c) {
                   (void*)c->rhs, (void*)c->dir, (void*)c->cg_r, (void*)c->cg_p[0], (void*)c->cg_p[1],
                   (void*)c->cg_ap, (void*)c->cg_y, (void*)c->gtrial, (void*)c->yv, (void*)c->ec, (void*)c->Mloc,
                   (void*)c->Mglob, (void*)c->Sloc, (void*)c->row_start, (void*)c->rowpre, (void*)c->row_len,
-                  (void*)c->cols, (void*)c->vals, (void*)c->ds, (void*)c->cg, (void*)c->scal})
+                  (void*)c->cols, (void*)c->vals, (void*)c->ds, (void*)c->cg, (void*)c->scal, (void*)c->cta_rb})
     if (p) cudaFree(p);
   if (c->hs) cudaFreeHost(c->hs);
   if (c->hcg) cudaFreeHost(c->hcg);

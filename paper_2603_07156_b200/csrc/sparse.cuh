@@ -30,6 +30,7 @@ struct Csr {
   const int64_t* row_start;
   const int* row_len;
   const int64_t* rowpre;   // m_loc + 1 prefix of row_len
+  const int* cta_rb;       // [nb + 1] nnz-balanced row bounds of the hv CTAs (or nullptr)
   const uint16_t* cols;
   const double* vals;
   int m_loc;
@@ -96,12 +97,35 @@ OTB_DEV int lower_bound_i64(const int64_t* a, int n, int64_t key) {
 }
 
 // Rows of CTA `b` out of `nb`: [rb, re), balanced by nonzeros.
-OTB_DEV void cta_rows(const Csr& A, int b, int nb, int& rb, int& re) {
+OTB_DEV void cta_rows_search(const Csr& A, int b, int nb, int& rb, int& re) {
   const int64_t total = A.rowpre[A.m_loc];
   const int64_t lo = (total * b) / nb;
   const int64_t hi = (total * (b + 1)) / nb;
   rb = (b == 0) ? 0 : lower_bound_i64(A.rowpre, A.m_loc, lo);
   re = (b + 1 == nb) ? A.m_loc : lower_bound_i64(A.rowpre, A.m_loc, hi);
+}
+
+// The bounds are computed once per sparsify (k_cta_bounds): a binary search
+// of dependent global loads at every kernel start costs several us.
+OTB_DEV void cta_rows(const Csr& A, int b, int nb, int& rb, int& re) {
+  if (A.cta_rb != nullptr) {
+    rb = A.cta_rb[b];
+    re = A.cta_rb[b + 1];
+  } else {
+    cta_rows_search(A, b, nb, rb, re);
+  }
+}
+
+__global__ void k_cta_bounds(Csr A, int nb, int* bounds) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > nb) return;
+  if (b == nb) {
+    bounds[b] = A.m_loc;
+    return;
+  }
+  int rb, re;
+  cta_rows_search(A, b, nb, rb, re);
+  bounds[b] = rb;
 }
 
 // Sum over the threads of one warp group (TG threads, named barrier `bar`).
@@ -198,8 +222,8 @@ OTB_DEV void hv_rows(const Csr& A, const double* a, const double* vsm, double* a
       load_chunk(A, st0, base, TG, len, ct);
       dot += chunk_dot(ct, vsm);
     }
-    const double s = group_sum(dot, slots, phase, tg, TG, bar);
-    const double w = __ldg(a + A.row0 + r) * s;       // sparsify.py:153: weights * pv
+    const double s_r = group_sum(dot, slots, phase, tg, TG, bar);
+    const double w = __ldg(a + A.row0 + r) * s_r;    // sparsify.py:153: weights * pv
     chunk_scatter(c0, tg, TG, len, myacc, w);
     chunk_scatter(c1, b1, TG, len, myacc, w);
     for (int base = b1 + span; base < len + tg; base += span) {
@@ -453,15 +477,16 @@ __global__ void __launch_bounds__(256) k_cg_init(int n, const double* rhs, doubl
 
 // ---------------------------------------------------------------------------
 // Persistent single-GPU CG: the whole krylov.py:68-84 loop in ONE
-// cooperative launch (one CTA per SM), three grid barriers per iteration:
-//   phase 1  p = r + beta p_prev (every CTA, into shared memory; the CTA's
-//            column slice also to HBM), group hess_apply partial row
-//   --sync-- phase 2  column slice: y = sum of partial rows, ap = (d p - y)/eta
-//            + shift p, curvature partial
-//   --sync-- every CTA sums the curvature partials in the same order ->
-//            identical alpha everywhere; x += alpha p, r -= alpha ap on the
-//            slice, r.r partial
-//   --sync-- identical r.r -> stop test / beta in every CTA.
+// cooperative launch (one CTA per SM), TWO grid barriers per iteration.
+// Every CTA keeps full copies of p and r in shared memory and updates them
+// redundantly, so only the H p product has to be exchanged:
+//   phase 1  group hess_apply of the CTA's rows -> one partial row (HBM)
+//   --sync-- phase 2  the CTA's column slice: y = fixed-order sum of the
+//            partial rows, ap = (d p - y)/eta + shift p (to HBM), p.ap partial
+//   --sync-- every CTA: curvature = fixed-order sum of the partials ->
+//            alpha; x += alpha p on its slice; r -= alpha ap and r.r over ALL
+//            columns (same order in every CTA -> bitwise-identical r.r, so
+//            every CTA takes the same stop / beta decision); p = r + beta p.
 // No host round trip; status, iteration count and residual end in *st.
 struct CgFusedArgs {
   Csr A;
@@ -471,27 +496,29 @@ struct CgFusedArgs {
   int ng;
   double eta;
   double* x;
-  double* r;
-  double* p0;
-  double* p1;
+  const double* r0;  // initial residual (= rhs)
   double* ap;
   double* colpart;   // [gridDim][n]
-  double* scal;      // [gridDim][2]
+  double* scal;      // [gridDim]
   CgState* st;
 };
+
+// Shared memory of k_cg_fused: p[npad] | r[npad] | acc[NG][npad] | slots.
+OTB_DEV size_t cg_fused_smem_doubles(int npad, int NG) { return (size_t)npad * (2 + NG) + 16 * 64; }
 
 __global__ void __launch_bounds__(512, 1) k_cg_fused(CgFusedArgs c) {
   namespace cgrp = cooperative_groups;
   extern __shared__ __align__(16) double hsm[];
   __shared__ double red[16 * 32];
   __shared__ double red2[2][32 * 4];
-  __shared__ double bcast[2];
+  __shared__ double bcast;
   cgrp::grid_group grid = cgrp::this_grid();
   if (c.st->status != CG_RUN) return;
   const int n = c.n, npad = (n + 1) & ~1, NG = c.ng;
-  const int B = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
-  double* vsm = hsm;
-  double* acc = hsm + npad;
+  const int B = gridDim.x, b = blockIdx.x, tid = threadIdx.x, nth = blockDim.x;
+  double* psm = hsm;
+  double* rsm = hsm + npad;
+  double* acc = rsm + npad;
   double* gslots = acc + (size_t)npad * NG;
   const double eta = c.eta, shift = c.st->shift, target = c.st->target;
   const long long max_iters = c.st->max_iters;
@@ -501,26 +528,19 @@ __global__ void __launch_bounds__(512, 1) k_cg_fused(CgFusedArgs c) {
   const int j0 = (int)(((int64_t)b * n) / B), j1 = (int)(((int64_t)(b + 1) * n) / B);
   int rb, re;
   cta_rows(c.A, b, B, rb, re);
+  for (int j = tid; j < n; j += nth) {                 // x0 = 0, r = p = rhs (krylov.py:60-62)
+    const double v = c.r0[j];
+    psm[j] = v;
+    rsm[j] = v;
+  }
   for (;;) {
-    double* pc = (it & 1) ? c.p1 : c.p0;
-    const double* pp = (it & 1) ? c.p0 : c.p1;
-    // ---- phase 1: p and the hess_apply partial row
-    for (int j = tid; j < n; j += blockDim.x) {
-      double v;
-      if (it == 0) {
-        v = pc[j];
-      } else {
-        v = c.r[j] + beta * pp[j];
-        if (j >= j0 && j < j1) pc[j] = v;
-      }
-      vsm[j] = v;
-    }
-    for (int j = tid; j < npad * NG; j += blockDim.x) acc[j] = 0.0;
+    // ---- phase 1: the hess_apply partial row of this CTA
+    for (int j = tid; j < npad * NG; j += nth) acc[j] = 0.0;
     __syncthreads();
-    hv_rows(c.A, c.a, vsm, acc, npad, rb, re, NG, gslots);
+    hv_rows(c.A, c.a, psm, acc, npad, rb, re, NG, gslots);
     __syncthreads();
     double* dst = c.colpart + (size_t)b * n;
-    for (int j = tid; j < n; j += blockDim.x) {
+    for (int j = tid; j < n; j += nth) {
       double t = acc[j];
       for (int g = 1; g < NG; ++g) t += acc[(size_t)g * npad + j];
       dst[j] = t;
@@ -532,8 +552,8 @@ __global__ void __launch_bounds__(512, 1) k_cg_fused(CgFusedArgs c) {
       const double y = reduce_partials32(c.colpart, B, n, jc, red);
       const int j = jc + (tid & 31);
       if (tid < 32 && j < j1) {
-        const double pj = vsm[j];
-        const double apj = div_rn(c.d[j] * pj - y, eta) + shift * pj;
+        const double pj = psm[j];
+        const double apj = div_rn(c.d[j] * pj - y, eta) + shift * pj;   // sparsify.py:153 + krylov.py:65
         c.ap[j] = apj;
         part += pj * apj;
       }
@@ -541,55 +561,49 @@ __global__ void __launch_bounds__(512, 1) k_cg_fused(CgFusedArgs c) {
     {
       int ph = 0;
       double t[1] = {part};
-      block_reduce<1, kSum>(t, &red2[0][0], ph, blockDim.x);
-      if (tid == 0) c.scal[2 * b] = t[0];
+      block_reduce<1, kSum>(t, &red2[0][0], ph, nth);
+      if (tid == 0) c.scal[b] = t[0];
     }
     grid.sync();
     if (tid < 32) {
-      const double v = warp_fixed_sum(c.scal, B, 2);
-      if (tid == 0) bcast[0] = v;
+      const double v = warp_fixed_sum(c.scal, B, 1);
+      if (tid == 0) bcast = v;
     }
     __syncthreads();
-    curv = bcast[0];
+    curv = bcast;
     if (curv <= 0.0) {                                   // krylov.py:70-74
       status = (sqrt(rs) <= target) ? CG_DONE : CG_NOTPD;
       break;
     }
     alpha = rs / curv;
-    // ---- phase 3: x, r on the slice; r.r partial
-    part = 0.0;
-    for (int j = j0 + tid; j < j1; j += blockDim.x) {
-      const double pj = vsm[j];
-      c.x[j] = c.x[j] + alpha * pj;
-      const double rj = c.r[j] - alpha * c.ap[j];
-      c.r[j] = rj;
-      part = fma(rj, rj, part);
+    // ---- phase 3 (redundant in every CTA): x on the slice, r and r.r everywhere
+    for (int j = j0 + tid; j < j1; j += nth) c.x[j] = c.x[j] + alpha * psm[j];
+    double rr = 0.0;
+    for (int j = tid; j < n; j += nth) {
+      const double rj = rsm[j] - alpha * c.ap[j];
+      rsm[j] = rj;
+      rr = fma(rj, rj, rr);
     }
     {
-      int ph = 0;
-      double t[1] = {part};
-      block_reduce<1, kSum>(t, &red2[0][0], ph, blockDim.x);
-      if (tid == 0) c.scal[2 * b + 1] = t[0];
+      int ph = 1;
+      double t[1] = {rr};
+      block_reduce<1, kSum>(t, &red2[0][0], ph, nth);
+      rr = t[0];
     }
-    grid.sync();
-    if (tid < 32) {
-      const double v = warp_fixed_sum(c.scal + 1, B, 2);
-      if (tid == 0) bcast[1] = v;
-    }
-    __syncthreads();
-    const double rsn = bcast[1];
     ++it;
-    if (sqrt(rsn) <= target) {                           // krylov.py:79-82
-      rs = rsn;
+    if (sqrt(rr) <= target) {                            // krylov.py:79-82
+      rs = rr;
       status = CG_DONE;
       break;
     }
-    beta = rsn / rs;
-    rs = rsn;
+    beta = rr / rs;
+    rs = rr;
     if (it >= max_iters) {
       status = CG_MAXIT;
       break;
     }
+    for (int j = tid; j < n; j += nth) psm[j] = rsm[j] + beta * psm[j];   // krylov.py:83
+    __syncthreads();
   }
   if (b == 0 && tid == 0) {
     CgState* s = c.st;
