@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_eval(Geom geo, EvalIO io) {
     return;
   }
   const double eta = io.eta;
+  const Divider DIV(eta);
   double alse = 0.0, nbad = 0.0;
   for (int r = D.r0; r < D.r1; ++r) {
     double z[2 * NS];
@@ -49,8 +50,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_eval(Geom geo, EvalIO io) {
         D.fetch(c, x);
         const int j = D.col(s, 0);
         const double2 gm = load_pair(io.gamma, j, D.c1);
-        if (j < D.c1) z[2 * s] = x.x + div_rn(gm.x - c.x, eta);
-        if (j + 1 < D.c1) z[2 * s + 1] = x.y + div_rn(gm.y - c.y, eta);
+        if (j < D.c1) z[2 * s] = x.x + DIV(gm.x - c.x);
+        if (j + 1 < D.c1) z[2 * s + 1] = x.y + DIV(gm.y - c.y);
         mx = fmax(mx, fmax(z[2 * s], z[2 * s + 1]));
       }
     }
@@ -79,7 +80,6 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_eval(Geom geo, EvalIO io) {
       M = Mg;
       S = Sg;
     }
-    const double l = M + log(S);
     const double ai = __ldg(io.a + D.g.row0 + r);
     const double w = (ai / S) * scale;
 #pragma unroll
@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_eval(Geom geo, EvalIO io) {
       }
     }
     if (D.tid == 0 && D.cr == 0) {
+      const double l = M + log(S);   // semidual.py:79
       io.rowM[r] = M;
       io.rowS[r] = S;
       io.lse[r] = l;
@@ -123,6 +124,7 @@ struct SparsifyIO {
   int64_t anchor_local;   // local row of the anchor, -1 if not on this rank
   const double* rowM;
   const double* rowS;
+  const double* rowL;     // lse of the same eval (M + log S)
   uint16_t* cols;
   double* vals;
   int64_t cap;
@@ -147,6 +149,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
   __shared__ int tab[kTabInts];
   __shared__ unsigned long long chunk_base;
   const double eta = io.eta, rho = io.rho;
+  const Divider DIV(eta);
+  const double log_rho = log(rho);
   const int nw = D.g.nt >> 5;
   const unsigned lt = (1u << D.lane) - 1u;
   unsigned long long cur = 0, end = 0;
@@ -154,8 +158,13 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
   for (int r = D.r0; r < D.r1; ++r) {
     const bool anc = (r == io.anchor_local);
     const double M = io.rowM[r], S = io.rowS[r];
-    double P[2 * NS];
-    unsigned keep = 0;
+    const Divider DS(S);
+    // P = exp(z - M) / S < rho whenever z - M < log(rho S): such entries are
+    // dropped without the exp and the division (margin 1e-9 >> rounding).
+    // log S = lse - M up to a few ulp of lse, far inside the margin.
+    const double dmin = (anc || !(rho > 0.0)) ? -INFINITY : (log_rho + (io.rowL[r] - M)) - 1e-9;
+    double P[2 * NS];       // P_ij, or z - M for skipped entries (bit set in `skip`)
+    unsigned keep = 0, skip = 0;
     double ks = 0.0;
     int* tb = tab + rowpar * kMaxNS * 32;
 #pragma unroll
@@ -167,13 +176,24 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
         D.fetch(c, x);
         const int j = D.col(s, 0);
         const double2 gm = load_pair(io.gamma, j, D.c1);
-        if (j < D.c1) P[2 * s] = div_rn(exp((x.x + div_rn(gm.x - c.x, eta)) - M), S);
-        if (j + 1 < D.c1) P[2 * s + 1] = div_rn(exp((x.y + div_rn(gm.y - c.y, eta)) - M), S);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (j + e < D.c1) {
+            const double dz = ((e ? x.y : x.x) + DIV((e ? gm.y : gm.x) - (e ? c.y : c.x))) - M;
+            if (dz < dmin) {
+              P[2 * s + e] = dz;
+              skip |= 1u << (2 * s + e);
+            } else {
+              P[2 * s + e] = DS(exp(dz));          // semidual.py:82-83: shifted / row_sum
+            }
+          }
+        }
       }
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const double p = P[2 * s + e];
-        const bool k = (p >= 0.0) && (anc || (p >= rho && p > 0.0));
+        const bool valid = D.col(s, e) < D.c1 && !((skip >> (2 * s + e)) & 1u);
+        const bool k = valid && (anc || (p >= rho && p > 0.0));
         if (k) {
           keep |= 1u << (2 * s + e);
           ks += p;
@@ -189,9 +209,14 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
     D.reduce<1, kSum>(t);   // barrier also publishes tb
     double ksum = t[0];
     // per-slice totals (lane s holds slice s), exclusive scan over slices
-    int tot = 0;
+    // and (pre) the kept entries of slice s in the warps before this one
+    int tot = 0, pre = 0;
     if (D.lane < D.nsl)
-      for (int w = 0; w < nw; ++w) tot += tb[D.lane * 32 + w];
+      for (int w = 0; w < nw; ++w) {
+        const int v = tb[D.lane * 32 + w];
+        tot += v;
+        if (w < D.warp) pre += v;
+      }
     int incl = tot;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -220,6 +245,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
     if (!anc && cnt == 0) {
       // sparsify.py:103-107: keep the first argmax of the row with value 1.
       fallback = true;
+#pragma unroll
+      for (int k = 0; k < 2 * NS; ++k)
+        if ((skip >> k) & 1u) P[k] = DS(exp(P[k]));   // skipped entries take part in the argmax
       double pm = -1.0;
 #pragma unroll
       for (int k = 0; k < 2 * NS; ++k) pm = fmax(pm, P[k]);
@@ -278,6 +306,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
     if (ovf && D.tid == 0 && D.cr == 0) atomicOr(io.flags, 2);
     const double ai = __ldg(io.a + D.g.row0 + r);
     const unsigned long long wbase = start + myoff;
+    const Divider DK(ksum);
     if (!ovf) {
       if (fallback) {
 #pragma unroll
@@ -297,19 +326,18 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
             const unsigned k0 = (keep >> (2 * s)) & 1u, k1 = (keep >> (2 * s + 1)) & 1u;
             const unsigned b0 = __ballot_sync(0xffffffffu, k0);
             const unsigned b1 = __ballot_sync(0xffffffffu, k1);
-            int base = __shfl_sync(0xffffffffu, excl, s);
-            for (int w = 0; w < D.warp; ++w) base += tb[s * 32 + w];
+            const int base = __shfl_sync(0xffffffffu, excl + pre, s);
             const int off = base + __popc(b0 & lt) + __popc(b1 & lt);
             const int j = D.col(s, 0);
             double2* a2 = D.acc2(0, s);
             if (k0) {
-              const double v = anc ? P[2 * s] : div_rn(P[2 * s], ksum);
+              const double v = anc ? P[2 * s] : DK(P[2 * s]);
               io.cols[wbase + off] = (uint16_t)j;
               io.vals[wbase + off] = v;
               a2->x += ai * v;
             }
             if (k1) {
-              const double v = anc ? P[2 * s + 1] : div_rn(P[2 * s + 1], ksum);
+              const double v = anc ? P[2 * s + 1] : DK(P[2 * s + 1]);
               io.cols[wbase + off + k0] = (uint16_t)(j + 1);
               io.vals[wbase + off + k0] = v;
               a2->y += ai * v;
@@ -357,6 +385,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_test_a(Geom geo, TestAIO io)
     return;
   }
   const double eta = io.eta;
+  const Divider DIV(eta);
   double sumx = 0.0;
   int bad = 0;
   for (int r = D.r0; r < D.r1; ++r) {
@@ -377,14 +406,14 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_test_a(Geom geo, TestAIO io)
         double* dst = io.Xout + (size_t)r * D.g.ld + j;
         if (io.recover) {
           if (j < D.c1) {
-            const double raw = ((la + x.x) + div_rn(gm.x - c.x, eta)) - l;
+            const double raw = ((la + x.x) + DIV(gm.x - c.x)) - l;
             bad |= (isnan(raw) || raw == INFINITY);
             const double xl = fmax(raw, kLogFloor);
             dst[0] = xl;
             xv[2 * s] = exp(xl);
           }
           if (j + 1 < D.c1) {
-            const double raw = ((la + x.y) + div_rn(gm.y - c.y, eta)) - l;
+            const double raw = ((la + x.y) + DIV(gm.y - c.y)) - l;
             bad |= (isnan(raw) || raw == INFINITY);
             const double xl = fmax(raw, kLogFloor);
             dst[1] = xl;
@@ -503,6 +532,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_test_c(Geom geo, TestCIO io)
     return;
   }
   const double deficit = *io.deficit;
+  const Divider DD(deficit);
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
   for (int r = D.r0; r < D.r1; ++r) {
     const double z = io.zrow[r];
@@ -530,7 +560,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_test_c(Geom geo, TestCIO io)
           if (j + e < D.c1) {
             const double xl = e ? x.y : x.x;
             double fv = (exp(xl) * z) * (e ? yy.y : yy.x);
-            if (deficit > 0.0) fv = fv + div_rn(e_r * (e ? ee.y : ee.x), deficit);
+            if (deficit > 0.0) fv = fv + DD(e_r * (e ? ee.y : ee.x));
             f[2 * s + e] = fv;
             if (fv > 0.0) acc[0] += fv * (log(fv) - xl);
             acc[1] += fv;
@@ -619,6 +649,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_warm_zeta(Geom geo, WarmZIO 
     return;
   }
   const double eta = io.eta;
+  const Divider DIV(eta);
   for (int r = D.r0; r < D.r1; ++r) {
     double xs[2 * NS], cs[2 * NS];
     double mx = -INFINITY;
@@ -635,8 +666,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_warm_zeta(Geom geo, WarmZIO 
         cs[2 * s + 1] = c.y;
         const int j = D.col(s, 0);
         const double2 gm = load_pair(io.gamma, j, D.c1);
-        if (j < D.c1) mx = fmax(mx, x.x + div_rn(gm.x - c.x, eta));
-        if (j + 1 < D.c1) mx = fmax(mx, x.y + div_rn(gm.y - c.y, eta));
+        if (j < D.c1) mx = fmax(mx, x.x + DIV(gm.x - c.x));
+        if (j + 1 < D.c1) mx = fmax(mx, x.y + DIV(gm.y - c.y));
       }
     }
     double t[1] = {mx};
@@ -648,8 +679,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_warm_zeta(Geom geo, WarmZIO 
       if (s < D.nsl) {
         const int j = D.col(s, 0);
         const double2 gm = load_pair(io.gamma, j, D.c1);
-        if (j < D.c1) se += exp((xs[2 * s] + div_rn(gm.x - cs[2 * s], eta)) - M);
-        if (j + 1 < D.c1) se += exp((xs[2 * s + 1] + div_rn(gm.y - cs[2 * s + 1], eta)) - M);
+        if (j < D.c1) se += exp((xs[2 * s] + DIV(gm.x - cs[2 * s])) - M);
+        if (j + 1 < D.c1) se += exp((xs[2 * s + 1] + DIV(gm.y - cs[2 * s + 1])) - M);
       }
     }
     t[0] = se;
@@ -674,8 +705,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_warm_zeta(Geom geo, WarmZIO 
         const int j = D.col(s, 0);
         const double2 gm = load_pair(io.gamma, j, D.c1);
         double e0 = 0.0, e1 = 0.0;
-        if (j < D.c1) e0 = exp(xs[2 * s] + div_rn((zeta + gm.x) - cs[2 * s], eta));
-        if (j + 1 < D.c1) e1 = exp(xs[2 * s + 1] + div_rn((zeta + gm.y) - cs[2 * s + 1], eta));
+        if (j < D.c1) e0 = exp(xs[2 * s] + DIV((zeta + gm.x) - cs[2 * s]));
+        if (j + 1 < D.c1) e1 = exp(xs[2 * s + 1] + DIV((zeta + gm.y) - cs[2 * s + 1]));
         double2* a2 = D.acc2(0, s);
         double2 v = *a2;
         v.x += e0;
@@ -710,6 +741,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_warm_gamma(Geom geo, WarmGIO
     return;
   }
   const double eta = io.eta;
+  const Divider DIV(eta);
 #pragma unroll
   for (int s = 0; s < NS; ++s)
     if (s < D.nsl) *D.acc2(0, s) = make_double2(-INFINITY, -INFINITY);
@@ -725,7 +757,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_warm_gamma(Geom geo, WarmGIO
         double2* s2 = D.acc2(1, s);
         double2 m = *m2, sm = *s2;
         if (j < D.c1) {
-          const double tv = x.x + div_rn(zi - c.x, eta);
+          const double tv = x.x + DIV(zi - c.x);
           if (tv > m.x) {
             sm.x = sm.x * exp(m.x - tv) + 1.0;
             m.x = tv;
@@ -734,7 +766,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_warm_gamma(Geom geo, WarmGIO
           }
         }
         if (j + 1 < D.c1) {
-          const double tv = x.y + div_rn(zi - c.y, eta);
+          const double tv = x.y + DIV(zi - c.y);
           if (tv > m.y) {
             sm.y = sm.y * exp(m.y - tv) + 1.0;
             m.y = tv;
@@ -763,7 +795,7 @@ __global__ void k_materialize_p(const double* C, const double* X, int64_t ld, in
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(idx / n), j = (int)(idx % n);
-    const double z = X[(size_t)r * ld + j] + div_rn(gamma[j] - C[(size_t)r * ld + j], eta);
+    const double z = X[(size_t)r * ld + j] + Divider(eta)(gamma[j] - C[(size_t)r * ld + j]);
     P[(size_t)r * ldp + j] = div_rn(exp(z - rowM[r]), rowS[r]);
   }
 }

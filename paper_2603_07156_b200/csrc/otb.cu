@@ -363,7 +363,7 @@ int do_sparsify(otb_ctx* c, const double* X, const double* gamma, double rho) {
     CUDA_TRY(cudaMemsetAsync(&c->ds->alloc, 0, sizeof(unsigned long long), c->stream));
     CUDA_TRY(cudaMemsetAsync(&c->ds->flags, 0, sizeof(int), c->stream));
     Geom geo = make_geom(c, DK_SPARSIFY, c->C, X);
-    SparsifyIO io{gamma, c->a, c->eta, rho, anchor_local, c->rowM, c->rowS, c->cols, c->vals, c->cap,
+    SparsifyIO io{gamma, c->a, c->eta, rho, anchor_local, c->rowM, c->rowS, c->lse, c->cols, c->vals, c->cap,
                   c->row_start, c->row_len, &c->ds->alloc, c->chunk, c->colpart, &c->ds->flags};
     cudaEvent_t e0 = nullptr;
     TRY(prof_begin(c, &e0));
@@ -1106,6 +1106,15 @@ int otb_info(otb_ctx* c, int64_t* o) {
                          c->hv_mode, c->hv_grid, c->nnz, c->cap, c->m_loc, c->n, c->ld, c->nranks, c->rank,
                          c->hv_ng,   c->cg_fused ? 1 : 0, (int64_t)c->hv_smem, c->launches};
   std::memcpy(o, v, sizeof v);
+  return OTB_OK;
+}
+
+int otb_selftest_div(const double* x, int64_t n, double y, double* out) {
+  if ((!x || !out) && n > 0) return fail(OTB_ERR_ARG, "null");
+  if (n <= 0) return OTB_OK;
+  k_selftest_div<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256>>>(x, n, y, out);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaDeviceSynchronize());
   return OTB_OK;
 }
 

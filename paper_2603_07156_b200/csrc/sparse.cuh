@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(256) k_cg_ap(CgApArgs c) {
   double part = 0.0;
   if (threadIdx.x < 32 && j < c.n) {
     const double pj = c.p[j];
-    const double apj = div_rn(c.d[j] * pj - y, c.eta) + shift * pj;   // sparsify.py:153 + krylov.py:65
+    const double apj = Divider(c.eta)(c.d[j] * pj - y) + shift * pj;   // sparsify.py:153 + krylov.py:65
     c.ap[j] = apj;
     part = pj * apj;
   }
@@ -521,6 +521,7 @@ __global__ void __launch_bounds__(512, 1) k_cg_fused(CgFusedArgs c) {
   double* acc = rsm + npad;
   double* gslots = acc + (size_t)npad * NG;
   const double eta = c.eta, shift = c.st->shift, target = c.st->target;
+  const Divider DIV(eta);
   const long long max_iters = c.st->max_iters;
   double rs = c.st->rs, beta = 0.0, alpha = 0.0, curv = 0.0;
   long long it = 0;
@@ -553,7 +554,7 @@ __global__ void __launch_bounds__(512, 1) k_cg_fused(CgFusedArgs c) {
       const int j = jc + (tid & 31);
       if (tid < 32 && j < j1) {
         const double pj = psm[j];
-        const double apj = div_rn(c.d[j] * pj - y, eta) + shift * pj;   // sparsify.py:153 + krylov.py:65
+        const double apj = DIV(c.d[j] * pj - y) + shift * pj;   // sparsify.py:153 + krylov.py:65
         c.ap[j] = apj;
         part += pj * apj;
       }
@@ -630,7 +631,7 @@ __global__ void __launch_bounds__(256) k_hv_out(int n, const double* colpart, in
   } else if (threadIdx.x < 32 && j < n) {
     y = yatomic[j];
   }
-  if (threadIdx.x < 32 && j < n) out[j] = div_rn(d[j] * v[j] - y, eta) + shift * v[j];
+  if (threadIdx.x < 32 && j < n) out[j] = Divider(eta)(d[j] * v[j] - y) + shift * v[j];
 }
 
 }  // namespace otb

@@ -282,3 +282,34 @@ def test_error_mapping(cuda):
     # rhs = 0 -> 0 iterations
     x, it, res = P.cg_solve(op, 1.0, np.zeros(8))
     assert it == 0 and res == 0.0 and not x.any()
+
+
+# ------------------------------------------------ fixed-divisor fast division
+@pytest.mark.parametrize("y", [1e-2, 5e-3, 1e-3, 0.7310585786300049, 3.0, 1e-17, 2.5e-290, 1e300])
+def test_fast_division_is_correctly_rounded(cuda, y):
+    """The kernels divide by eta / row sums / the rounding deficit through a
+    reciprocal + one FMA residual step (csrc/common.cuh Divider); it must give
+    numpy's x / y bit for bit, including zeros, signs, infinities and NaN."""
+    import torch
+
+    from paper_2603_07156_b200 import _lib
+
+    rng = np.random.default_rng(11)
+    parts = [
+        rng.standard_normal(200_000) * 10.0 ** rng.uniform(-30, 30, 200_000),
+        rng.uniform(-1.0, 1.0, 100_000),
+        np.exp(rng.uniform(-745, 709, 50_000)),
+        np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, -5e-324, 1.7e308, 2.2250738585072014e-308]),
+        y * np.arange(-1000, 1000, dtype=np.float64),
+        np.nextafter(y * np.arange(1, 1000, dtype=np.float64), np.inf),
+    ]
+    x = np.concatenate(parts)
+    xd = torch.from_numpy(x).cuda()
+    out = torch.empty_like(xd)
+    _lib.check(_lib.lib.otb_selftest_div(xd.data_ptr(), x.size, float(y), out.data_ptr()))
+    got = out.cpu().numpy()
+    with np.errstate(all="ignore"):
+        want = x / y
+    bad = got.view(np.uint64) != want.view(np.uint64)
+    bad &= ~(np.isnan(got) & np.isnan(want))
+    assert not bad.any(), (x[bad][:5], got[bad][:5], want[bad][:5])
