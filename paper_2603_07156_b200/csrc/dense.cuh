@@ -134,6 +134,8 @@ struct SparsifyIO {
   int64_t chunk;
   double* colpart;        // [ncl][n] partial of d
   int* flags;             // bit 1: capacity overflow
+  uint4* bm;              // bitmap index [m_loc][nq] (sparse.cuh), or nullptr
+  int nq;
 };
 
 template <int NS>
@@ -319,6 +321,20 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
             else a2->x += ai * 1.0;
           }
         }
+        if (io.bm != nullptr && D.lane == 0) {
+          for (int s = 0; s < D.nsl; ++s) {
+            const int cs = D.c0 + s * D.slice + 64 * D.warp;   // this warp's 64-column word
+            if (cs < D.c1) {
+              uint4 w = make_uint4(0u, 0u, 0u, 0u);
+              const int o = jbest - cs;
+              if (o >= 0 && o < 64) {
+                if (o & 1) w.y = 1u << (o >> 1);
+                else w.x = 1u << (o >> 1);
+              }
+              io.bm[(size_t)r * io.nq + cs / 64] = w;
+            }
+          }
+        }
       } else {
 #pragma unroll
         for (int s = 0; s < NS; ++s) {
@@ -329,6 +345,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
             const int base = __shfl_sync(0xffffffffu, excl + pre, s);
             const int off = base + __popc(b0 & lt) + __popc(b1 & lt);
             const int j = D.col(s, 0);
+            if (io.bm != nullptr && D.lane == 0) {
+              const int cs = D.c0 + s * D.slice + 64 * D.warp;
+              if (cs < D.c1) io.bm[(size_t)r * io.nq + cs / 64] = make_uint4(b0, b1, (unsigned)(myoff + base), 0u);
+            }
             double2* a2 = D.acc2(0, s);
             if (k0) {
               const double v = anc ? P[2 * s] : DK(P[2 * s]);

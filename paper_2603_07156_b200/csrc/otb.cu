@@ -98,6 +98,14 @@ const void* const kDenseFn[DK_COUNT][kMaxNS + 1] = {
      (const void*)k_test_c<7, true>, (const void*)k_test_c<8, true>},
     NS_ROW(k_warm_zeta), NS_ROW(k_warm_gamma)};
 
+#define HV_ROW(K)                                                                                    \
+  {                                                                                                  \
+    (const void*)K<0>, (const void*)K<1>, (const void*)K<2>, (const void*)K<3>, (const void*)K<4>,   \
+        (const void*)K<5>, (const void*)K<6>, (const void*)K<7>, (const void*)K<8>                   \
+  }
+const void* const kHvFn[kHvVariants] = HV_ROW(k_hv_grp);     // variant codes: sparse.cuh HvVar
+const void* const kCgFn[kHvVariants] = HV_ROW(k_cg_fused);
+
 enum ProfClass {
   PC_EVAL = 0, PC_SPARSIFY, PC_HV, PC_CGVEC, PC_TESTA, PC_TESTB, PC_TESTC, PC_WARMZ, PC_WARMG, PC_CGFUSED, PC_N = 16
 };
@@ -117,7 +125,9 @@ struct otb_ctx {
   int nstage[DK_COUNT] = {};
   size_t smem[DK_COUNT] = {};
   // hess_apply
-  int hv_mode = 0, hv_grid = 0, hv_ng = 1;
+  int hv_mode = 0, hv_grid = 0, hv_ng = 1;   // hv_mode 0 group smem, 1 global RED, 2 bitmap
+  int hv_var = 0, nq = 0, hv_threads = 512;   // kernel variant (sparse.cuh HvVar), bitmap words per row
+  uint4* bm = nullptr;
   size_t hv_smem = 0;
   bool cg_fused = false;     // persistent cooperative CG available (1 rank, smem hv)
   int fused_ng = 1;
@@ -351,7 +361,7 @@ int grow_csr(otb_ctx* c, int64_t want) {
   c->vals = nullptr;
   c->cap = 0;
   TRY(dalloc(&c->cols, (size_t)ncap));
-  TRY(dalloc(&c->vals, (size_t)ncap));
+  TRY(dalloc(&c->vals, (size_t)ncap + 16));   // slack: hess_apply reads up to 2 entries past a run
   c->cap = ncap;
   return OTB_OK;
 }
@@ -364,7 +374,8 @@ int do_sparsify(otb_ctx* c, const double* X, const double* gamma, double rho) {
     CUDA_TRY(cudaMemsetAsync(&c->ds->flags, 0, sizeof(int), c->stream));
     Geom geo = make_geom(c, DK_SPARSIFY, c->C, X);
     SparsifyIO io{gamma, c->a, c->eta, rho, anchor_local, c->rowM, c->rowS, c->lse, c->cols, c->vals, c->cap,
-                  c->row_start, c->row_len, &c->ds->alloc, c->chunk, c->colpart, &c->ds->flags};
+                  c->row_start, c->row_len, &c->ds->alloc, c->chunk, c->colpart, &c->ds->flags,
+                  c->hv_mode == 2 ? c->bm : nullptr, c->nq};
     cudaEvent_t e0 = nullptr;
     TRY(prof_begin(c, &e0));
     TRY(launch_dense(c, DK_SPARSIFY, geo, &io));
@@ -410,7 +421,12 @@ Csr csr_view(const otb_ctx* c) {
   return A;
 }
 
-double hv_bytes(const otb_ctx* c) { return 10.0 * c->nnz + 12.0 * c->m_loc + 16.0 * c->n; }
+// Algorithmic bytes of one hess_apply: the values (+ 16-bit
+// columns, or the 16-byte bitmap words), row starts and a_r, v read, y written.
+double hv_bytes(const otb_ctx* c) {
+  if (c->hv_mode == 2) return 8.0 * c->nnz + 16.0 * c->m_loc * c->nq + 16.0 * c->m_loc + 16.0 * c->n;
+  return 10.0 * c->nnz + 12.0 * c->m_loc + 16.0 * c->n;
+}
 
 // y = P_rho^T (a * (P_rho v)) reduced to: (mode smem) colpart[hv_grid][n] or
 // sendbuf (multi-rank), (mode atomic) cg_y or sendbuf.  Returns via
@@ -426,10 +442,12 @@ int run_hv(otb_ctx* c, const double* v_src, const double* r, const double* p_pre
            const CgState* st, HvResult* res) {
   const int n = (int)c->n;
   cudaEvent_t e0 = nullptr;
-  if (c->hv_mode == 0) {
-    HvArgs h{csr_view(c), c->a, n, c->hv_ng, v_src, r, p_prev, p_cur, update, st, c->colpart};
+  if (c->hv_mode != 1) {
+    HvArgs h{csr_view(c), c->a, n, c->hv_ng, v_src, r, p_prev, p_cur, update, st, c->colpart, c->bm, c->nq};
     TRY(prof_begin(c, &e0));
-    k_hv_grp<<<c->hv_grid, 512, c->hv_smem, c->stream>>>(h);
+    void* args[1] = {&h};
+    CUDA_TRY(cudaLaunchKernel(kHvFn[c->hv_var], dim3(c->hv_grid), dim3(c->hv_threads), args, c->hv_smem,
+                              c->stream));
     LAUNCH_CHECK();
     TRY(prof_end(c, PC_HV, e0, hv_bytes(c)));
     if (c->nranks > 1) {
@@ -491,12 +509,13 @@ int do_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t m
     return fail(OTB_ERR_INCONSISTENT, "unshifted system with right-hand side outside the range");
   if (c->cg_fused && c->hcg->status == CG_RUN) {
     // whole CG loop in one cooperative launch (k_cg_fused)
-    CgFusedArgs fa{csr_view(c), c->a, c->d, n, c->fused_ng, c->eta, x, rhs, c->cg_ap, c->colpart, c->scal, c->cg};
+    CgFusedArgs fa{csr_view(c), c->a,     c->d,  n,     c->fused_ng, c->eta, x, rhs, c->cg_ap,
+                   c->colpart,  c->scal, c->cg, c->bm, c->nq};
     void* args[1] = {&fa};
     cudaEvent_t e0 = nullptr;
     TRY(prof_begin(c, &e0));
-    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_cg_fused, dim3(c->hv_grid), dim3(512), args, c->fused_smem,
-                                         c->stream));
+    CUDA_TRY(cudaLaunchCooperativeKernel(kCgFn[c->hv_var], dim3(c->hv_grid), dim3(c->hv_threads), args,
+                                         c->fused_smem, c->stream));
     ++c->launches;
     TRY(prof_end(c, PC_CGFUSED, e0, 0.0));
     CUDA_TRY(cudaMemcpyAsync(c->hcg, c->cg, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
@@ -643,7 +662,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   int cl = 1;
   while (cdiv(n, cl) > 2 * 512 * kMaxNS && cl < kMaxCluster) cl *= 2;
   c->cl = cl;
-  c->colw = (int)rup(cdiv(n, cl), 2);
+  c->colw = (int)rup(cdiv(n, cl), cl > 1 ? 64 : 2);   // cluster windows start on 64-column words
   int ns = (int)std::min<int64_t>(kMaxNS, std::max<int64_t>(1, cdiv(c->colw, 1024)));
   int nt = (int)rup(cdiv(c->colw, 2 * ns), 32);
   const char* env_nt = std::getenv("OTB_DENSE_NT");
@@ -684,7 +703,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   // hess_apply variant: shared-memory group accumulators (NG groups of
   // 512/NG threads, as many as fit) or, for very wide n, global RED.
   const int64_t npad = rup(n, 2);
-  const size_t hv_budget = kMaxDynSmem - 8192;   // static smem of k_cg_fused
+  const size_t hv_budget = kMaxDynSmem - 12288;   // static smem of k_cg_fused (~10.3 KB)
   int ng = 8;
   const char* env_ng = std::getenv("OTB_HV_GROUPS");
   if (env_ng) ng = std::max(1, std::min(16, std::atoi(env_ng)));
@@ -694,22 +713,34 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   const char* env_hv = std::getenv("OTB_HV_MODE");
   c->hv_mode = (c->hv_smem <= hv_budget) ? 0 : 1;
   if (env_hv && std::atoi(env_hv) == 1) c->hv_mode = 1;
-  if (c->hv_mode == 0) {
+  // bitmap hess_apply (sparse.cuh) whenever a thread's columns fit registers
+  const int nwords = (int)rup(cdiv(n, 64), 16);   // words per row, zero past n
+  const char* env_bm = std::getenv("OTB_HV_BITMAP");
+  if (c->hv_mode == 0 && nwords / 16 <= kMaxNQ && !(env_bm && std::atoi(env_bm) == 0)) {
+    c->hv_mode = 2;
+    c->nq = nwords;
+    c->hv_var = nwords / 16;
+    c->hv_ng = 0;
+    c->hv_smem = (size_t)(npad + 16 * 64) * 8 + kBmSmemBytes;
+  }
+  if (c->hv_mode != 1) {
     c->hv_grid = sms;
-    cudaError_t e = allow_max_smem((const void*)k_hv_grp, device);
-    if (e == cudaSuccess) e = allow_max_smem((const void*)k_cg_fused, device);
+    cudaError_t e = allow_max_smem(kHvFn[c->hv_var], device);
+    if (e == cudaSuccess) e = allow_max_smem(kCgFn[c->hv_var], device);
     if (e != cudaSuccess) {
       delete c;
       return fail(OTB_ERR_CUDA, std::string("cudaFuncSetAttribute(hv): ") + cudaGetErrorString(e));
     }
     // the persistent CG keeps p and r in shared memory as well: (2 + NG) rows
-    int fng = ng;
+    int fng = c->hv_ng;
     while (fng > 1 && (size_t)((2 + fng) * npad + 16 * 64) * 8 > hv_budget) fng >>= 1;
     c->fused_ng = fng;
-    c->fused_smem = (size_t)((2 + fng) * npad + 16 * 64) * 8;
+    c->fused_smem =
+        (size_t)((2 + fng) * npad + 16 * 64) * 8 + (c->hv_mode == 2 ? kBmSmemBytes : 0);
     int per_sm_fused = 0;
     if (c->fused_smem <= hv_budget)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fused, (const void*)k_cg_fused, 512, c->fused_smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fused, kCgFn[c->hv_var], c->hv_threads,
+                                                    c->fused_smem);
     const char* env_f = std::getenv("OTB_CG_FUSED");
     c->cg_fused = per_sm_fused >= 1 && !(env_f && std::atoi(env_f) == 0);
   } else {
@@ -730,7 +761,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   A(&c->zrow, m_loc);
   A(&c->er, m_loc);
   A(&c->rowpart, (size_t)m_loc * cl);
-  const int64_t parts = std::max<int64_t>(2 * c->ncl, c->hv_mode == 0 ? c->hv_grid : 1);
+  const int64_t parts = std::max<int64_t>(2 * c->ncl, c->hv_mode != 1 ? c->hv_grid : 1);
   A(&c->colpart, (size_t)parts * n);
   A(&c->vpart, (size_t)std::max(c->grid, c->ncl) * 8 + 8);
   A(&c->sendbuf, nv);
@@ -745,6 +776,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   if (st == OTB_OK) st = dalloc(&c->cta_rb, (size_t)c->hv_grid + 2);
   if (st == OTB_OK) st = dalloc(&c->ds, 1);
   if (st == OTB_OK) st = dalloc(&c->cg, 1);
+  if (st == OTB_OK && c->hv_mode == 2) st = dalloc(&c->bm, (size_t)m_loc * c->nq);
   if (st != OTB_OK) {
     otb_destroy(c);
     return st;
@@ -768,6 +800,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   cudaMemset(c->cg, 0, sizeof(CgState));
   cudaMemset(c->cg_y, 0, sizeof(double) * nv);
   cudaMemset(c->row_len, 0, sizeof(int) * m_loc);
+  if (c->bm) cudaMemset(c->bm, 0, sizeof(uint4) * m_loc * c->nq);
   cudaMemset(c->rowpre, 0, sizeof(int64_t) * (m_loc + 1));
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -787,7 +820,8 @@ int otb_destroy(otb_ctx* c) {
                   (void*)c->rhs, (void*)c->dir, (void*)c->cg_r, (void*)c->cg_p[0], (void*)c->cg_p[1],
                   (void*)c->cg_ap, (void*)c->cg_y, (void*)c->gtrial, (void*)c->yv, (void*)c->ec, (void*)c->Mloc,
                   (void*)c->Mglob, (void*)c->Sloc, (void*)c->row_start, (void*)c->rowpre, (void*)c->row_len,
-                  (void*)c->cols, (void*)c->vals, (void*)c->ds, (void*)c->cg, (void*)c->scal, (void*)c->cta_rb})
+                  (void*)c->cols, (void*)c->vals, (void*)c->ds, (void*)c->cg, (void*)c->scal, (void*)c->cta_rb,
+                  (void*)c->bm})
     if (p) cudaFree(p);
   if (c->hs) cudaFreeHost(c->hs);
   if (c->hcg) cudaFreeHost(c->hcg);

@@ -234,6 +234,170 @@ OTB_DEV void hv_rows(const Csr& A, const double* a, const double* vsm, double* a
   }
 }
 
+// ------------------------------------------------------------ bitmap rows
+// Second index over the same CSR values, written by k_sparsify: per local
+// row, 16*NQ words of 64 columns (zero past n), each a uint4 {b0, b1, off,
+// 0}.  Bit l of b0 (b1) marks column 64q+2l (64q+2l+1) as kept and `off`
+// is the position, relative to the row start, of the word's first kept
+// entry.  Values are in column order, so the entry of column 64q+2l+e sits
+// at off + popc(b0 & lt) + popc(b1 & lt) + (e ? bit l of b0 : 0).
+//
+// hess_apply over it: thread (warp w, lane l) owns the columns
+// 64(w + 16t) + 2l + e (t < NQ, e < 2), so its slices of v and of the
+// accumulator live in registers.  Rows go R at a time: the words, row
+// starts and a_r of the next R rows are staged in shared memory by
+// cp.async while the current ones are processed; every thread issues the
+// loads of all its kept values of the R rows at once (a warp's entries of
+// one word are contiguous, so they coalesce), forms its partial dots, ONE
+// block reduction yields the R row dots, and every thread adds
+// val * a_r * dot_r to its own columns.  No shared-memory scatter, no
+// atomics, rows summed in order (deterministic).  n <= 8192 (NQ <= 8).
+constexpr int kMaxNQ = 8;
+
+// Column ownership: thread (warp w, lane l) of a CTA with W = 16 warps owns
+// the columns 64(w + W t) + 2l + e, t < NQ, e < 2; bitmap rows hold
+// 16 NQ words.
+template <int W>
+OTB_DEV int bm_col(int t, int e) { return 64 * ((threadIdx.x >> 5) + W * t) + 2 * (threadIdx.x & 31) + e; }
+
+OTB_DEV void cp_async(void* dst, const void* src, int bytes, bool ok) {
+  // src-size 0 zero-fills the destination (rows past the CTA's range)
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 16 : 0)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(ok ? 8 : 0)
+                 : "memory");
+}
+OTB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+OTB_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// The lane's two candidate entries of word w: e[0] is the entry of column
+// 2l when it is kept, e[1] (or e[0] if 2l is not kept) that of 2l+1.  The
+// position is always inside the run or its padding (the value buffer has
+// 16 entries of slack), so both loads are issued unconditionally.
+OTB_DEV const double* bm_entry(const double* vr, const uint4& w, unsigned lt) {
+  return vr + ((int)w.z + __popc(w.x & lt) + __popc(w.y & lt));
+}
+// Keep / zero the loaded pair by the word's bits (no FP op on unkept data).
+OTB_DEV void bm_select(const uint4& w, unsigned lb, double& e0, double& e1) {
+  const bool k0 = (w.x & lb) != 0u, k1 = (w.y & lb) != 0u;
+  const double a = e0, b = e1;
+  e0 = k0 ? a : 0.0;
+  e1 = k1 ? (k0 ? b : a) : 0.0;
+}
+
+// ---- one pass, 16 warps: R rows per block reduction
+template <int NQ>
+struct BmCfg {
+  static constexpr int R = NQ <= 4 ? 4 : 2;   // rows per block reduction
+  static constexpr int NQP = 16 * NQ;         // words per row
+};
+constexpr int kBmStageBytes = 256 * 16 + 4 * 16;   // words of R rows, R row starts, R a_r
+constexpr int kBmSmemBytes = 2 * kBmStageBytes;
+
+template <int NQ>
+OTB_DEV void bm_stage(const Csr& A, const uint4* bm, const double* a, int r0, int re, unsigned char* stage) {
+  constexpr int R = BmCfg<NQ>::R, NQP = BmCfg<NQ>::NQP;
+  const int t = threadIdx.x;
+  if (t < R * NQP) {
+    const bool ok = r0 + t / NQP < re;
+    cp_async(reinterpret_cast<uint4*>(stage) + t, ok ? bm + (size_t)r0 * NQP + t : bm, 16, ok);
+  } else if (t >= 256 && t < 256 + R) {
+    const int k = t - 256;
+    const bool ok = r0 + k < re;
+    cp_async(stage + 256 * 16 + 8 * k, ok ? A.row_start + r0 + k : A.row_start, 8, ok);
+  } else if (t >= 288 && t < 288 + R) {
+    const int k = t - 288;
+    const bool ok = r0 + k < re;
+    cp_async(stage + 256 * 16 + 32 + 8 * k, ok ? a + A.row0 + r0 + k : a, 8, ok);
+  }
+  cp_async_commit();
+}
+
+template <int NQ>
+OTB_DEV void hv_bitmap_rows(const Csr& A, const uint4* __restrict__ bm, const double* __restrict__ a,
+                            const double (&v)[2 * NQ], double (&acc)[2 * NQ], int rb, int re, double* slots,
+                            unsigned char* ring) {
+  constexpr int R = BmCfg<NQ>::R, NQP = BmCfg<NQ>::NQP;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lb = 1u << lane, lt = lb - 1u;
+  int phase = 0, buf = 0;
+  if (rb < re) bm_stage<NQ>(A, bm, a, rb, re, ring);
+  cp_async_wait_all();
+  __syncthreads();
+  for (int r0 = rb; r0 < re; r0 += R, buf ^= 1) {
+    if (r0 + R < re) bm_stage<NQ>(A, bm, a, r0 + R, re, ring + (buf ^ 1) * kBmStageBytes);
+    const unsigned char* cur = ring + buf * kBmStageBytes;
+    const uint4* wsm = reinterpret_cast<const uint4*>(cur);
+    const int64_t* rsm = reinterpret_cast<const int64_t*>(cur + 256 * 16);
+    const double* asm_ = reinterpret_cast<const double*>(cur + 256 * 16 + 32);
+    double val[R][2 * NQ];
+    double dot[R], ar[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const double* vr = A.vals + rsm[k];
+      ar[k] = asm_[k];
+#pragma unroll
+      for (int t = 0; t < NQ; ++t) {
+        const double* e = bm_entry(vr, wsm[k * NQP + warp + 16 * t], lt);
+        val[k][2 * t] = __ldg(e);
+        val[k][2 * t + 1] = __ldg(e + 1);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      dot[k] = 0.0;
+#pragma unroll
+      for (int t = 0; t < NQ; ++t) {
+        bm_select(wsm[k * NQP + warp + 16 * t], lb, val[k][2 * t], val[k][2 * t + 1]);
+        dot[k] = fma(val[k][2 * t], v[2 * t], dot[k]);
+        dot[k] = fma(val[k][2 * t + 1], v[2 * t + 1], dot[k]);
+      }
+    }
+    cp_async_wait_all();   // next stage lands before the barrier below publishes it
+    block_sum_split<R>(dot, slots, phase, blockDim.x);
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      const double w = ar[k] * dot[k];   // sparsify.py:153: weights * pv
+#pragma unroll
+      for (int i = 0; i < 2 * NQ; ++i) acc[i] = fma(val[k][i], w, acc[i]);
+    }
+  }
+}
+
+// Variant code of the hess_apply kernels: 0 group smem accumulators,
+// 1..8 bitmap with NQ = V words per warp.
+constexpr int kHvVariants = kMaxNQ + 1;
+template <int V>
+struct HvVar {
+  static constexpr bool kBitmap = V > 0;
+  static constexpr int NQ = V > 0 ? V : 1;
+  static constexpr int W = 16;
+  static constexpr int kThreads = 512;
+};
+
+// Partial row of y = P^T (a * (P v)) over this CTA's rows, bitmap variants:
+// v read from shared memory (vsm), result to dst (its own columns).
+template <int V>
+OTB_DEV void hv_bitmap_partial(const Csr& A, const uint4* bm, const double* a, const double* vsm, int n, int rb,
+                               int re, double* slots, unsigned char* scratch, double* dst) {
+  constexpr int NQ = HvVar<V>::NQ, W = HvVar<V>::W;
+  double vr[2 * NQ], ar[2 * NQ];
+#pragma unroll
+  for (int i = 0; i < 2 * NQ; ++i) {
+    const int j = bm_col<W>(i >> 1, i & 1);
+    vr[i] = (j < n) ? vsm[j] : 0.0;
+    ar[i] = 0.0;
+  }
+  hv_bitmap_rows<NQ>(A, bm, a, vr, ar, rb, re, slots, scratch);
+#pragma unroll
+  for (int i = 0; i < 2 * NQ; ++i) {
+    const int j = bm_col<W>(i >> 1, i & 1);
+    if (j < n) dst[j] = ar[i];
+  }
+}
+
 // Shared-memory layout of the group hv: v[npad] | acc[NG][npad] | slots.
 OTB_DEV size_t hv_smem_doubles(int npad, int NG) { return (size_t)npad * (1 + NG) + 16 * 64; }
 
@@ -249,10 +413,13 @@ struct HvArgs {
   int update;
   const CgState* st;       // nullptr: standalone product
   double* colpart;         // [gridDim][n]
+  const uint4* bm;         // bitmap index (NQ > 0)
+  int nq;
 };
 
 // Standalone hess_apply partials (multi-rank CG iterations, otb_hess_apply).
-__global__ void __launch_bounds__(512, 1) k_hv_grp(HvArgs h) {
+template <int V>
+__global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_hv_grp(HvArgs h) {
   extern __shared__ __align__(16) double hsm[];
   if (h.st != nullptr && h.st->status != CG_RUN) return;
   const int n = h.n, npad = (n + 1) & ~1, NG = h.ng;
@@ -272,17 +439,23 @@ __global__ void __launch_bounds__(512, 1) k_hv_grp(HvArgs h) {
     }
     vsm[j] = v;
   }
-  for (int j = threadIdx.x; j < npad * NG; j += blockDim.x) acc[j] = 0.0;
-  __syncthreads();
   int rb, re;
   cta_rows(h.A, blockIdx.x, gridDim.x, rb, re);
-  hv_rows(h.A, h.a, vsm, acc, npad, rb, re, NG, gslots);
-  __syncthreads();
   double* dst = h.colpart + (size_t)blockIdx.x * n;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    double t = acc[j];
-    for (int g = 1; g < NG; ++g) t += acc[(size_t)g * npad + j];
-    dst[j] = t;
+  if constexpr (HvVar<V>::kBitmap) {
+    __syncthreads();
+    hv_bitmap_partial<V>(h.A, h.bm, h.a, vsm, n, rb, re, gslots, reinterpret_cast<unsigned char*>(gslots + 16 * 64),
+                        dst);
+  } else {
+    for (int j = threadIdx.x; j < npad * NG; j += blockDim.x) acc[j] = 0.0;
+    __syncthreads();
+    hv_rows(h.A, h.a, vsm, acc, npad, rb, re, NG, gslots);
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      double t = acc[j];
+      for (int g = 1; g < NG; ++g) t += acc[(size_t)g * npad + j];
+      dst[j] = t;
+    }
   }
 }
 
@@ -501,12 +674,15 @@ struct CgFusedArgs {
   double* colpart;   // [gridDim][n]
   double* scal;      // [gridDim]
   CgState* st;
+  const uint4* bm;   // bitmap index (NQ > 0)
+  int nq;
 };
 
 // Shared memory of k_cg_fused: p[npad] | r[npad] | acc[NG][npad] | slots.
 OTB_DEV size_t cg_fused_smem_doubles(int npad, int NG) { return (size_t)npad * (2 + NG) + 16 * 64; }
 
-__global__ void __launch_bounds__(512, 1) k_cg_fused(CgFusedArgs c) {
+template <int V>
+__global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_cg_fused(CgFusedArgs c) {
   namespace cgrp = cooperative_groups;
   extern __shared__ __align__(16) double hsm[];
   __shared__ double red[16 * 32];
@@ -534,17 +710,23 @@ __global__ void __launch_bounds__(512, 1) k_cg_fused(CgFusedArgs c) {
     psm[j] = v;
     rsm[j] = v;
   }
+  __syncthreads();
   for (;;) {
     // ---- phase 1: the hess_apply partial row of this CTA
-    for (int j = tid; j < npad * NG; j += nth) acc[j] = 0.0;
-    __syncthreads();
-    hv_rows(c.A, c.a, psm, acc, npad, rb, re, NG, gslots);
-    __syncthreads();
     double* dst = c.colpart + (size_t)b * n;
-    for (int j = tid; j < n; j += nth) {
-      double t = acc[j];
-      for (int g = 1; g < NG; ++g) t += acc[(size_t)g * npad + j];
-      dst[j] = t;
+    if constexpr (HvVar<V>::kBitmap) {
+      hv_bitmap_partial<V>(c.A, c.bm, c.a, psm, n, rb, re, gslots,
+                          reinterpret_cast<unsigned char*>(gslots + 16 * 64), dst);
+    } else {
+      for (int j = tid; j < npad * NG; j += nth) acc[j] = 0.0;
+      __syncthreads();
+      hv_rows(c.A, c.a, psm, acc, npad, rb, re, NG, gslots);
+      __syncthreads();
+      for (int j = tid; j < n; j += nth) {
+        double t = acc[j];
+        for (int g = 1; g < NG; ++g) t += acc[(size_t)g * npad + j];
+        dst[j] = t;
+      }
     }
     grid.sync();
     // ---- phase 2: column slice of ap, curvature partial
