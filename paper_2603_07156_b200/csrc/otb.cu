@@ -332,7 +332,7 @@ int do_eval(otb_ctx* c, const double* X, const double* gamma) {
   cudaEvent_t e0 = nullptr;
   TRY(prof_begin(c, &e0));
   TRY(launch_dense(c, DK_EVAL, geo, &io));
-  TRY(prof_end(c, PC_EVAL, e0, 16.0 * c->m_loc * n + 24.0 * c->m_loc + 16.0 * n));
+  TRY(prof_end(c, PC_EVAL, e0, 16.0 * c->m_loc * n + 8.0 * c->m_loc + 24.0 * n));
   TRY(colreduce(c, c->ncl, c->vpart, c->ncl, 2, 2));
   TRY(allreduce(c, c->sendbuf, (size_t)n + 2, kNcclSum));
   k_eval_post<<<c->colgrid, 256, 0, c->stream>>>(n, c->sendbuf, c->b, gamma, c->eta, c->g, c->ds, c->bpart);
@@ -385,7 +385,7 @@ int do_sparsify(otb_ctx* c, const double* X, const double* gamma, double rho) {
     TRY(sync_scalars(c));
     int64_t nnz;
     std::memcpy(&nnz, c->hbuf, sizeof(int64_t));
-    TRY(prof_end(c, PC_SPARSIFY, e0, 16.0 * c->m_loc * n + 10.0 * nnz + 12.0 * c->m_loc));
+    TRY(prof_end(c, PC_SPARSIFY, e0, 16.0 * c->m_loc * n + 12.0 * nnz + 8.0 * (c->m_loc + 1)));
     if (c->hs->flags & 2) {
       const int64_t need = (int64_t)c->hs->alloc + (int64_t)c->ncl * c->chunk;
       TRY(grow_csr(c, need + need / 8));
@@ -421,12 +421,10 @@ Csr csr_view(const otb_ctx* c) {
   return A;
 }
 
-// Algorithmic bytes of one hess_apply: the values (+ 16-bit
-// columns, or the 16-byte bitmap words), row starts and a_r, v read, y written.
-double hv_bytes(const otb_ctx* c) {
-  if (c->hv_mode == 2) return 8.0 * c->nnz + 16.0 * c->m_loc * c->nq + 16.0 * c->m_loc + 16.0 * c->n;
-  return 10.0 * c->nnz + 12.0 * c->m_loc + 16.0 * c->n;
-}
+// Algorithmic bytes of one hess_apply, SURVEY §8(d) / DESIGN.md: CSR with
+// int32 columns, 12 nnz + 8 (m + 1) + 16 n, whatever the stored format
+// (the bitmap index moves 8 nnz + m nq 16 bytes; ncu traffic shows it).
+double hv_bytes(const otb_ctx* c) { return 12.0 * c->nnz + 8.0 * (c->m_loc + 1) + 16.0 * c->n; }
 
 // y = P_rho^T (a * (P_rho v)) reduced to: (mode smem) colpart[hv_grid][n] or
 // sendbuf (multi-rank), (mode atomic) cg_y or sendbuf.  Returns via
@@ -521,7 +519,7 @@ int do_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t m
     CUDA_TRY(cudaMemcpyAsync(c->hcg, c->cg, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (c->prof && !c->recs.empty())
-      c->recs.back().bytes = (double)c->hcg->iters * (hv_bytes(c) + 72.0 * n);
+      c->recs.back().bytes = (double)c->hcg->iters * hv_bytes(c);
   }
   int64_t k = 0;
   while (c->hcg->status == CG_RUN) {
