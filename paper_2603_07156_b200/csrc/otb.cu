@@ -101,7 +101,8 @@ const void* const kDenseFn[DK_COUNT][kMaxNS + 1] = {
 #define HV_ROW(K)                                                                                    \
   {                                                                                                  \
     (const void*)K<0>, (const void*)K<1>, (const void*)K<2>, (const void*)K<3>, (const void*)K<4>,   \
-        (const void*)K<5>, (const void*)K<6>, (const void*)K<7>, (const void*)K<8>                   \
+        (const void*)K<5>, (const void*)K<6>, (const void*)K<7>, (const void*)K<8>, (const void*)K<9>, \
+        (const void*)K<10>, (const void*)K<11>, (const void*)K<12>                                   \
   }
 const void* const kHvFn[kHvVariants] = HV_ROW(k_hv_grp);     // variant codes: sparse.cuh HvVar
 const void* const kCgFn[kHvVariants] = HV_ROW(k_cg_fused);
@@ -125,7 +126,8 @@ struct otb_ctx {
   int nstage[DK_COUNT] = {};
   size_t smem[DK_COUNT] = {};
   // hess_apply
-  int hv_mode = 0, hv_grid = 0, hv_ng = 1;   // hv_mode 0 group smem, 1 global RED, 2 bitmap
+  int hv_mode = 0, hv_grid = 0, hv_ng = 1;   // hv_mode 0 group smem, 1 global RED, 2 bitmap, 3 window clusters
+  int hv_nb = 0, hv_win = 1;                   // row blocks (partial rows), CTAs per cluster (mode 3)
   int hv_var = 0, nq = 0, hv_threads = 512;   // kernel variant (sparse.cuh HvVar), bitmap words per row
   uint4* bm = nullptr;
   size_t hv_smem = 0;
@@ -375,7 +377,7 @@ int do_sparsify(otb_ctx* c, const double* X, const double* gamma, double rho) {
     Geom geo = make_geom(c, DK_SPARSIFY, c->C, X);
     SparsifyIO io{gamma, c->a, c->eta, rho, anchor_local, c->rowM, c->rowS, c->lse, c->cols, c->vals, c->cap,
                   c->row_start, c->row_len, &c->ds->alloc, c->chunk, c->colpart, &c->ds->flags,
-                  c->hv_mode == 2 ? c->bm : nullptr, c->nq};
+                  (c->hv_mode == 2 || c->hv_mode == 3) ? c->bm : nullptr, c->nq};
     cudaEvent_t e0 = nullptr;
     TRY(prof_begin(c, &e0));
     TRY(launch_dense(c, DK_SPARSIFY, geo, &io));
@@ -396,7 +398,7 @@ int do_sparsify(otb_ctx* c, const double* X, const double* gamma, double rho) {
       // nnz-balanced row bounds of the hess_apply CTAs, once per sparsify
       Csr A = csr_view(c);
       A.cta_rb = nullptr;
-      k_cta_bounds<<<(int)cdiv(c->hv_grid + 1, 256), 256, 0, c->stream>>>(A, c->hv_grid, c->cta_rb);
+      k_cta_bounds<<<(int)cdiv(c->hv_nb + 1, 256), 256, 0, c->stream>>>(A, c->hv_nb, c->cta_rb);
       LAUNCH_CHECK();
     }
     TRY(colreduce(c, c->ncl, nullptr, 0, 0, 0));
@@ -441,19 +443,36 @@ int run_hv(otb_ctx* c, const double* v_src, const double* r, const double* p_pre
   const int n = (int)c->n;
   cudaEvent_t e0 = nullptr;
   if (c->hv_mode != 1) {
-    HvArgs h{csr_view(c), c->a, n, c->hv_ng, v_src, r, p_prev, p_cur, update, st, c->colpart, c->bm, c->nq};
+    HvArgs h{csr_view(c), c->a, n, c->hv_ng, v_src, r, p_prev, p_cur, update, st, c->colpart, c->bm, c->nq,
+             c->hv_win};
     TRY(prof_begin(c, &e0));
     void* args[1] = {&h};
-    CUDA_TRY(cudaLaunchKernel(kHvFn[c->hv_var], dim3(c->hv_grid), dim3(c->hv_threads), args, c->hv_smem,
-                              c->stream));
+    if (c->hv_mode == 3) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(c->hv_grid);
+      cfg.blockDim = dim3(kStThreads);
+      cfg.dynamicSmemBytes = kWcSmemBytes;
+      cfg.stream = c->stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = (unsigned)c->hv_win;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      CUDA_TRY(cudaLaunchKernelExC(&cfg, (const void*)k_hv_wc, args));
+    } else {
+      CUDA_TRY(cudaLaunchKernel(kHvFn[c->hv_var], dim3(c->hv_grid), dim3(c->hv_threads), args, c->hv_smem,
+                                c->stream));
+    }
     LAUNCH_CHECK();
     TRY(prof_end(c, PC_HV, e0, hv_bytes(c)));
     if (c->nranks > 1) {
-      TRY(colreduce(c, c->hv_grid, nullptr, 0, 0, 0));
+      TRY(colreduce(c, c->hv_nb, nullptr, 0, 0, 0));
       TRY(allreduce(c, c->sendbuf, (size_t)n, kNcclSum));
       *res = {nullptr, 0, nullptr, c->sendbuf};
     } else {
-      *res = {c->colpart, c->hv_grid, nullptr, nullptr};
+      *res = {c->colpart, c->hv_nb, nullptr, nullptr};
     }
   } else {
     const double* v = update ? p_cur : v_src;
@@ -714,15 +733,59 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   // bitmap hess_apply (sparse.cuh) whenever a thread's columns fit registers
   const int nwords = (int)rup(cdiv(n, 64), 16);   // words per row, zero past n
   const char* env_bm = std::getenv("OTB_HV_BITMAP");
+  const char* env_st = std::getenv("OTB_HV_STAGED");
   if (c->hv_mode == 0 && nwords / 16 <= kMaxNQ && !(env_bm && std::atoi(env_bm) == 0)) {
     c->hv_mode = 2;
     c->nq = nwords;
     c->hv_var = nwords / 16;
     c->hv_ng = 0;
     c->hv_smem = (size_t)(npad + 16 * 64) * 8 + kBmSmemBytes;
+    if (nwords <= 64 && env_st && std::atoi(env_st) == 1) {   // n <= 4096: TMA-staged values (opt-in)
+      c->hv_var = 8 + nwords / 16;
+      c->hv_threads = kStThreads;
+      c->hv_smem = (size_t)(npad + 16 * 64) * 8 + 2 * (size_t)kStBytes + 32;
+    }
   }
-  if (c->hv_mode != 1) {
+  // n > 8192 and too wide for the group accumulators (hv_mode 1): window
+  // clusters of W = ceil(n / 4096) CTAs (bitmap words per row = 64 W), when
+  // the device runs such a cluster (OTB_HV_WC=1 forces them for any n > 8192)
+  const int nwin = (int)cdiv(n, kWinCols);
+  const char* env_wc = std::getenv("OTB_HV_WC");
+  const bool want_wc = (c->hv_mode == 1 || (env_wc && std::atoi(env_wc) == 1)) && c->hv_mode != 2;
+  if (want_wc && nwin >= 2 && nwin <= 16 && !(env_bm && std::atoi(env_bm) == 0) &&
+      !(env_wc && std::atoi(env_wc) == 0) && !(env_hv && std::atoi(env_hv) == 1)) {
+    cudaError_t e = allow_max_smem((const void*)k_hv_wc, device);
+    if (e == cudaSuccess && nwin > 8)
+      e = cudaFuncSetAttribute((const void*)k_hv_wc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    int nclusters = 0;
+    if (e == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(nwin * (sms / nwin)));
+      cfg.blockDim = dim3(kStThreads);
+      cfg.dynamicSmemBytes = kWcSmemBytes;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = (unsigned)nwin;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      e = cudaOccupancyMaxActiveClusters(&nclusters, (const void*)k_hv_wc, &cfg);
+    }
+    cudaGetLastError();
+    if (e == cudaSuccess && nclusters >= 1) {
+      c->hv_mode = 3;
+      c->hv_win = nwin;
+      c->nq = 64 * nwin;
+      c->hv_ng = 0;
+      c->hv_smem = kWcSmemBytes;
+      c->hv_nb = std::min(nclusters, sms / nwin);
+      c->hv_grid = c->hv_nb * nwin;
+    }
+  }
+  if (c->hv_mode == 0 || c->hv_mode == 2) {
     c->hv_grid = sms;
+    c->hv_nb = sms;
     cudaError_t e = allow_max_smem(kHvFn[c->hv_var], device);
     if (e == cudaSuccess) e = allow_max_smem(kCgFn[c->hv_var], device);
     if (e != cudaSuccess) {
@@ -733,16 +796,17 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
     int fng = c->hv_ng;
     while (fng > 1 && (size_t)((2 + fng) * npad + 16 * 64) * 8 > hv_budget) fng >>= 1;
     c->fused_ng = fng;
-    c->fused_smem =
-        (size_t)((2 + fng) * npad + 16 * 64) * 8 + (c->hv_mode == 2 ? kBmSmemBytes : 0);
+    c->fused_smem = (size_t)((2 + fng) * npad + 16 * 64) * 8 +
+                    (c->hv_var > kMaxNQ ? 2 * (size_t)kStBytes + 32 : (c->hv_mode == 2 ? kBmSmemBytes : 0));
     int per_sm_fused = 0;
     if (c->fused_smem <= hv_budget)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fused, kCgFn[c->hv_var], c->hv_threads,
                                                     c->fused_smem);
     const char* env_f = std::getenv("OTB_CG_FUSED");
     c->cg_fused = per_sm_fused >= 1 && !(env_f && std::atoi(env_f) == 0);
-  } else {
+  } else if (c->hv_mode == 1) {
     c->hv_grid = sms * 8;
+    c->hv_nb = 1;
   }
   c->colgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 2 * sms));
   c->col32 = (int)cdiv(n, 32);
@@ -759,7 +823,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   A(&c->zrow, m_loc);
   A(&c->er, m_loc);
   A(&c->rowpart, (size_t)m_loc * cl);
-  const int64_t parts = std::max<int64_t>(2 * c->ncl, c->hv_mode != 1 ? c->hv_grid : 1);
+  const int64_t parts = std::max<int64_t>(2 * c->ncl, c->hv_nb);
   A(&c->colpart, (size_t)parts * n);
   A(&c->vpart, (size_t)std::max(c->grid, c->ncl) * 8 + 8);
   A(&c->sendbuf, nv);
@@ -774,7 +838,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   if (st == OTB_OK) st = dalloc(&c->cta_rb, (size_t)c->hv_grid + 2);
   if (st == OTB_OK) st = dalloc(&c->ds, 1);
   if (st == OTB_OK) st = dalloc(&c->cg, 1);
-  if (st == OTB_OK && c->hv_mode == 2) st = dalloc(&c->bm, (size_t)m_loc * c->nq);
+  if (st == OTB_OK && (c->hv_mode == 2 || c->hv_mode == 3)) st = dalloc(&c->bm, (size_t)m_loc * c->nq);
   if (st != OTB_OK) {
     otb_destroy(c);
     return st;

@@ -296,13 +296,17 @@ struct BmCfg {
 constexpr int kBmStageBytes = 256 * 16 + 4 * 16;   // words of R rows, R row starts, R a_r
 constexpr int kBmSmemBytes = 2 * kBmStageBytes;
 
+// Words [woff, woff + NQP) of rows r0..r0+R-1 (row stride `stride` words).
 template <int NQ>
-OTB_DEV void bm_stage(const Csr& A, const uint4* bm, const double* a, int r0, int re, unsigned char* stage) {
+OTB_DEV void bm_stage(const Csr& A, const uint4* bm, const double* a, int r0, int re, unsigned char* stage,
+                      int stride, int woff) {
   constexpr int R = BmCfg<NQ>::R, NQP = BmCfg<NQ>::NQP;
   const int t = threadIdx.x;
   if (t < R * NQP) {
-    const bool ok = r0 + t / NQP < re;
-    cp_async(reinterpret_cast<uint4*>(stage) + t, ok ? bm + (size_t)r0 * NQP + t : bm, 16, ok);
+    const int k = t / NQP;
+    const bool ok = r0 + k < re;
+    cp_async(reinterpret_cast<uint4*>(stage) + t, ok ? bm + (size_t)(r0 + k) * stride + woff + (t - k * NQP) : bm,
+             16, ok);
   } else if (t >= 256 && t < 256 + R) {
     const int k = t - 256;
     const bool ok = r0 + k < re;
@@ -315,19 +319,57 @@ OTB_DEV void bm_stage(const Csr& A, const uint4* bm, const double* a, int r0, in
   cp_async_commit();
 }
 
-template <int NQ>
+// Row dots split over the column windows of a thread-block cluster: each
+// CTA's partial dots of a batch go to every CTA of the cluster through DSMEM
+// (remote stores + a release arrive on the peer's mbarrier), and every CTA
+// adds the W partials in window order, so all windows apply the same dots.
+// Two buffers/barriers alternate between batches.
+struct ClusterDots {
+  double* xbuf;     // [2][16][4]
+  uint64_t* xbar;   // [2], initialised with W arrivals
+  int W, cr, count;
+  int nthreads;     // threads taking part (the consumer warps)
+
+  template <int R>
+  OTB_DEV void exchange(double (&v)[R]) {
+    const int q = count & 1;
+    const uint32_t par = (uint32_t)((count >> 1) & 1);
+    double* base = xbuf + q * 16 * 4;
+    if (threadIdx.x == 0) {
+      for (int rk = 0; rk < W; ++rk) {
+        const uint32_t dst = mapa(smem_u32(base + cr * 4), (uint32_t)rk);
+#pragma unroll
+        for (int k = 0; k < R; ++k) st_cluster_f64(dst + 8u * k, v[k]);
+        mbar_arrive_remote(mapa(smem_u32(&xbar[q]), (uint32_t)rk));
+      }
+      while (!mbar_try_wait_cluster(&xbar[q], par)) {
+      }
+    }
+    bar_sync(1, nthreads);
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      double t = 0.0;
+      for (int rk = 0; rk < W; ++rk) t += base[rk * 4 + k];
+      v[k] = t;
+    }
+    ++count;
+  }
+};
+
+template <int NQ, bool CL = false>
 OTB_DEV void hv_bitmap_rows(const Csr& A, const uint4* __restrict__ bm, const double* __restrict__ a,
                             const double (&v)[2 * NQ], double (&acc)[2 * NQ], int rb, int re, double* slots,
-                            unsigned char* ring) {
+                            unsigned char* ring, int stride = BmCfg<NQ>::NQP, int woff = 0,
+                            ClusterDots* cx = nullptr) {
   constexpr int R = BmCfg<NQ>::R, NQP = BmCfg<NQ>::NQP;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lb = 1u << lane, lt = lb - 1u;
   int phase = 0, buf = 0;
-  if (rb < re) bm_stage<NQ>(A, bm, a, rb, re, ring);
+  if (rb < re) bm_stage<NQ>(A, bm, a, rb, re, ring, stride, woff);
   cp_async_wait_all();
   __syncthreads();
   for (int r0 = rb; r0 < re; r0 += R, buf ^= 1) {
-    if (r0 + R < re) bm_stage<NQ>(A, bm, a, r0 + R, re, ring + (buf ^ 1) * kBmStageBytes);
+    if (r0 + R < re) bm_stage<NQ>(A, bm, a, r0 + R, re, ring + (buf ^ 1) * kBmStageBytes, stride, woff);
     const unsigned char* cur = ring + buf * kBmStageBytes;
     const uint4* wsm = reinterpret_cast<const uint4*>(cur);
     const int64_t* rsm = reinterpret_cast<const int64_t*>(cur + 256 * 16);
@@ -357,6 +399,7 @@ OTB_DEV void hv_bitmap_rows(const Csr& A, const uint4* __restrict__ bm, const do
     }
     cp_async_wait_all();   // next stage lands before the barrier below publishes it
     block_sum_split<R>(dot, slots, phase, blockDim.x);
+    if constexpr (CL) cx->exchange<R>(dot);
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       const double w = ar[k] * dot[k];   // sparsify.py:153: weights * pv
@@ -366,15 +409,205 @@ OTB_DEV void hv_bitmap_rows(const Csr& A, const uint4* __restrict__ bm, const do
   }
 }
 
+// ---- staged variant: values and words brought in by TMA
+// One producer lane streams, for each batch of kStR rows, the row's run of
+// values (or, in a cluster, the segment of this CTA's 4096-column window)
+// and its bitmap words into a ring of shared-memory stages with 1-D bulk
+// copies (cp.async.bulk, completion on the stage's mbarrier).  The 512
+// consumer threads never touch global memory inside the row loop: offsets
+// from the staged words, values from the staged run, select, dot, one
+// split-shuffle block reduction (+ the cluster exchange), update of the
+// owned columns.  The next stages are in flight meanwhile.
+constexpr int kStR = 2;                      // rows per batch
+constexpr int kStWords = 64;                 // staged words per row (one 4096-column window)
+constexpr int kStRowVals = 4096 + 8;         // staged values per row (window + alignment slack)
+constexpr int kStHdrBytes = 128;
+constexpr int kStBytes = kStR * kStWords * 16 + kStHdrBytes + kStR * kStRowVals * 8;
+constexpr int kStConsumers = 512;
+constexpr int kStThreads = kStConsumers + 32;   // + one producer warp
+
+struct StHdr {
+  int base[kStR];     // stage index of the row's entry 0 (row-relative offsets add to it)
+  int count;          // valid rows in the batch
+  int pad;
+  double ar[kStR];    // a_r
+};
+
+struct StRing {
+  unsigned char* mem;
+  uint64_t* full;
+  uint64_t* empty;
+  int S;
+  int stage;
+  uint32_t phase;
+  OTB_DEV unsigned char* at(int s) const { return mem + (size_t)s * kStBytes; }
+  OTB_DEV void advance() {
+    if (++stage == S) {
+      stage = 0;
+      phase ^= 1u;
+    }
+  }
+};
+
+OTB_DEV size_t st_smem_bytes(int S) { return (size_t)S * kStBytes + 2 * (size_t)S * 8; }
+
+// Carve a ring of S stages at `p` (16-byte aligned); thread 0 initialises
+// the barriers (the caller synchronises before use).
+OTB_DEV StRing st_ring(unsigned char* p, int S) {
+  StRing rg;
+  rg.mem = p;
+  rg.full = reinterpret_cast<uint64_t*>(p + (size_t)S * kStBytes);
+  rg.empty = rg.full + S;
+  rg.S = S;
+  rg.stage = 0;
+  rg.phase = 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&rg.full[s], 1);
+      mbar_init(&rg.empty[s], kStConsumers);
+    }
+    fence_mbar_init();
+  }
+  return rg;
+}
+
+// Producer (the whole producer warp): batches of rows [rb, re).  NQP words
+// per row are staged from word `woff` of each row (row stride `stride`
+// words); the value segment is the row's whole run (last_window with
+// woff == 0), or the entries of this window: from word woff's `off` to the
+// next window's first word's `off` (the row length for the last window).
+// The row metadata of 32 rows is fetched at once, one row per lane, so the
+// per-batch work of lane 0 is a barrier wait and the bulk-copy issue.
+OTB_DEV void st_produce(const Csr& A, const uint4* bm, const double* a, int rb, int re, int stride, int woff, int nqp,
+                        bool last_window, StRing& rg) {
+  const int lane = threadIdx.x & 31;
+  for (int g0 = rb; g0 < re; g0 += 32) {
+    const int r = g0 + lane;
+    int64_t a0 = 0;
+    int cnt = 0, off = 0;
+    double ar = 0.0;
+    if (r < re) {
+      const int64_t st = A.row_start[r];
+      const int fo = (woff > 0) ? (int)bm[(size_t)r * stride + woff].z : 0;
+      const int lo = last_window ? A.row_len[r] : (int)bm[(size_t)r * stride + woff + nqp].z;
+      a0 = (st + fo) & ~(int64_t)1;                        // 16-byte aligned source
+      cnt = (int)(((st + lo + 1) & ~(int64_t)1) - a0);
+      off = (int)(st - a0);
+      ar = a[A.row0 + r];
+    }
+    const int rows = min(32, re - g0);
+    for (int k0 = 0; k0 < rows; k0 += kStR) {
+      int64_t ka0[kStR];
+      int kcnt[kStR], koff[kStR];
+      double kar[kStR];
+#pragma unroll
+      for (int k = 0; k < kStR; ++k) {
+        ka0[k] = __shfl_sync(0xffffffffu, a0, k0 + k);
+        kcnt[k] = __shfl_sync(0xffffffffu, cnt, k0 + k);
+        koff[k] = __shfl_sync(0xffffffffu, off, k0 + k);
+        kar[k] = __shfl_sync(0xffffffffu, ar, k0 + k);
+      }
+      if (lane == 0) {
+        mbar_wait(&rg.empty[rg.stage], rg.phase ^ 1u);
+        unsigned char* sp = rg.at(rg.stage);
+        StHdr* h = reinterpret_cast<StHdr*>(sp + kStR * kStWords * 16);
+        double* vdst = reinterpret_cast<double*>(sp + kStR * kStWords * 16 + kStHdrBytes);
+        uint32_t bytes = 0;
+        int count = 0;
+#pragma unroll
+        for (int k = 0; k < kStR; ++k) {
+          const bool ok = k0 + k < rows;
+          h->base[k] = koff[k] + k * kStRowVals;
+          h->ar[k] = kar[k];
+          if (ok) {
+            bytes += (uint32_t)kcnt[k] * 8u + (uint32_t)nqp * 16u;
+            ++count;
+          }
+        }
+        h->count = count;
+        mbar_arrive_expect_tx(&rg.full[rg.stage], bytes);
+#pragma unroll
+        for (int k = 0; k < kStR; ++k) {
+          if (k0 + k < rows) {
+            if (kcnt[k] > 0)
+              bulk_g2s(vdst + k * kStRowVals, A.vals + ka0[k], (uint32_t)kcnt[k] * 8u, &rg.full[rg.stage]);
+            bulk_g2s(sp + k * kStWords * 16, bm + (size_t)(g0 + k0 + k) * stride + woff, (uint32_t)nqp * 16u,
+                     &rg.full[rg.stage]);
+          }
+        }
+      }
+      rg.advance();
+    }
+  }
+}
+
+// Consumers (512 threads): the same batches.  Column 2l keeps e0, column
+// 2l+1 keeps e1 (e0 when 2l is not kept); columns that are not kept carry
+// 0, and fma(0, x, s) == s for finite x.
+template <int NQ, bool CL>
+OTB_DEV void st_consume(int rb, int re, const double (&v)[2 * NQ], double (&acc)[2 * NQ], double* slots, StRing& rg,
+                        ClusterDots* cx) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lb = 1u << lane, lt = lb - 1u;
+  int rphase = 0;
+  for (int r0 = rb; r0 < re; r0 += kStR) {
+    mbar_wait(&rg.full[rg.stage], rg.phase);
+    const unsigned char* sp = rg.at(rg.stage);
+    const uint4* words = reinterpret_cast<const uint4*>(sp);
+    const StHdr* h = reinterpret_cast<const StHdr*>(sp + kStR * kStWords * 16);
+    const double* vals = reinterpret_cast<const double*>(sp + kStR * kStWords * 16 + kStHdrBytes);
+    const int count = h->count;
+    double val[kStR][2 * NQ];
+    double dot[kStR], ar[kStR];
+#pragma unroll
+    for (int k = 0; k < kStR; ++k) {
+      dot[k] = 0.0;
+      ar[k] = 0.0;
+#pragma unroll
+      for (int i = 0; i < 2 * NQ; ++i) val[k][i] = 0.0;
+      if (k < count) {
+        const int base = h->base[k];
+        ar[k] = h->ar[k];
+#pragma unroll
+        for (int t = 0; t < NQ; ++t) {
+          const uint4 w = words[k * kStWords + warp + 16 * t];
+          // words past n are zero (off 0 lies before a later window's segment):
+          // keep the address inside the row's stage slot; their masks are 0
+          const int idx = min(max(base + (int)w.z + __popc(w.x & lt) + __popc(w.y & lt), k * kStRowVals),
+                              (k + 1) * kStRowVals - 2);
+          double e0 = vals[idx], e1 = vals[idx + 1];
+          bm_select(w, lb, e0, e1);
+          val[k][2 * t] = e0;
+          val[k][2 * t + 1] = e1;
+          dot[k] = fma(e0, v[2 * t], dot[k]);
+          dot[k] = fma(e1, v[2 * t + 1], dot[k]);
+        }
+      }
+    }
+    mbar_arrive(&rg.empty[rg.stage]);   // stage consumed (every consumer thread); values live on in registers
+    rg.advance();
+    block_sum_split<kStR>(dot, slots, rphase, kStConsumers);
+    if constexpr (CL) cx->exchange<kStR>(dot);
+#pragma unroll
+    for (int k = 0; k < kStR; ++k) {
+      const double w = ar[k] * dot[k];   // sparsify.py:153: weights * pv
+#pragma unroll
+      for (int i = 0; i < 2 * NQ; ++i) acc[i] = fma(val[k][i], w, acc[i]);
+    }
+  }
+}
+
 // Variant code of the hess_apply kernels: 0 group smem accumulators,
-// 1..8 bitmap with NQ = V words per warp.
-constexpr int kHvVariants = kMaxNQ + 1;
+// 1..8 bitmap with NQ = V words per warp (cp.async-staged words, loads from
+// global), 9..12 TMA-staged bitmap with NQ = V - 8 (n <= 4096).
+constexpr int kHvVariants = kMaxNQ + 5;
 template <int V>
 struct HvVar {
   static constexpr bool kBitmap = V > 0;
-  static constexpr int NQ = V > 0 ? V : 1;
+  static constexpr bool kStaged = V > 8;
+  static constexpr int NQ = V > 8 ? V - 8 : (V > 0 ? V : 1);
   static constexpr int W = 16;
-  static constexpr int kThreads = 512;
+  static constexpr int kThreads = V > 8 ? kStThreads : 512;
 };
 
 // Partial row of y = P^T (a * (P v)) over this CTA's rows, bitmap variants:
@@ -398,6 +631,31 @@ OTB_DEV void hv_bitmap_partial(const Csr& A, const uint4* bm, const double* a, c
   }
 }
 
+// Staged variant of hv_bitmap_partial: the producer warp streams, the 512
+// consumer threads compute; `rg` persists across calls (ring position).
+template <int V>
+OTB_DEV void hv_staged_partial(const Csr& A, const uint4* bm, const double* a, const double* vsm, int n, int nq, int rb,
+                               int re, double* slots, StRing& rg, double* dst) {
+  constexpr int NQ = HvVar<V>::NQ;
+  if (threadIdx.x >= kStConsumers) {
+    st_produce(A, bm, a, rb, re, nq, 0, 16 * NQ, true, rg);
+    return;
+  }
+  double vr[2 * NQ], ar[2 * NQ];
+#pragma unroll
+  for (int i = 0; i < 2 * NQ; ++i) {
+    const int j = bm_col<16>(i >> 1, i & 1);
+    vr[i] = (j < n) ? vsm[j] : 0.0;
+    ar[i] = 0.0;
+  }
+  st_consume<NQ, false>(rb, re, vr, ar, slots, rg, nullptr);
+#pragma unroll
+  for (int i = 0; i < 2 * NQ; ++i) {
+    const int j = bm_col<16>(i >> 1, i & 1);
+    if (j < n) dst[j] = ar[i];
+  }
+}
+
 // Shared-memory layout of the group hv: v[npad] | acc[NG][npad] | slots.
 OTB_DEV size_t hv_smem_doubles(int npad, int NG) { return (size_t)npad * (1 + NG) + 16 * 64; }
 
@@ -415,6 +673,7 @@ struct HvArgs {
   double* colpart;         // [gridDim][n]
   const uint4* bm;         // bitmap index (NQ > 0)
   int nq;
+  int nwin;                // window-cluster variant: CTAs per cluster
 };
 
 // Standalone hess_apply partials (multi-rank CG iterations, otb_hess_apply).
@@ -442,7 +701,11 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_hv_grp(HvArgs h) {
   int rb, re;
   cta_rows(h.A, blockIdx.x, gridDim.x, rb, re);
   double* dst = h.colpart + (size_t)blockIdx.x * n;
-  if constexpr (HvVar<V>::kBitmap) {
+  if constexpr (HvVar<V>::kStaged) {
+    StRing rg = st_ring(reinterpret_cast<unsigned char*>(gslots + 16 * 64), 2);
+    __syncthreads();
+    hv_staged_partial<V>(h.A, h.bm, h.a, vsm, n, h.nq, rb, re, gslots, rg, dst);
+  } else if constexpr (HvVar<V>::kBitmap) {
     __syncthreads();
     hv_bitmap_partial<V>(h.A, h.bm, h.a, vsm, n, rb, re, gslots, reinterpret_cast<unsigned char*>(gslots + 16 * 64),
                         dst);
@@ -457,6 +720,70 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_hv_grp(HvArgs h) {
       dst[j] = t;
     }
   }
+}
+
+// Window-cluster hess_apply for n > 8192: a cluster of W = ceil(n / 4096)
+// CTAs shares one row block; CTA rank q owns the 4096 columns of window q
+// (bitmap words [64 q, 64 q + 64), NQ = 4 words per warp, v and the
+// accumulator in registers).  Each CTA's producer warp stages its window's
+// words and value segment of every row (TMA), the row dots of each batch are
+// completed across the windows by ClusterDots (DSMEM), so every value is
+// read once, nothing is scattered through atomics and the result is
+// deterministic.  Partial rows go to colpart[cluster][n].
+constexpr int kWinCols = 4096;
+constexpr int kWcStages = 3;
+constexpr size_t kWcSmemBytes = 16 * 64 * 8 + kWcStages * (size_t)kStBytes + 2 * kWcStages * 8;
+
+__global__ void __launch_bounds__(kStThreads, 1) k_hv_wc(HvArgs h) {
+  extern __shared__ __align__(16) double hsm[];
+  __shared__ double xbuf[2 * 16 * 4];
+  __shared__ uint64_t xbar[2];
+  const int W = h.nwin;
+  const int cr = (int)cluster_ctarank(), cid = blockIdx.x / W, ncl = gridDim.x / W;
+  StRing rg = st_ring(reinterpret_cast<unsigned char*>(hsm + 16 * 64), kWcStages);
+  if (threadIdx.x == 0) {
+    mbar_init(&xbar[0], W);
+    mbar_init(&xbar[1], W);
+    fence_mbar_init();
+  }
+  __syncwarp();
+  cluster_sync_all();
+  if (h.st == nullptr || h.st->status == CG_RUN) {   // same decision in every CTA
+    const int n = h.n, cb = kWinCols * cr;
+    int rb, re;
+    cta_rows(h.A, cid, ncl, rb, re);
+    if (threadIdx.x >= kStConsumers) {
+      st_produce(h.A, h.bm, h.a, rb, re, h.nq, 64 * cr, 64, cr + 1 == W, rg);
+    } else {
+      const double beta = h.update ? h.st->beta : 0.0;
+      double vr[8], ar[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int j = cb + bm_col<16>(i >> 1, i & 1);
+        double v = 0.0;
+        if (j < n) {
+          if (h.update) {
+            v = h.r[j] + beta * h.p_prev[j];      // krylov.py:83
+            if (cid == 0) h.p_cur[j] = v;
+          } else {
+            v = h.v_src[j];
+          }
+        }
+        vr[i] = v;
+        ar[i] = 0.0;
+      }
+      ClusterDots cx{xbuf, xbar, W, cr, 0, kStConsumers};
+      st_consume<4, true>(rb, re, vr, ar, hsm, rg, &cx);
+      double* dst = h.colpart + (size_t)cid * n;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int j = cb + bm_col<16>(i >> 1, i & 1);
+        if (j < n) dst[j] = ar[i];
+      }
+    }
+  }
+  __syncwarp();
+  cluster_sync_all();   // no CTA leaves while a peer may still address its shared memory
 }
 
 // Warp-per-row variant for n too large for shared accumulators: the
@@ -685,7 +1012,7 @@ template <int V>
 __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_cg_fused(CgFusedArgs c) {
   namespace cgrp = cooperative_groups;
   extern __shared__ __align__(16) double hsm[];
-  __shared__ double red[16 * 32];
+  __shared__ double red[32 * 32];
   __shared__ double red2[2][32 * 4];
   __shared__ double bcast;
   cgrp::grid_group grid = cgrp::this_grid();
@@ -710,11 +1037,15 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_cg_fused(CgFusedArgs 
     psm[j] = v;
     rsm[j] = v;
   }
+  StRing rg;
+  if constexpr (HvVar<V>::kStaged) rg = st_ring(reinterpret_cast<unsigned char*>(gslots + 16 * 64), 2);
   __syncthreads();
   for (;;) {
     // ---- phase 1: the hess_apply partial row of this CTA
     double* dst = c.colpart + (size_t)b * n;
-    if constexpr (HvVar<V>::kBitmap) {
+    if constexpr (HvVar<V>::kStaged) {
+      hv_staged_partial<V>(c.A, c.bm, c.a, psm, n, c.nq, rb, re, gslots, rg, dst);
+    } else if constexpr (HvVar<V>::kBitmap) {
       hv_bitmap_partial<V>(c.A, c.bm, c.a, psm, n, rb, re, gslots,
                           reinterpret_cast<unsigned char*>(gslots + 16 * 64), dst);
     } else {

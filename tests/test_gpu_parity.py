@@ -313,3 +313,33 @@ def test_fast_division_is_correctly_rounded(cuda, y):
     bad = got.view(np.uint64) != want.view(np.uint64)
     bad &= ~(np.isnan(got) & np.isnan(want))
     assert not bad.any(), (x[bad][:5], got[bad][:5], want[bad][:5])
+
+
+@pytest.mark.parametrize("m,n,env", [(300, 4100, None), (200, 9000, None), (120, 16400, None),
+                                     (310, 4000, "OTB_HV_STAGED"), (190, 9000, "OTB_HV_WC"),
+                                     (70, 50001, None)])
+def test_hess_apply_deterministic_and_matches_oracle(cuda, monkeypatch, m, n, env):
+    """hess_apply (cp.async bitmap, TMA-staged bitmap, warp-group and
+    window-cluster variants) is bitwise reproducible run to run and matches
+    the oracle's H v (sparsify.py:151-153).  `env` opts into a variant the
+    library would not pick for this shape (read when the context is made)."""
+    if env:
+        monkeypatch.setenv(env, "1")
+    P = _api()
+    from paper_2603_07156_b200 import instances
+
+    C, a, b = instances.small_uniform(m, n, 5 + n)
+    prob = P.OtProblem(C, a, b)
+    eta = 1e-2
+    lx = O.product_log_plan(a, b)
+    rng = np.random.default_rng(n)
+    gam = rng.standard_normal(n) * 1e-3
+    cache = P.compute_p(P.LogPlan(lx), P.DualState(gam), prob, eta)
+    rho = eta * float(np.linalg.norm(P.semidual_gradient(cache, prob))) / (m * n)
+    op = P.SparseHessianOp(P.sparsify_p(cache, rho, int(np.argmax(a))))
+    v = rng.standard_normal(n)
+    h1, h2 = op.matvec(v), op.matvec(v)
+    assert np.array_equal(h1.view(np.uint64), h2.view(np.uint64))
+    Pm, _ = O.softmax_rows(lx, C, gam, eta)
+    ref = O.SparseHessian(O.threshold_rows(Pm, rho, int(np.argmax(a))), a, eta).matvec(v)
+    assert rel(h1, ref) <= 1e-12
