@@ -23,6 +23,7 @@ struct EvalIO {
   double* lse;
   double* colpart;      // [ncl][n]
   double* vpart;        // [ncl][2]: a.lse, count of non-finite rows
+  double* P;            // optional: P = shifted / row_sum (local rows x ld), read by sparsify
 };
 
 template <int NS>
@@ -55,33 +56,27 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_eval(Geom geo, EvalIO io) {
         mx = fmax(mx, fmax(z[2 * s], z[2 * s + 1]));
       }
     }
+    // row max over the whole row (cluster-wide when the row is split), so
+    // that exp(z - M) is the reference's shifted value bit for bit
     double t[1] = {mx};
     D.reduce<1, kMax>(t);
     double M = t[0];
+    if (D.g.cl > 1) {
+      double all[kMaxCluster * 4];
+      D.exchange<1>(t, all);
+      M = all[0];
+      for (int q = 1; q < D.g.cl; ++q) M = fmax(M, all[q * 4]);
+    }
     double se = 0.0;
 #pragma unroll
     for (int k = 0; k < 2 * NS; ++k) {
       z[k] = exp(z[k] - M);
       se += z[k];
     }
-    t[0] = se;
-    D.reduce<1, kSum>(t);
-    double S = t[0];
-    double scale = 1.0;
-    if (D.g.cl > 1) {
-      double v2[2] = {M, S};
-      double all[kMaxCluster * 4];
-      D.exchange<2>(v2, all);
-      double Mg = all[0];
-      for (int q = 1; q < D.g.cl; ++q) Mg = fmax(Mg, all[q * 4]);
-      double Sg = 0.0;
-      for (int q = 0; q < D.g.cl; ++q) Sg += all[q * 4 + 1] * exp(all[q * 4] - Mg);
-      scale = exp(M - Mg);
-      M = Mg;
-      S = Sg;
-    }
+    const double S = D.row_sum(se);
     const double ai = __ldg(io.a + D.g.row0 + r);
-    const double w = (ai / S) * scale;
+    const double w = ai / S;
+    const Divider DS(S);
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       if (s < D.nsl) {
@@ -90,6 +85,15 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_eval(Geom geo, EvalIO io) {
         v.x = fma(w, z[2 * s], v.x);
         v.y = fma(w, z[2 * s + 1], v.y);
         *a2 = v;
+        if (io.P != nullptr) {                    // semidual.py:82-83: shifted / row_sum
+          const int j = D.col(s, 0);
+          double* dst = io.P + (size_t)r * D.g.ld + j;
+          if (j + 1 < D.c1) {
+            *reinterpret_cast<double2*>(dst) = make_double2(DS(z[2 * s]), DS(z[2 * s + 1]));
+          } else if (j < D.c1) {
+            dst[0] = DS(z[2 * s]);
+          }
+        }
       }
     }
     if (D.tid == 0 && D.cr == 0) {
@@ -138,10 +142,12 @@ struct SparsifyIO {
   int nq;
 };
 
-template <int NS>
+// FROMP: stream the P stored by the eval of the same gamma (one matrix, no
+// exp / division) instead of recomputing it from C and log X.
+template <int NS, bool FROMP>
 __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
-  Dense<2> D;
+  Dense<FROMP ? 1 : 2> D;
   D.setup(geo, smem);
   if (D.producer) {
     D.produce();
@@ -177,16 +183,21 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
         double2 c, x;
         D.fetch(c, x);
         const int j = D.col(s, 0);
-        const double2 gm = load_pair(io.gamma, j, D.c1);
+        if constexpr (FROMP) {
+          if (j < D.c1) P[2 * s] = c.x;
+          if (j + 1 < D.c1) P[2 * s + 1] = c.y;
+        } else {
+          const double2 gm = load_pair(io.gamma, j, D.c1);
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          if (j + e < D.c1) {
-            const double dz = ((e ? x.y : x.x) + DIV((e ? gm.y : gm.x) - (e ? c.y : c.x))) - M;
-            if (dz < dmin) {
-              P[2 * s + e] = dz;
-              skip |= 1u << (2 * s + e);
-            } else {
-              P[2 * s + e] = DS(exp(dz));          // semidual.py:82-83: shifted / row_sum
+          for (int e = 0; e < 2; ++e) {
+            if (j + e < D.c1) {
+              const double dz = ((e ? x.y : x.x) + DIV((e ? gm.y : gm.x) - (e ? c.y : c.x))) - M;
+              if (dz < dmin) {
+                P[2 * s + e] = dz;
+                skip |= 1u << (2 * s + e);
+              } else {
+                P[2 * s + e] = DS(exp(dz));          // semidual.py:82-83: shifted / row_sum
+              }
             }
           }
         }
@@ -208,7 +219,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
       }
     }
     double t[1] = {ks};
-    D.reduce<1, kSum>(t);   // barrier also publishes tb
+    D.template reduce<1, kSum>(t);   // barrier also publishes tb
     double ksum = t[0];
     // per-slice totals (lane s holds slice s), exclusive scan over slices
     // and (pre) the kept entries of slice s in the warps before this one
@@ -232,7 +243,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
     if (D.g.cl > 1) {
       double v2[2] = {(double)need, ksum};
       double all[kMaxCluster * 4];
-      D.exchange<2>(v2, all);
+      D.template exchange<2>(v2, all);
       double cs = 0.0, kss = 0.0;
       for (int q = 0; q < D.g.cl; ++q) {
         if (q < D.cr) myoff += (int)all[q * 4];
@@ -254,19 +265,19 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
 #pragma unroll
       for (int k = 0; k < 2 * NS; ++k) pm = fmax(pm, P[k]);
       double u[1] = {pm};
-      D.reduce<1, kMax>(u);
+      D.template reduce<1, kMax>(u);
       double pmax = u[0];
       double jm = 1e300;
 #pragma unroll
       for (int k = 0; k < 2 * NS; ++k)
         if (P[k] >= 0.0 && P[k] == pmax) jm = fmin(jm, (double)D.col(k >> 1, k & 1));
       u[0] = jm;
-      D.reduce<1, kMin>(u);
+      D.template reduce<1, kMin>(u);
       jm = u[0];
       if (D.g.cl > 1) {
         double v2[2] = {pmax, jm};
         double all[kMaxCluster * 4];
-        D.exchange<2>(v2, all);
+        D.template exchange<2>(v2, all);
         double bp = all[0], bj = all[1];
         for (int q = 1; q < D.g.cl; ++q) {
           if (all[q * 4] > bp || (all[q * 4] == bp && all[q * 4 + 1] < bj)) {
@@ -301,7 +312,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
     if (D.g.cl > 1) {
       double v1[1] = {(double)start};
       double all[kMaxCluster * 4];
-      D.exchange<1>(v1, all);
+      D.template exchange<1>(v1, all);
       start = (unsigned long long)all[0];
     }
     const bool ovf = (int64_t)(start + cnt_al) > io.cap;

@@ -80,23 +80,32 @@ int load_nccl(const char* path, Nccl& api) {
 }
 
 // ------------------------------------------------------------- kernels
-enum DenseKind { DK_EVAL = 0, DK_SPARSIFY, DK_TESTA, DK_TESTB, DK_TESTC0, DK_TESTC1, DK_WARMZ, DK_WARMG, DK_COUNT };
-const int kNmat[DK_COUNT] = {2, 2, 2, 1, 1, 2, 2, 2};
-const int kNacc[DK_COUNT] = {1, 1, 1, 1, 1, 1, 1, 2};
-const int kStaticSmem[DK_COUNT] = {0, (int)(kTabInts * 4 + 16), 0, 0, 0, 0, 0, 0};
+enum DenseKind {
+  DK_EVAL = 0, DK_SPARSIFY, DK_TESTA, DK_TESTB, DK_TESTC0, DK_TESTC1, DK_WARMZ, DK_WARMG, DK_SPARSP, DK_COUNT
+};
+const int kNmat[DK_COUNT] = {2, 2, 2, 1, 1, 2, 2, 2, 1};
+const int kNacc[DK_COUNT] = {1, 1, 1, 1, 1, 1, 1, 2, 1};
+const int kStaticSmem[DK_COUNT] = {0, (int)(kTabInts * 4 + 16), 0, 0, 0, 0, 0, 0, (int)(kTabInts * 4 + 16)};
 
 #define NS_ROW(K) \
   { nullptr, (const void*)K<1>, (const void*)K<2>, (const void*)K<3>, (const void*)K<4>, \
     (const void*)K<5>, (const void*)K<6>, (const void*)K<7>, (const void*)K<8> }
 const void* const kDenseFn[DK_COUNT][kMaxNS + 1] = {
-    NS_ROW(k_eval), NS_ROW(k_sparsify), NS_ROW(k_test_a), NS_ROW(k_test_b),
+    NS_ROW(k_eval),
+    {nullptr, (const void*)k_sparsify<1, false>, (const void*)k_sparsify<2, false>, (const void*)k_sparsify<3, false>,
+     (const void*)k_sparsify<4, false>, (const void*)k_sparsify<5, false>, (const void*)k_sparsify<6, false>,
+     (const void*)k_sparsify<7, false>, (const void*)k_sparsify<8, false>},
+    NS_ROW(k_test_a), NS_ROW(k_test_b),
     {nullptr, (const void*)k_test_c<1, false>, (const void*)k_test_c<2, false>, (const void*)k_test_c<3, false>,
      (const void*)k_test_c<4, false>, (const void*)k_test_c<5, false>, (const void*)k_test_c<6, false>,
      (const void*)k_test_c<7, false>, (const void*)k_test_c<8, false>},
     {nullptr, (const void*)k_test_c<1, true>, (const void*)k_test_c<2, true>, (const void*)k_test_c<3, true>,
      (const void*)k_test_c<4, true>, (const void*)k_test_c<5, true>, (const void*)k_test_c<6, true>,
      (const void*)k_test_c<7, true>, (const void*)k_test_c<8, true>},
-    NS_ROW(k_warm_zeta), NS_ROW(k_warm_gamma)};
+    NS_ROW(k_warm_zeta), NS_ROW(k_warm_gamma),
+    {nullptr, (const void*)k_sparsify<1, true>, (const void*)k_sparsify<2, true>, (const void*)k_sparsify<3, true>,
+     (const void*)k_sparsify<4, true>, (const void*)k_sparsify<5, true>, (const void*)k_sparsify<6, true>,
+     (const void*)k_sparsify<7, true>, (const void*)k_sparsify<8, true>}};
 
 #define HV_ROW(K)                                                                                    \
   {                                                                                                  \
@@ -130,6 +139,8 @@ struct otb_ctx {
   int hv_nb = 0, hv_win = 1;                   // row blocks (partial rows), CTAs per cluster (mode 3)
   int hv_var = 0, nq = 0, hv_threads = 512;   // kernel variant (sparse.cuh HvVar), bitmap words per row
   uint4* bm = nullptr;
+  double* Pbuf = nullptr;    // P of the last eval (local rows x ld), streamed by sparsify
+  bool p_valid = false;
   size_t hv_smem = 0;
   bool cg_fused = false;     // persistent cooperative CG available (1 rank, smem hv)
   int fused_ng = 1;
@@ -330,7 +341,8 @@ int require_bound(const otb_ctx* c) {
 int do_eval(otb_ctx* c, const double* X, const double* gamma) {
   const int n = (int)c->n;
   Geom geo = make_geom(c, DK_EVAL, c->C, X);
-  EvalIO io{gamma, c->a, c->eta, c->rowM, c->rowS, c->lse, c->colpart, c->vpart};
+  EvalIO io{gamma, c->a, c->eta, c->rowM, c->rowS, c->lse, c->colpart, c->vpart, c->Pbuf};
+  c->p_valid = false;
   cudaEvent_t e0 = nullptr;
   TRY(prof_begin(c, &e0));
   TRY(launch_dense(c, DK_EVAL, geo, &io));
@@ -347,6 +359,7 @@ int do_eval(otb_ctx* c, const double* X, const double* gamma) {
   c->last_value = c->hs->value;
   c->last_gnorm = c->hs->gnorm;
   c->have_eval = true;
+  c->p_valid = c->Pbuf != nullptr;
   return OTB_OK;
 }
 
@@ -374,13 +387,14 @@ int do_sparsify(otb_ctx* c, const double* X, const double* gamma, double rho) {
   for (int attempt = 0; attempt < 8; ++attempt) {
     CUDA_TRY(cudaMemsetAsync(&c->ds->alloc, 0, sizeof(unsigned long long), c->stream));
     CUDA_TRY(cudaMemsetAsync(&c->ds->flags, 0, sizeof(int), c->stream));
-    Geom geo = make_geom(c, DK_SPARSIFY, c->C, X);
+    const int kind = c->p_valid ? DK_SPARSP : DK_SPARSIFY;
+    Geom geo = c->p_valid ? make_geom(c, DK_SPARSP, c->Pbuf, nullptr) : make_geom(c, DK_SPARSIFY, c->C, X);
     SparsifyIO io{gamma, c->a, c->eta, rho, anchor_local, c->rowM, c->rowS, c->lse, c->cols, c->vals, c->cap,
                   c->row_start, c->row_len, &c->ds->alloc, c->chunk, c->colpart, &c->ds->flags,
                   (c->hv_mode == 2 || c->hv_mode == 3) ? c->bm : nullptr, c->nq};
     cudaEvent_t e0 = nullptr;
     TRY(prof_begin(c, &e0));
-    TRY(launch_dense(c, DK_SPARSIFY, geo, &io));
+    TRY(launch_dense(c, kind, geo, &io));
     k_row_prefix<<<1, 1024, 0, c->stream>>>(c->row_len, (int)c->m_loc, c->rowpre);
     LAUNCH_CHECK();
     CUDA_TRY(cudaMemcpyAsync(c->hbuf, c->rowpre + c->m_loc, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
@@ -839,6 +853,10 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   if (st == OTB_OK) st = dalloc(&c->ds, 1);
   if (st == OTB_OK) st = dalloc(&c->cg, 1);
   if (st == OTB_OK && (c->hv_mode == 2 || c->hv_mode == 3)) st = dalloc(&c->bm, (size_t)m_loc * c->nq);
+  // P of the eval, so that sparsify streams one matrix and does no exp
+  // (OTB_STORE_P=0: sparsify recomputes P from C and log X)
+  const char* env_p = std::getenv("OTB_STORE_P");
+  if (st == OTB_OK && !(env_p && std::atoi(env_p) == 0)) st = dalloc(&c->Pbuf, (size_t)m_loc * ld);
   if (st != OTB_OK) {
     otb_destroy(c);
     return st;
@@ -883,7 +901,7 @@ int otb_destroy(otb_ctx* c) {
                   (void*)c->cg_ap, (void*)c->cg_y, (void*)c->gtrial, (void*)c->yv, (void*)c->ec, (void*)c->Mloc,
                   (void*)c->Mglob, (void*)c->Sloc, (void*)c->row_start, (void*)c->rowpre, (void*)c->row_len,
                   (void*)c->cols, (void*)c->vals, (void*)c->ds, (void*)c->cg, (void*)c->scal, (void*)c->cta_rb,
-                  (void*)c->bm})
+                  (void*)c->bm, (void*)c->Pbuf})
     if (p) cudaFree(p);
   if (c->hs) cudaFreeHost(c->hs);
   if (c->hcg) cudaFreeHost(c->hcg);

@@ -343,3 +343,27 @@ def test_hess_apply_deterministic_and_matches_oracle(cuda, monkeypatch, m, n, en
     Pm, _ = O.softmax_rows(lx, C, gam, eta)
     ref = O.SparseHessian(O.threshold_rows(Pm, rho, int(np.argmax(a))), a, eta).matvec(v)
     assert rel(h1, ref) <= 1e-12
+
+
+@pytest.mark.parametrize("m,n", [(97, 1203), (41, 9100)])
+def test_sparsify_from_stored_p_equals_recomputed(cuda, monkeypatch, m, n):
+    """sparsify streams the P stored by the eval of the same gamma; with
+    OTB_STORE_P=0 it recomputes P from C and log X.  Both give the same CSR
+    bit for bit (the stored P is the reference's shifted / row_sum)."""
+    P = _api()
+    from paper_2603_07156_b200 import instances
+
+    C, a, b = instances.small_uniform(m, n, 3 + n)
+    lx = O.product_log_plan(a, b)
+    gam = np.random.default_rng(m).standard_normal(n) * 1e-3
+    outs = []
+    for store in ("1", "0"):
+        monkeypatch.setenv("OTB_STORE_P", store)
+        prob = P.OtProblem(C.copy(), a, b)          # fresh problem -> fresh context (env read at creation)
+        cache = P.compute_p(P.LogPlan(lx), P.DualState(gam), prob, 1e-2)
+        rho = 1e-2 * float(np.linalg.norm(P.semidual_gradient(cache, prob))) / (m * n)
+        sp = P.sparsify_p(cache, rho, int(np.argmax(a)))
+        outs.append((sp.row_offsets, sp.col_indices, sp.values, sp.anchor_row))
+    for x, y in zip(*outs):
+        assert np.array_equal(np.asarray(x).view(np.uint64) if np.asarray(x).dtype == np.float64 else x,
+                              np.asarray(y).view(np.uint64) if np.asarray(y).dtype == np.float64 else y)
