@@ -135,6 +135,7 @@ struct SparsifyIO {
   int64_t* row_start;     // [m_loc]
   int* row_len;           // [m_loc]
   unsigned long long* alloc;
+  unsigned long long* nnzc;   // += kept entries (one atomic per CTA)
   int64_t chunk;
   double* colpart;        // [ncl][n] partial of d
   int* flags;             // bit 1: capacity overflow
@@ -162,6 +163,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
   const int nw = D.g.nt >> 5;
   const unsigned lt = (1u << D.lane) - 1u;
   unsigned long long cur = 0, end = 0;
+  unsigned long long kept = 0;
   int rowpar = 0;
   for (int r = D.r0; r < D.r1; ++r) {
     const bool anc = (r == io.anchor_local);
@@ -380,9 +382,11 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyI
     if (D.tid == 0 && D.cr == 0) {
       io.row_start[r] = (int64_t)start;
       io.row_len[r] = ovf ? 0 : cnt;
+      kept += ovf ? 0 : cnt;
     }
     rowpar ^= 1;
   }
+  if (D.tid == 0 && D.cr == 0 && kept) atomicAdd(io.nnzc, kept);
   bar_sync(1, D.g.nt);
   D.store_acc(0, io.colpart + (size_t)D.cid * D.g.n);
   D.finish();

@@ -20,6 +20,7 @@ struct DevScalars {
   double drift;
   double scratch[4];
   unsigned long long alloc;            // CSR bump allocator
+  unsigned long long nnzc;             // kept entries of the last sparsify
   int flags;
   int pad;
   unsigned int cnt[16];                // last-block counters

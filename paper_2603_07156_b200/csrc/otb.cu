@@ -140,7 +140,9 @@ struct otb_ctx {
   int hv_var = 0, nq = 0, hv_threads = 512;   // kernel variant (sparse.cuh HvVar), bitmap words per row
   uint4* bm = nullptr;
   double* Pbuf = nullptr;    // P of the last eval (local rows x ld), streamed by sparsify
+  unsigned long long* cg_trace = nullptr;   // OTB_CG_TRACE=1: phase stamps of the fused CG
   bool p_valid = false;
+  bool rowpre_valid = false;
   size_t hv_smem = 0;
   bool cg_fused = false;     // persistent cooperative CG available (1 rank, smem hv)
   int fused_ng = 1;
@@ -381,26 +383,32 @@ int grow_csr(otb_ctx* c, int64_t want) {
   return OTB_OK;
 }
 
+int row_prefix(otb_ctx* c) {
+  k_row_prefix<<<1, 1024, 0, c->stream>>>(c->row_len, (int)c->m_loc, c->rowpre);
+  LAUNCH_CHECK();
+  return OTB_OK;
+}
+
 int do_sparsify(otb_ctx* c, const double* X, const double* gamma, double rho) {
   const int n = (int)c->n;
   const int64_t anchor_local = (c->anchor >= c->row0 && c->anchor < c->row1) ? c->anchor - c->row0 : -1;
   for (int attempt = 0; attempt < 8; ++attempt) {
-    CUDA_TRY(cudaMemsetAsync(&c->ds->alloc, 0, sizeof(unsigned long long), c->stream));
-    CUDA_TRY(cudaMemsetAsync(&c->ds->flags, 0, sizeof(int), c->stream));
+    // alloc, nnzc, flags are adjacent in DevScalars
+    CUDA_TRY(cudaMemsetAsync(&c->ds->alloc, 0, 2 * sizeof(unsigned long long) + sizeof(int), c->stream));
     const int kind = c->p_valid ? DK_SPARSP : DK_SPARSIFY;
     Geom geo = c->p_valid ? make_geom(c, DK_SPARSP, c->Pbuf, nullptr) : make_geom(c, DK_SPARSIFY, c->C, X);
     SparsifyIO io{gamma, c->a, c->eta, rho, anchor_local, c->rowM, c->rowS, c->lse, c->cols, c->vals, c->cap,
-                  c->row_start, c->row_len, &c->ds->alloc, c->chunk, c->colpart, &c->ds->flags,
+                  c->row_start, c->row_len, &c->ds->alloc, &c->ds->nnzc, c->chunk, c->colpart, &c->ds->flags,
                   (c->hv_mode == 2 || c->hv_mode == 3) ? c->bm : nullptr, c->nq};
     cudaEvent_t e0 = nullptr;
     TRY(prof_begin(c, &e0));
     TRY(launch_dense(c, kind, geo, &io));
-    k_row_prefix<<<1, 1024, 0, c->stream>>>(c->row_len, (int)c->m_loc, c->rowpre);
-    LAUNCH_CHECK();
-    CUDA_TRY(cudaMemcpyAsync(c->hbuf, c->rowpre + c->m_loc, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    // the row prefix (CSR export, nnz-balanced bounds) only where it is used
+    const bool bitmap = c->hv_mode == 2 || c->hv_mode == 3;
+    if (!bitmap) TRY(row_prefix(c));
+    c->rowpre_valid = !bitmap;
     TRY(sync_scalars(c));
-    int64_t nnz;
-    std::memcpy(&nnz, c->hbuf, sizeof(int64_t));
+    const int64_t nnz = (int64_t)c->hs->nnzc;
     TRY(prof_end(c, PC_SPARSIFY, e0, 16.0 * c->m_loc * n + 12.0 * nnz + 8.0 * (c->m_loc + 1)));
     if (c->hs->flags & 2) {
       const int64_t need = (int64_t)c->hs->alloc + (int64_t)c->ncl * c->chunk;
@@ -408,11 +416,12 @@ int do_sparsify(otb_ctx* c, const double* X, const double* gamma, double rho) {
       continue;
     }
     c->nnz = nnz;
-    {
+    if (!bitmap) {
       // nnz-balanced row bounds of the hess_apply CTAs, once per sparsify
+      // (the bitmap kernels use fixed equal row counts, set at creation)
       Csr A = csr_view(c);
       A.cta_rb = nullptr;
-      k_cta_bounds<<<(int)cdiv(c->hv_nb + 1, 256), 256, 0, c->stream>>>(A, c->hv_nb, c->cta_rb);
+      k_cta_bounds<<<(int)cdiv(c->hv_nb + 1, 256), 256, 0, c->stream>>>(A, c->hv_nb, c->cta_rb, 0);
       LAUNCH_CHECK();
     }
     TRY(colreduce(c, c->ncl, nullptr, 0, 0, 0));
@@ -540,8 +549,8 @@ int do_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t m
     return fail(OTB_ERR_INCONSISTENT, "unshifted system with right-hand side outside the range");
   if (c->cg_fused && c->hcg->status == CG_RUN) {
     // whole CG loop in one cooperative launch (k_cg_fused)
-    CgFusedArgs fa{csr_view(c), c->a,     c->d,  n,     c->fused_ng, c->eta, x, rhs, c->cg_ap,
-                   c->colpart,  c->scal, c->cg, c->bm, c->nq};
+    CgFusedArgs fa{csr_view(c), c->a,     c->d,  n,     c->fused_ng, c->eta, x,          rhs, c->cg_ap,
+                   c->colpart,  c->scal, c->cg, c->bm, c->nq,       c->cg_trace};
     void* args[1] = {&fa};
     cudaEvent_t e0 = nullptr;
     TRY(prof_begin(c, &e0));
@@ -754,7 +763,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
     c->hv_var = nwords / 16;
     c->hv_ng = 0;
     c->hv_smem = (size_t)(npad + 16 * 64) * 8 + kBmSmemBytes;
-    if (nwords <= 64 && env_st && std::atoi(env_st) == 1) {   // n <= 4096: TMA-staged values (opt-in)
+    if (nwords <= 64 && !(env_st && std::atoi(env_st) == 0)) {   // n <= 4096: TMA-staged values
       c->hv_var = 8 + nwords / 16;
       c->hv_threads = kStThreads;
       c->hv_smem = (size_t)(npad + 16 * 64) * 8 + 2 * (size_t)kStBytes + 32;
@@ -857,6 +866,12 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   // (OTB_STORE_P=0: sparsify recomputes P from C and log X)
   const char* env_p = std::getenv("OTB_STORE_P");
   if (st == OTB_OK && !(env_p && std::atoi(env_p) == 0)) st = dalloc(&c->Pbuf, (size_t)m_loc * ld);
+  const char* env_tr = std::getenv("OTB_CG_TRACE");
+  if (st == OTB_OK && env_tr && std::atoi(env_tr) == 1) {
+    const size_t cnt = (size_t)c->hv_grid * kCgTraceIters * 6;
+    if (cudaMalloc((void**)&c->cg_trace, cnt * sizeof(unsigned long long)) != cudaSuccess) st = OTB_ERR_NOMEM;
+    else cudaMemset(c->cg_trace, 0, cnt * sizeof(unsigned long long));
+  }
   if (st != OTB_OK) {
     otb_destroy(c);
     return st;
@@ -877,6 +892,11 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
     return fail(OTB_ERR_NOMEM, "cudaMallocHost failed");
   }
   cudaMemset(c->ds, 0, sizeof(DevScalars));
+  if (c->hv_mode == 2 || c->hv_mode == 3) {   // equal row counts per hess_apply CTA / cluster, fixed
+    Csr A = csr_view(c);
+    A.cta_rb = nullptr;
+    k_cta_bounds<<<(int)cdiv(c->hv_nb + 1, 256), 256>>>(A, c->hv_nb, c->cta_rb, 1);
+  }
   cudaMemset(c->cg, 0, sizeof(CgState));
   cudaMemset(c->cg_y, 0, sizeof(double) * nv);
   cudaMemset(c->row_len, 0, sizeof(int) * m_loc);
@@ -901,7 +921,7 @@ int otb_destroy(otb_ctx* c) {
                   (void*)c->cg_ap, (void*)c->cg_y, (void*)c->gtrial, (void*)c->yv, (void*)c->ec, (void*)c->Mloc,
                   (void*)c->Mglob, (void*)c->Sloc, (void*)c->row_start, (void*)c->rowpre, (void*)c->row_len,
                   (void*)c->cols, (void*)c->vals, (void*)c->ds, (void*)c->cg, (void*)c->scal, (void*)c->cta_rb,
-                  (void*)c->bm, (void*)c->Pbuf})
+                  (void*)c->bm, (void*)c->Pbuf, (void*)c->cg_trace})
     if (p) cudaFree(p);
   if (c->hs) cudaFreeHost(c->hs);
   if (c->hcg) cudaFreeHost(c->hcg);
@@ -999,6 +1019,10 @@ int otb_sparsify(otb_ctx* c, const double* logX, const double* gamma, double rho
 
 int otb_csr_export(otb_ctx* c, int64_t* row_ptr, int32_t* cols, double* vals, double* d) {
   TRY(require_bound(c));
+  if (!c->rowpre_valid && (row_ptr || (cols && vals))) {
+    TRY(row_prefix(c));
+    c->rowpre_valid = true;
+  }
   if (row_ptr)
     CUDA_TRY(cudaMemcpyAsync(row_ptr, c->rowpre, sizeof(int64_t) * (c->m_loc + 1), cudaMemcpyDeviceToDevice,
                              c->stream));
@@ -1229,6 +1253,17 @@ int otb_selftest_div(const double* x, int64_t n, double y, double* out) {
   k_selftest_div<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256>>>(x, n, y, out);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaDeviceSynchronize());
+  return OTB_OK;
+}
+
+int otb_cg_trace(otb_ctx* c, uint64_t* out, int64_t cap, int64_t* count) {
+  if (!c || !count) return fail(OTB_ERR_ARG, "null");
+  const int64_t cnt = c->cg_trace ? (int64_t)c->hv_grid * kCgTraceIters * 6 : 0;
+  *count = cnt;
+  if (cnt && out && cap >= cnt) {
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    CUDA_TRY(cudaMemcpy(out, c->cg_trace, (size_t)cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  }
   return OTB_OK;
 }
 

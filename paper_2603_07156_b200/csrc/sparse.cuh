@@ -116,11 +116,17 @@ OTB_DEV void cta_rows(const Csr& A, int b, int nb, int& rb, int& re) {
   }
 }
 
-__global__ void k_cta_bounds(Csr A, int nb, int* bounds) {
+// by_rows: equal row counts — the bitmap kernels visit every column slot of
+// a row whatever its nnz, so their cost is per row, not per entry.
+__global__ void k_cta_bounds(Csr A, int nb, int* bounds, int by_rows) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b > nb) return;
   if (b == nb) {
     bounds[b] = A.m_loc;
+    return;
+  }
+  if (by_rows) {
+    bounds[b] = (int)(((int64_t)b * A.m_loc) / nb);
     return;
   }
   int rb, re;
@@ -323,17 +329,19 @@ OTB_DEV void bm_stage(const Csr& A, const uint4* bm, const double* a, int r0, in
 // CTA's partial dots of a batch go to every CTA of the cluster through DSMEM
 // (remote stores + a release arrive on the peer's mbarrier), and every CTA
 // adds the W partials in window order, so all windows apply the same dots.
-// Two buffers/barriers alternate between batches.
+// send(b) and recv(b) are split so that the exchange of batch b overlaps the
+// loads and dots of batch b+1; four buffers / barriers rotate (a CTA can be
+// at most three sends ahead of a peer's reads).
+constexpr int kXBufs = 4;
 struct ClusterDots {
-  double* xbuf;     // [2][16][4]
-  uint64_t* xbar;   // [2], initialised with W arrivals
-  int W, cr, count;
+  double* xbuf;     // [kXBufs][16][4]
+  uint64_t* xbar;   // [kXBufs], initialised with W arrivals
+  int W, cr, nsend, nrecv;
   int nthreads;     // threads taking part (the consumer warps)
 
   template <int R>
-  OTB_DEV void exchange(double (&v)[R]) {
-    const int q = count & 1;
-    const uint32_t par = (uint32_t)((count >> 1) & 1);
+  OTB_DEV void send(const double (&v)[R]) {
+    const int q = nsend % kXBufs;
     double* base = xbuf + q * 16 * 4;
     if (threadIdx.x == 0) {
       for (int rk = 0; rk < W; ++rk) {
@@ -342,6 +350,15 @@ struct ClusterDots {
         for (int k = 0; k < R; ++k) st_cluster_f64(dst + 8u * k, v[k]);
         mbar_arrive_remote(mapa(smem_u32(&xbar[q]), (uint32_t)rk));
       }
+    }
+    ++nsend;
+  }
+  template <int R>
+  OTB_DEV void recv(double (&v)[R]) {
+    const int q = nrecv % kXBufs;
+    const uint32_t par = (uint32_t)((nrecv / kXBufs) & 1);
+    const double* base = xbuf + q * 16 * 4;
+    if (threadIdx.x == 0) {
       while (!mbar_try_wait_cluster(&xbar[q], par)) {
       }
     }
@@ -352,15 +369,14 @@ struct ClusterDots {
       for (int rk = 0; rk < W; ++rk) t += base[rk * 4 + k];
       v[k] = t;
     }
-    ++count;
+    ++nrecv;
   }
 };
 
-template <int NQ, bool CL = false>
+template <int NQ>
 OTB_DEV void hv_bitmap_rows(const Csr& A, const uint4* __restrict__ bm, const double* __restrict__ a,
                             const double (&v)[2 * NQ], double (&acc)[2 * NQ], int rb, int re, double* slots,
-                            unsigned char* ring, int stride = BmCfg<NQ>::NQP, int woff = 0,
-                            ClusterDots* cx = nullptr) {
+                            unsigned char* ring, int stride = BmCfg<NQ>::NQP, int woff = 0) {
   constexpr int R = BmCfg<NQ>::R, NQP = BmCfg<NQ>::NQP;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lb = 1u << lane, lt = lb - 1u;
@@ -399,7 +415,6 @@ OTB_DEV void hv_bitmap_rows(const Csr& A, const uint4* __restrict__ bm, const do
     }
     cp_async_wait_all();   // next stage lands before the barrier below publishes it
     block_sum_split<R>(dot, slots, phase, blockDim.x);
-    if constexpr (CL) cx->exchange<R>(dot);
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       const double w = ar[k] * dot[k];   // sparsify.py:153: weights * pv
@@ -544,12 +559,51 @@ OTB_DEV void st_produce(const Csr& A, const uint4* bm, const double* a, int rb, 
 // Consumers (512 threads): the same batches.  Column 2l keeps e0, column
 // 2l+1 keeps e1 (e0 when 2l is not kept); columns that are not kept carry
 // 0, and fma(0, x, s) == s for finite x.
+// One staged row against the thread's columns: select the pair of every
+// word; accumulate the dot (DOT) or add val * w to the columns (!DOT).
+template <int NQ, bool DOT>
+OTB_DEV void st_row(const uint4* words, const double* vals, int k, int base, unsigned lb, unsigned lt,
+                    const double (&v)[2 * NQ], double (&acc)[2 * NQ], double& dot, double w,
+                    double (*val)[2 * NQ] = nullptr) {
+  const int warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int t = 0; t < NQ; ++t) {
+    const uint4 wd = words[k * kStWords + warp + 16 * t];
+    // words past n are zero (off 0 lies before a later window's segment):
+    // keep the address inside the row's stage slot; their masks are 0
+    const int idx = min(max(base + (int)wd.z + __popc(wd.x & lt) + __popc(wd.y & lt), k * kStRowVals),
+                        (k + 1) * kStRowVals - 2);
+    double e0 = vals[idx], e1 = vals[idx + 1];
+    bm_select(wd, lb, e0, e1);
+    if constexpr (DOT) {
+      dot = fma(e0, v[2 * t], dot);
+      dot = fma(e1, v[2 * t + 1], dot);
+      if (val != nullptr) {
+        (*val)[2 * t] = e0;
+        (*val)[2 * t + 1] = e1;
+      }
+    } else {
+      acc[2 * t] = fma(e0, w, acc[2 * t]);
+      acc[2 * t + 1] = fma(e1, w, acc[2 * t + 1]);
+    }
+  }
+}
+
+// Consumers (512 threads): the same batches.  Single CTA: the values of a
+// batch stay in registers from the dot to the update and the stage is
+// released right after the dots.  Cluster (CL): the exchange of batch b's
+// window partials overlaps batch b+1 (send b, dots of b+1, receive b), and
+// batch b is applied by re-reading its stage, released only then — no
+// second register copy of the values.
 template <int NQ, bool CL>
 OTB_DEV void st_consume(int rb, int re, const double (&v)[2 * NQ], double (&acc)[2 * NQ], double* slots, StRing& rg,
                         ClusterDots* cx) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const unsigned lb = 1u << lane, lt = lb - 1u;
   int rphase = 0;
+  int pstage = 0;          // CL: stage of the batch still to be applied
+  bool have_prev = false;
+  double pdot[kStR];
   for (int r0 = rb; r0 < re; r0 += kStR) {
     mbar_wait(&rg.full[rg.stage], rg.phase);
     const unsigned char* sp = rg.at(rg.stage);
@@ -557,42 +611,69 @@ OTB_DEV void st_consume(int rb, int re, const double (&v)[2 * NQ], double (&acc)
     const StHdr* h = reinterpret_cast<const StHdr*>(sp + kStR * kStWords * 16);
     const double* vals = reinterpret_cast<const double*>(sp + kStR * kStWords * 16 + kStHdrBytes);
     const int count = h->count;
-    double val[kStR][2 * NQ];
-    double dot[kStR], ar[kStR];
+    double dot[kStR];
+    if constexpr (CL) {
 #pragma unroll
-    for (int k = 0; k < kStR; ++k) {
-      dot[k] = 0.0;
-      ar[k] = 0.0;
+      for (int k = 0; k < kStR; ++k) {
+        dot[k] = 0.0;
+        if (k < count) st_row<NQ, true>(words, vals, k, h->base[k], lb, lt, v, acc, dot[k], 0.0);
+      }
+      block_sum_split<kStR>(dot, slots, rphase, kStConsumers);
+      cx->send<kStR>(dot);                 // this batch's window partials go out ...
+      if (have_prev) {                     // ... while the previous batch's come in
+        cx->recv<kStR>(pdot);
+        const unsigned char* pp = rg.at(pstage);
+        const uint4* pw = reinterpret_cast<const uint4*>(pp);
+        const StHdr* ph = reinterpret_cast<const StHdr*>(pp + kStR * kStWords * 16);
+        const double* pv = reinterpret_cast<const double*>(pp + kStR * kStWords * 16 + kStHdrBytes);
+        double unused = 0.0;
 #pragma unroll
-      for (int i = 0; i < 2 * NQ; ++i) val[k][i] = 0.0;
-      if (k < count) {
-        const int base = h->base[k];
-        ar[k] = h->ar[k];
+        for (int k = 0; k < kStR; ++k)
+          if (k < ph->count)
+            st_row<NQ, false>(pw, pv, k, ph->base[k], lb, lt, v, acc, unused, ph->ar[k] * pdot[k]);
+        mbar_arrive(&rg.empty[pstage]);
+      }
 #pragma unroll
-        for (int t = 0; t < NQ; ++t) {
-          const uint4 w = words[k * kStWords + warp + 16 * t];
-          // words past n are zero (off 0 lies before a later window's segment):
-          // keep the address inside the row's stage slot; their masks are 0
-          const int idx = min(max(base + (int)w.z + __popc(w.x & lt) + __popc(w.y & lt), k * kStRowVals),
-                              (k + 1) * kStRowVals - 2);
-          double e0 = vals[idx], e1 = vals[idx + 1];
-          bm_select(w, lb, e0, e1);
-          val[k][2 * t] = e0;
-          val[k][2 * t + 1] = e1;
-          dot[k] = fma(e0, v[2 * t], dot[k]);
-          dot[k] = fma(e1, v[2 * t + 1], dot[k]);
+      for (int k = 0; k < kStR; ++k) pdot[k] = dot[k];
+      pstage = rg.stage;
+      have_prev = true;
+      rg.advance();
+    } else {
+      double val[kStR][2 * NQ], ar[kStR];
+#pragma unroll
+      for (int k = 0; k < kStR; ++k) {
+        dot[k] = 0.0;
+        ar[k] = 0.0;
+#pragma unroll
+        for (int i = 0; i < 2 * NQ; ++i) val[k][i] = 0.0;
+        if (k < count) {
+          ar[k] = h->ar[k];
+          st_row<NQ, true>(words, vals, k, h->base[k], lb, lt, v, acc, dot[k], 0.0, &val[k]);
         }
       }
+      mbar_arrive(&rg.empty[rg.stage]);   // stage consumed; values live on in registers
+      rg.advance();
+      block_sum_split<kStR>(dot, slots, rphase, kStConsumers);
+#pragma unroll
+      for (int k = 0; k < kStR; ++k) {
+        const double w = ar[k] * dot[k];   // sparsify.py:153: weights * pv
+#pragma unroll
+        for (int i = 0; i < 2 * NQ; ++i) acc[i] = fma(val[k][i], w, acc[i]);
+      }
     }
-    mbar_arrive(&rg.empty[rg.stage]);   // stage consumed (every consumer thread); values live on in registers
-    rg.advance();
-    block_sum_split<kStR>(dot, slots, rphase, kStConsumers);
-    if constexpr (CL) cx->exchange<kStR>(dot);
+  }
+  if constexpr (CL) {
+    if (have_prev) {
+      cx->recv<kStR>(pdot);
+      const unsigned char* pp = rg.at(pstage);
+      const uint4* pw = reinterpret_cast<const uint4*>(pp);
+      const StHdr* ph = reinterpret_cast<const StHdr*>(pp + kStR * kStWords * 16);
+      const double* pv = reinterpret_cast<const double*>(pp + kStR * kStWords * 16 + kStHdrBytes);
+      double unused = 0.0;
 #pragma unroll
-    for (int k = 0; k < kStR; ++k) {
-      const double w = ar[k] * dot[k];   // sparsify.py:153: weights * pv
-#pragma unroll
-      for (int i = 0; i < 2 * NQ; ++i) acc[i] = fma(val[k][i], w, acc[i]);
+      for (int k = 0; k < kStR; ++k)
+        if (k < ph->count) st_row<NQ, false>(pw, pv, k, ph->base[k], lb, lt, v, acc, unused, ph->ar[k] * pdot[k]);
+      mbar_arrive(&rg.empty[pstage]);
     }
   }
 }
@@ -736,14 +817,13 @@ constexpr size_t kWcSmemBytes = 16 * 64 * 8 + kWcStages * (size_t)kStBytes + 2 *
 
 __global__ void __launch_bounds__(kStThreads, 1) k_hv_wc(HvArgs h) {
   extern __shared__ __align__(16) double hsm[];
-  __shared__ double xbuf[2 * 16 * 4];
-  __shared__ uint64_t xbar[2];
+  __shared__ double xbuf[kXBufs * 16 * 4];
+  __shared__ uint64_t xbar[kXBufs];
   const int W = h.nwin;
   const int cr = (int)cluster_ctarank(), cid = blockIdx.x / W, ncl = gridDim.x / W;
   StRing rg = st_ring(reinterpret_cast<unsigned char*>(hsm + 16 * 64), kWcStages);
   if (threadIdx.x == 0) {
-    mbar_init(&xbar[0], W);
-    mbar_init(&xbar[1], W);
+    for (int q = 0; q < kXBufs; ++q) mbar_init(&xbar[q], W);
     fence_mbar_init();
   }
   __syncwarp();
@@ -772,7 +852,7 @@ __global__ void __launch_bounds__(kStThreads, 1) k_hv_wc(HvArgs h) {
         vr[i] = v;
         ar[i] = 0.0;
       }
-      ClusterDots cx{xbuf, xbar, W, cr, 0, kStConsumers};
+      ClusterDots cx{xbuf, xbar, W, cr, 0, 0, kStConsumers};
       st_consume<4, true>(rb, re, vr, ar, hsm, rg, &cx);
       double* dst = h.colpart + (size_t)cid * n;
 #pragma unroll
@@ -1003,7 +1083,22 @@ struct CgFusedArgs {
   CgState* st;
   const uint4* bm;   // bitmap index (NQ > 0)
   int nq;
+  unsigned long long* trace;   // optional: [gridDim][kCgTraceIters][6] globaltimer stamps
 };
+
+constexpr int kCgTraceIters = 16;
+OTB_DEV unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// phase stamps of the first kCgTraceIters iterations, thread 0 of each CTA:
+// 0 start, 1 hv done, 2 after barrier 1, 3 column slice done, 4 after barrier 2, 5 end
+#define CG_STAMP(k)                                                                         \
+  do {                                                                                      \
+    if (c.trace != nullptr && tid == 0 && it < kCgTraceIters)                               \
+      c.trace[((size_t)b * kCgTraceIters + (size_t)it) * 6 + (k)] = globaltimer();           \
+  } while (0)
 
 // Shared memory of k_cg_fused: p[npad] | r[npad] | acc[NG][npad] | slots.
 OTB_DEV size_t cg_fused_smem_doubles(int npad, int NG) { return (size_t)npad * (2 + NG) + 16 * 64; }
@@ -1041,6 +1136,7 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_cg_fused(CgFusedArgs 
   if constexpr (HvVar<V>::kStaged) rg = st_ring(reinterpret_cast<unsigned char*>(gslots + 16 * 64), 2);
   __syncthreads();
   for (;;) {
+    CG_STAMP(0);
     // ---- phase 1: the hess_apply partial row of this CTA
     double* dst = c.colpart + (size_t)b * n;
     if constexpr (HvVar<V>::kStaged) {
@@ -1059,7 +1155,9 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_cg_fused(CgFusedArgs 
         dst[j] = t;
       }
     }
+    CG_STAMP(1);
     grid.sync();
+    CG_STAMP(2);
     // ---- phase 2: column slice of ap, curvature partial
     double part = 0.0;
     for (int jc = j0; jc < j1; jc += 32) {
@@ -1078,7 +1176,9 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_cg_fused(CgFusedArgs 
       block_reduce<1, kSum>(t, &red2[0][0], ph, nth);
       if (tid == 0) c.scal[b] = t[0];
     }
+    CG_STAMP(3);
     grid.sync();
+    CG_STAMP(4);
     if (tid < 32) {
       const double v = warp_fixed_sum(c.scal, B, 1);
       if (tid == 0) bcast = v;
@@ -1117,6 +1217,8 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_cg_fused(CgFusedArgs 
       break;
     }
     for (int j = tid; j < n; j += nth) psm[j] = rsm[j] + beta * psm[j];   // krylov.py:83
+    if (c.trace != nullptr && tid == 0 && it - 1 < kCgTraceIters)          // (it already counts this one)
+      c.trace[((size_t)b * kCgTraceIters + (size_t)(it - 1)) * 6 + 5] = globaltimer();
     __syncthreads();
   }
   if (b == 0 && tid == 0) {

@@ -44,3 +44,20 @@ def cg():
 x, its, res = cg()
 t_cg = timeit(cg, 5)
 print(f"cg: {its} iterations, {t_cg:.0f} us total, {t_cg/its:.1f} us/iteration")
+if os.environ.get("OTB_CG_TRACE") == "1":
+    import ctypes as C
+    from paper_2603_07156_b200 import _lib
+    cnt = C.c_int64()
+    _lib.check(_lib.lib.otb_cg_trace(s.ctx, None, 0, C.byref(cnt)))
+    buf = (C.c_uint64 * cnt.value)()
+    _lib.check(_lib.lib.otb_cg_trace(s.ctx, buf, cnt.value, C.byref(cnt)))
+    t = np.array(buf, dtype=np.float64).reshape(-1, 16, 6)          # [cta][iteration][stamp], ns
+    iters = min(its, 16) - 1
+    t = t[:, 1:iters, :]                                             # skip the first iteration
+    names = ("hess_apply", "barrier 1", "column slice", "barrier 2", "vectors")
+    d = np.diff(t, axis=2)                                           # [cta][it][5]
+    print("CG phases (us, mean over CTAs and iterations; max over CTAs in brackets):")
+    for k, nm in enumerate(names):
+        print(f"  {nm:13s} {d[:, :, k].mean() / 1e3:7.2f}  [{d[:, :, k].max(axis=0).mean() / 1e3:7.2f}]")
+    per_it = np.diff(t[:, :, 0], axis=1)
+    print(f"  iteration     {per_it.mean() / 1e3:7.2f}")
