@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(256) k_colreduce(const double* part, int npart
 // buf[0..n) = column sums of a_i P_ij, buf[n] = a.lse.
 __global__ void __launch_bounds__(256) k_eval_post(int n, const double* buf, const double* b, const double* gamma,
                                                    double eta, double* g, DevScalars* ds, double* bpart) {
-  __shared__ double red[2][32 * 4];
+  __shared__ double red[2][kMaxWarps * 4];
   double sq = 0.0, bg = 0.0;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const double gj = buf[j] - b[j];
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) k_eval_post(int n, const double* buf, con
 // Dot product x.y into *out (fixed-order), e.g. slope = g.dir.
 __global__ void __launch_bounds__(256) k_dot(int n, const double* x, const double* y, DevScalars* ds,
                                              double* bpart, double* out) {
-  __shared__ double red[2][32 * 4];
+  __shared__ double red[2][kMaxWarps * 4];
   double s = 0.0;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) s = fma(x[j], y[j], s);
   int ph = 0;
@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(256) k_dot(int n, const double* x, const doubl
 
 // Sum of v into *out.
 __global__ void __launch_bounds__(256) k_sum(int n, const double* v, DevScalars* ds, double* bpart, double* out) {
-  __shared__ double red[2][32 * 4];
+  __shared__ double red[2][kMaxWarps * 4];
   double s = 0.0;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) s += v[j];
   int ph = 0;
@@ -149,7 +149,7 @@ enum VecPost { POST_COPY = 0, POST_Y = 1, POST_EC = 2, POST_COLRES = 3, POST_WAR
 // POST_WARMERR:  *out_s = sum (buf - b)^2                   (sinkhorn.py:65)
 __global__ void __launch_bounds__(256) k_vec_post(int mode, int n, const double* buf, const double* b,
                                                   double* out, DevScalars* ds, double* bpart, double* out_s) {
-  __shared__ double red[2][32 * 4];
+  __shared__ double red[2][kMaxWarps * 4];
   double s = 0.0;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const double v = buf[j];
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(256) k_vec_post(int mode, int n, const double*
 __global__ void __launch_bounds__(256) k_rows_post(int mode, int m_loc, int cl, const double* rowpart,
                                                    const double* a, int64_t row0, double* er, DevScalars* ds,
                                                    double* bpart, double* out_s) {
-  __shared__ double red[2][32 * 4];
+  __shared__ double red[2][kMaxWarps * 4];
   double s = 0.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m_loc; i += gridDim.x * blockDim.x) {
     double rs = 0.0;

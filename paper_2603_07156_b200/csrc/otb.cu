@@ -226,7 +226,7 @@ cudaError_t allow_max_smem(const void* fn, int device) {
 
 size_t dense_smem(const otb_ctx* c, int kind, int nstage) {
   const size_t slice = 2 * (size_t)c->nt;
-  const size_t dbl = (size_t)nstage * kNmat[kind] * slice + (size_t)kNacc[kind] * c->ns * slice + 2 * 32 * 4 + 2 * 8 * 4;
+  const size_t dbl = (size_t)nstage * kNmat[kind] * slice + (size_t)kNacc[kind] * c->ns * slice + 2 * kMaxWarps * 4 + 2 * 8 * 4;
   return dbl * 8 + (2 * (size_t)nstage + 2) * 8 + 64 * 4;
 }
 
@@ -743,7 +743,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   // hess_apply variant: shared-memory group accumulators (NG groups of
   // 512/NG threads, as many as fit) or, for very wide n, global RED.
   const int64_t npad = rup(n, 2);
-  const size_t hv_budget = kMaxDynSmem - 12288;   // static smem of k_cg_fused (~10.3 KB)
+  const size_t hv_budget = kMaxDynSmem - 16384;   // static smem of k_cg_fused (~14.4 KB)
   int ng = 8;
   const char* env_ng = std::getenv("OTB_HV_GROUPS");
   if (env_ng) ng = std::max(1, std::min(16, std::atoi(env_ng)));

@@ -47,7 +47,7 @@ struct Geom {
 struct SmemMap {
   double* ring;      // nstage * nmat * 2nt
   double* acc;       // nacc * ns * 2nt
-  double* slots;     // 2 * 32 * 4
+  double* slots;     // 2 * kMaxWarps * 4
   double* xbuf;      // 2 * 8 * 4
   uint64_t* full;    // nstage
   uint64_t* empty;   // nstage
@@ -57,7 +57,7 @@ struct SmemMap {
 
 OTB_DEV size_t smem_bytes_for(const Geom& g, int nmat) {
   size_t slice = 2 * (size_t)g.nt;
-  size_t d = (size_t)g.nstage * nmat * slice + (size_t)g.nacc * g.ns * slice + 2 * 32 * 4 + 2 * 8 * 4;
+  size_t d = (size_t)g.nstage * nmat * slice + (size_t)g.nacc * g.ns * slice + 2 * kMaxWarps * 4 + 2 * 8 * 4;
   return d * 8 + (2 * (size_t)g.nstage + 2) * 8 + 64 * 4;
 }
 
@@ -70,7 +70,7 @@ OTB_DEV SmemMap carve(const Geom& g, int nmat, unsigned char* base) {
   s.acc = p;
   p += (size_t)g.nacc * g.ns * slice;
   s.slots = p;
-  p += 2 * 32 * 4;
+  p += 2 * kMaxWarps * 4;
   s.xbuf = p;
   p += 2 * 8 * 4;
   uint64_t* b = reinterpret_cast<uint64_t*>(p);

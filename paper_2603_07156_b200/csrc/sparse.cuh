@@ -468,7 +468,7 @@ OTB_DEV size_t st_smem_bytes(int S) { return (size_t)S * kStBytes + 2 * (size_t)
 
 // Carve a ring of S stages at `p` (16-byte aligned); thread 0 initialises
 // the barriers (the caller synchronises before use).
-OTB_DEV StRing st_ring(unsigned char* p, int S) {
+OTB_DEV StRing st_ring(unsigned char* p, int S, int consumers = kStConsumers) {
   StRing rg;
   rg.mem = p;
   rg.full = reinterpret_cast<uint64_t*>(p + (size_t)S * kStBytes);
@@ -479,7 +479,7 @@ OTB_DEV StRing st_ring(unsigned char* p, int S) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&rg.full[s], 1);
-      mbar_init(&rg.empty[s], kStConsumers);
+      mbar_init(&rg.empty[s], consumers);
     }
     fence_mbar_init();
   }
@@ -561,18 +561,19 @@ OTB_DEV void st_produce(const Csr& A, const uint4* bm, const double* a, int rb, 
 // 0, and fma(0, x, s) == s for finite x.
 // One staged row against the thread's columns: select the pair of every
 // word; accumulate the dot (DOT) or add val * w to the columns (!DOT).
-template <int NQ, bool DOT>
+template <int NQ, bool DOT, int CW = 16, bool CLAMP = true>
 OTB_DEV void st_row(const uint4* words, const double* vals, int k, int base, unsigned lb, unsigned lt,
                     const double (&v)[2 * NQ], double (&acc)[2 * NQ], double& dot, double w,
                     double (*val)[2 * NQ] = nullptr) {
   const int warp = threadIdx.x >> 5;
 #pragma unroll
   for (int t = 0; t < NQ; ++t) {
-    const uint4 wd = words[k * kStWords + warp + 16 * t];
-    // words past n are zero (off 0 lies before a later window's segment):
-    // keep the address inside the row's stage slot; their masks are 0
-    const int idx = min(max(base + (int)wd.z + __popc(wd.x & lt) + __popc(wd.y & lt), k * kStRowVals),
-                        (k + 1) * kStRowVals - 2);
+    const uint4 wd = words[k * kStWords + warp + CW * t];
+    // window kernels: words past n are zero (off 0 lies before a later
+    // window's segment); keep the address inside the row's stage slot —
+    // their masks are 0.  Single CTA: off 0 is the row start, no clamp.
+    int idx = base + (int)wd.z + __popc(wd.x & lt) + __popc(wd.y & lt);
+    if constexpr (CLAMP) idx = min(max(idx, k * kStRowVals), (k + 1) * kStRowVals - 2);
     double e0 = vals[idx], e1 = vals[idx + 1];
     bm_select(wd, lb, e0, e1);
     if constexpr (DOT) {
@@ -595,9 +596,10 @@ OTB_DEV void st_row(const uint4* words, const double* vals, int k, int base, uns
 // window partials overlaps batch b+1 (send b, dots of b+1, receive b), and
 // batch b is applied by re-reading its stage, released only then — no
 // second register copy of the values.
-template <int NQ, bool CL>
+template <int NQ, bool CL, int CW = 16>
 OTB_DEV void st_consume(int rb, int re, const double (&v)[2 * NQ], double (&acc)[2 * NQ], double* slots, StRing& rg,
                         ClusterDots* cx) {
+  constexpr int kCons = CW * 32;
   const int lane = threadIdx.x & 31;
   const unsigned lb = 1u << lane, lt = lb - 1u;
   int rphase = 0;
@@ -618,7 +620,7 @@ OTB_DEV void st_consume(int rb, int re, const double (&v)[2 * NQ], double (&acc)
         dot[k] = 0.0;
         if (k < count) st_row<NQ, true>(words, vals, k, h->base[k], lb, lt, v, acc, dot[k], 0.0);
       }
-      block_sum_split<kStR>(dot, slots, rphase, kStConsumers);
+      block_sum_split<kStR>(dot, slots, rphase, kCons);
       cx->send<kStR>(dot);                 // this batch's window partials go out ...
       if (have_prev) {                     // ... while the previous batch's come in
         cx->recv<kStR>(pdot);
@@ -648,12 +650,12 @@ OTB_DEV void st_consume(int rb, int re, const double (&v)[2 * NQ], double (&acc)
         for (int i = 0; i < 2 * NQ; ++i) val[k][i] = 0.0;
         if (k < count) {
           ar[k] = h->ar[k];
-          st_row<NQ, true>(words, vals, k, h->base[k], lb, lt, v, acc, dot[k], 0.0, &val[k]);
+          st_row<NQ, true, CW, false>(words, vals, k, h->base[k], lb, lt, v, acc, dot[k], 0.0, &val[k]);
         }
       }
       mbar_arrive(&rg.empty[rg.stage]);   // stage consumed; values live on in registers
       rg.advance();
-      block_sum_split<kStR>(dot, slots, rphase, kStConsumers);
+      block_sum_split<kStR>(dot, slots, rphase, kCons);
 #pragma unroll
       for (int k = 0; k < kStR; ++k) {
         const double w = ar[k] * dot[k];   // sparsify.py:153: weights * pv
@@ -680,15 +682,17 @@ OTB_DEV void st_consume(int rb, int re, const double (&v)[2 * NQ], double (&acc)
 
 // Variant code of the hess_apply kernels: 0 group smem accumulators,
 // 1..8 bitmap with NQ = V words per warp (cp.async-staged words, loads from
-// global), 9..12 TMA-staged bitmap with NQ = V - 8 (n <= 4096).
+// global), 9..12 TMA-staged bitmap (n <= 4096) with NQ = V - 8.  (32
+// consumer warps + the producer would exceed 1024 threads per CTA.)
 constexpr int kHvVariants = kMaxNQ + 5;
 template <int V>
 struct HvVar {
   static constexpr bool kBitmap = V > 0;
   static constexpr bool kStaged = V > 8;
+  static constexpr int CW = 16;                               // consumer warps
   static constexpr int NQ = V > 8 ? V - 8 : (V > 0 ? V : 1);
-  static constexpr int W = 16;
-  static constexpr int kThreads = V > 8 ? kStThreads : 512;
+  static constexpr int W = CW;
+  static constexpr int kThreads = V > 8 ? CW * 32 + 32 : 512;
 };
 
 // Partial row of y = P^T (a * (P v)) over this CTA's rows, bitmap variants:
@@ -717,22 +721,22 @@ OTB_DEV void hv_bitmap_partial(const Csr& A, const uint4* bm, const double* a, c
 template <int V>
 OTB_DEV void hv_staged_partial(const Csr& A, const uint4* bm, const double* a, const double* vsm, int n, int nq, int rb,
                                int re, double* slots, StRing& rg, double* dst) {
-  constexpr int NQ = HvVar<V>::NQ;
-  if (threadIdx.x >= kStConsumers) {
-    st_produce(A, bm, a, rb, re, nq, 0, 16 * NQ, true, rg);
+  constexpr int NQ = HvVar<V>::NQ, CW = HvVar<V>::CW;
+  if (threadIdx.x >= CW * 32) {
+    st_produce(A, bm, a, rb, re, nq, 0, CW * NQ, true, rg);
     return;
   }
   double vr[2 * NQ], ar[2 * NQ];
 #pragma unroll
   for (int i = 0; i < 2 * NQ; ++i) {
-    const int j = bm_col<16>(i >> 1, i & 1);
+    const int j = bm_col<CW>(i >> 1, i & 1);
     vr[i] = (j < n) ? vsm[j] : 0.0;
     ar[i] = 0.0;
   }
-  st_consume<NQ, false>(rb, re, vr, ar, slots, rg, nullptr);
+  st_consume<NQ, false, CW>(rb, re, vr, ar, slots, rg, nullptr);
 #pragma unroll
   for (int i = 0; i < 2 * NQ; ++i) {
-    const int j = bm_col<16>(i >> 1, i & 1);
+    const int j = bm_col<CW>(i >> 1, i & 1);
     if (j < n) dst[j] = ar[i];
   }
 }
@@ -783,7 +787,7 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_hv_grp(HvArgs h) {
   cta_rows(h.A, blockIdx.x, gridDim.x, rb, re);
   double* dst = h.colpart + (size_t)blockIdx.x * n;
   if constexpr (HvVar<V>::kStaged) {
-    StRing rg = st_ring(reinterpret_cast<unsigned char*>(gslots + 16 * 64), 2);
+    StRing rg = st_ring(reinterpret_cast<unsigned char*>(gslots + 16 * 64), 2, HvVar<V>::CW * 32);
     __syncthreads();
     hv_staged_partial<V>(h.A, h.bm, h.a, vsm, n, h.nq, rb, re, gslots, rg, dst);
   } else if constexpr (HvVar<V>::kBitmap) {
@@ -931,7 +935,7 @@ struct CgApArgs {
 __global__ void __launch_bounds__(256) k_cg_ap(CgApArgs c) {
   if (c.st->status != CG_RUN) return;
   __shared__ double red[8 * 32];
-  __shared__ double red2[2][32 * 4];
+  __shared__ double red2[2][kMaxWarps * 4];
   const double shift = c.st->shift;
   const int j = blockIdx.x * 32 + (threadIdx.x & 31);
   double y = 0.0;
@@ -977,7 +981,7 @@ __global__ void __launch_bounds__(256) k_cg_ap(CgApArgs c) {
 __global__ void __launch_bounds__(256) k_cg_update(int n, double* x, double* r, const double* p, const double* ap,
                                                    CgState* st, double* bpart) {
   if (st->status != CG_RUN) return;
-  __shared__ double red[2][32 * 4];
+  __shared__ double red[2][kMaxWarps * 4];
   const double alpha = st->alpha;
   double part = 0.0;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
@@ -1013,7 +1017,7 @@ __global__ void __launch_bounds__(256) k_cg_update(int n, double* x, double* r, 
 __global__ void __launch_bounds__(256) k_cg_init(int n, const double* rhs, double* x, double* r, double* p0,
                                                  CgState* st, double* bpart, double shift, double rel_tol,
                                                  long long max_iters) {
-  __shared__ double red[2][32 * 4];
+  __shared__ double red[2][kMaxWarps * 4];
   double sq = 0.0, sm = 0.0;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const double v = rhs[j];
@@ -1107,8 +1111,8 @@ template <int V>
 __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_cg_fused(CgFusedArgs c) {
   namespace cgrp = cooperative_groups;
   extern __shared__ __align__(16) double hsm[];
-  __shared__ double red[32 * 32];
-  __shared__ double red2[2][32 * 4];
+  __shared__ double red[40 * 32];   // reduce_partials32: one row of 32 per warp (<= 40 warps)
+  __shared__ double red2[2][kMaxWarps * 4];
   __shared__ double bcast;
   cgrp::grid_group grid = cgrp::this_grid();
   if (c.st->status != CG_RUN) return;
@@ -1133,7 +1137,7 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_cg_fused(CgFusedArgs 
     rsm[j] = v;
   }
   StRing rg;
-  if constexpr (HvVar<V>::kStaged) rg = st_ring(reinterpret_cast<unsigned char*>(gslots + 16 * 64), 2);
+  if constexpr (HvVar<V>::kStaged) rg = st_ring(reinterpret_cast<unsigned char*>(gslots + 16 * 64), 2, HvVar<V>::CW * 32);
   __syncthreads();
   for (;;) {
     CG_STAMP(0);
@@ -1179,6 +1183,17 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_cg_fused(CgFusedArgs 
     CG_STAMP(3);
     grid.sync();
     CG_STAMP(4);
+    // ap (written by every CTA in phase 2) and this CTA's slice of x are
+    // loaded now, so their latency overlaps the curvature reduction
+    constexpr int kApRegs = HvVar<V>::kThreads > 600 ? 4 : 16;   // covers n <= 4096 / 8192 (loop beyond)
+    double apr[kApRegs];
+#pragma unroll
+    for (int i = 0; i < kApRegs; ++i) {
+      const int j = tid + i * nth;
+      apr[i] = (j < n) ? c.ap[j] : 0.0;
+    }
+    const int jx = j0 + tid;
+    const double xj = (jx < j1) ? c.x[jx] : 0.0;
     if (tid < 32) {
       const double v = warp_fixed_sum(c.scal, B, 1);
       if (tid == 0) bcast = v;
@@ -1191,9 +1206,19 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_cg_fused(CgFusedArgs 
     }
     alpha = rs / curv;
     // ---- phase 3 (redundant in every CTA): x on the slice, r and r.r everywhere
-    for (int j = j0 + tid; j < j1; j += nth) c.x[j] = c.x[j] + alpha * psm[j];
+    if (jx < j1) c.x[jx] = xj + alpha * psm[jx];
+    for (int j = jx + nth; j < j1; j += nth) c.x[j] = c.x[j] + alpha * psm[j];
     double rr = 0.0;
-    for (int j = tid; j < n; j += nth) {
+#pragma unroll
+    for (int i = 0; i < kApRegs; ++i) {
+      const int j = tid + i * nth;
+      if (j < n) {
+        const double rj = rsm[j] - alpha * apr[i];
+        rsm[j] = rj;
+        rr = fma(rj, rj, rr);
+      }
+    }
+    for (int j = tid + kApRegs * nth; j < n; j += nth) {
       const double rj = rsm[j] - alpha * c.ap[j];
       rsm[j] = rj;
       rr = fma(rj, rj, rr);
