@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1) k_test_c(Geom geo, TestCIO io)
             double fv = (exp(xl) * z) * (e ? yy.y : yy.x);
             if (deficit > 0.0) fv = fv + DD(e_r * (e ? ee.y : ee.x));
             f[2 * s + e] = fv;
-            if (fv > 0.0) acc[0] += fv * (log(fv) - xl);
+            if (fv > 0.0) acc[0] += fv * (log_fast(fv) - xl);   // feasibility.py:84
             acc[1] += fv;
             rs += fv;
             if constexpr (METRICS) {

@@ -302,6 +302,12 @@ __global__ void k_init_plan(double* X, int64_t ld, int m_loc, int n, const doubl
     X[(size_t)r * ld + j] = fmax(log_a[row0 + r] + log_b[j], kLogFloor);
   }
 }
+// Test hook for log_fast (common.cuh).
+__global__ void k_selftest_log(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = log_fast(x[i]);
+}
+
 // Test hook for Divider (common.cuh): out_i = x_i / y.
 __global__ void k_selftest_div(const double* __restrict__ x, int64_t n, double y, double* __restrict__ out) {
   const Divider D(y);

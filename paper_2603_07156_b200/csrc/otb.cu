@@ -543,12 +543,10 @@ int do_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t m
   k_cg_init<<<c->colgrid, 256, 0, c->stream>>>(n, rhs, x, c->cg_r, c->cg_p[0], c->cg, c->bpart, shift, rel_tol,
                                                (long long)max_iters);
   LAUNCH_CHECK();
-  CUDA_TRY(cudaMemcpyAsync(c->hcg, c->cg, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
-  if (c->hcg->status == CG_INCONSISTENT)
-    return fail(OTB_ERR_INCONSISTENT, "unshifted system with right-hand side outside the range");
-  if (c->cg_fused && c->hcg->status == CG_RUN) {
-    // whole CG loop in one cooperative launch (k_cg_fused)
+  if (c->cg_fused) {
+    // whole CG loop in one cooperative launch (k_cg_fused); it returns at
+    // once when k_cg_init already decided (rhs = 0, inconsistent system),
+    // so the status is read back once, after it
     CgFusedArgs fa{csr_view(c), c->a,     c->d,  n,     c->fused_ng, c->eta, x,          rhs, c->cg_ap,
                    c->colpart,  c->scal, c->cg, c->bm, c->nq,       c->cg_trace};
     void* args[1] = {&fa};
@@ -562,7 +560,12 @@ int do_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t m
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     if (c->prof && !c->recs.empty())
       c->recs.back().bytes = (double)c->hcg->iters * hv_bytes(c);
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(c->hcg, c->cg, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
   }
+  if (c->hcg->status == CG_INCONSISTENT)
+    return fail(OTB_ERR_INCONSISTENT, "unshifted system with right-hand side outside the range");
   int64_t k = 0;
   while (c->hcg->status == CG_RUN) {
     for (int j = 0; j < kCgBatch; ++j, ++k) TRY(cg_iteration(c, k, x));
@@ -1264,6 +1267,15 @@ int otb_cg_trace(otb_ctx* c, uint64_t* out, int64_t cap, int64_t* count) {
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     CUDA_TRY(cudaMemcpy(out, c->cg_trace, (size_t)cnt * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   }
+  return OTB_OK;
+}
+
+int otb_selftest_log(const double* x, int64_t n, double* out) {
+  if ((!x || !out) && n > 0) return fail(OTB_ERR_ARG, "null");
+  if (n <= 0) return OTB_OK;
+  k_selftest_log<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256>>>(x, n, out);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaDeviceSynchronize());
   return OTB_OK;
 }
 

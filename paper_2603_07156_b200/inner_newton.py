@@ -120,7 +120,11 @@ def inner_solve(logplan: LogPlan, gamma0: DualState, problem: OtProblem, config:
     else:
         g_cur, g_nxt = gamma_bufs
         if not (_is_device(gamma0.gamma) and gamma0.gamma.data_ptr() == g_cur.data_ptr()):
-            g_cur[:n].copy_(s._vec(gamma0.gamma)[:n])
+            src = gamma0.gamma
+            if _is_device(src):
+                g_cur[:n].copy_(src.reshape(-1)[:n])
+            else:
+                g_cur[:n].copy_(s._vec(src)[:n])
     cand_t = out_plan if out_plan is not None else s.new_plan()
 
     value, grad_norm = s.ops.eval(plan_t, g_cur)

@@ -367,3 +367,28 @@ def test_sparsify_from_stored_p_equals_recomputed(cuda, monkeypatch, m, n):
     for x, y in zip(*outs):
         assert np.array_equal(np.asarray(x).view(np.uint64) if np.asarray(x).dtype == np.float64 else x,
                               np.asarray(y).view(np.uint64) if np.asarray(y).dtype == np.float64 else y)
+
+
+def test_fast_log_accuracy(cuda):
+    """The device log of the Bregman sum (common.cuh log_fast) is within 2
+    ulp of numpy's log over the positive doubles, and defers to CUDA's log
+    for zero, subnormals, negatives, inf and NaN."""
+    import torch
+
+    from paper_2603_07156_b200 import _lib
+
+    rng = np.random.default_rng(5)
+    x = np.concatenate([np.exp(rng.uniform(-744, 709, 400_000)), rng.uniform(0.5, 2.0, 200_000),
+                        1.0 + rng.standard_normal(50_000) * 1e-9, np.array([1.0, 2.0, 0.5, np.sqrt(2.0), 1e-310,
+                                                                               0.0, -1.0, np.inf, np.nan])])
+    xd = torch.from_numpy(x).cuda()
+    out = torch.empty_like(xd)
+    _lib.check(_lib.lib.otb_selftest_log(xd.data_ptr(), x.size, out.data_ptr()))
+    got = out.cpu().numpy()
+    with np.errstate(all="ignore"):
+        want = np.log(x)
+    fin = np.isfinite(want) & (want != 0)
+    ulp = np.abs(got[fin] - want[fin]) / np.spacing(np.abs(want[fin]))
+    assert ulp.max() <= 2.0, (ulp.max(), x[fin][np.argmax(ulp)])
+    assert got[x == 1.0][0] == 0.0
+    assert np.isneginf(got[x == 0.0]).all() and np.isnan(got[x == -1.0]).all() and np.isposinf(got[x == np.inf]).all()
