@@ -542,3 +542,22 @@ def solve(cost, a, b, eta, kkt_tol=1e-11, mu0=1e-4, mu_floor=1e-11, min_dim_scal
             break
     return SolveResult(log_x, rounded, obj, kkt_value, outer_iters, newton_total, cg_total,
                        gamma, zeta, records)
+
+
+def eot_solve(cost, a, b, eta, kkt_tol, warm_tol=1e-3, max_inner=500, cg_rel_tol=1e-10, cg_max_iters=None,
+              sigma=1e-4, beta=0.8, min_dim_scale=True):
+    """bregman_outer.py:284-327 — one entropic subproblem on the all-ones
+    reference plan (log X = 0): warm start, Newton to the gradient target
+    kkt_tol (pre-check off), metrics of the candidate.  Returns (candidate
+    log plan, rounded plan, objective, kkt, newton_iters, cg_total, gamma,
+    grad_norm)."""
+    m, n = cost.shape
+    scale = float(min(m, n)) if min_dim_scale else 1.0
+    log_x = np.zeros((m, n))
+    gamma, _, _ = warm_start(log_x, cost, a, b, eta, warm_tol)
+    res = inner(log_x, cost, a, b, gamma, eta, 0.0, scale, max_inner, sigma, beta, cg_rel_tol, cg_max_iters,
+                grad_target=kkt_tol)
+    rounded = round_plan(np.exp(res.candidate), a, b)
+    obj = float((cost * rounded).sum())
+    kkt_value = kkt(rounded, res.gamma, cost, a, b)["delta_kkt"]
+    return res.candidate, rounded, obj, kkt_value, res.newton_iters, res.cg_total, res.gamma, res.grad_norm

@@ -154,6 +154,49 @@ def ibsn_solve(
                        _session=s, _gamma_t=g0)
 
 
+def eot_single_solve(
+    problem: OtProblem,
+    config: SolverConfig,
+    clock: Callable[[], float] | None = None,
+    *,
+    comm=None,
+) -> OuterResult:
+    """bregman_outer.py:284-327 — one entropic (EOT) subproblem: the
+    reference log plan is fixed at 0 (the all-ones plan), so the subproblem
+    is entropic regularisation of the original cost; warm start, then the
+    Newton phase to the gradient-norm target ``config.kkt_tol`` (pre-check
+    off), then the metrics of the candidate.  Same kernels as ibsn_solve."""
+    validate(problem)
+    now = clock if clock is not None else time.perf_counter
+    eta = config.eta
+    s = session_for(problem, eta, comm)
+    n = s.n
+    cur, spare = s.new_plan(), s.new_plan()
+    cur.zero_()                                            # LogPlan(np.zeros((m, n)))
+    g0, g1 = s.new_vec(), s.new_vec()
+    zeta = s.new_vec(s.m_loc)
+    t0 = now()
+    logplan = LogPlan.from_padded(cur, n)
+    warm_start(logplan, problem, eta, config.warm_tol, session=s, gamma_buf=g0, zeta_buf=zeta, generation=0)
+    gstate, cand, report = inner_solve(logplan, DualState(g0), problem, config, mu_k=0.0, outer_k=0,
+                                       grad_target=config.kkt_tol, session=s, out_plan=spare, gamma_bufs=(g0, g1))
+    if gstate.gamma.data_ptr() != g0.data_ptr():
+        g0, g1 = g1, g0
+    objective, kkt_value = report.objective, report.kkt    # _metrics(candidate, gamma)
+    if not math.isfinite(objective):
+        raise NumericalFailure(f"non-finite objective {objective!r}")
+    traj = Trajectory()
+    traj.record(TrajectoryRecord(
+        outer_k=0, inner_total=report.newton_iters, cg_total=report.cg_iters_total, wall_seconds=now() - t0,
+        objective=objective, kkt=kkt_value, grad_norm=report.final_grad_norm))
+    device_out = _is_torch(problem.cost)
+    gamma_out = g0[:n] if device_out else g0[:n].cpu().numpy()
+    return OuterResult(final_logplan=LogPlan.from_padded(spare, n), objective=objective, kkt=kkt_value,
+                       outer_iters=1, trajectory=traj, gamma=gamma_out, zeta=None,
+                       newton_iters=report.newton_iters, cg_iters=report.cg_iters_total,
+                       warm_sweeps=s._last_warm[0], _session=s, _gamma_t=g0)
+
+
 def _chain_inner_logger(observer, traj, s, plan_t, now, t0, totals, optimal_value):
     """bregman_outer.py:162-188 — one trajectory row per inner step: the
     candidate of the step's dual on the current reference plan, rounded,

@@ -163,6 +163,20 @@ def solve_cases():
              traj_objective=np.array([r.objective for r in tr]), traj_kkt=np.array([r.kkt for r in tr]))
 
 
+def eot_cases():
+    """eot_single_solve (bregman_outer.py:284-327): one entropic subproblem on
+    the all-ones reference plan, Newton to the gradient target kkt_tol."""
+    cases = [("uniform", 20, 16, 0, 5e-2, 1e-9), ("square", 24, 24, 1, 2e-2, 1e-10), ("spherical", 18, 30, 2, 1e-1, 1e-9)]
+    for i, (kind, m, n, seed, eta, tol) in enumerate(cases):
+        p = problem(kind, m, n, seed)
+        cfg = core.SolverConfig(eta=eta, kkt_tol=tol)
+        res = bregman_outer.eot_single_solve(p, cfg)
+        rec = res.trajectory.records[-1]
+        save(f"eot_{i}", C=p.cost, a=p.source_marginal, b=p.target_marginal, eta=eta, kkt_tol=tol,
+             objective=res.objective, kkt=res.kkt, rounded=res.rounded_plan, final_log=res.final_logplan.log_entries,
+             newton_iters=rec.inner_total, cg_total=rec.cg_total, grad_norm=rec.grad_norm)
+
+
 def config_scalars():
     """BASELINE configs 1 and 2 (seed 0): the reference's end-to-end numbers."""
     out = {}
@@ -181,10 +195,10 @@ def config_scalars():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["eval", "sparsify", "newton", "rounding", "candidate", "warm", "inner", "solve",
-                             "configs"]
+                             "eot", "configs"]
     fns = {"eval": eval_cases, "sparsify": sparsify_cases, "newton": newton_cases, "rounding": rounding_cases,
            "candidate": candidate_cases, "warm": warm_cases, "inner": inner_cases, "solve": solve_cases,
-           "configs": config_scalars}
+           "eot": eot_cases, "configs": config_scalars}
     for w in which:
         fns[w]()
         print("done", w)

@@ -392,3 +392,18 @@ def test_fast_log_accuracy(cuda):
     assert ulp.max() <= 2.0, (ulp.max(), x[fin][np.argmax(ulp)])
     assert got[x == 1.0][0] == 0.0
     assert np.isneginf(got[x == 0.0]).all() and np.isnan(got[x == -1.0]).all() and np.isposinf(got[x == np.inf]).all()
+
+
+@pytest.mark.parametrize("name", golden_names("eot"))
+def test_eot_single_solve_matches_reference(cuda, name):
+    """eot_single_solve on the device against the reference's run."""
+    P = _api()
+    g = golden(name)
+    res = P.eot_single_solve(problem_of(g), P.SolverConfig(eta=float(g["eta"]), kkt_tol=float(g["kkt_tol"])))
+    rec = res.trajectory.records[-1]
+    assert rec.inner_total == int(g["newton_iters"])
+    assert abs(rec.cg_total - int(g["cg_total"])) <= max(1, rec.inner_total)
+    assert res.objective == pytest.approx(float(g["objective"]), rel=1e-8)      # the BASELINE gate
+    assert res.kkt == pytest.approx(float(g["kkt"]), rel=1e-6)
+    assert rel(res.rounded_plan, g["rounded"]) <= 1e-7
+    assert rec.grad_norm <= float(g["kkt_tol"])

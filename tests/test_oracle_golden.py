@@ -164,3 +164,16 @@ def test_spec_cg_trivial():
     rhs = np.array([1.0, -2.0, 0.5])
     x, it, _ = O.conjugate_gradient(lambda v: np.zeros_like(v), 1.0, rhs)
     np.testing.assert_allclose(x, rhs)
+
+
+@pytest.mark.parametrize("name", golden_names("eot"))
+def test_oracle_eot_matches_reference(name):
+    """eot_single_solve (bregman_outer.py:284-327) restated by the oracle."""
+    g = golden(name)
+    cand, rounded, obj, kkt, newton, cg, gamma, gn = O.eot_solve(g["C"], g["a"], g["b"], float(g["eta"]),
+                                                                 float(g["kkt_tol"]))
+    assert newton == int(g["newton_iters"])
+    assert abs(cg - int(g["cg_total"])) <= 1
+    assert obj == pytest.approx(float(g["objective"]), rel=1e-12)
+    assert kkt == pytest.approx(float(g["kkt"]), rel=1e-9)
+    assert np.max(np.abs(rounded - g["rounded"])) <= 1e-12
