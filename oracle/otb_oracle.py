@@ -561,3 +561,49 @@ def eot_solve(cost, a, b, eta, kkt_tol, warm_tol=1e-3, max_inner=500, cg_rel_tol
     obj = float((cost * rounded).sum())
     kkt_value = kkt(rounded, res.gamma, cost, a, b)["delta_kkt"]
     return res.candidate, rounded, obj, kkt_value, res.newton_iters, res.cg_total, res.gamma, res.grad_norm
+
+
+def ibsink_solve(cost, a, b, eta, kkt_tol=1e-11, mu0=1e-4, mu_floor=1e-11, min_dim_scale=True, max_outer=300,
+                 max_inner=500):
+    """bregman_outer.py:191-281 — outer loop with alternating dual sweeps as
+    the inner solver.  Returns (log plan, rounded, objective, kkt,
+    outer_iters, sweep_total, records)."""
+    m, n = cost.shape
+    scale = float(min(m, n)) if min_dim_scale else 1.0
+    log_x = product_log_plan(a, b)
+    gamma, zeta = np.zeros(n), np.zeros(m)
+    sweep_total = 0
+    records = []
+    rounded, obj, kkt_value, outer_iters = None, math.nan, math.inf, 0
+    for k in range(max_outer):
+        mu_k = mu(k, mu0, mu_floor)
+        cand = None
+        sweeps = 0
+        err = math.inf
+        for _ in range(max_inner):
+            zeta = zeta_sweep(log_x, cost, a, gamma, eta)
+            sweeps += 1
+            chi = log_x + (zeta[:, None] + gamma[None, :] - cost) / eta          # sinkhorn.py:41-43
+            err = float(np.linalg.norm(np.exp(chi).sum(axis=0) - b))
+            if err < mu_k:
+                cand = clamp_log_plan(chi)
+                if bregman(round_plan(np.exp(cand), a, b), cand) <= scale * mu_k:
+                    break
+                cand = None
+            gamma = gamma_sweep(log_x, cost, b, zeta, eta)
+        if cand is None:
+            zeta = zeta_sweep(log_x, cost, a, gamma, eta)
+            sweeps += 1
+            chi = log_x + (zeta[:, None] + gamma[None, :] - cost) / eta
+            err = float(np.linalg.norm(np.exp(chi).sum(axis=0) - b))
+            cand = clamp_log_plan(chi)
+        log_x = cand
+        outer_iters = k + 1
+        sweep_total += sweeps
+        rounded = round_plan(np.exp(log_x), a, b)
+        obj = float((cost * rounded).sum())
+        kkt_value = kkt(rounded, gamma, cost, a, b)["delta_kkt"]
+        records.append(dict(outer_k=k, inner_total=sweep_total, objective=obj, kkt=kkt_value, grad_norm=err))
+        if kkt_value < kkt_tol:
+            break
+    return log_x, rounded, obj, kkt_value, outer_iters, sweep_total, records

@@ -31,6 +31,7 @@ from .core import (
 _LAZY = {
     "ibsn_solve": "bregman_outer",
     "eot_single_solve": "bregman_outer",
+    "ibsink_solve": "bregman_outer",
     "OuterResult": "bregman_outer",
     "MuSchedule": "bregman_outer",
     "mu": "bregman_outer",

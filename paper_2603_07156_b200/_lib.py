@@ -72,6 +72,9 @@ SIGNATURES = {
     "otb_materialize_rounded": (C.c_int, [vp, vp, i64]),
     "otb_warm_start": (C.c_int, [vp, vp, vp, vp, dbl, i64, C.POINTER(WarmOut)]),
     "otb_zeta_from_lse": (C.c_int, [vp, vp]),
+    "otb_sinkhorn_zeta": (C.c_int, [vp, vp, vp, vp, C.POINTER(dbl)]),
+    "otb_sinkhorn_gamma": (C.c_int, [vp, vp, vp, vp]),
+    "otb_scaled_plan": (C.c_int, [vp, vp, vp, vp, vp]),
     "otb_init_plan": (C.c_int, [vp, vp]),
     "otb_materialize_p": (C.c_int, [vp, vp, vp, vp, i64]),
     "otb_info": (C.c_int, [vp, C.POINTER(i64)]),

@@ -22,7 +22,7 @@ from typing import Callable
 
 import numpy as np
 
-from .core import LogPlan, OtProblem, SolverConfig, _is_torch, validate
+from .core import InnerScale, LogPlan, OtProblem, SolverConfig, _is_torch, validate
 from .errors import NumericalFailure
 from .inner_newton import NewtonStepRecord, inner_solve
 from .semidual import DualState
@@ -152,6 +152,83 @@ def ibsn_solve(
                        outer_iters=outer_iters, trajectory=traj, gamma=gamma_out, zeta=zeta_out,
                        newton_iters=inner_total, cg_iters=cg_total, warm_sweeps=sweeps_total,
                        _session=s, _gamma_t=g0)
+
+
+def ibsink_solve(
+    problem: OtProblem,
+    config: SolverConfig,
+    optimal_value: float | None = None,
+    on_outer: Callable[[int, LogPlan, np.ndarray], None] | None = None,
+    clock: Callable[[], float] | None = None,
+    deadline_seconds: float | None = None,
+    *,
+    comm=None,
+) -> OuterResult:
+    """bregman_outer.py:191-281 — the same outer loop with alternating dual
+    sweeps as the inner solver.  Per sweep: zeta update fused with the
+    column-marginal error (the pre-check), the scaled plan and its rounding
+    / Bregman test when the error is below mu_k, else the gamma update.
+    Three device buffers rotate: the reference plan, the scaled candidate,
+    and a scratch plan."""
+    validate(problem)
+    now = clock if clock is not None else time.perf_counter
+    eta = config.eta
+    schedule = MuSchedule(config.mu0, config.mu_floor)
+    s = session_for(problem, eta, comm)
+    m, n = s.m, s.n
+    scale = float(min(m, n)) if config.inner_scale is InnerScale.MIN_DIM else 1.0
+    cur, cand_t, spare = s.new_plan(), s.new_plan(), s.new_plan()
+    s.ops.init_plan(cur)                                   # bregman_outer.py:210-212
+    gamma = s.new_vec()
+    zeta = s.new_vec(s.m_loc)
+    traj = Trajectory()
+    t0 = now()
+    sweep_total = 0
+    outer_iters = 0
+    kkt_value = math.inf
+    objective = math.nan
+    err = math.inf
+    for k in range(config.max_outer):
+        mu_k = mu(schedule, k)
+        accepted = False
+        sweeps_this = 0
+        for _ in range(config.max_inner):
+            err = s.ops.sinkhorn_zeta(cur, gamma, zeta)    # zeta_update + column error
+            sweeps_this += 1
+            if err < mu_k:
+                s.ops.scaled_plan(cur, gamma, zeta, cand_t)
+                res = s.ops.recover_round(cand_t, gamma, None, recover=False, metrics=False)
+                if res.bregman <= scale * mu_k:
+                    accepted = True
+                    break
+            s.ops.sinkhorn_gamma(cur, gamma, zeta)
+        if not accepted:
+            # sweep cap reached; accept the latest row-exact scaled plan
+            err = s.ops.sinkhorn_zeta(cur, gamma, zeta)
+            sweeps_this += 1
+            s.ops.scaled_plan(cur, gamma, zeta, cand_t)
+        cur, cand_t = cand_t, cur
+        outer_iters = k + 1
+        sweep_total += sweeps_this
+        if on_outer is not None:
+            on_outer(k, LogPlan.from_padded(cur.clone(), n), gamma[:n].cpu().numpy())
+        res = s.ops.recover_round(cur, gamma, None, recover=False, metrics=True)   # _metrics
+        objective, kkt_value = float(res.objective), float(res.delta_kkt)
+        if not math.isfinite(objective):
+            raise NumericalFailure(f"non-finite objective {objective!r}")
+        traj.record(TrajectoryRecord(
+            outer_k=k, inner_total=sweep_total, cg_total=0, wall_seconds=now() - t0, objective=objective,
+            kkt=kkt_value, grad_norm=err, gap=None if optimal_value is None else abs(objective - optimal_value)))
+        if kkt_value < config.kkt_tol:
+            break
+        if deadline_seconds is not None and now() - t0 > deadline_seconds:
+            break
+    device_out = _is_torch(problem.cost)
+    gamma_out = gamma[:n] if device_out else gamma[:n].cpu().numpy()
+    zeta_out = zeta[: s.m_loc] if device_out else zeta[: s.m_loc].cpu().numpy()
+    return OuterResult(final_logplan=LogPlan.from_padded(cur, n), objective=objective, kkt=kkt_value,
+                       outer_iters=outer_iters, trajectory=traj, gamma=gamma_out, zeta=zeta_out,
+                       warm_sweeps=sweep_total, _session=s, _gamma_t=gamma)
 
 
 def eot_single_solve(

@@ -27,7 +27,8 @@ struct DevScalars {
 };
 
 enum CounterIdx {
-  CNT_COLRED = 0, CNT_EVALPOST = 1, CNT_DOT = 2, CNT_ROWS = 3, CNT_VECPOST = 4, CNT_SUM = 5, CNT_WARM = 6
+  CNT_COLRED = 0, CNT_EVALPOST = 1, CNT_DOT = 2, CNT_ROWS = 3, CNT_VECPOST = 4, CNT_SUM = 5, CNT_WARM = 6,
+  CNT_SCALED = 7
 };
 
 // out[j] = sum_c part[c*n + j]; out[n + k] = sum_c spart[c*sstride + k].
@@ -302,6 +303,25 @@ __global__ void k_init_plan(double* X, int64_t ld, int m_loc, int n, const doubl
     X[(size_t)r * ld + j] = fmax(log_a[row0 + r] + log_b[j], kLogFloor);
   }
 }
+// sinkhorn.py:41-43 scaled_plan_log, then core.py:141-145: log X + (zeta_i +
+// gamma_j - C_ij)/eta, NaN / +inf counted in *bad, clamped at LOG_FLOOR.
+__global__ void k_scaled_plan(const double* __restrict__ C, const double* __restrict__ X, int64_t ld, int m_loc, int n,
+                              const double* __restrict__ zeta, const double* __restrict__ gamma, double eta,
+                              double* __restrict__ out, unsigned int* bad) {
+  const Divider DIV(eta);
+  const int64_t total = (int64_t)m_loc * n;
+  unsigned int nb = 0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n), j = (int)(idx % n);
+    const size_t o = (size_t)r * ld + j;
+    const double v = X[o] + DIV((zeta[r] + gamma[j]) - C[o]);
+    nb += (isnan(v) || v == INFINITY) ? 1u : 0u;
+    out[o] = fmax(v, kLogFloor);
+  }
+  if (nb) atomicAdd(bad, nb);
+}
+
 // Test hook for log_fast (common.cuh).
 __global__ void k_selftest_log(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

@@ -1139,59 +1139,44 @@ int otb_materialize_rounded(otb_ctx* c, double* out, int64_t ldo) {
   return OTB_OK;
 }
 
+// sinkhorn.py:47-51 + 61-65: zeta sweep fused with the column sums of the
+// scaled plan; *err = ||colsum - b|| (host read).
+int sweep_zeta(otb_ctx* c, const double* logX, const double* gamma, double* zeta, double* err) {
+  const int n = (int)c->n;
+  const double mn = (double)c->m_loc * n;
+  Geom geo = make_geom(c, DK_WARMZ, c->C, logX);
+  WarmZIO io{gamma, c->log_a, c->eta, zeta, c->colpart};
+  cudaEvent_t e0 = nullptr;
+  TRY(prof_begin(c, &e0));
+  TRY(launch_dense(c, DK_WARMZ, geo, &io));
+  TRY(prof_end(c, PC_WARMZ, e0, 16.0 * mn));
+  TRY(colreduce(c, c->ncl, nullptr, 0, 0, 0));
+  TRY(allreduce(c, c->sendbuf, (size_t)n, kNcclSum));
+  k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_WARMERR, n, c->sendbuf, c->b, nullptr, c->ds, c->bpart,
+                                                &c->ds->warm_err);
+  LAUNCH_CHECK();
+  TRY(sync_scalars(c));
+  *err = std::sqrt(c->hs->warm_err);
+  return OTB_OK;
+}
+
+int sweep_gamma(otb_ctx* c, const double* logX, double* gamma, const double* zeta);
+
 int otb_warm_start(otb_ctx* c, const double* logX, double* gamma, double* zeta, double warm_tol, int64_t max_sweeps,
                    otb_warm_out* out) {
   TRY(require_bound(c));
   const int n = (int)c->n;
-  const double mn = (double)c->m_loc * n;
   int64_t sweeps = 0;
   double err = INFINITY;
   bool done = false;
   for (int64_t s = 0; s < max_sweeps; ++s) {
-    {
-      Geom geo = make_geom(c, DK_WARMZ, c->C, logX);
-      WarmZIO io{gamma, c->log_a, c->eta, zeta, c->colpart};
-      cudaEvent_t e0 = nullptr;
-      TRY(prof_begin(c, &e0));
-      TRY(launch_dense(c, DK_WARMZ, geo, &io));
-      TRY(prof_end(c, PC_WARMZ, e0, 16.0 * mn));
-      TRY(colreduce(c, c->ncl, nullptr, 0, 0, 0));
-      TRY(allreduce(c, c->sendbuf, (size_t)n, kNcclSum));
-      k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_WARMERR, n, c->sendbuf, c->b, nullptr, c->ds, c->bpart,
-                                                    &c->ds->warm_err);
-      LAUNCH_CHECK();
-      TRY(sync_scalars(c));
-      err = std::sqrt(c->hs->warm_err);
-      sweeps = s + 1;
-      if (err < warm_tol) {
-        done = true;
-        break;
-      }
+    TRY(sweep_zeta(c, logX, gamma, zeta, &err));
+    sweeps = s + 1;
+    if (err < warm_tol) {
+      done = true;
+      break;
     }
-    {
-      Geom geo = make_geom(c, DK_WARMG, c->C, logX);
-      WarmGIO io{zeta, c->eta, c->colpart};
-      cudaEvent_t e0 = nullptr;
-      TRY(prof_begin(c, &e0));
-      TRY(launch_dense(c, DK_WARMG, geo, &io));
-      TRY(prof_end(c, PC_WARMG, e0, 16.0 * mn));
-      if (c->nranks == 1) {
-        k_warm_gamma_combine<<<c->col32, 256, 0, c->stream>>>(1, n, c->colpart, c->ncl, nullptr, nullptr, c->log_b,
-                                                                c->eta, gamma);
-        LAUNCH_CHECK();
-      } else {
-        k_warm_gamma_combine<<<c->col32, 256, 0, c->stream>>>(0, n, c->colpart, c->ncl, c->Mloc, c->Sloc, c->log_b,
-                                                                c->eta, gamma);
-        LAUNCH_CHECK();
-        CUDA_TRY(cudaMemcpyAsync(c->Mglob, c->Mloc, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
-        TRY(allreduce(c, c->Mglob, (size_t)n, kNcclMax));
-        k_warm_rescale<<<c->colgrid, 256, 0, c->stream>>>(n, c->Mloc, c->Mglob, c->Sloc);
-        LAUNCH_CHECK();
-        TRY(allreduce(c, c->Sloc, (size_t)n, kNcclSum));
-        k_warm_gamma_post<<<c->colgrid, 256, 0, c->stream>>>(n, c->Mglob, c->Sloc, c->log_b, c->eta, gamma);
-        LAUNCH_CHECK();
-      }
-    }
+    TRY(sweep_gamma(c, logX, gamma, zeta));
   }
   if (!done) {
     char buf[96];
@@ -1211,6 +1196,62 @@ int otb_warm_start(otb_ctx* c, const double* logX, double* gamma, double* zeta, 
     out->sweeps = sweeps;
     out->err = err;
   }
+  return OTB_OK;
+}
+
+// sinkhorn.py:54-58: gamma sweep (column log-sum-exp).
+int sweep_gamma(otb_ctx* c, const double* logX, double* gamma, const double* zeta) {
+  const int n = (int)c->n;
+  const double mn = (double)c->m_loc * n;
+  Geom geo = make_geom(c, DK_WARMG, c->C, logX);
+  WarmGIO io{zeta, c->eta, c->colpart};
+  cudaEvent_t e0 = nullptr;
+  TRY(prof_begin(c, &e0));
+  TRY(launch_dense(c, DK_WARMG, geo, &io));
+  TRY(prof_end(c, PC_WARMG, e0, 16.0 * mn));
+  if (c->nranks == 1) {
+    k_warm_gamma_combine<<<c->col32, 256, 0, c->stream>>>(1, n, c->colpart, c->ncl, nullptr, nullptr, c->log_b,
+                                                            c->eta, gamma);
+    LAUNCH_CHECK();
+  } else {
+    k_warm_gamma_combine<<<c->col32, 256, 0, c->stream>>>(0, n, c->colpart, c->ncl, c->Mloc, c->Sloc, c->log_b,
+                                                            c->eta, gamma);
+    LAUNCH_CHECK();
+    CUDA_TRY(cudaMemcpyAsync(c->Mglob, c->Mloc, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+    TRY(allreduce(c, c->Mglob, (size_t)n, kNcclMax));
+    k_warm_rescale<<<c->colgrid, 256, 0, c->stream>>>(n, c->Mloc, c->Mglob, c->Sloc);
+    LAUNCH_CHECK();
+    TRY(allreduce(c, c->Sloc, (size_t)n, kNcclSum));
+    k_warm_gamma_post<<<c->colgrid, 256, 0, c->stream>>>(n, c->Mglob, c->Sloc, c->log_b, c->eta, gamma);
+    LAUNCH_CHECK();
+  }
+  return OTB_OK;
+}
+
+int otb_sinkhorn_zeta(otb_ctx* c, const double* logX, const double* gamma, double* zeta, double* col_err) {
+  TRY(require_bound(c));
+  if (!col_err) return fail(OTB_ERR_ARG, "null");
+  TRY(sweep_zeta(c, logX, gamma, zeta, col_err));
+  c->have_eval = false;
+  return OTB_OK;
+}
+
+int otb_sinkhorn_gamma(otb_ctx* c, const double* logX, double* gamma, const double* zeta) {
+  TRY(require_bound(c));
+  TRY(sweep_gamma(c, logX, gamma, zeta));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->have_eval = false;
+  return OTB_OK;
+}
+
+int otb_scaled_plan(otb_ctx* c, const double* logX, const double* gamma, const double* zeta, double* logX_out) {
+  TRY(require_bound(c));
+  CUDA_TRY(cudaMemsetAsync(&c->ds->cnt[CNT_SCALED], 0, sizeof(unsigned int), c->stream));
+  k_scaled_plan<<<c->num_sms * 8, 256, 0, c->stream>>>(c->C, logX, c->ld, (int)c->m_loc, (int)c->n, zeta, gamma,
+                                                       c->eta, logX_out, &c->ds->cnt[CNT_SCALED]);
+  LAUNCH_CHECK();
+  TRY(sync_scalars(c));
+  if (c->hs->cnt[CNT_SCALED] != 0) return fail(OTB_ERR_BAD_LOGPLAN, "log plan contains NaN or +inf entries");
   return OTB_OK;
 }
 

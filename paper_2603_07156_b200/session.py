@@ -297,6 +297,20 @@ class Ops:
                                            float(warm_tol), int(max_sweeps), C.byref(out)))
         return int(out.sweeps), float(out.err)
 
+    def sinkhorn_zeta(self, plan_t, gamma_t, zeta_t) -> float:
+        err = C.c_double()
+        _lib.check(_lib.lib.otb_sinkhorn_zeta(self.s.ctx, plan_t.data_ptr(), gamma_t.data_ptr(), zeta_t.data_ptr(),
+                                              C.byref(err)))
+        return float(err.value)
+
+    def sinkhorn_gamma(self, plan_t, gamma_t, zeta_t):
+        _lib.check(_lib.lib.otb_sinkhorn_gamma(self.s.ctx, plan_t.data_ptr(), gamma_t.data_ptr(), zeta_t.data_ptr()))
+
+    def scaled_plan(self, plan_t, gamma_t, zeta_t, out_t):
+        _lib.check(_lib.lib.otb_scaled_plan(self.s.ctx, plan_t.data_ptr(), gamma_t.data_ptr(), zeta_t.data_ptr(),
+                                            out_t.data_ptr()))
+        return out_t
+
     def init_plan(self, plan_t):
         _lib.check(_lib.lib.otb_init_plan(self.s.ctx, plan_t.data_ptr()))
         return plan_t

@@ -177,6 +177,21 @@ def eot_cases():
              newton_iters=rec.inner_total, cg_total=rec.cg_total, grad_norm=rec.grad_norm)
 
 
+def ibsink_cases():
+    """ibsink_solve (bregman_outer.py:191-281): Sinkhorn sweeps as the inner solver."""
+    # truncated at 6 outers: the Sinkhorn inner loop needs 10^4-10^5 sweeps to tol
+    cases = [("uniform", 14, 12, 0, 5e-2, 1e-8), ("square", 16, 16, 1, 2e-2, 1e-8), ("spherical", 12, 20, 2, 1e-1, 1e-9)]
+    for i, (kind, m, n, seed, eta, tol) in enumerate(cases):
+        p = problem(kind, m, n, seed)
+        cfg = core.SolverConfig(eta=eta, kkt_tol=tol, max_outer=6)
+        res = bregman_outer.ibsink_solve(p, cfg)
+        tr = res.trajectory.records
+        save(f"ibsink_{i}", C=p.cost, a=p.source_marginal, b=p.target_marginal, eta=eta, kkt_tol=tol,
+             objective=res.objective, kkt=res.kkt, outer_iters=res.outer_iters, rounded=res.rounded_plan,
+             final_log=res.final_logplan.log_entries, inner_total=np.array([r.inner_total for r in tr]),
+             traj_objective=np.array([r.objective for r in tr]), max_outer=6)
+
+
 def config_scalars():
     """BASELINE configs 1 and 2 (seed 0): the reference's end-to-end numbers."""
     out = {}
@@ -195,10 +210,10 @@ def config_scalars():
 
 if __name__ == "__main__":
     which = sys.argv[1:] or ["eval", "sparsify", "newton", "rounding", "candidate", "warm", "inner", "solve",
-                             "eot", "configs"]
+                             "eot", "ibsink", "configs"]
     fns = {"eval": eval_cases, "sparsify": sparsify_cases, "newton": newton_cases, "rounding": rounding_cases,
            "candidate": candidate_cases, "warm": warm_cases, "inner": inner_cases, "solve": solve_cases,
-           "eot": eot_cases, "configs": config_scalars}
+           "eot": eot_cases, "ibsink": ibsink_cases, "configs": config_scalars}
     for w in which:
         fns[w]()
         print("done", w)

@@ -407,3 +407,18 @@ def test_eot_single_solve_matches_reference(cuda, name):
     assert res.kkt == pytest.approx(float(g["kkt"]), rel=1e-6)
     assert rel(res.rounded_plan, g["rounded"]) <= 1e-7
     assert rec.grad_norm <= float(g["kkt_tol"])
+
+
+@pytest.mark.parametrize("name", golden_names("ibsink"))
+def test_ibsink_solve_matches_reference(cuda, name):
+    """ibsink_solve (Sinkhorn sweeps as the inner solver) on the device
+    against the reference's run: same outers, same sweep counts per outer,
+    objectives within the BASELINE gate."""
+    P = _api()
+    g = golden(name)
+    cfg = P.SolverConfig(eta=float(g["eta"]), kkt_tol=float(g["kkt_tol"]), max_outer=int(g["max_outer"]))
+    res = P.ibsink_solve(problem_of(g), cfg)
+    assert res.outer_iters == int(g["outer_iters"])
+    assert [r.inner_total for r in res.trajectory.records] == list(g["inner_total"])
+    np.testing.assert_allclose([r.objective for r in res.trajectory.records], g["traj_objective"], rtol=1e-8)
+    assert rel(res.rounded_plan, g["rounded"]) <= 1e-8

@@ -177,3 +177,15 @@ def test_oracle_eot_matches_reference(name):
     assert obj == pytest.approx(float(g["objective"]), rel=1e-12)
     assert kkt == pytest.approx(float(g["kkt"]), rel=1e-9)
     assert np.max(np.abs(rounded - g["rounded"])) <= 1e-12
+
+
+@pytest.mark.parametrize("name", golden_names("ibsink"))
+def test_oracle_ibsink_matches_reference(name):
+    """ibsink_solve (bregman_outer.py:191-281) restated by the oracle."""
+    g = golden(name)
+    log_x, rounded, obj, kkt, outer, sweeps, recs = O.ibsink_solve(g["C"], g["a"], g["b"], float(g["eta"]),
+                                                                   float(g["kkt_tol"]), max_outer=int(g["max_outer"]))
+    assert outer == int(g["outer_iters"])
+    assert [r["inner_total"] for r in recs] == list(g["inner_total"])
+    assert obj == pytest.approx(float(g["objective"]), rel=1e-12)
+    assert np.max(np.abs(rounded - g["rounded"])) <= 1e-12
