@@ -45,6 +45,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK_GBS = 6650.0
+E2E_DEFAULT = 10
 
 
 def parse():
@@ -55,7 +56,7 @@ def parse():
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
     p.add_argument("--config", type=int, default=2)
     p.add_argument("--seed", type=int, default=0)
-    p.add_argument("--e2e-steps", type=int, default=10)
+    p.add_argument("--e2e-steps", type=int, default=E2E_DEFAULT)
     p.add_argument("--cpu-sample", type=float, default=15.0, help="seconds of CPU oracle work (cpu_baseline)")
     p.add_argument("--no-solve", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
@@ -72,7 +73,7 @@ def peaks():
 
 
 def workload_name(idx, inst):
-    m, n = inst.cost.shape
+    m, n = len(inst.a), len(inst.b)
     return f"{inst.name}: m={m} n={n} eta={inst.eta} tol={inst.kkt_tol}"
 
 
@@ -219,10 +220,20 @@ def run_ours(args):
 
         comm = RowComm()
 
-    inst = instances.config(args.config, args.seed)
-    m, n = inst.cost.shape
+    pts = instances.config_points(args.config, args.seed)
+    m, n = len(pts.a), len(pts.b)
+    # configs 4-5 (C is 8.6 / 20 GB): C built on the GPU, bit-identical to the
+    # host recipe (instances.device_cost), no m x n host array; those runs
+    # skip the CPU arm, the e2e line (unless --e2e-steps is given) and the solve
+    big = m * n >= 5e8
+    if big:
+        inst = instances.Instance(pts.name, None, pts.a, pts.b, pts.eta, pts.kkt_tol)
+        cost_dev = instances.device_cost(pts, dev, rows=None, ld=(n + 31) // 32 * 32)
+    else:
+        inst = pts.build()
+        cost_dev = torch.from_numpy(inst.cost).to(dev)
     cfg = SolverConfig(eta=inst.eta, kkt_tol=inst.kkt_tol, max_inner=1)
-    prob = OtProblem(torch.from_numpy(inst.cost).to(dev), inst.a, inst.b)
+    prob = OtProblem(cost_dev, inst.a, inst.b)
     s = session_for(prob, inst.eta, comm)
     X0 = s.new_plan()
     s.ops.init_plan(X0)
@@ -298,43 +309,49 @@ def run_ours(args):
 
     # end to end through the public API with pinned host buffers
     m_loc = s.m_loc
-    C_pin = torch.from_numpy(inst.cost).pin_memory()
-    lx_host = np.log(inst.a)[s.row_begin:s.row_end, None] + np.log(inst.b)[None, :]
-    lx_pin = torch.from_numpy(np.maximum(lx_host, -1e6)).pin_memory()
-    g_pin = g0[:n].cpu().pin_memory()
+    e2e = None
+    if big and args.e2e_steps == E2E_DEFAULT:
+        args.e2e_steps = 0
+    host_cost = (inst.cost if inst.cost is not None else cost_dev.cpu().numpy()) if args.e2e_steps > 0 else None
+    C_pin = torch.from_numpy(np.ascontiguousarray(host_cost)).pin_memory() if host_cost is not None else None
+    e2e_steps = args.e2e_steps
+    if e2e_steps > 0:
+        lx_host = np.log(inst.a)[s.row_begin:s.row_end, None] + np.log(inst.b)[None, :]
+        lx_pin = torch.from_numpy(np.maximum(lx_host, -1e6)).pin_memory()
+        g_pin = g0[:n].cpu().pin_memory()
     torch.cuda.synchronize()
-    e2e_steps = max(1, args.e2e_steps)
 
-    def e2e_step():
-        # inputs from pinned host memory every step; the step's result read back
-        # to the host: the dual (n doubles) and the report's objective / kkt.
-        # The candidate plan stays in HBM, as ibsn_solve keeps it.
-        hprob = OtProblem(C_pin, inst.a, inst.b)
-        gs, cand, rep = inner_solve(LogPlan(lx_pin), DualState(g_pin), hprob, cfg, mu_k=1e3, outer_k=0, comm=comm)
-        return np.asarray(gs.gamma).sum() + rep.objective + rep.kkt
+    if e2e_steps > 0:
+        def e2e_step():
+            # inputs from pinned host memory every step; the step's result read back
+            # to the host: the dual (n doubles) and the report's objective / kkt.
+            # The candidate plan stays in HBM, as ibsn_solve keeps it.
+            hprob = OtProblem(C_pin, inst.a, inst.b)
+            gs, cand, rep = inner_solve(LogPlan(lx_pin), DualState(g_pin), hprob, cfg, mu_k=1e3, outer_k=0, comm=comm)
+            return np.asarray(gs.gamma).sum() + rep.objective + rep.kkt
 
-    for _ in range(nwarm):      # first call pays context creation and pinned-buffer allocation
-        e2e_step()
-    torch.cuda.synchronize()
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        e2e_step()
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e = {"value": e2e_steps / e2e_s, "unit": "newton_it/s",
-           "h2d_bytes_per_step": int(8 * m_loc * n * 2 + 8 * (m + 2 * n)),
-           "d2h_bytes_per_step": int(8 * n + 8 * 16),
-           "path": "inner_solve(LogPlan(pinned host), DualState(pinned host), OtProblem(pinned host C), "
-                   "max_inner=1): H2D of C, log X, marginals, dual; D2H of the dual and the report scalars "
-                   "(the candidate plan stays in HBM, as in ibsn_solve)"}
+        for _ in range(nwarm):      # first call pays context creation and pinned-buffer allocation
+            e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": e2e_steps / e2e_s, "unit": "newton_it/s",
+               "h2d_bytes_per_step": int(8 * m_loc * n * 2 + 8 * (m + 2 * n)),
+               "d2h_bytes_per_step": int(8 * n + 8 * 16),
+               "path": "inner_solve(LogPlan(pinned host), DualState(pinned host), OtProblem(pinned host C), "
+                       "max_inner=1): H2D of C, log X, marginals, dual; D2H of the dual and the report scalars "
+                       "(the candidate plan stays in HBM, as in ibsn_solve)"}
 
     solve = None
-    if not args.no_solve:
+    if not args.no_solve and not big:
         from paper_2603_07156_b200.bregman_outer import ibsn_solve
 
         sprob = OtProblem(torch.from_numpy(inst.cost).to(dev), inst.a, inst.b)
@@ -352,7 +369,7 @@ def run_ours(args):
                  "newton_it_per_s": res.newton_iters / (e0.elapsed_time(e1) / 1e3)}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and not big:
         cpu = cpu_baseline(inst, args.cpu_sample)
 
     if rank == 0:

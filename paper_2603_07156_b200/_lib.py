@@ -79,6 +79,8 @@ SIGNATURES = {
     "otb_materialize_p": (C.c_int, [vp, vp, vp, vp, i64]),
     "otb_info": (C.c_int, [vp, C.POINTER(i64)]),
     "otb_launch_count": (C.c_int, [vp, C.POINTER(i64)]),
+    "otb_sq_dist": (C.c_int, [vp, vp, i64, i64, C.c_int, i64, vp, i64, C.POINTER(dbl), vp]),
+    "otb_scale_cost": (C.c_int, [vp, i64, i64, i64, dbl, vp]),
     "otb_selftest_div": (C.c_int, [vp, i64, dbl, vp]),
     "otb_selftest_log": (C.c_int, [vp, i64, vp]),
     "otb_cg_trace": (C.c_int, [vp, vp, i64, C.POINTER(i64)]),

@@ -31,10 +31,13 @@ def _as_float_array(x, ndim: int):
     if _is_torch(x):
         import torch
 
-        t = x.detach().to(torch.float64).contiguous()
+        t = x.detach().to(torch.float64)
         if t.dim() != ndim:
             raise ShapeMismatch(f"expected {ndim}-dimensional array, got shape {tuple(t.shape)}")
-        return t
+        # row-major with padded rows (stride (ld, 1), ld >= n) is kept as is:
+        # the device path reads such a matrix in place
+        padded_rows = ndim == 2 and t.stride(1) == 1 and t.stride(0) >= t.shape[1]
+        return t if padded_rows else t.contiguous()
     arr = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
     if arr.ndim != ndim:
         raise ShapeMismatch(f"expected {ndim}-dimensional array, got shape {arr.shape}")

@@ -322,6 +322,44 @@ __global__ void k_scaled_plan(const double* __restrict__ C, const double* __rest
   if (nb) atomicAdd(bad, nb);
 }
 
+// On-device instance construction: C_rj = sum_k (x_rk -
+// y_jk)^2 over the coordinates in order (numpy's axis-sum of d*d), rows
+// [row0, row0 + m_loc) of x; the local maximum goes to *peak (as ordered
+// bits: C >= 0).  --fmad=false keeps every product and sum one rounding,
+// so the matrix equals numpy's bit for bit.
+__global__ void k_sq_dist(const double* __restrict__ x, const double* __restrict__ y, int m_loc, int n, int dim,
+                          int64_t row0, double* __restrict__ C, int64_t ld, unsigned long long* peak) {
+  const int64_t total = (int64_t)m_loc * n;
+  double mx = 0.0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n), j = (int)(idx % n);
+    const double* xr = x + (row0 + r) * dim;
+    const double* yj = y + (int64_t)j * dim;
+    double acc = 0.0;
+    for (int k = 0; k < dim; ++k) {
+      const double d = xr[k] - yj[k];
+      acc = (k == 0) ? d * d : acc + d * d;
+    }
+    C[(size_t)r * ld + j] = acc;
+    mx = fmax(mx, acc);
+  }
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) atomicMax(peak, (unsigned long long)__double_as_longlong(mx));
+}
+
+// C /= peak (core.py:174: cost / peak), skipped when peak == 0.
+__global__ void k_scale_cost(double* C, int64_t ld, int m_loc, int n, double peak) {
+  if (peak == 0.0) return;
+  const Divider D(peak);
+  const int64_t total = (int64_t)m_loc * n;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n), j = (int)(idx % n);
+    C[(size_t)r * ld + j] = D(C[(size_t)r * ld + j]);
+  }
+}
+
 // Test hook for log_fast (common.cuh).
 __global__ void k_selftest_log(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

@@ -743,6 +743,31 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
       return fail(OTB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     }
   }
+  // Clusters must fit in a GPC: with cl > 1 fewer than sms / cl clusters may
+  // be co-resident, and a second wave would double every dense pass.  Size
+  // the row blocks to the clusters that actually run at once.
+  if (cl > 1) {
+    int fit = c->ncl;
+    for (int k = 0; k < DK_COUNT; ++k) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)c->grid);
+      cfg.blockDim = dim3((unsigned)(c->nt + 32));
+      cfg.dynamicSmemBytes = c->smem[k];
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = (unsigned)cl;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int nclus = 0;
+      if (cudaOccupancyMaxActiveClusters(&nclus, kDenseFn[k][c->ns], &cfg) == cudaSuccess && nclus > 0)
+        fit = std::min(fit, nclus);
+      cudaGetLastError();
+    }
+    c->ncl = std::max(1, fit);
+    c->grid = c->ncl * cl;
+  }
   // hess_apply variant: shared-memory group accumulators (NG groups of
   // 512/NG threads, as many as fit) or, for very wide n, global RED.
   const int64_t npad = rup(n, 2);
@@ -1317,6 +1342,42 @@ int otb_selftest_log(const double* x, int64_t n, double* out) {
   k_selftest_log<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256>>>(x, n, out);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaDeviceSynchronize());
+  return OTB_OK;
+}
+
+int otb_sq_dist(const double* x, const double* y, int64_t m_loc, int64_t n, int dim, int64_t row0, double* C,
+                int64_t ld, double* local_peak, void* stream) {
+  if (!x || !y || !C || !local_peak || dim < 1 || m_loc < 0 || n < 1 || ld < n) return fail(OTB_ERR_ARG, "bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned long long* dpeak = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&dpeak, sizeof(unsigned long long), st));
+  CUDA_TRY(cudaMemsetAsync(dpeak, 0, sizeof(unsigned long long), st));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (m_loc > 0) {
+    k_sq_dist<<<sms * 8, 256, 0, st>>>(x, y, (int)m_loc, (int)n, dim, row0, C, ld, dpeak);
+    CUDA_TRY(cudaGetLastError());
+  }
+  unsigned long long bits = 0;
+  CUDA_TRY(cudaMemcpyAsync(&bits, dpeak, sizeof bits, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  cudaFreeAsync(dpeak, st);
+  std::memcpy(local_peak, &bits, sizeof(double));
+  return OTB_OK;
+}
+
+int otb_scale_cost(double* C, int64_t m_loc, int64_t n, int64_t ld, double peak, void* stream) {
+  if (!C || ld < n) return fail(OTB_ERR_ARG, "bad arguments");
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (m_loc > 0) {
+    k_scale_cost<<<sms * 8, 256, 0, st>>>(C, ld, (int)m_loc, (int)n, peak);
+    CUDA_TRY(cudaGetLastError());
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
   return OTB_OK;
 }
 

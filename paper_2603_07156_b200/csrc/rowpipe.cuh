@@ -209,13 +209,13 @@ struct Dense {
     const int q = xcount & 1;
     const uint32_t par = (uint32_t)((xcount >> 1) & 1);
     double* mine = sm.xbuf + (q * kMaxCluster + cr) * 4;
-    if (tid == 0) {
-      for (int rk = 0; rk < g.cl; ++rk) {
-        const uint32_t dst = mapa(smem_u32(mine), (uint32_t)rk);
+    if (warp == 0 && lane < g.cl) {   // lane rk serves cluster rank rk: the remote ops go out in parallel
+      const uint32_t dst = mapa(smem_u32(mine), (uint32_t)lane);
 #pragma unroll
-        for (int k = 0; k < K; ++k) st_cluster_f64(dst + 8u * k, v[k]);
-        mbar_arrive_remote(mapa(smem_u32(&sm.xbar[q]), (uint32_t)rk));
-      }
+      for (int k = 0; k < K; ++k) st_cluster_f64(dst + 8u * k, v[k]);
+      mbar_arrive_remote(mapa(smem_u32(&sm.xbar[q]), (uint32_t)lane));
+    }
+    if (tid == 0) {
       while (!mbar_try_wait_cluster(&sm.xbar[q], par)) {
       }
     }

@@ -343,13 +343,12 @@ struct ClusterDots {
   OTB_DEV void send(const double (&v)[R]) {
     const int q = nsend % kXBufs;
     double* base = xbuf + q * 16 * 4;
-    if (threadIdx.x == 0) {
-      for (int rk = 0; rk < W; ++rk) {
-        const uint32_t dst = mapa(smem_u32(base + cr * 4), (uint32_t)rk);
+    if (threadIdx.x < W) {            // thread rk serves cluster rank rk, in parallel
+      const uint32_t rk = threadIdx.x;
+      const uint32_t dst = mapa(smem_u32(base + cr * 4), rk);
 #pragma unroll
-        for (int k = 0; k < R; ++k) st_cluster_f64(dst + 8u * k, v[k]);
-        mbar_arrive_remote(mapa(smem_u32(&xbar[q]), (uint32_t)rk));
-      }
+      for (int k = 0; k < R; ++k) st_cluster_f64(dst + 8u * k, v[k]);
+      mbar_arrive_remote(mapa(smem_u32(&xbar[q]), rk));
     }
     ++nsend;
   }

@@ -73,19 +73,42 @@ def _gmm(rng, count, comps, dim, std):
     return means[label] + std * rng.standard_normal((count, dim))
 
 
-def uniform2d(m: int, n: int, seed: int, eta: float = 1e-2, tol: float = 1e-6, name=None) -> Instance:
+@dataclass(frozen=True)
+class PointInstance:
+    """The points and marginals an Instance is built from (cost = squared
+    Euclidean distances, normalised to max 1 when `normalised`)."""
+    name: str
+    x: np.ndarray
+    y: np.ndarray
+    a: np.ndarray
+    b: np.ndarray
+    normalised: bool
+    eta: float
+    kkt_tol: float
+
+    def build(self) -> "Instance":
+        cost = sq_dist(self.x, self.y)
+        if self.normalised:
+            cost = normalise(cost)
+        return Instance(self.name, cost, self.a, self.b, self.eta, self.kkt_tol)
+
+
+def uniform2d_points(m: int, n: int, seed: int, eta: float = 1e-2, tol: float = 1e-6, name=None) -> PointInstance:
     """Configs 1 and 5: points U[0,1]^2, normalised squared distance,
     random positive marginals."""
     rng = np.random.default_rng(seed)
     x = rng.random((m, 2))
     y = rng.random((n, 2))
-    cost = normalise(sq_dist(x, y))
     a = positive_uniform(rng, m)
     b = positive_uniform(rng, n)
-    return Instance(name or f"uniform2d-{m}x{n}-s{seed}", cost, a / a.sum(), b / b.sum(), eta, tol)
+    return PointInstance(name or f"uniform2d-{m}x{n}-s{seed}", x, y, a / a.sum(), b / b.sum(), True, eta, tol)
 
 
-def grid_histograms(side: int, seed: int, eta: float = 1e-2, tol: float = 1e-6, sigma: float = 3.0) -> Instance:
+def uniform2d(m: int, n: int, seed: int, eta: float = 1e-2, tol: float = 1e-6, name=None) -> Instance:
+    return uniform2d_points(m, n, seed, eta, tol, name).build()
+
+
+def grid_points(side: int, seed: int, eta: float = 1e-2, tol: float = 1e-6, sigma: float = 3.0) -> PointInstance:
     """Config 2: side x side pixel grid, unnormalised squared distance,
     marginals exp(gaussian_filter(N(0,1))) + 1e-6 normalised."""
     from scipy.ndimage import gaussian_filter
@@ -93,52 +116,104 @@ def grid_histograms(side: int, seed: int, eta: float = 1e-2, tol: float = 1e-6, 
     rng = np.random.default_rng(seed)
     r, c = np.divmod(np.arange(side * side), side)
     pts = np.stack(((r + 0.5) / side, (c + 0.5) / side), axis=1)
-    cost = sq_dist(pts, pts)
     ha = np.exp(gaussian_filter(rng.standard_normal((side, side)), sigma)) + 1e-6
     hb = np.exp(gaussian_filter(rng.standard_normal((side, side)), sigma)) + 1e-6
     a = ha.ravel()
     b = hb.ravel()
-    return Instance(f"grid{side}-s{seed}", cost, a / a.sum(), b / b.sum(), eta, tol)
+    return PointInstance(f"grid{side}-s{seed}", pts, pts, a / a.sum(), b / b.sum(), False, eta, tol)
 
 
-def gmm_clouds(m: int, n: int, seed: int, eta: float = 5e-3, tol: float = 1e-7) -> Instance:
+def grid_histograms(side: int, seed: int, eta: float = 1e-2, tol: float = 1e-6, sigma: float = 3.0) -> Instance:
+    return grid_points(side, seed, eta, tol, sigma).build()
+
+
+def gmm_points(m: int, n: int, seed: int, eta: float = 5e-3, tol: float = 1e-7) -> PointInstance:
     """Config 3: two 8-component 3-D Gaussian mixtures (std 0.05),
     normalised squared distance, uniform marginals."""
     rng = np.random.default_rng(seed)
     x = _gmm(rng, m, 8, 3, 0.05)
     y = _gmm(rng, n, 8, 3, 0.05)
-    cost = normalise(sq_dist(x, y))
-    return Instance(f"gmm3d-{m}x{n}-s{seed}", cost, np.full(m, 1.0 / m), np.full(n, 1.0 / n), eta, tol)
+    return PointInstance(f"gmm3d-{m}x{n}-s{seed}", x, y, np.full(m, 1.0 / m), np.full(n, 1.0 / n), True, eta, tol)
 
 
-def colour_transfer(m: int, n: int, seed: int, eta: float = 1e-2, tol: float = 1e-6) -> Instance:
+def gmm_clouds(m: int, n: int, seed: int, eta: float = 5e-3, tol: float = 1e-7) -> Instance:
+    return gmm_points(m, n, seed, eta, tol).build()
+
+
+def colour_points(m: int, n: int, seed: int, eta: float = 1e-2, tol: float = 1e-6) -> PointInstance:
     """Config 4: source RGB from a 16-component GMM (std 0.05) clipped to
     [0,1]^3, target RGB uniform, unnormalised squared distance, uniform
     marginals."""
     rng = np.random.default_rng(seed)
     x = np.clip(_gmm(rng, m, 16, 3, 0.05), 0.0, 1.0)
     y = rng.random((n, 3))
-    cost = sq_dist(x, y)
-    return Instance(f"colour-{m}x{n}-s{seed}", cost, np.full(m, 1.0 / m), np.full(n, 1.0 / n), eta, tol)
+    return PointInstance(f"colour-{m}x{n}-s{seed}", x, y, np.full(m, 1.0 / m), np.full(n, 1.0 / n), False, eta, tol)
+
+
+def colour_transfer(m: int, n: int, seed: int, eta: float = 1e-2, tol: float = 1e-6) -> Instance:
+    return colour_points(m, n, seed, eta, tol).build()
+
+
+def config_points(idx: int, seed: int = 0) -> PointInstance:
+    """The points and marginals of BASELINE.json configuration ``idx``."""
+    c = CONFIGS[idx]
+    name = f"{c['name']}-s{seed}"
+    if idx == 1:
+        p = uniform2d_points(1000, 1000, seed, c["eta"], c["tol"])
+    elif idx == 2:
+        p = grid_points(64, seed, c["eta"], c["tol"])
+    elif idx == 3:
+        p = gmm_points(10000, 10000, seed, c["eta"], c["tol"])
+    elif idx == 4:
+        p = colour_points(65536, 16384, seed, c["eta"], c["tol"])
+    elif idx == 5:
+        p = uniform2d_points(50000, 50000, seed, c["eta"], c["tol"])
+    else:
+        raise KeyError(idx)
+    return PointInstance(name, p.x, p.y, p.a, p.b, p.normalised, p.eta, p.kkt_tol)
 
 
 def config(idx: int, seed: int = 0) -> Instance:
-    """The BASELINE.json configuration ``idx`` (1-based) at ``seed``."""
-    c = CONFIGS[idx]
-    if idx == 1:
-        return uniform2d(1000, 1000, seed, c["eta"], c["tol"], name=f"{c['name']}-s{seed}")
-    if idx == 2:
-        inst = grid_histograms(64, seed, c["eta"], c["tol"])
-        return Instance(f"{c['name']}-s{seed}", inst.cost, inst.a, inst.b, inst.eta, inst.kkt_tol)
-    if idx == 3:
-        inst = gmm_clouds(10000, 10000, seed, c["eta"], c["tol"])
-        return Instance(f"{c['name']}-s{seed}", inst.cost, inst.a, inst.b, inst.eta, inst.kkt_tol)
-    if idx == 4:
-        inst = colour_transfer(65536, 16384, seed, c["eta"], c["tol"])
-        return Instance(f"{c['name']}-s{seed}", inst.cost, inst.a, inst.b, inst.eta, inst.kkt_tol)
-    if idx == 5:
-        return uniform2d(50000, 50000, seed, c["eta"], c["tol"], name=f"{c['name']}-s{seed}")
-    raise KeyError(idx)
+    """The BASELINE.json configuration ``idx`` (1-based) at ``seed``, built on the host."""
+    return config_points(idx, seed).build()
+
+
+def device_cost(points: PointInstance, device, rows: tuple[int, int] | None = None, ld: int | None = None,
+                comm=None):
+    """Rows [r0, r1) of the instance's cost matrix built on the GPU by libotb
+    (otb_sq_dist + otb_scale_cost): bit-identical to ``points.build().cost``
+    without the m x n host array.  Returns a (r1 - r0, n) float64 CUDA
+    tensor (a view of an (r1 - r0, ld) buffer when ld > n).  Multi-rank:
+    the normalising peak is max-reduced over `comm` (torch.distributed)."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+
+    m, n = points.x.shape[0], points.y.shape[0]
+    r0, r1 = rows if rows is not None else (0, m)
+    ld = n if ld is None else ld
+    dim = points.x.shape[1]
+    x = torch.from_numpy(np.ascontiguousarray(points.x)).to(device)
+    y = torch.from_numpy(np.ascontiguousarray(points.y)).to(device)
+    buf = torch.empty((r1 - r0, ld), dtype=torch.float64, device=device)
+    if ld > n:
+        buf[:, n:].zero_()
+    stream = torch.cuda.current_stream(device).cuda_stream
+    peak = C.c_double()
+    _lib.check(_lib.lib.otb_sq_dist(x.data_ptr(), y.data_ptr(), r1 - r0, n, dim, r0, buf.data_ptr(), ld,
+                                    C.byref(peak), C.c_void_p(stream)))
+    if points.normalised:
+        p = peak.value
+        if comm is not None and getattr(comm, "world", 1) > 1:
+            import torch.distributed as dist
+
+            t = torch.tensor([p], dtype=torch.float64, device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            p = float(t.item())
+        _lib.check(_lib.lib.otb_scale_cost(buf.data_ptr(), r1 - r0, n, ld, p, C.c_void_p(stream)))
+    return buf[:, :n] if ld > n else buf
 
 
 def small_uniform(m: int, n: int, seed: int) -> tuple[np.ndarray, np.ndarray, np.ndarray]:

@@ -63,12 +63,22 @@ class Session:
         b_h = host(problem.target_marginal)
         if a_h.shape[0] != m or b_h.shape[0] != n:
             raise ShapeMismatch("marginal lengths do not match the cost matrix")
-        # padded local rows of C
-        self.C = torch.empty((self.m_loc, self.ld), dtype=f64, device=dev)
-        if self.ld > n:
-            self.C[:, n:].zero_()
+        # padded local rows of C (a CUDA cost that already has this layout —
+        # e.g. instances.device_cost with ld — is used in place, not copied)
         rows = slice(self.row_begin, self.row_end)
-        if _is_torch(cost):
+        adopt = (_is_torch(cost) and cost.is_cuda and cost.device == dev and cost.dtype == f64
+                 and cost.stride() == (self.ld, 1) and self.m_loc == m and cost.storage_offset() == 0
+                 and cost.untyped_storage().nbytes() >= self.m_loc * self.ld * 8)
+        if adopt:
+            self.C = torch.as_strided(cost, (self.m_loc, self.ld), (self.ld, 1))
+        else:
+            self.C = torch.empty((self.m_loc, self.ld), dtype=f64, device=dev)
+            if self.ld > n:
+                self.C[:, n:].zero_()
+        if adopt:
+            sq = torch.linalg.vector_norm(self.C).reshape(1) ** 2
+            self.norm_c = float(torch.sqrt(sq))
+        elif _is_torch(cost):
             self.C[:, :n].copy_(cost[rows], non_blocking=True)
             sq = torch.linalg.vector_norm(self.C).reshape(1) ** 2   # ||C||_F^2 of the local rows
             if comm is not None and comm.world > 1:

@@ -422,3 +422,27 @@ def test_ibsink_solve_matches_reference(cuda, name):
     assert [r.inner_total for r in res.trajectory.records] == list(g["inner_total"])
     np.testing.assert_allclose([r.objective for r in res.trajectory.records], g["traj_objective"], rtol=1e-8)
     assert rel(res.rounded_plan, g["rounded"]) <= 1e-8
+
+
+@pytest.mark.parametrize("kind", ["uniform2d", "gmm", "colour", "grid"])
+def test_device_cost_construction_is_bitwise_numpy(cuda, kind):
+    """instances.device_cost (otb_sq_dist + otb_scale_cost) builds the cost
+    matrix on the GPU bit-identically to the host numpy recipe, including a
+    row sub-range into a padded buffer (one rank's shard)."""
+    import torch
+
+    from paper_2603_07156_b200 import instances as I
+
+    pts = {"uniform2d": lambda: I.uniform2d_points(300, 211, 4), "gmm": lambda: I.gmm_points(150, 170, 5),
+           "colour": lambda: I.colour_points(200, 97, 6), "grid": lambda: I.grid_points(16, 7)}[kind]()
+    host = pts.build().cost
+    dev = I.device_cost(pts, torch.device("cuda", 0)).cpu().numpy()
+    assert np.array_equal(dev.view(np.uint64), host.view(np.uint64))
+    m, n = host.shape
+    r0, r1 = m // 3, m // 3 + 17
+    part = I.device_cost(pts, torch.device("cuda", 0), rows=(r0, r1), ld=(n + 31) // 32 * 32)
+    if pts.normalised:   # without a comm a shard normalises by its own peak
+        want = I.normalise(I.sq_dist(pts.x[r0:r1], pts.y))
+    else:
+        want = host[r0:r1]
+    assert np.array_equal(part.cpu().numpy().view(np.uint64), want.view(np.uint64))
