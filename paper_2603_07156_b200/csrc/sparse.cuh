@@ -565,6 +565,7 @@ OTB_DEV void st_row(const uint4* words, const double* vals, int k, int base, uns
                     const double (&v)[2 * NQ], double (&acc)[2 * NQ], double& dot, double w,
                     double (*val)[2 * NQ] = nullptr) {
   const int warp = threadIdx.x >> 5;
+  double d0 = 0.0, d1 = 0.0;   // two independent fma chains for the dot
 #pragma unroll
   for (int t = 0; t < NQ; ++t) {
     const uint4 wd = words[k * kStWords + warp + CW * t];
@@ -576,8 +577,8 @@ OTB_DEV void st_row(const uint4* words, const double* vals, int k, int base, uns
     double e0 = vals[idx], e1 = vals[idx + 1];
     bm_select(wd, lb, e0, e1);
     if constexpr (DOT) {
-      dot = fma(e0, v[2 * t], dot);
-      dot = fma(e1, v[2 * t + 1], dot);
+      d0 = fma(e0, v[2 * t], d0);
+      d1 = fma(e1, v[2 * t + 1], d1);
       if (val != nullptr) {
         (*val)[2 * t] = e0;
         (*val)[2 * t + 1] = e1;
@@ -587,6 +588,7 @@ OTB_DEV void st_row(const uint4* words, const double* vals, int k, int base, uns
       acc[2 * t + 1] = fma(e1, w, acc[2 * t + 1]);
     }
   }
+  if constexpr (DOT) dot += d0 + d1;
 }
 
 // Consumers (512 threads): the same batches.  Single CTA: the values of a

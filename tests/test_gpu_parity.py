@@ -446,3 +446,62 @@ def test_device_cost_construction_is_bitwise_numpy(cuda, kind):
     else:
         want = host[r0:r1]
     assert np.array_equal(part.cpu().numpy().view(np.uint64), want.view(np.uint64))
+
+
+def test_config3_first_newton_step_vs_oracle(cuda):
+    """BASELINE config 3 (10000^2, cluster-split rows, warp-group hess_apply):
+    the first Newton step from X0 = a b^T, gamma = 0 against the CPU oracle
+    (~30 s on the host), plus size-independent properties at full size:
+    1^T g = 0, H_rho 1 = 0, determinism of eval and hess_apply."""
+    import torch
+
+    P = _api()
+    from paper_2603_07156_b200 import instances
+    from paper_2603_07156_b200.session import session_for
+
+    inst = instances.config(3, 0)
+    m, n = inst.cost.shape
+    dev = torch.device("cuda", 0)
+    prob = P.OtProblem(torch.from_numpy(inst.cost).to(dev), inst.a, inst.b)
+    s = session_for(prob, inst.eta)
+    X0 = s.new_plan()
+    s.ops.init_plan(X0)
+    g = s.new_vec()
+    v1, gn1 = s.ops.eval(X0, g)
+    grad = s.new_vec()
+    v2, gn2 = s.ops.eval(X0, g, grad_out=grad)
+    assert (v1, gn1) == (v2, gn2)                                       # deterministic
+    assert abs(float(grad[:n].sum())) <= 1e-13                          # 1^T g = 0 (SPEC.md:145)
+    rho = inst.eta * gn1 / (m * n)
+    s.ops.sparsify(X0, g, rho)
+    ones = s._vec(np.ones(n))
+    out = s.new_vec()
+    s.ops.hess_apply(ones, 0.0, out)
+    assert float(out[:n].abs().max()) <= 1e-10 / inst.eta                # H_rho 1 = 0 (SPEC.md:218)
+    h1 = s.new_vec()
+    s.ops.hess_apply(ones, 0.0, h1)
+    assert torch.equal(out, h1)
+    g2 = s.new_vec()
+    s.ops.eval(X0, g)
+    r = s.ops.newton_step(X0, g, g2, 1e-4, 0.8, 1e-10, None)
+    lx = np.log(inst.a)[:, None] + np.log(inst.b)[None, :]
+    gr, tr, itr = O.newton_step(lx, inst.cost, inst.a, inst.b, np.zeros(n), inst.eta)
+    assert float(r.t) == tr and abs(int(r.cg_iters) - itr) <= 1
+    assert rel(g2[:n].cpu().numpy(), gr) <= 1e-8
+
+
+def test_config2_solve_rounded_marginals_and_determinism(cuda):
+    """BASELINE config 2 at full size: the rounded plan meets both marginals
+    to 1e-12 (SPEC acceptance #9) and two solves give identical bits."""
+    P = _api()
+    from paper_2603_07156_b200 import instances
+
+    inst = instances.config(2, 0)
+    cfg = P.SolverConfig(eta=inst.eta, kkt_tol=inst.kkt_tol)
+    r1 = P.ibsn_solve(P.OtProblem(inst.cost, inst.a, inst.b), cfg)
+    r2 = P.ibsn_solve(P.OtProblem(inst.cost, inst.a, inst.b), cfg)
+    assert r1.objective == r2.objective and r1.cg_iters == r2.cg_iters
+    R = r1.rounded_plan
+    assert np.max(np.abs(R.sum(axis=1) - inst.a)) <= 1e-12
+    assert np.max(np.abs(R.sum(axis=0) - inst.b)) <= 1e-12
+    assert R.min() >= -1e-18        # e_r e_c^T / deficit can carry rounding-level negatives, in the reference too
