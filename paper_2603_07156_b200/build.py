@@ -51,7 +51,8 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and up_to_date():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, f"-I{REPO / 'include'}", "-o", str(LIB) + ".tmp",
+    extra = os.environ.get("OTB_NVCC_EXTRA", "").split()     # experiments, e.g. -DOTB_DENSE_MINB=2
+    cmd = [_nvcc(), *NVCC_FLAGS, *extra, f"-I{REPO / 'include'}", "-o", str(LIB) + ".tmp",
            str(CSRC / "otb.cu"), "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)

@@ -7,6 +7,9 @@
 namespace otb {
 
 constexpr int kMaxThreads = 544;   // 512 consumers + 1 producer warp
+#ifndef OTB_DENSE_MINB
+#define OTB_DENSE_MINB 1           // CTAs per SM the register allocation is sized for
+#endif
 constexpr int kTabInts = 2 * kMaxNS * 32;
 
 // ---------------------------------------------------------------- eval (K1)
@@ -27,7 +30,7 @@ struct EvalIO {
 };
 
 template <int NS>
-__global__ void __launch_bounds__(kMaxThreads, 1) k_eval(Geom geo, EvalIO io) {
+__global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_eval(Geom geo, EvalIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
   Dense<2> D;
   D.setup(geo, smem);
@@ -146,7 +149,7 @@ struct SparsifyIO {
 // FROMP: stream the P stored by the eval of the same gamma (one matrix, no
 // exp / division) instead of recomputing it from C and log X.
 template <int NS, bool FROMP>
-__global__ void __launch_bounds__(kMaxThreads, 1) k_sparsify(Geom geo, SparsifyIO io) {
+__global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom geo, SparsifyIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
   Dense<FROMP ? 1 : 2> D;
   D.setup(geo, smem);
@@ -410,7 +413,7 @@ struct TestAIO {
 };
 
 template <int NS>
-__global__ void __launch_bounds__(kMaxThreads, 1) k_test_a(Geom geo, TestAIO io) {
+__global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_a(Geom geo, TestAIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
   Dense<2> D;
   D.setup(geo, smem);
@@ -499,7 +502,7 @@ struct TestBIO {
 };
 
 template <int NS>
-__global__ void __launch_bounds__(kMaxThreads, 1) k_test_b(Geom geo, TestBIO io) {
+__global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_b(Geom geo, TestBIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
   Dense<1> D;
   D.setup(geo, smem);
@@ -557,7 +560,7 @@ struct TestCIO {
 };
 
 template <int NS, bool METRICS>
-__global__ void __launch_bounds__(kMaxThreads, 1) k_test_c(Geom geo, TestCIO io) {
+__global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_c(Geom geo, TestCIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
   Dense<METRICS ? 2 : 1> D;
   D.setup(geo, smem);
@@ -674,7 +677,7 @@ struct WarmZIO {
 };
 
 template <int NS>
-__global__ void __launch_bounds__(kMaxThreads, 1) k_warm_zeta(Geom geo, WarmZIO io) {
+__global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_warm_zeta(Geom geo, WarmZIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
   Dense<2> D;
   D.setup(geo, smem);
@@ -766,7 +769,7 @@ struct WarmGIO {
 };
 
 template <int NS>
-__global__ void __launch_bounds__(kMaxThreads, 1) k_warm_gamma(Geom geo, WarmGIO io) {
+__global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_warm_gamma(Geom geo, WarmGIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
   Dense<2> D;
   D.setup(geo, smem);
