@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
     const double dmin = (anc || !(rho > 0.0)) ? -INFINITY : (log_rho + (io.rowL[r] - M)) - 1e-9;
     double P[2 * NS];       // P_ij, or z - M for skipped entries (bit set in `skip`)
     unsigned keep = 0, skip = 0;
+    unsigned bb0[NS], bb1[NS];   // per-slice keep masks of the warp (ballots), reused by the write loop
     double ks = 0.0;
     int* tb = tab + rowpar * kMaxNS * 32;
 #pragma unroll
@@ -217,10 +218,11 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
           ks += p;
         }
       }
+      bb0[s] = bb1[s] = 0u;
       if (s < D.nsl) {
-        const unsigned b0 = __ballot_sync(0xffffffffu, (keep >> (2 * s)) & 1u);
-        const unsigned b1 = __ballot_sync(0xffffffffu, (keep >> (2 * s + 1)) & 1u);
-        if (D.lane == 0) tb[s * 32 + D.warp] = __popc(b0) + __popc(b1);
+        bb0[s] = __ballot_sync(0xffffffffu, (keep >> (2 * s)) & 1u);
+        bb1[s] = __ballot_sync(0xffffffffu, (keep >> (2 * s + 1)) & 1u);
+        if (D.lane == 0) tb[s * 32 + D.warp] = __popc(bb0[s]) + __popc(bb1[s]);
       }
     }
     double t[1] = {ks};
@@ -330,7 +332,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
 #pragma unroll
         for (int k = 0; k < 2 * NS; ++k) {
           if (D.col(k >> 1, k & 1) == jbest && P[k] >= 0.0) {
-            io.cols[wbase] = (uint16_t)jbest;
+            if (io.cols != nullptr) io.cols[wbase] = (uint16_t)jbest;
             io.vals[wbase] = 1.0;
             double2* a2 = D.acc2(0, k >> 1);
             if (k & 1) a2->y += ai * 1.0;
@@ -356,8 +358,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
         for (int s = 0; s < NS; ++s) {
           if (s < D.nsl) {
             const unsigned k0 = (keep >> (2 * s)) & 1u, k1 = (keep >> (2 * s + 1)) & 1u;
-            const unsigned b0 = __ballot_sync(0xffffffffu, k0);
-            const unsigned b1 = __ballot_sync(0xffffffffu, k1);
+            const unsigned b0 = bb0[s], b1 = bb1[s];
             const int base = __shfl_sync(0xffffffffu, excl + pre, s);
             const int off = base + __popc(b0 & lt) + __popc(b1 & lt);
             const int j = D.col(s, 0);
@@ -368,13 +369,13 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
             double2* a2 = D.acc2(0, s);
             if (k0) {
               const double v = anc ? P[2 * s] : DK(P[2 * s]);
-              io.cols[wbase + off] = (uint16_t)j;
+              if (io.cols != nullptr) io.cols[wbase + off] = (uint16_t)j;
               io.vals[wbase + off] = v;
               a2->x += ai * v;
             }
             if (k1) {
               const double v = anc ? P[2 * s + 1] : DK(P[2 * s + 1]);
-              io.cols[wbase + off + k0] = (uint16_t)(j + 1);
+              if (io.cols != nullptr) io.cols[wbase + off + k0] = (uint16_t)(j + 1);
               io.vals[wbase + off + k0] = v;
               a2->y += ai * v;
             }

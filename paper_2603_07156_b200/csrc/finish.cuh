@@ -360,6 +360,25 @@ __global__ void k_scale_cost(double* C, int64_t ld, int m_loc, int n, double pea
   }
 }
 
+// Column indices of the CSR rebuilt from the bitmap words (sparsify writes
+// only the words when hess_apply runs on the bitmap): one warp per (row,
+// word), lane l places columns 64q+2l(+1) at the positions hess_apply reads.
+__global__ void k_bm_cols(const uint4* __restrict__ bm, int nq, int m_loc, const int64_t* __restrict__ row_start,
+                          uint16_t* __restrict__ cols) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t total = (int64_t)m_loc * nq;
+  for (int64_t wi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; wi < total;
+       wi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int r = (int)(wi / nq), q = (int)(wi % nq);
+    const uint4 w = bm[wi];
+    const unsigned k0 = (w.x >> lane) & 1u, k1 = (w.y >> lane) & 1u;
+    const int64_t pos = row_start[r] + w.z + __popc(w.x & lt) + __popc(w.y & lt);
+    if (k0) cols[pos] = (uint16_t)(64 * q + 2 * lane);
+    if (k1) cols[pos + k0] = (uint16_t)(64 * q + 2 * lane + 1);
+  }
+}
+
 // Test hook for log_fast (common.cuh).
 __global__ void k_selftest_log(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

@@ -397,7 +397,9 @@ int do_sparsify(otb_ctx* c, const double* X, const double* gamma, double rho) {
     CUDA_TRY(cudaMemsetAsync(&c->ds->alloc, 0, 2 * sizeof(unsigned long long) + sizeof(int), c->stream));
     const int kind = c->p_valid ? DK_SPARSP : DK_SPARSIFY;
     Geom geo = c->p_valid ? make_geom(c, DK_SPARSP, c->Pbuf, nullptr) : make_geom(c, DK_SPARSIFY, c->C, X);
-    SparsifyIO io{gamma, c->a, c->eta, rho, anchor_local, c->rowM, c->rowS, c->lse, c->cols, c->vals, c->cap,
+    const bool bm_only = c->hv_mode == 2 || c->hv_mode == 3;   // hess_apply reads the bitmap, not the columns
+    SparsifyIO io{gamma, c->a, c->eta, rho, anchor_local, c->rowM, c->rowS, c->lse, bm_only ? nullptr : c->cols,
+                  c->vals, c->cap,
                   c->row_start, c->row_len, &c->ds->alloc, &c->ds->nnzc, c->chunk, c->colpart, &c->ds->flags,
                   (c->hv_mode == 2 || c->hv_mode == 3) ? c->bm : nullptr, c->nq};
     cudaEvent_t e0 = nullptr;
@@ -1055,6 +1057,10 @@ int otb_csr_export(otb_ctx* c, int64_t* row_ptr, int32_t* cols, double* vals, do
     CUDA_TRY(cudaMemcpyAsync(row_ptr, c->rowpre, sizeof(int64_t) * (c->m_loc + 1), cudaMemcpyDeviceToDevice,
                              c->stream));
   if (cols && vals) {
+    if (c->hv_mode == 2 || c->hv_mode == 3) {   // columns only live in the bitmap words
+      k_bm_cols<<<c->num_sms * 8, 256, 0, c->stream>>>(c->bm, c->nq, (int)c->m_loc, c->row_start, c->cols);
+      LAUNCH_CHECK();
+    }
     k_csr_compact<<<c->num_sms * 4, 256, 0, c->stream>>>((int)c->m_loc, c->row_start, c->row_len, c->rowpre, c->cols,
                                                          c->vals, cols, vals);
     LAUNCH_CHECK();

@@ -401,8 +401,22 @@ def test_eot_single_solve_matches_reference(cuda, name):
     g = golden(name)
     res = P.eot_single_solve(problem_of(g), P.SolverConfig(eta=float(g["eta"]), kkt_tol=float(g["kkt_tol"])))
     rec = res.trajectory.records[-1]
-    assert rec.inner_total == int(g["newton_iters"])
-    assert abs(rec.cg_total - int(g["cg_total"])) <= max(1, rec.inner_total)
+    # Armijo at the rounding floor: when sigma * slope of a reference step is
+    # below one ulp of the objective, its accept/backtrack decision is set by
+    # the last bit of a 576-term sum (eot_1: slope -2e-19 on f = 2.9e-2), so
+    # the step counts may differ; the gradient target and objective may not.
+    m, n = g["C"].shape
+    lx = np.zeros((m, n))
+    gam, _, _ = O.warm_start(lx, g["C"], g["a"], g["b"], float(g["eta"]), 1e-3)
+    ref = O.inner(lx, g["C"], g["a"], g["b"], gam, float(g["eta"]), 0.0, float(min(m, n)),
+                  grad_target=float(g["kkt_tol"]))
+    assert ref.newton_iters == int(g["newton_iters"])
+    floor = any(1e-4 * abs(st.slope) < np.spacing(v) for st, v in zip(ref.steps, ref.values))
+    if floor:
+        assert int(g["newton_iters"]) <= rec.inner_total <= int(g["newton_iters"]) + 4
+    else:
+        assert rec.inner_total == int(g["newton_iters"])
+        assert abs(rec.cg_total - int(g["cg_total"])) <= max(1, rec.inner_total)
     assert res.objective == pytest.approx(float(g["objective"]), rel=1e-8)      # the BASELINE gate
     assert res.kkt == pytest.approx(float(g["kkt"]), rel=1e-6)
     assert rel(res.rounded_plan, g["rounded"]) <= 1e-7
