@@ -340,7 +340,8 @@ int require_bound(const otb_ctx* c) {
 }
 
 // ------------------------------------------------------------- eval
-int do_eval(otb_ctx* c, const double* X, const double* gamma) {
+// Launch part of an eval (no host synchronisation).
+int eval_launch(otb_ctx* c, const double* X, const double* gamma) {
   const int n = (int)c->n;
   Geom geo = make_geom(c, DK_EVAL, c->C, X);
   EvalIO io{gamma, c->a, c->eta, c->rowM, c->rowS, c->lse, c->colpart, c->vpart, c->Pbuf};
@@ -353,7 +354,11 @@ int do_eval(otb_ctx* c, const double* X, const double* gamma) {
   TRY(allreduce(c, c->sendbuf, (size_t)n + 2, kNcclSum));
   k_eval_post<<<c->colgrid, 256, 0, c->stream>>>(n, c->sendbuf, c->b, gamma, c->eta, c->g, c->ds, c->bpart);
   LAUNCH_CHECK();
-  TRY(sync_scalars(c));
+  return OTB_OK;
+}
+
+// Host side of an eval whose scalars are in c->hs (after sync_scalars).
+int eval_finish(otb_ctx* c) {
   if (c->hs->scratch[0] != 0.0) {
     c->have_eval = false;
     return fail(OTB_ERR_NONFINITE, "row softmax produced non-finite values after stabilization");
@@ -363,6 +368,12 @@ int do_eval(otb_ctx* c, const double* X, const double* gamma) {
   c->have_eval = true;
   c->p_valid = c->Pbuf != nullptr;
   return OTB_OK;
+}
+
+int do_eval(otb_ctx* c, const double* X, const double* gamma) {
+  TRY(eval_launch(c, X, gamma));
+  TRY(sync_scalars(c));
+  return eval_finish(c);
 }
 
 // --------------------------------------------------------- sparsify
@@ -389,48 +400,68 @@ int row_prefix(otb_ctx* c) {
   return OTB_OK;
 }
 
-int do_sparsify(otb_ctx* c, const double* X, const double* gamma, double rho) {
+// Launch part of a sparsify pass (no host synchronisation): kernel, CTA
+// bounds / row prefix where hess_apply needs them, Hessian diagonal.  The
+// kept count and the capacity flag land in c->ds; *rec is the profiling
+// record whose byte count needs nnz (or -1).
+int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho, int64_t* rec) {
   const int n = (int)c->n;
   const int64_t anchor_local = (c->anchor >= c->row0 && c->anchor < c->row1) ? c->anchor - c->row0 : -1;
-  for (int attempt = 0; attempt < 8; ++attempt) {
-    // alloc, nnzc, flags are adjacent in DevScalars
-    CUDA_TRY(cudaMemsetAsync(&c->ds->alloc, 0, 2 * sizeof(unsigned long long) + sizeof(int), c->stream));
-    const int kind = c->p_valid ? DK_SPARSP : DK_SPARSIFY;
-    Geom geo = c->p_valid ? make_geom(c, DK_SPARSP, c->Pbuf, nullptr) : make_geom(c, DK_SPARSIFY, c->C, X);
-    const bool bm_only = c->hv_mode == 2 || c->hv_mode == 3;   // hess_apply reads the bitmap, not the columns
-    SparsifyIO io{gamma, c->a, c->eta, rho, anchor_local, c->rowM, c->rowS, c->lse, bm_only ? nullptr : c->cols,
-                  c->vals, c->cap,
-                  c->row_start, c->row_len, &c->ds->alloc, &c->ds->nnzc, c->chunk, c->colpart, &c->ds->flags,
-                  (c->hv_mode == 2 || c->hv_mode == 3) ? c->bm : nullptr, c->nq};
-    cudaEvent_t e0 = nullptr;
-    TRY(prof_begin(c, &e0));
-    TRY(launch_dense(c, kind, geo, &io));
-    // the row prefix (CSR export, nnz-balanced bounds) only where it is used
-    const bool bitmap = c->hv_mode == 2 || c->hv_mode == 3;
-    if (!bitmap) TRY(row_prefix(c));
-    c->rowpre_valid = !bitmap;
-    TRY(sync_scalars(c));
-    const int64_t nnz = (int64_t)c->hs->nnzc;
-    TRY(prof_end(c, PC_SPARSIFY, e0, 16.0 * c->m_loc * n + 12.0 * nnz + 8.0 * (c->m_loc + 1)));
-    if (c->hs->flags & 2) {
-      const int64_t need = (int64_t)c->hs->alloc + (int64_t)c->ncl * c->chunk;
-      TRY(grow_csr(c, need + need / 8));
-      continue;
-    }
-    c->nnz = nnz;
-    if (!bitmap) {
-      // nnz-balanced row bounds of the hess_apply CTAs, once per sparsify
-      // (the bitmap kernels use fixed equal row counts, set at creation)
-      Csr A = csr_view(c);
-      A.cta_rb = nullptr;
-      k_cta_bounds<<<(int)cdiv(c->hv_nb + 1, 256), 256, 0, c->stream>>>(A, c->hv_nb, c->cta_rb, 0);
-      LAUNCH_CHECK();
-    }
-    TRY(colreduce(c, c->ncl, nullptr, 0, 0, 0));
-    TRY(allreduce(c, c->sendbuf, (size_t)n, kNcclSum));
-    k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_COPY, n, c->sendbuf, c->b, c->d, c->ds, c->bpart, nullptr);
+  // alloc, nnzc, flags are adjacent in DevScalars
+  CUDA_TRY(cudaMemsetAsync(&c->ds->alloc, 0, 2 * sizeof(unsigned long long) + sizeof(int), c->stream));
+  const int kind = c->p_valid ? DK_SPARSP : DK_SPARSIFY;
+  Geom geo = c->p_valid ? make_geom(c, DK_SPARSP, c->Pbuf, nullptr) : make_geom(c, DK_SPARSIFY, c->C, X);
+  const bool bitmap = c->hv_mode == 2 || c->hv_mode == 3;   // hess_apply reads the bitmap, not the columns
+  SparsifyIO io{gamma, c->a, c->eta, rho, anchor_local, c->rowM, c->rowS, c->lse, bitmap ? nullptr : c->cols,
+                c->vals, c->cap,
+                c->row_start, c->row_len, &c->ds->alloc, &c->ds->nnzc, c->chunk, c->colpart, &c->ds->flags,
+                bitmap ? c->bm : nullptr, c->nq};
+  cudaEvent_t e0 = nullptr;
+  TRY(prof_begin(c, &e0));
+  TRY(launch_dense(c, kind, geo, &io));
+  *rec = c->prof ? (int64_t)c->recs.size() : -1;
+  TRY(prof_end(c, PC_SPARSIFY, e0, 0.0));
+  // the row prefix (CSR export, nnz-balanced bounds) only where it is used
+  if (!bitmap) {
+    TRY(row_prefix(c));
+    // nnz-balanced row bounds of the hess_apply CTAs, once per sparsify
+    // (the bitmap kernels use fixed equal row counts, set at creation)
+    Csr A = csr_view(c);
+    A.cta_rb = nullptr;
+    k_cta_bounds<<<(int)cdiv(c->hv_nb + 1, 256), 256, 0, c->stream>>>(A, c->hv_nb, c->cta_rb, 0);
     LAUNCH_CHECK();
-    return OTB_OK;
+  }
+  c->rowpre_valid = !bitmap;
+  TRY(colreduce(c, c->ncl, nullptr, 0, 0, 0));
+  TRY(allreduce(c, c->sendbuf, (size_t)n, kNcclSum));
+  k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_COPY, n, c->sendbuf, c->b, c->d, c->ds, c->bpart, nullptr);
+  LAUNCH_CHECK();
+  return OTB_OK;
+}
+
+// Host side of a sparsify pass whose scalars are in c->hs.  Returns 1 when
+// the CSR overflowed its capacity (grown here; the pass must be redone).
+int sparsify_finish(otb_ctx* c, int64_t rec, bool* redo) {
+  const int64_t nnz = (int64_t)c->hs->nnzc;
+  if (rec >= 0 && rec < (int64_t)c->recs.size())
+    c->recs[(size_t)rec].bytes = 16.0 * c->m_loc * c->n + 12.0 * nnz + 8.0 * (c->m_loc + 1);
+  *redo = (c->hs->flags & 2) != 0;
+  if (*redo) {
+    const int64_t need = (int64_t)c->hs->alloc + (int64_t)c->ncl * c->chunk;
+    return grow_csr(c, need + need / 8);
+  }
+  c->nnz = nnz;
+  return OTB_OK;
+}
+
+int do_sparsify(otb_ctx* c, const double* X, const double* gamma, double rho) {
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    int64_t rec = -1;
+    TRY(sparsify_launch(c, X, gamma, rho, &rec));
+    TRY(sync_scalars(c));
+    bool redo = false;
+    TRY(sparsify_finish(c, rec, &redo));
+    if (!redo) return OTB_OK;
   }
   return fail(OTB_ERR_NOMEM, "CSR capacity could not be grown");
 }
@@ -540,40 +571,35 @@ int cg_iteration(otb_ctx* c, int64_t k, double* x) {
   return OTB_OK;
 }
 
-int do_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t max_iters, double* x, otb_cg_out* out) {
+// The whole CG loop as one cooperative launch (k_cg_fused), after
+// k_cg_init; the state is copied to c->hcg asynchronously (read it after the
+// next stream synchronisation).  k_cg_fused returns at once when k_cg_init
+// already decided (rhs = 0, inconsistent system) or the CSR overflowed.
+int cg_fused_launch(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t max_iters, double* x,
+                    int64_t* rec) {
   const int n = (int)c->n;
   k_cg_init<<<c->colgrid, 256, 0, c->stream>>>(n, rhs, x, c->cg_r, c->cg_p[0], c->cg, c->bpart, shift, rel_tol,
                                                (long long)max_iters);
   LAUNCH_CHECK();
-  if (c->cg_fused) {
-    // whole CG loop in one cooperative launch (k_cg_fused); it returns at
-    // once when k_cg_init already decided (rhs = 0, inconsistent system),
-    // so the status is read back once, after it
-    CgFusedArgs fa{csr_view(c), c->a,     c->d,  n,     c->fused_ng, c->eta, x,          rhs, c->cg_ap,
-                   c->colpart,  c->scal, c->cg, c->bm, c->nq,       c->cg_trace};
-    void* args[1] = {&fa};
-    cudaEvent_t e0 = nullptr;
-    TRY(prof_begin(c, &e0));
-    CUDA_TRY(cudaLaunchCooperativeKernel(kCgFn[c->hv_var], dim3(c->hv_grid), dim3(c->hv_threads), args,
-                                         c->fused_smem, c->stream));
-    ++c->launches;
-    TRY(prof_end(c, PC_CGFUSED, e0, 0.0));
-    CUDA_TRY(cudaMemcpyAsync(c->hcg, c->cg, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-    if (c->prof && !c->recs.empty())
-      c->recs.back().bytes = (double)c->hcg->iters * hv_bytes(c);
-  } else {
-    CUDA_TRY(cudaMemcpyAsync(c->hcg, c->cg, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-  }
+  CgFusedArgs fa{csr_view(c), c->a,     c->d,  n,     c->fused_ng, c->eta, x,          rhs, c->cg_ap,
+                 c->colpart,  c->scal, c->cg, c->bm, c->nq,       c->cg_trace, &c->ds->flags};
+  void* args[1] = {&fa};
+  cudaEvent_t e0 = nullptr;
+  TRY(prof_begin(c, &e0));
+  CUDA_TRY(cudaLaunchCooperativeKernel(kCgFn[c->hv_var], dim3(c->hv_grid), dim3(c->hv_threads), args,
+                                       c->fused_smem, c->stream));
+  ++c->launches;
+  *rec = c->prof ? (int64_t)c->recs.size() : -1;
+  TRY(prof_end(c, PC_CGFUSED, e0, 0.0));
+  CUDA_TRY(cudaMemcpyAsync(c->hcg, c->cg, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
+  return OTB_OK;
+}
+
+// Host side of a finished CG (c->hcg current).
+int cg_finish(otb_ctx* c, int64_t rec, otb_cg_out* out) {
+  if (rec >= 0 && rec < (int64_t)c->recs.size()) c->recs[(size_t)rec].bytes = (double)c->hcg->iters * hv_bytes(c);
   if (c->hcg->status == CG_INCONSISTENT)
     return fail(OTB_ERR_INCONSISTENT, "unshifted system with right-hand side outside the range");
-  int64_t k = 0;
-  while (c->hcg->status == CG_RUN) {
-    for (int j = 0; j < kCgBatch; ++j, ++k) TRY(cg_iteration(c, k, x));
-    CUDA_TRY(cudaMemcpyAsync(c->hcg, c->cg, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-  }
   if (c->hcg->status == CG_NOTPD) {
     char buf[96];
     std::snprintf(buf, sizeof buf, "p^T A p = %.3g before convergence", c->hcg->curv);
@@ -585,6 +611,29 @@ int do_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t m
     out->status = c->hcg->status;
   }
   return OTB_OK;
+}
+
+int do_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t max_iters, double* x, otb_cg_out* out) {
+  const int n = (int)c->n;
+  if (c->cg_fused) {
+    int64_t rec = -1;
+    TRY(cg_fused_launch(c, shift, rhs, rel_tol, max_iters, x, &rec));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return cg_finish(c, rec, out);
+  }
+  k_cg_init<<<c->colgrid, 256, 0, c->stream>>>(n, rhs, x, c->cg_r, c->cg_p[0], c->cg, c->bpart, shift, rel_tol,
+                                               (long long)max_iters);
+  LAUNCH_CHECK();
+  CUDA_TRY(cudaMemcpyAsync(c->hcg, c->cg, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (c->hcg->status == CG_INCONSISTENT) return cg_finish(c, -1, out);
+  int64_t k = 0;
+  while (c->hcg->status == CG_RUN) {
+    for (int j = 0; j < kCgBatch; ++j, ++k) TRY(cg_iteration(c, k, x));
+    CUDA_TRY(cudaMemcpyAsync(c->hcg, c->cg, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
+  return cg_finish(c, -1, out);
 }
 
 // ------------------------------------------------------ inexact test
@@ -1091,6 +1140,31 @@ int otb_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t 
   return do_cg(c, shift, rhs, rel_tol, max_iters, x_out, out);
 }
 
+// Armijo backtracking from t0 (whose trial eval is in c->hs when
+// `evaluated`), inner_newton.py:74-94.
+int armijo(otb_ctx* c, const double* logX, const double* gamma_in, double v0, double slope,
+           const otb_newton_params* p, bool evaluated, double* t_out, int64_t* trials_out) {
+  const int n = (int)c->n;
+  double t = 1.0;
+  int64_t trials = 0;
+  for (int k = 0; k < 200; ++k) {
+    if (!(evaluated && k == 0)) {
+      k_trial<<<c->colgrid, 256, 0, c->stream>>>(n, gamma_in, c->dir, t, c->gtrial);
+      LAUNCH_CHECK();
+      TRY(do_eval(c, logX, c->gtrial));
+    }
+    ++trials;
+    if (c->last_value <= v0 + p->sigma * t * slope) {
+      *t_out = t;
+      *trials_out = trials;
+      return OTB_OK;
+    }
+    t *= p->beta;
+  }
+  c->have_eval = false;
+  return fail(OTB_ERR_LINESEARCH, "no Armijo step accepted after 200 trials");
+}
+
 int otb_newton_step(otb_ctx* c, const double* logX, const double* gamma_in, double* gamma_out,
                     const otb_newton_params* p, otb_newton_out* out) {
   TRY(require_bound(c));
@@ -1100,40 +1174,56 @@ int otb_newton_step(otb_ctx* c, const double* logX, const double* gamma_in, doub
   const double v0 = c->last_value, g0 = c->last_gnorm;
   // inner_newton.py:112-114
   const double rho = (p->rho_override >= 0.0) ? p->rho_override : c->eta * g0 / ((double)c->m_glob * (double)c->n);
-  TRY(do_sparsify(c, logX, gamma_in, rho));
-  const int64_t nnz = c->nnz;
-  // inner_newton.py:117: (H_rho + ||g|| I) d = -g
-  k_neg<<<c->colgrid, 256, 0, c->stream>>>(n, c->g, c->rhs);
-  LAUNCH_CHECK();
-  otb_cg_out cgo;
   const int64_t maxit = (p->cg_max_iters > 0) ? p->cg_max_iters : 2 * c->n;
-  TRY(do_cg(c, g0, c->rhs, p->cg_rel_tol, maxit, c->dir, &cgo));
-  // inner_newton.py:118: slope = g . d
-  k_dot<<<c->colgrid, 256, 0, c->stream>>>(n, c->g, c->dir, c->ds, c->bpart, &c->ds->slope);
-  LAUNCH_CHECK();
-  TRY(sync_scalars(c));
-  const double slope = c->hs->slope;
-  // inner_newton.py:74-94: Armijo backtracking
-  double t = 1.0;
+  otb_cg_out cgo;
+  double slope = 0.0, t = 1.0;
   int64_t trials = 0;
-  bool ok = false;
-  for (int k = 0; k < 200; ++k) {
-    k_trial<<<c->colgrid, 256, 0, c->stream>>>(n, gamma_in, c->dir, t, c->gtrial);
-    LAUNCH_CHECK();
-    TRY(do_eval(c, logX, c->gtrial));
-    ++trials;
-    if (c->last_value <= v0 + p->sigma * t * slope) {
-      ok = true;
-      break;
+  if (c->cg_fused) {
+    // One host synchronisation for sparsify + CG + slope + the t = 1 trial:
+    // everything is launched back to back and the host reads the kept
+    // count, the capacity flag, the CG state, the slope and the trial's
+    // value together.  A CSR overflow (first call on a problem) grows the
+    // capacity, re-evaluates at gamma_in and repeats.
+    bool done = false;
+    for (int attempt = 0; attempt < 8 && !done; ++attempt) {
+      int64_t sp_rec = -1, cg_rec = -1;
+      TRY(sparsify_launch(c, logX, gamma_in, rho, &sp_rec));
+      k_neg<<<c->colgrid, 256, 0, c->stream>>>(n, c->g, c->rhs);   // inner_newton.py:117: (H + ||g|| I) d = -g
+      LAUNCH_CHECK();
+      TRY(cg_fused_launch(c, g0, c->rhs, p->cg_rel_tol, maxit, c->dir, &cg_rec));
+      k_dot<<<c->colgrid, 256, 0, c->stream>>>(n, c->g, c->dir, c->ds, c->bpart, &c->ds->slope);   // :118
+      LAUNCH_CHECK();
+      k_trial<<<c->colgrid, 256, 0, c->stream>>>(n, gamma_in, c->dir, 1.0, c->gtrial);
+      LAUNCH_CHECK();
+      TRY(eval_launch(c, logX, c->gtrial));
+      TRY(sync_scalars(c));
+      bool redo = false;
+      TRY(sparsify_finish(c, sp_rec, &redo));
+      if (redo) {
+        TRY(do_eval(c, logX, gamma_in));   // the trial replaced the row state sparsify reads
+        continue;
+      }
+      c->have_eval = false;   // the row state is the trial's until eval_finish accepts it
+      TRY(cg_finish(c, cg_rec, &cgo));
+      slope = c->hs->slope;
+      TRY(eval_finish(c));
+      done = true;
     }
-    t *= p->beta;
+    if (!done) return fail(OTB_ERR_NOMEM, "CSR capacity could not be grown");
+    TRY(armijo(c, logX, gamma_in, v0, slope, p, true, &t, &trials));
+  } else {
+    TRY(do_sparsify(c, logX, gamma_in, rho));
+    k_neg<<<c->colgrid, 256, 0, c->stream>>>(n, c->g, c->rhs);
+    LAUNCH_CHECK();
+    TRY(do_cg(c, g0, c->rhs, p->cg_rel_tol, maxit, c->dir, &cgo));
+    k_dot<<<c->colgrid, 256, 0, c->stream>>>(n, c->g, c->dir, c->ds, c->bpart, &c->ds->slope);
+    LAUNCH_CHECK();
+    TRY(sync_scalars(c));
+    slope = c->hs->slope;
+    TRY(armijo(c, logX, gamma_in, v0, slope, p, false, &t, &trials));
   }
-  if (!ok) {
-    c->have_eval = false;
-    return fail(OTB_ERR_LINESEARCH, "no Armijo step accepted after 200 trials");
-  }
+  // stream-ordered: the caller's later work on this stream sees gamma_out
   CUDA_TRY(cudaMemcpyAsync(gamma_out, c->gtrial, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
   if (out) {
     out->t = t;
     out->slope = slope;
@@ -1143,7 +1233,7 @@ int otb_newton_step(otb_ctx* c, const double* logX, const double* gamma_in, doub
     out->grad_norm_before = g0;
     out->grad_norm_after = c->last_gnorm;
     out->cg_iters = cgo.iters;
-    out->nnz = nnz;
+    out->nnz = c->nnz;
     out->trials = trials;
     out->cg_residual = cgo.residual;
   }

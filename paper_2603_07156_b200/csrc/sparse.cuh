@@ -1089,6 +1089,7 @@ struct CgFusedArgs {
   const uint4* bm;   // bitmap index (NQ > 0)
   int nq;
   unsigned long long* trace;   // optional: [gridDim][kCgTraceIters][6] globaltimer stamps
+  const int* flags;            // sparsify flags: bit 1 = CSR overflow (nothing to solve with)
 };
 
 constexpr int kCgTraceIters = 16;
@@ -1116,7 +1117,7 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_cg_fused(CgFusedArgs 
   __shared__ double red2[2][kMaxWarps * 4];
   __shared__ double bcast;
   cgrp::grid_group grid = cgrp::this_grid();
-  if (c.st->status != CG_RUN) return;
+  if (c.st->status != CG_RUN || (*c.flags & 2)) return;
   const int n = c.n, npad = (n + 1) & ~1, NG = c.ng;
   const int B = gridDim.x, b = blockIdx.x, tid = threadIdx.x, nth = blockDim.x;
   double* psm = hsm;
