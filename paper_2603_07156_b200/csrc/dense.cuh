@@ -145,6 +145,12 @@ struct SparsifyIO {
   uint4* bm;              // bitmap index [m_loc][nq] (sparse.cuh), or nullptr
   int nq;
 };
+// With the bitmap index, a row's run holds column PAIRS (2l, 2l+1) with at
+// least one kept entry, 16 bytes each (the unkept one stored as 0.0), and
+// the word's offset counts pairs: lane l of hess_apply finds its pair at
+// 2 (off + popc(pairs below l)) with no per-element select.  Kept entries
+// come in long runs (cfg2: 40 columns on average), so pairs cost ~1.5% more
+// bytes than single entries.  Without it, runs hold the kept entries.
 
 // FROMP: stream the P stored by the eval of the same gamma (one matrix, no
 // exp / division) instead of recomputing it from C and log X.
@@ -165,6 +171,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
   const double log_rho = log(rho);
   const int nw = D.g.nt >> 5;
   const unsigned lt = (1u << D.lane) - 1u;
+  const bool pairs = io.bm != nullptr;
   unsigned long long cur = 0, end = 0;
   unsigned long long kept = 0;
   int rowpar = 0;
@@ -222,12 +229,13 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
       if (s < D.nsl) {
         bb0[s] = __ballot_sync(0xffffffffu, (keep >> (2 * s)) & 1u);
         bb1[s] = __ballot_sync(0xffffffffu, (keep >> (2 * s + 1)) & 1u);
-        if (D.lane == 0) tb[s * 32 + D.warp] = __popc(bb0[s]) + __popc(bb1[s]);
+        if (D.lane == 0) tb[s * 32 + D.warp] = pairs ? __popc(bb0[s] | bb1[s]) : __popc(bb0[s]) + __popc(bb1[s]);
       }
     }
-    double t[1] = {ks};
-    D.template reduce<1, kSum>(t);   // barrier also publishes tb
+    double t[2] = {ks, (double)__popc(keep)};
+    D.template reduce<2, kSum>(t);   // barrier also publishes tb
     double ksum = t[0];
+    int ecnt = (int)t[1];            // kept entries of the row (this window)
     // per-slice totals (lane s holds slice s), exclusive scan over slices
     // and (pre) the kept entries of slice s in the warps before this one
     int tot = 0, pre = 0;
@@ -244,21 +252,23 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
       if (D.lane >= o) incl += v;
     }
     const int excl = incl - tot;
-    int need = __shfl_sync(0xffffffffu, incl, 31);   // kept in this CTA's window
-    int cnt = need;                                    // kept in the whole row
+    int need = __shfl_sync(0xffffffffu, incl, 31);   // kept (entries or pairs) in this CTA's window
+    int cnt = need;                                    // ... in the whole row
     int myoff = 0;                                     // offset of this window in the row
     if (D.g.cl > 1) {
-      double v2[2] = {(double)need, ksum};
+      double v3[3] = {(double)need, ksum, (double)ecnt};
       double all[kMaxCluster * 4];
-      D.template exchange<2>(v2, all);
-      double cs = 0.0, kss = 0.0;
+      D.template exchange<3>(v3, all);
+      double cs = 0.0, kss = 0.0, es = 0.0;
       for (int q = 0; q < D.g.cl; ++q) {
         if (q < D.cr) myoff += (int)all[q * 4];
         cs += all[q * 4];
         kss += all[q * 4 + 1];
+        es += all[q * 4 + 2];
       }
       cnt = (int)cs;
       ksum = kss;
+      ecnt = (int)es;
     }
     bool fallback = false;
     int jbest = -1;
@@ -297,13 +307,15 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
       jbest = (int)jm;
       need = (jbest >= D.c0 && jbest < D.c1) ? 1 : 0;
       cnt = 1;
+      ecnt = 1;
       myoff = 0;
     }
     // Contiguous row run: cluster rank 0 bump-allocates from its current
     // chunk (state replicated in all of its consumer threads) and shares
     // the start with the other ranks of the cluster.
     unsigned long long start = 0;
-    const int cnt_al = (cnt + 7) & ~7;   // runs start on 8-entry boundaries (vector loads in hess_apply)
+    const int sto = pairs ? 2 * cnt : cnt;   // stored doubles of the row
+    const int cnt_al = (sto + 7) & ~7;      // runs start on 8-entry boundaries (vector loads in hess_apply)
     if (D.cr == 0) {
       if (cur + (unsigned long long)cnt_al > end) {
         const unsigned long long want = (unsigned long long)max((int64_t)cnt_al, io.chunk);
@@ -325,7 +337,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
     const bool ovf = (int64_t)(start + cnt_al) > io.cap;
     if (ovf && D.tid == 0 && D.cr == 0) atomicOr(io.flags, 2);
     const double ai = __ldg(io.a + D.g.row0 + r);
-    const unsigned long long wbase = start + myoff;
+    const unsigned long long wbase = start + (pairs ? 2 * myoff : myoff);
     const Divider DK(ksum);
     if (!ovf) {
       if (fallback) {
@@ -333,7 +345,12 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
         for (int k = 0; k < 2 * NS; ++k) {
           if (D.col(k >> 1, k & 1) == jbest && P[k] >= 0.0) {
             if (io.cols != nullptr) io.cols[wbase] = (uint16_t)jbest;
-            io.vals[wbase] = 1.0;
+            if (pairs) {
+              io.vals[wbase + (k & 1)] = 1.0;
+              io.vals[wbase + 1 - (k & 1)] = 0.0;
+            } else {
+              io.vals[wbase] = 1.0;
+            }
             double2* a2 = D.acc2(0, k >> 1);
             if (k & 1) a2->y += ai * 1.0;
             else a2->x += ai * 1.0;
@@ -360,13 +377,24 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
             const unsigned k0 = (keep >> (2 * s)) & 1u, k1 = (keep >> (2 * s + 1)) & 1u;
             const unsigned b0 = bb0[s], b1 = bb1[s];
             const int base = __shfl_sync(0xffffffffu, excl + pre, s);
-            const int off = base + __popc(b0 & lt) + __popc(b1 & lt);
             const int j = D.col(s, 0);
             if (io.bm != nullptr && D.lane == 0) {
               const int cs = D.c0 + s * D.slice + 64 * D.warp;
               if (cs < D.c1) io.bm[(size_t)r * io.nq + cs / 64] = make_uint4(b0, b1, (unsigned)(myoff + base), 0u);
             }
             double2* a2 = D.acc2(0, s);
+            if (pairs) {
+              if (k0 | k1) {
+                const int off = base + __popc((b0 | b1) & lt);
+                const double v0 = k0 ? (anc ? P[2 * s] : DK(P[2 * s])) : 0.0;
+                const double v1 = k1 ? (anc ? P[2 * s + 1] : DK(P[2 * s + 1])) : 0.0;
+                *reinterpret_cast<double2*>(io.vals + wbase + 2 * off) = make_double2(v0, v1);
+                if (k0) a2->x += ai * v0;
+                if (k1) a2->y += ai * v1;
+              }
+              continue;
+            }
+            const int off = base + __popc(b0 & lt) + __popc(b1 & lt);
             if (k0) {
               const double v = anc ? P[2 * s] : DK(P[2 * s]);
               if (io.cols != nullptr) io.cols[wbase + off] = (uint16_t)j;
@@ -385,8 +413,8 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
     }
     if (D.tid == 0 && D.cr == 0) {
       io.row_start[r] = (int64_t)start;
-      io.row_len[r] = ovf ? 0 : cnt;
-      kept += ovf ? 0 : cnt;
+      io.row_len[r] = ovf ? 0 : sto;
+      kept += ovf ? 0 : ecnt;
     }
     rowpar ^= 1;
   }

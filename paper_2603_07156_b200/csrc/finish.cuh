@@ -360,22 +360,45 @@ __global__ void k_scale_cost(double* C, int64_t ld, int m_loc, int n, double pea
   }
 }
 
-// Column indices of the CSR rebuilt from the bitmap words (sparsify writes
-// only the words when hess_apply runs on the bitmap): one warp per (row,
-// word), lane l places columns 64q+2l(+1) at the positions hess_apply reads.
-__global__ void k_bm_cols(const uint4* __restrict__ bm, int nq, int m_loc, const int64_t* __restrict__ row_start,
-                          uint16_t* __restrict__ cols) {
+// CSR export with the bitmap index (pair-layout runs, dense.cuh): kept
+// entries per row, then, one warp per row walking its words in order, the
+// kept entries of each lane's pair at their element position.
+__global__ void k_bm_rownnz(const uint4* __restrict__ bm, int nq, int m_loc, int* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < m_loc; r += (gridDim.x * blockDim.x) >> 5) {
+    int k = 0;
+    for (int q = lane; q < nq; q += 32) {
+      const uint4 w = bm[(size_t)r * nq + q];
+      k += __popc(w.x) + __popc(w.y);
+    }
+    for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+    if (lane == 0) cnt[r] = k;
+  }
+}
+
+__global__ void k_bm_export(const uint4* __restrict__ bm, int nq, int m_loc, const int64_t* __restrict__ row_start,
+                            const double* __restrict__ vals, const int64_t* __restrict__ rowpre,
+                            int32_t* __restrict__ out_cols, double* __restrict__ out_vals) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  const int64_t total = (int64_t)m_loc * nq;
-  for (int64_t wi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; wi < total;
-       wi += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int r = (int)(wi / nq), q = (int)(wi % nq);
-    const uint4 w = bm[wi];
-    const unsigned k0 = (w.x >> lane) & 1u, k1 = (w.y >> lane) & 1u;
-    const int64_t pos = row_start[r] + w.z + __popc(w.x & lt) + __popc(w.y & lt);
-    if (k0) cols[pos] = (uint16_t)(64 * q + 2 * lane);
-    if (k1) cols[pos + k0] = (uint16_t)(64 * q + 2 * lane + 1);
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < m_loc; r += (gridDim.x * blockDim.x) >> 5) {
+    const double* vr = vals + row_start[r];
+    int64_t o = rowpre[r];
+    for (int q = 0; q < nq; ++q) {
+      const uint4 w = bm[(size_t)r * nq + q];
+      const unsigned k0 = (w.x >> lane) & 1u, k1 = (w.y >> lane) & 1u;
+      const int64_t pos = o + __popc(w.x & lt) + __popc(w.y & lt);
+      const double* e = vr + 2 * ((int)w.z + __popc((w.x | w.y) & lt));
+      if (k0) {
+        out_cols[pos] = 64 * q + 2 * lane;
+        out_vals[pos] = e[0];
+      }
+      if (k1) {
+        out_cols[pos + k0] = 64 * q + 2 * lane + 1;
+        out_vals[pos + k0] = e[1];
+      }
+      o += __popc(w.x) + __popc(w.y);
+    }
   }
 }
 

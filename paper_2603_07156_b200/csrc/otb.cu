@@ -162,7 +162,8 @@ struct otb_ctx {
   double *cg_ap = nullptr, *cg_y = nullptr, *gtrial = nullptr, *yv = nullptr, *ec = nullptr;
   double *Mloc = nullptr, *Mglob = nullptr, *Sloc = nullptr;
   int64_t *row_start = nullptr, *rowpre = nullptr;
-  int* row_len = nullptr;
+  int* row_len = nullptr;        // stored doubles of each row run
+  int* row_nnz = nullptr;        // kept entries per row (CSR export with the bitmap index)
   uint16_t* cols = nullptr;
   double* vals = nullptr;
   int64_t cap = 0, chunk = 0, nnz = 0;
@@ -998,7 +999,7 @@ int otb_destroy(otb_ctx* c) {
                   (void*)c->colpart, (void*)c->vpart, (void*)c->sendbuf, (void*)c->bpart, (void*)c->g, (void*)c->d,
                   (void*)c->rhs, (void*)c->dir, (void*)c->cg_r, (void*)c->cg_p[0], (void*)c->cg_p[1],
                   (void*)c->cg_ap, (void*)c->cg_y, (void*)c->gtrial, (void*)c->yv, (void*)c->ec, (void*)c->Mloc,
-                  (void*)c->Mglob, (void*)c->Sloc, (void*)c->row_start, (void*)c->rowpre, (void*)c->row_len,
+                  (void*)c->Mglob, (void*)c->Sloc, (void*)c->row_start, (void*)c->rowpre, (void*)c->row_len, (void*)c->row_nnz,
                   (void*)c->cols, (void*)c->vals, (void*)c->ds, (void*)c->cg, (void*)c->scal, (void*)c->cta_rb,
                   (void*)c->bm, (void*)c->Pbuf, (void*)c->cg_trace})
     if (p) cudaFree(p);
@@ -1098,20 +1099,29 @@ int otb_sparsify(otb_ctx* c, const double* logX, const double* gamma, double rho
 
 int otb_csr_export(otb_ctx* c, int64_t* row_ptr, int32_t* cols, double* vals, double* d) {
   TRY(require_bound(c));
+  const bool bitmap = c->hv_mode == 2 || c->hv_mode == 3;   // pair-layout runs, columns in the bitmap words
   if (!c->rowpre_valid && (row_ptr || (cols && vals))) {
-    TRY(row_prefix(c));
+    if (bitmap) {
+      if (!c->row_nnz) TRY(dalloc(&c->row_nnz, c->m_loc));
+      k_bm_rownnz<<<c->num_sms * 8, 256, 0, c->stream>>>(c->bm, c->nq, (int)c->m_loc, c->row_nnz);
+      LAUNCH_CHECK();
+      k_row_prefix<<<1, 1024, 0, c->stream>>>(c->row_nnz, (int)c->m_loc, c->rowpre);
+      LAUNCH_CHECK();
+    } else {
+      TRY(row_prefix(c));
+    }
     c->rowpre_valid = true;
   }
   if (row_ptr)
     CUDA_TRY(cudaMemcpyAsync(row_ptr, c->rowpre, sizeof(int64_t) * (c->m_loc + 1), cudaMemcpyDeviceToDevice,
                              c->stream));
   if (cols && vals) {
-    if (c->hv_mode == 2 || c->hv_mode == 3) {   // columns only live in the bitmap words
-      k_bm_cols<<<c->num_sms * 8, 256, 0, c->stream>>>(c->bm, c->nq, (int)c->m_loc, c->row_start, c->cols);
-      LAUNCH_CHECK();
-    }
-    k_csr_compact<<<c->num_sms * 4, 256, 0, c->stream>>>((int)c->m_loc, c->row_start, c->row_len, c->rowpre, c->cols,
-                                                         c->vals, cols, vals);
+    if (bitmap)
+      k_bm_export<<<c->num_sms * 8, 256, 0, c->stream>>>(c->bm, c->nq, (int)c->m_loc, c->row_start, c->vals,
+                                                         c->rowpre, cols, vals);
+    else
+      k_csr_compact<<<c->num_sms * 4, 256, 0, c->stream>>>((int)c->m_loc, c->row_start, c->row_len, c->rowpre,
+                                                           c->cols, c->vals, cols, vals);
     LAUNCH_CHECK();
   }
   if (d) CUDA_TRY(cudaMemcpyAsync(d, c->d, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, c->stream));

@@ -278,19 +278,21 @@ OTB_DEV void cp_async(void* dst, const void* src, int bytes, bool ok) {
 OTB_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 OTB_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// The lane's two candidate entries of word w: e[0] is the entry of column
-// 2l when it is kept, e[1] (or e[0] if 2l is not kept) that of 2l+1.  The
-// position is always inside the run or its padding (the value buffer has
-// 16 entries of slack), so both loads are issued unconditionally.
+// Pair layout (dense.cuh, SparsifyIO): the lane's pair (columns 2l, 2l+1)
+// of word w sits at 2 (w.z + popc(pairs below l)) of the row run, 16-byte
+// aligned, with 0.0 for an unkept half.  The position is always inside the
+// run or its padding (the value buffer has 16 entries of slack), so the load
+// is issued unconditionally.
+OTB_DEV unsigned bm_pairs(const uint4& w) { return w.x | w.y; }
 OTB_DEV const double* bm_entry(const double* vr, const uint4& w, unsigned lt) {
-  return vr + ((int)w.z + __popc(w.x & lt) + __popc(w.y & lt));
+  return vr + 2 * ((int)w.z + __popc(bm_pairs(w) & lt));
 }
-// Keep / zero the loaded pair by the word's bits (no FP op on unkept data).
+// Zero the loaded pair when the lane's pair is not in the run (it then read
+// a later pair; no FP op on that data).
 OTB_DEV void bm_select(const uint4& w, unsigned lb, double& e0, double& e1) {
-  const bool k0 = (w.x & lb) != 0u, k1 = (w.y & lb) != 0u;
-  const double a = e0, b = e1;
-  e0 = k0 ? a : 0.0;
-  e1 = k1 ? (k0 ? b : a) : 0.0;
+  const bool kp = (bm_pairs(w) & lb) != 0u;
+  e0 = kp ? e0 : 0.0;
+  e1 = kp ? e1 : 0.0;
 }
 
 // ---- one pass, 16 warps: R rows per block reduction
@@ -397,9 +399,9 @@ OTB_DEV void hv_bitmap_rows(const Csr& A, const uint4* __restrict__ bm, const do
       ar[k] = asm_[k];
 #pragma unroll
       for (int t = 0; t < NQ; ++t) {
-        const double* e = bm_entry(vr, wsm[k * NQP + warp + 16 * t], lt);
-        val[k][2 * t] = __ldg(e);
-        val[k][2 * t + 1] = __ldg(e + 1);
+        const double2 e = __ldg(reinterpret_cast<const double2*>(bm_entry(vr, wsm[k * NQP + warp + 16 * t], lt)));
+        val[k][2 * t] = e.x;
+        val[k][2 * t + 1] = e.y;
       }
     }
 #pragma unroll
@@ -435,6 +437,7 @@ OTB_DEV void hv_bitmap_rows(const Csr& A, const uint4* __restrict__ bm, const do
 constexpr int kStR = 2;                      // rows per batch
 constexpr int kStWords = 64;                 // staged words per row (one 4096-column window)
 constexpr int kStRowVals = 4096 + 8;         // staged values per row (window + alignment slack)
+constexpr int kStZero = 4096;                // zero pair in each row slot (never a copy target)
 constexpr int kStHdrBytes = 128;
 constexpr int kStBytes = kStR * kStWords * 16 + kStHdrBytes + kStR * kStRowVals * 8;
 constexpr int kStConsumers = 512;
@@ -482,6 +485,10 @@ OTB_DEV StRing st_ring(unsigned char* p, int S, int consumers = kStConsumers) {
     }
     fence_mbar_init();
   }
+  if (threadIdx.x < S * kStR * 2) {   // the zero pairs read by lanes without a pair
+    const int s = threadIdx.x / (kStR * 2), k = (threadIdx.x / 2) % kStR, h = threadIdx.x & 1;
+    reinterpret_cast<double*>(rg.at(s) + kStR * kStWords * 16 + kStHdrBytes)[k * kStRowVals + kStZero + h] = 0.0;
+  }
   return rg;
 }
 
@@ -502,8 +509,9 @@ OTB_DEV void st_produce(const Csr& A, const uint4* bm, const double* a, int rb, 
     double ar = 0.0;
     if (r < re) {
       const int64_t st = A.row_start[r];
-      const int fo = (woff > 0) ? (int)bm[(size_t)r * stride + woff].z : 0;
-      const int lo = last_window ? A.row_len[r] : (int)bm[(size_t)r * stride + woff + nqp].z;
+      // pair offsets -> doubles (row_len counts stored doubles)
+      const int fo = (woff > 0) ? 2 * (int)bm[(size_t)r * stride + woff].z : 0;
+      const int lo = last_window ? A.row_len[r] : 2 * (int)bm[(size_t)r * stride + woff + nqp].z;
       a0 = (st + fo) & ~(int64_t)1;                        // 16-byte aligned source
       cnt = (int)(((st + lo + 1) & ~(int64_t)1) - a0);
       off = (int)(st - a0);
@@ -569,13 +577,16 @@ OTB_DEV void st_row(const uint4* words, const double* vals, int k, int base, uns
 #pragma unroll
   for (int t = 0; t < NQ; ++t) {
     const uint4 wd = words[k * kStWords + warp + CW * t];
+    const unsigned pm = bm_pairs(wd);
     // window kernels: words past n are zero (off 0 lies before a later
     // window's segment); keep the address inside the row's stage slot —
     // their masks are 0.  Single CTA: off 0 is the row start, no clamp.
-    int idx = base + (int)wd.z + __popc(wd.x & lt) + __popc(wd.y & lt);
+    int idx = base + 2 * ((int)wd.z + __popc(pm & lt));
     if constexpr (CLAMP) idx = min(max(idx, k * kStRowVals), (k + 1) * kStRowVals - 2);
-    double e0 = vals[idx], e1 = vals[idx + 1];
-    bm_select(wd, lb, e0, e1);
+    // a lane whose pair is not in the run reads the slot's zero pair
+    idx = (pm & lb) ? idx : k * kStRowVals + kStZero;
+    const double2 e = *reinterpret_cast<const double2*>(vals + idx);
+    const double e0 = e.x, e1 = e.y;
     if constexpr (DOT) {
       d0 = fma(e0, v[2 * t], d0);
       d1 = fma(e1, v[2 * t + 1], d1);
