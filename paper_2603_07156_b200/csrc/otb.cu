@@ -958,8 +958,10 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   }
   c->chunk = rup(std::max<int64_t>(8192, 2 * n), kCsrAlign);
   // first Newton steps keep 50-70% of P: start at 3/4
-  const int64_t init_cap =
+  int64_t init_cap =
       std::max<int64_t>((int64_t)1 << 20, m_loc * (rup(n, kCsrAlign)) * 3 / 4) + (int64_t)c->ncl * c->chunk;
+  const char* env_cap = std::getenv("OTB_CSR_CAP0");   // tests: start small to exercise the overflow path
+  if (env_cap && std::atoll(env_cap) > 0) init_cap = std::atoll(env_cap);
   st = grow_csr(c, init_cap);
   if (st != OTB_OK) {
     otb_destroy(c);

@@ -519,3 +519,32 @@ def test_config2_solve_rounded_marginals_and_determinism(cuda):
     assert np.max(np.abs(R.sum(axis=1) - inst.a)) <= 1e-12
     assert np.max(np.abs(R.sum(axis=0) - inst.b)) <= 1e-12
     assert R.min() >= -1e-18        # e_r e_c^T / deficit can carry rounding-level negatives, in the reference too
+
+
+def test_newton_step_csr_overflow_retry_is_identical(cuda, monkeypatch):
+    """The single-synchronisation Newton step (sparsify, CG, slope and the
+    t = 1 trial launched back to back) detects a CSR capacity overflow only
+    after the trial: it grows the CSR, re-evaluates at gamma_in and repeats.
+    Starting from a tiny capacity must give bit-identical results to a
+    context whose capacity suffices from the start."""
+    import torch
+
+    P = _api()
+    from paper_2603_07156_b200 import instances
+
+    inst = instances.uniform2d_points(701, 899, seed=3, eta=2e-2).build()
+    X = np.log(np.outer(inst.a, inst.b))
+    outs = []
+    for cap0 in ("4096", None):            # fresh contexts (shape used nowhere else)
+        if cap0 is None:
+            monkeypatch.delenv("OTB_CSR_CAP0", raising=False)
+        else:
+            monkeypatch.setenv("OTB_CSR_CAP0", cap0)
+        prob = P.OtProblem(torch.from_numpy(inst.cost.copy()).cuda(), inst.a, inst.b)
+        gam, _ = P.warm_start(P.LogPlan(X), prob, inst.eta, 1e-3, gamma0=np.zeros(899))
+        new, t, its = P.newton_step(P.LogPlan(X), gam, prob, inst.eta)
+        g = new.gamma.cpu().numpy() if hasattr(new.gamma, "cpu") else np.asarray(new.gamma)
+        outs.append((g, t, its, prob))     # keep the problem (and its context) alive
+    monkeypatch.delenv("OTB_CSR_CAP0", raising=False)
+    assert outs[0][1] == outs[1][1] and outs[0][2] == outs[1][2]
+    assert np.array_equal(outs[0][0], outs[1][0])

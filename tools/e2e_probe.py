@@ -59,5 +59,23 @@ def main():
         del prob, s, lp, gs, cand
 
 
+
+
+def h2d_bandwidth():
+    """Pinned host -> device copy rate of one 134 MB buffer (the size of C)."""
+    src = torch.empty(4096 * 4096, dtype=torch.float64).pin_memory()
+    dst = torch.empty_like(src, device="cuda")
+    for _ in range(3):
+        dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(10):
+        dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / 10
+    print(f"H2D pinned 134 MB: {dt * 1e3:.2f} ms = {src.numel() * 8 / dt / 1e9:.1f} GB/s")
+
+
 if __name__ == "__main__":
+    h2d_bandwidth()
     main()
