@@ -6,7 +6,10 @@
 
 namespace otb {
 
-constexpr int kMaxThreads = 544;   // 512 consumers + 1 producer warp
+#ifndef OTB_DENSE_MAXT
+#define OTB_DENSE_MAXT 544
+#endif
+constexpr int kMaxThreads = OTB_DENSE_MAXT;   // 512 consumers + 1 producer warp (register budget: 96)
 #ifndef OTB_DENSE_MINB
 #define OTB_DENSE_MINB 1           // CTAs per SM the register allocation is sized for
 #endif

@@ -285,7 +285,8 @@ def test_error_mapping(cuda):
 
 
 # ------------------------------------------------ fixed-divisor fast division
-@pytest.mark.parametrize("y", [1e-2, 5e-3, 1e-3, 0.7310585786300049, 3.0, 1e-17, 2.5e-290, 1e300])
+@pytest.mark.parametrize("y", [1e-2, 5e-3, 1e-3, 0.7310585786300049, 3.0, 1e-17, 2.5e-290, 1e300, 1.0, 2.0 ** 600,
+                               2.0 ** -1020, -3.7, 5e-320, 0.0, np.inf])
 def test_fast_division_is_correctly_rounded(cuda, y):
     """The kernels divide by eta / row sums / the rounding deficit through a
     reciprocal + one FMA residual step (csrc/common.cuh Divider); it must give
@@ -302,6 +303,10 @@ def test_fast_division_is_correctly_rounded(cuda, y):
         np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, -5e-324, 1.7e308, 2.2250738585072014e-308]),
         y * np.arange(-1000, 1000, dtype=np.float64),
         np.nextafter(y * np.arange(1, 1000, dtype=np.float64), np.inf),
+        # every power of two and its neighbours: the edges of the fast path's range
+        2.0 ** np.arange(-1074, 1024, dtype=np.float64),
+        np.nextafter(2.0 ** np.arange(-1074, 1024, dtype=np.float64), np.inf),
+        -np.nextafter(2.0 ** np.arange(-1074, 1024, dtype=np.float64), 0.0),
     ]
     x = np.concatenate(parts)
     xd = torch.from_numpy(x).cuda()
