@@ -87,25 +87,19 @@ const int kNmat[DK_COUNT] = {2, 2, 2, 1, 1, 2, 2, 2, 1};
 const int kNacc[DK_COUNT] = {1, 1, 1, 1, 1, 1, 1, 2, 1};
 const int kStaticSmem[DK_COUNT] = {0, (int)(kTabInts * 4 + 16), 0, 0, 0, 0, 0, 0, (int)(kTabInts * 4 + 16)};
 
-#define NS_ROW(K) \
-  { nullptr, (const void*)K<1>, (const void*)K<2>, (const void*)K<3>, (const void*)K<4>, \
-    (const void*)K<5>, (const void*)K<6>, (const void*)K<7>, (const void*)K<8> }
+#define NS_ROW(K)                                                                                   \
+  { nullptr, (const void*)K<1>, (const void*)K<2>, (const void*)K<3>, (const void*)K<4>,             \
+    (const void*)K<5>, (const void*)K<6>, (const void*)K<7>, (const void*)K<8>, (const void*)K<9>,  \
+    (const void*)K<10> }
+#define NS_ROW2(K, B)                                                                                \
+  { nullptr, (const void*)K<1, B>, (const void*)K<2, B>, (const void*)K<3, B>, (const void*)K<4, B>, \
+    (const void*)K<5, B>, (const void*)K<6, B>, (const void*)K<7, B>, (const void*)K<8, B>,          \
+    (const void*)K<9, B>, (const void*)K<10, B> }
+static_assert(kMaxNS == 10, "kDenseFn rows list NS = 1..10");
 const void* const kDenseFn[DK_COUNT][kMaxNS + 1] = {
-    NS_ROW(k_eval),
-    {nullptr, (const void*)k_sparsify<1, false>, (const void*)k_sparsify<2, false>, (const void*)k_sparsify<3, false>,
-     (const void*)k_sparsify<4, false>, (const void*)k_sparsify<5, false>, (const void*)k_sparsify<6, false>,
-     (const void*)k_sparsify<7, false>, (const void*)k_sparsify<8, false>},
-    NS_ROW(k_test_a), NS_ROW(k_test_b),
-    {nullptr, (const void*)k_test_c<1, false>, (const void*)k_test_c<2, false>, (const void*)k_test_c<3, false>,
-     (const void*)k_test_c<4, false>, (const void*)k_test_c<5, false>, (const void*)k_test_c<6, false>,
-     (const void*)k_test_c<7, false>, (const void*)k_test_c<8, false>},
-    {nullptr, (const void*)k_test_c<1, true>, (const void*)k_test_c<2, true>, (const void*)k_test_c<3, true>,
-     (const void*)k_test_c<4, true>, (const void*)k_test_c<5, true>, (const void*)k_test_c<6, true>,
-     (const void*)k_test_c<7, true>, (const void*)k_test_c<8, true>},
-    NS_ROW(k_warm_zeta), NS_ROW(k_warm_gamma),
-    {nullptr, (const void*)k_sparsify<1, true>, (const void*)k_sparsify<2, true>, (const void*)k_sparsify<3, true>,
-     (const void*)k_sparsify<4, true>, (const void*)k_sparsify<5, true>, (const void*)k_sparsify<6, true>,
-     (const void*)k_sparsify<7, true>, (const void*)k_sparsify<8, true>}};
+    NS_ROW(k_eval),          NS_ROW2(k_sparsify, false), NS_ROW(k_test_a),    NS_ROW(k_test_b),
+    NS_ROW2(k_test_c, false), NS_ROW2(k_test_c, true),   NS_ROW(k_warm_zeta), NS_ROW(k_warm_gamma),
+    NS_ROW2(k_sparsify, true)};
 
 #define HV_ROW(K)                                                                                    \
   {                                                                                                  \

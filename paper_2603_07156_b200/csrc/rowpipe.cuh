@@ -26,7 +26,7 @@
 namespace otb {
 
 constexpr int kMaxCluster = 8;
-constexpr int kMaxNS = 8;
+constexpr int kMaxNS = 10;   // 1024-column slices per CTA: one CTA per row up to n = 10240
 
 struct Geom {
   const double* mat0;   // first streamed matrix (row-major, ld)
