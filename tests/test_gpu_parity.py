@@ -384,7 +384,10 @@ def test_fast_log_accuracy(cuda):
 
     rng = np.random.default_rng(5)
     x = np.concatenate([np.exp(rng.uniform(-744, 709, 400_000)), rng.uniform(0.5, 2.0, 200_000),
-                        1.0 + rng.standard_normal(50_000) * 1e-9, np.array([1.0, 2.0, 0.5, np.sqrt(2.0), 1e-310,
+                        1.0 + rng.standard_normal(50_000) * 1e-9,
+                        # |s| largest at m = sqrt(2)^-+, the series' truncation edge, at many exponents
+                        np.sqrt(2.0) * (1.0 + rng.uniform(-1e-3, 1e-3, 50_000)) * 2.0 ** rng.integers(-1000, 1000, 50_000),
+                        np.array([1.0, 2.0, 0.5, np.sqrt(2.0), 1e-310,
                                                                                0.0, -1.0, np.inf, np.nan])])
     xd = torch.from_numpy(x).cuda()
     out = torch.empty_like(xd)
