@@ -442,6 +442,7 @@ struct TestAIO {
   double* colpart;   // [ncl][n]
   double* spart;     // [gridDim][2]: sum of exp(candidate), count of NaN/+inf
   int recover;       // 0: round the given log plan as is (no candidate write)
+  double* czeta;     // metrics: c-transform zeta_i = min_j (C_ij - gamma_j) per row (feasibility.py:103), or nullptr
 };
 
 template <int NS>
@@ -458,12 +459,16 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_a(Geom geo
   const Divider DIV(eta);
   double sumx = 0.0;
   int bad = 0;
+  // wide rows (NS > 6) also reduce the c-transform for pass C (see k_test_c)
+  constexpr bool kCtr = NS > 6;
+  const bool ctr = kCtr && io.czeta != nullptr;
   for (int r = D.r0; r < D.r1; ++r) {
     const int64_t gi = D.g.row0 + r;
     const double la = io.recover ? __ldg(io.log_a + gi) : 0.0;
     const double l = io.recover ? io.lse[r] : 0.0;
     double xv[2 * NS];
     double rs = 0.0;
+    double shmin = INFINITY;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
       xv[2 * s] = 0.0;
@@ -473,6 +478,10 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_a(Geom geo
         D.fetch(c, x);
         const int j = D.col(s, 0);
         const double2 gm = load_pair(io.gamma, j, D.c1);
+        if (kCtr && ctr) {   // the slack's c-transform for pass C's KKT metrics
+          if (j < D.c1) shmin = fmin(shmin, c.x - gm.x);
+          if (j + 1 < D.c1) shmin = fmin(shmin, c.y - gm.y);
+        }
         double* dst = io.Xout + (size_t)r * D.g.ld + j;
         if (io.recover) {
           if (j < D.c1) {
@@ -496,7 +505,14 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_a(Geom geo
         rs += xv[2 * s] + xv[2 * s + 1];
       }
     }
-    const double rsum = D.row_sum(rs);
+    double rsum;
+    if (kCtr && ctr) {
+      double zeta;
+      D.row_sum_min(rs, shmin, rsum, zeta);
+      if (D.tid == 0 && D.cr == 0) io.czeta[r] = zeta;
+    } else {
+      rsum = D.row_sum(rs);
+    }
     const double ai = __ldg(io.a + gi);
     const double z = (rsum > 0.0) ? fmin(div_rn(ai, rsum), 1.0) : 1.0;
 #pragma unroll
@@ -589,6 +605,7 @@ struct TestCIO {
   double* rowpart;   // [m_loc * cl] row sums of the rounded plan
   double* colpart;   // [ncl][n] column sums of the rounded plan
   double* spart;     // [gridDim][8]
+  const double* czeta;   // METRICS: row c-transform from pass A
 };
 
 template <int NS, bool METRICS>
@@ -603,20 +620,26 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_c(Geom geo
   }
   const double deficit = *io.deficit;
   const Divider DD(deficit);
+  // The slack needs the row c-transform zeta (feasibility.py:103, row min of
+  // C - gamma).  Up to 6 slices the row's f and C - gamma stay in registers
+  // and zeta is reduced here; wider rows take zeta from pass A (k_test_a,
+  // czeta) so that they do not spill.  Same values, same summation order.
+  constexpr bool kZetaFromA = NS > 6;
+  constexpr int KR = (METRICS && !kZetaFromA) ? 2 * NS : 1;
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
   for (int r = D.r0; r < D.r1; ++r) {
     const double z = io.zrow[r];
     const double e_r = io.er[r];
-    double f[2 * NS];
-    double sh[2 * NS];
+    const double zeta_a = (METRICS && kZetaFromA) ? io.czeta[r] : 0.0;
+    double fk[KR], shk[KR];
     double shmin = INFINITY;
     double rs = 0.0;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      f[2 * s] = 0.0;
-      f[2 * s + 1] = 0.0;
-      sh[2 * s] = 0.0;
-      sh[2 * s + 1] = 0.0;
+      if constexpr (KR > 1) {
+        fk[2 * s] = fk[2 * s + 1] = 0.0;
+        shk[2 * s] = shk[2 * s + 1] = 0.0;
+      }
       if (s < D.nsl) {
         double2 x, c;
         D.fetch(x, c);
@@ -625,13 +648,14 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_c(Geom geo
         const double2 ee = load_pair(io.ec, j, D.c1);
         double2 gm = make_double2(0.0, 0.0);
         if constexpr (METRICS) gm = load_pair(io.gamma, j, D.c1);
+        double f2[2] = {0.0, 0.0};
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           if (j + e < D.c1) {
             const double xl = e ? x.y : x.x;
             double fv = (exp(xl) * z) * (e ? yy.y : yy.x);
             if (deficit > 0.0) fv = fv + DD(e_r * (e ? ee.y : ee.x));
-            f[2 * s + e] = fv;
+            f2[e] = fv;
             if (fv > 0.0) acc[0] += fv * (log_fast(fv) - xl);   // feasibility.py:84
             acc[1] += fv;
             rs += fv;
@@ -642,19 +666,27 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_c(Geom geo
               const double fm = fmin(fv, 0.0);
               acc[4] += fm * fm;
               const double shv = cv - (e ? gm.y : gm.x);
-              sh[2 * s + e] = shv;
-              shmin = fmin(shmin, shv);
+              if constexpr (kZetaFromA) {
+                const double sl = shv - zeta_a;
+                const double sm = fmin(sl, 0.0);
+                acc[5] += sm * sm;
+                acc[6] += fv * sl;
+              } else {
+                fk[2 * s + e] = fv;
+                shk[2 * s + e] = shv;
+                shmin = fmin(shmin, shv);
+              }
             }
           }
         }
         double2* a2 = D.acc2(0, s);
         double2 v = *a2;
-        v.x += f[2 * s];
-        v.y += f[2 * s + 1];
+        v.x += f2[0];
+        v.y += f2[1];
         *a2 = v;
       }
     }
-    if constexpr (METRICS) {
+    if constexpr (KR > 1) {
       const double zeta = D.row_min(shmin);
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
@@ -662,10 +694,10 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_c(Geom geo
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             if (D.col(s, e) < D.c1) {
-              const double sl = sh[2 * s + e] - zeta;
+              const double sl = shk[2 * s + e] - zeta;
               const double sm = fmin(sl, 0.0);
               acc[5] += sm * sm;
-              acc[6] += f[2 * s + e] * sl;
+              acc[6] += fk[2 * s + e] * sl;
             }
           }
         }

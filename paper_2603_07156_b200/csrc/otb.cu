@@ -151,6 +151,7 @@ struct otb_ctx {
   bool bound = false;
   // buffers
   double *rowM = nullptr, *rowS = nullptr, *lse = nullptr, *zrow = nullptr, *er = nullptr, *rowpart = nullptr;
+  double* czeta = nullptr;   // row c-transform of the KKT metrics (pass A -> pass C)
   double *colpart = nullptr, *vpart = nullptr, *sendbuf = nullptr, *bpart = nullptr;
   double *g = nullptr, *d = nullptr, *rhs = nullptr, *dir = nullptr, *cg_r = nullptr, *cg_p[2] = {nullptr, nullptr};
   double *cg_ap = nullptr, *cg_y = nullptr, *gtrial = nullptr, *yv = nullptr, *ec = nullptr;
@@ -639,7 +640,8 @@ int do_round(otb_ctx* c, const double* X, const double* gamma, double* Xout, int
   // pass A: candidate + row scaling + column sums
   {
     Geom geo = make_geom(c, DK_TESTA, c->C, X);
-    TestAIO io{gamma, c->a, c->log_a, c->lse, c->eta, Xout, c->zrow, c->colpart, c->vpart, recover};
+    TestAIO io{gamma,  c->a,     c->log_a, c->lse, c->eta, Xout, c->zrow, c->colpart, c->vpart, recover,
+               (metrics && c->ns > 6) ? c->czeta : nullptr};   // k_test_c: wide rows take zeta from pass A
     cudaEvent_t e0 = nullptr;
     TRY(prof_begin(c, &e0));
     TRY(launch_dense(c, DK_TESTA, geo, &io));
@@ -674,7 +676,7 @@ int do_round(otb_ctx* c, const double* X, const double* gamma, double* Xout, int
   {
     const int kind = metrics ? DK_TESTC1 : DK_TESTC0;
     Geom geo = make_geom(c, kind, src, metrics ? c->C : nullptr);
-    TestCIO io{c->zrow, c->yv, c->er, c->ec, &c->ds->deficit, gamma, c->rowpart, c->colpart, c->vpart};
+    TestCIO io{c->zrow, c->yv, c->er, c->ec, &c->ds->deficit, gamma, c->rowpart, c->colpart, c->vpart, c->czeta};
     cudaEvent_t e0 = nullptr;
     TRY(prof_begin(c, &e0));
     TRY(launch_dense(c, kind, geo, &io));
@@ -918,6 +920,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   A(&c->rowS, m_loc);
   A(&c->lse, m_loc);
   A(&c->zrow, m_loc);
+  A(&c->czeta, m_loc);
   A(&c->er, m_loc);
   A(&c->rowpart, (size_t)m_loc * cl);
   const int64_t parts = std::max<int64_t>(2 * c->ncl, c->hv_nb);
@@ -991,7 +994,8 @@ int otb_destroy(otb_ctx* c) {
   if (!c) return OTB_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  for (void* p : {(void*)c->rowM, (void*)c->rowS, (void*)c->lse, (void*)c->zrow, (void*)c->er, (void*)c->rowpart,
+  for (void* p : {(void*)c->rowM, (void*)c->rowS, (void*)c->lse, (void*)c->zrow, (void*)c->czeta, (void*)c->er,
+                  (void*)c->rowpart,
                   (void*)c->colpart, (void*)c->vpart, (void*)c->sendbuf, (void*)c->bpart, (void*)c->g, (void*)c->d,
                   (void*)c->rhs, (void*)c->dir, (void*)c->cg_r, (void*)c->cg_p[0], (void*)c->cg_p[1],
                   (void*)c->cg_ap, (void*)c->cg_y, (void*)c->gtrial, (void*)c->yv, (void*)c->ec, (void*)c->Mloc,

@@ -238,6 +238,23 @@ struct Dense {
     for (int q = 0; q < g.cl; ++q) s += all[q * 4];
     return s;
   }
+  // row_sum and row_min of two per-thread values with one barrier (and one
+  // exchange when the row is split); same bits as the separate calls.
+  OTB_DEV void row_sum_min(double s, double mn, double& S, double& MN) {
+    block_reduce2<kSum, kMin>(s, mn, sm.slots, rphase, g.nt);
+    if (g.cl == 1) {
+      S = s;
+      MN = mn;
+      return;
+    }
+    const double t[2] = {s, mn};
+    double all[kMaxCluster * 4];
+    exchange<2>(t, all);
+    S = 0.0;
+    MN = all[1];
+    for (int q = 0; q < g.cl; ++q) S += all[q * 4];
+    for (int q = 1; q < g.cl; ++q) MN = fmin(MN, all[q * 4 + 1]);
+  }
   OTB_DEV double row_min(double v) {
     double t[1] = {v};
     reduce<1, kMin>(t);

@@ -296,18 +296,19 @@ def test_fast_division_is_correctly_rounded(cuda, y):
     from paper_2603_07156_b200 import _lib
 
     rng = np.random.default_rng(11)
-    parts = [
-        rng.standard_normal(200_000) * 10.0 ** rng.uniform(-30, 30, 200_000),
-        rng.uniform(-1.0, 1.0, 100_000),
-        np.exp(rng.uniform(-745, 709, 50_000)),
-        np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, -5e-324, 1.7e308, 2.2250738585072014e-308]),
-        y * np.arange(-1000, 1000, dtype=np.float64),
-        np.nextafter(y * np.arange(1, 1000, dtype=np.float64), np.inf),
-        # every power of two and its neighbours: the edges of the fast path's range
-        2.0 ** np.arange(-1074, 1024, dtype=np.float64),
-        np.nextafter(2.0 ** np.arange(-1074, 1024, dtype=np.float64), np.inf),
-        -np.nextafter(2.0 ** np.arange(-1074, 1024, dtype=np.float64), 0.0),
-    ]
+    with np.errstate(all="ignore"):   # y = inf: inf * 0 in the multiples of y
+        parts = [
+            rng.standard_normal(200_000) * 10.0 ** rng.uniform(-30, 30, 200_000),
+            rng.uniform(-1.0, 1.0, 100_000),
+            np.exp(rng.uniform(-745, 709, 50_000)),
+            np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, -5e-324, 1.7e308, 2.2250738585072014e-308]),
+            y * np.arange(-1000, 1000, dtype=np.float64),
+            np.nextafter(y * np.arange(1, 1000, dtype=np.float64), np.inf),
+            # every power of two and its neighbours: the edges of the fast path's range
+            2.0 ** np.arange(-1074, 1024, dtype=np.float64),
+            np.nextafter(2.0 ** np.arange(-1074, 1024, dtype=np.float64), np.inf),
+            -np.nextafter(2.0 ** np.arange(-1074, 1024, dtype=np.float64), 0.0),
+        ]
     x = np.concatenate(parts)
     xd = torch.from_numpy(x).cuda()
     out = torch.empty_like(xd)
@@ -556,3 +557,32 @@ def test_newton_step_csr_overflow_retry_is_identical(cuda, monkeypatch):
     monkeypatch.delenv("OTB_CSR_CAP0", raising=False)
     assert outs[0][1] == outs[1][1] and outs[0][2] == outs[1][2]
     assert np.array_equal(outs[0][0], outs[1][0])
+
+
+@pytest.mark.parametrize("m,n", [(48, 6000), (40, 10240), (32, 16400)])
+def test_rounding_metrics_wide_rows_match_oracle(cuda, m, n):
+    """Pass C's KKT metrics on rows of more than 6 slices take the row
+    c-transform from pass A (k_test_c kZetaFromA), and above 10240 columns
+    the row is split over a cluster (cl = 2 at 16400): rounded plan,
+    Bregman divergence, objective and KKT residuals against the oracle."""
+    P = _api()
+    rng = np.random.default_rng(n)
+    x = rng.random((m, 2))
+    y = rng.random((n, 2))
+    C = ((x[:, None, :] - y[None, :, :]) ** 2).sum(axis=2)
+    C /= C.max()
+    a = rng.random(m) + 0.1
+    a /= a.sum()
+    b = rng.random(n) + 0.1
+    b /= b.sum()
+    gamma = rng.standard_normal(n) * 1e-3
+    logX = np.log(np.outer(a, b)) + rng.standard_normal((m, n)) * 0.3
+    prob = P.OtProblem(C, a, b)
+    f = P.round_log_plan(P.LogPlan(logX), prob, gamma=gamma, metrics=True)
+    R = O.round_plan(np.exp(logX), a, b)
+    assert rel(f.entries, R) <= 1e-13
+    assert f.bregman == pytest.approx(O.bregman(R, logX), rel=1e-9, abs=1e-14)
+    assert f.objective == pytest.approx(float((C * R).sum()), rel=1e-12)
+    k = O.kkt(R, gamma, C, a, b)
+    for key in ("delta_p", "delta_d", "delta_c", "delta_kkt"):
+        assert getattr(f, key) == pytest.approx(float(k[key]), rel=1e-6, abs=1e-15)
