@@ -59,7 +59,8 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_eval(Geom geo, 
         const double2 gm = load_pair(io.gamma, j, D.c1);
         if (j < D.c1) z[2 * s] = x.x + DIV(gm.x - c.x);
         if (j + 1 < D.c1) z[2 * s + 1] = x.y + DIV(gm.y - c.y);
-        mx = fmax(mx, fmax(z[2 * s], z[2 * s + 1]));
+        const double zm = z[2 * s] > z[2 * s + 1] ? z[2 * s] : z[2 * s + 1];   // DSETP + 2 FSEL (fmax: 4)
+        mx = zm > mx ? zm : mx;
       }
     }
     // row max over the whole row (cluster-wide when the row is split), so
