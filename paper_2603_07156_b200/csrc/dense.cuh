@@ -233,30 +233,43 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
       if (s < D.nsl) {
         bb0[s] = __ballot_sync(0xffffffffu, (keep >> (2 * s)) & 1u);
         bb1[s] = __ballot_sync(0xffffffffu, (keep >> (2 * s + 1)) & 1u);
-        if (D.lane == 0) tb[s * 32 + D.warp] = pairs ? __popc(bb0[s] | bb1[s]) : __popc(bb0[s]) + __popc(bb1[s]);
+        // packed count of the warp's chunk: stored units (pairs, or entries) | entries << 16
+        // (a window has at most 10240 columns, so neither field carries)
+        const int ents = __popc(bb0[s]) + __popc(bb1[s]);
+        if (D.lane == 0) tb[s * 32 + D.warp] = (pairs ? __popc(bb0[s] | bb1[s]) : ents) | (ents << 16);
       }
     }
-    double t[2] = {ks, (double)__popc(keep)};
-    D.template reduce<2, kSum>(t);   // barrier also publishes tb
+    double t[1] = {ks};
+    D.template reduce<1, kSum>(t);   // barrier also publishes tb
     double ksum = t[0];
-    int ecnt = (int)t[1];            // kept entries of the row (this window)
-    // per-slice totals (lane s holds slice s), exclusive scan over slices
-    // and (pre) the kept entries of slice s in the warps before this one
-    int tot = 0, pre = 0;
-    if (D.lane < D.nsl)
-      for (int w = 0; w < nw; ++w) {
-        const int v = tb[D.lane * 32 + w];
-        tot += v;
-        if (w < D.warp) pre += v;
-      }
-    int incl = tot;
+    // Exclusive scan of the packed counts over (slice, warp) — the order of
+    // the row run.  Two slices per round, one 16-lane segment each (lane =
+    // warp index); pre[s] = start of this warp's chunk of slice s.
+    int pre[NS];
+    int run = 0;
+    {
+      const int seg = D.lane >> 4, wl = D.lane & 15;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, o);
-      if (D.lane >= o) incl += v;
+      for (int q = 0; q < (NS + 1) / 2; ++q) {
+        const int sl = 2 * q + seg;
+        const int v = (sl < D.nsl && wl < nw) ? tb[sl * 32 + wl] : 0;
+        int inc = v;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, inc, o, 16);
+          if (wl >= o) inc += u;
+        }
+        const int tot0 = __shfl_sync(0xffffffffu, inc, 15), tot1 = __shfl_sync(0xffffffffu, inc, 31);
+        const int ex0 = __shfl_sync(0xffffffffu, inc - v, D.warp);
+        const int ex1 = __shfl_sync(0xffffffffu, inc - v, 16 + D.warp);
+        pre[2 * q] = run + ex0;
+        run += tot0;
+        if (2 * q + 1 < NS) pre[2 * q + 1] = run + ex1;
+        run += tot1;
+      }
     }
-    const int excl = incl - tot;
-    int need = __shfl_sync(0xffffffffu, incl, 31);   // kept (entries or pairs) in this CTA's window
+    int ecnt = run >> 16;                              // kept entries of the row (this window)
+    int need = run & 0xffff;                           // kept (entries or pairs) in this CTA's window
     int cnt = need;                                    // ... in the whole row
     int myoff = 0;                                     // offset of this window in the row
     if (D.g.cl > 1) {
@@ -380,7 +393,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
           if (s < D.nsl) {
             const unsigned k0 = (keep >> (2 * s)) & 1u, k1 = (keep >> (2 * s + 1)) & 1u;
             const unsigned b0 = bb0[s], b1 = bb1[s];
-            const int base = __shfl_sync(0xffffffffu, excl + pre, s);
+            const int base = pre[s] & 0xffff;
             const int j = D.col(s, 0);
             if (io.bm != nullptr && D.lane == 0) {
               const int cs = D.c0 + s * D.slice + 64 * D.warp;
