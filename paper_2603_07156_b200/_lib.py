@@ -83,6 +83,7 @@ SIGNATURES = {
     "otb_scale_cost": (C.c_int, [vp, i64, i64, i64, dbl, vp]),
     "otb_selftest_div": (C.c_int, [vp, i64, dbl, vp]),
     "otb_selftest_log": (C.c_int, [vp, i64, vp]),
+    "otb_selftest_exp": (C.c_int, [vp, i64, vp]),
     "otb_cg_trace": (C.c_int, [vp, vp, i64, C.POINTER(i64)]),
     "otb_prof_enable": (C.c_int, [vp, C.c_int]),
     "otb_prof_read": (C.c_int, [vp, C.POINTER(dbl), C.POINTER(i64), C.POINTER(dbl), C.c_int]),

@@ -497,25 +497,29 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_a(Geom geo
           if (j + 1 < D.c1) shmin = fmin(shmin, c.y - gm.y);
         }
         double* dst = io.Xout + (size_t)r * D.g.ld + j;
+        double l0 = x.x, l1 = x.y;   // the slice's log entries (candidate, or the plan as given)
         if (io.recover) {
           if (j < D.c1) {
             const double raw = ((la + x.x) + DIV(gm.x - c.x)) - l;
             bad |= (isnan(raw) || raw == INFINITY);
-            const double xl = fmax(raw, kLogFloor);
-            dst[0] = xl;
-            xv[2 * s] = exp(xl);
+            l0 = fmax(raw, kLogFloor);
+            dst[0] = l0;
           }
           if (j + 1 < D.c1) {
             const double raw = ((la + x.y) + DIV(gm.y - c.y)) - l;
             bad |= (isnan(raw) || raw == INFINITY);
-            const double xl = fmax(raw, kLogFloor);
-            dst[1] = xl;
-            xv[2 * s + 1] = exp(xl);
+            l1 = fmax(raw, kLogFloor);
+            dst[1] = l1;
           }
-        } else {
-          if (j < D.c1) xv[2 * s] = exp(x.x);
-          if (j + 1 < D.c1) xv[2 * s + 1] = exp(x.y);
         }
+        bool ok = true;   // both exps branch-free (exp() only when out of range)
+        double e0 = exp_fast(l0, ok), e1 = exp_fast(l1, ok);
+        if (!ok) {
+          e0 = exp(l0);
+          e1 = exp(l1);
+        }
+        if (j < D.c1) xv[2 * s] = e0;
+        if (j + 1 < D.c1) xv[2 * s + 1] = e1;
         rs += xv[2 * s] + xv[2 * s + 1];
       }
     }
@@ -576,22 +580,61 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_b(Geom geo
   for (int r = D.r0; r < D.r1; ++r) {
     const double z = io.zrow[r];
     double rs = 0.0;
+    if constexpr (NS <= 6) {
+      // the row's slices first (barrier waits are control flow), then all
+      // its exps branch-free so that their FMA chains overlap
+      double xs[2 * NS], ex[2 * NS];
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      if (s < D.nsl) {
-        double2 x, unused;
-        D.fetch(x, unused);
-        const int j = D.col(s, 0);
-        const double2 yy = load_pair(io.y, j, D.c1);
-        double f0 = 0.0, f1 = 0.0;
-        if (j < D.c1) f0 = (exp(x.x) * z) * yy.x;
-        if (j + 1 < D.c1) f1 = (exp(x.y) * z) * yy.y;
-        rs += f0 + f1;
-        double2* a2 = D.acc2(0, s);
-        double2 v = *a2;
-        v.x += f0;
-        v.y += f1;
-        *a2 = v;
+      for (int s = 0; s < NS; ++s) {
+        xs[2 * s] = xs[2 * s + 1] = 0.0;
+        if (s < D.nsl) {
+          double2 x, unused;
+          D.fetch(x, unused);
+          xs[2 * s] = x.x;
+          xs[2 * s + 1] = x.y;
+        }
+      }
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < 2 * NS; ++k) ex[k] = exp_fast(xs[k], ok);
+      if (!ok) {
+#pragma unroll
+        for (int k = 0; k < 2 * NS; ++k) ex[k] = exp(xs[k]);
+      }
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        if (s < D.nsl) {
+          const int j = D.col(s, 0);
+          const double2 yy = load_pair(io.y, j, D.c1);
+          double f0 = 0.0, f1 = 0.0;
+          if (j < D.c1) f0 = (ex[2 * s] * z) * yy.x;
+          if (j + 1 < D.c1) f1 = (ex[2 * s + 1] * z) * yy.y;
+          rs += f0 + f1;
+          double2* a2 = D.acc2(0, s);
+          double2 v = *a2;
+          v.x += f0;
+          v.y += f1;
+          *a2 = v;
+        }
+      }
+    } else {   // wide rows: registers are short; one slice at a time
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        if (s < D.nsl) {
+          double2 x, unused;
+          D.fetch(x, unused);
+          const int j = D.col(s, 0);
+          const double2 yy = load_pair(io.y, j, D.c1);
+          double f0 = 0.0, f1 = 0.0;
+          if (j < D.c1) f0 = (exp(x.x) * z) * yy.x;
+          if (j + 1 < D.c1) f1 = (exp(x.y) * z) * yy.y;
+          rs += f0 + f1;
+          double2* a2 = D.acc2(0, s);
+          double2 v = *a2;
+          v.x += f0;
+          v.y += f1;
+          *a2 = v;
+        }
       }
     }
     double t[1] = {rs};
@@ -663,11 +706,17 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_c(Geom geo
         double2 gm = make_double2(0.0, 0.0);
         if constexpr (METRICS) gm = load_pair(io.gamma, j, D.c1);
         double f2[2] = {0.0, 0.0};
+        bool ok = true;   // both exps of the slice branch-free (exp() only when out of range)
+        double ex2[2] = {exp_fast(x.x, ok), exp_fast(x.y, ok)};
+        if (!ok) {
+          ex2[0] = exp(x.x);
+          ex2[1] = exp(x.y);
+        }
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           if (j + e < D.c1) {
             const double xl = e ? x.y : x.x;
-            double fv = (exp(xl) * z) * (e ? yy.y : yy.x);
+            double fv = (ex2[e] * z) * (e ? yy.y : yy.x);
             if (deficit > 0.0) fv = fv + DD(e_r * (e ? ee.y : ee.x));
             f2[e] = fv;
             if (fv > 0.0) acc[0] += fv * (log_fast(fv) - xl);   // feasibility.py:84

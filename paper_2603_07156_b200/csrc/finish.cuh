@@ -408,6 +408,17 @@ __global__ void k_selftest_log(const double* __restrict__ x, int64_t n, double* 
     out[i] = log_fast(x[i]);
 }
 
+// Test hook for exp_fast (common.cuh): out[i] = exp_fast(x_i) (exp() where
+// the fast path does not apply), out[n + i] = exp(x_i).
+__global__ void k_selftest_exp(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    bool ok = true;
+    const double f = exp_fast(x[i], ok);
+    out[i] = ok ? f : exp(x[i]);
+    out[n + i] = exp(x[i]);
+  }
+}
+
 // Test hook for Divider (common.cuh): out_i = x_i / y.
 __global__ void k_selftest_div(const double* __restrict__ x, int64_t n, double y, double* __restrict__ out) {
   const Divider D(y);

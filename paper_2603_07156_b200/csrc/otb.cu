@@ -1442,6 +1442,15 @@ int otb_cg_trace(otb_ctx* c, uint64_t* out, int64_t cap, int64_t* count) {
   return OTB_OK;
 }
 
+int otb_selftest_exp(const double* x, int64_t n, double* out) {
+  if ((!x || !out) && n > 0) return fail(OTB_ERR_ARG, "null");
+  if (n <= 0) return OTB_OK;
+  k_selftest_exp<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256>>>(x, n, out);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaDeviceSynchronize());
+  return OTB_OK;
+}
+
 int otb_selftest_log(const double* x, int64_t n, double* out) {
   if ((!x || !out) && n > 0) return fail(OTB_ERR_ARG, "null");
   if (n <= 0) return OTB_OK;

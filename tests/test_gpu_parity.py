@@ -586,3 +586,28 @@ def test_rounding_metrics_wide_rows_match_oracle(cuda, m, n):
     k = O.kkt(R, gamma, C, a, b)
     for key in ("delta_p", "delta_d", "delta_c", "delta_kkt"):
         assert getattr(f, key) == pytest.approx(float(k[key]), rel=1e-6, abs=1e-15)
+
+
+def test_fast_exp_is_cuda_exp(cuda):
+    """The dense passes' branch-free exp (common.cuh exp_fast, with exp() for
+    |x| >= 708.4) returns CUDA exp()'s bits on every input, including the
+    range edges, subnormal results, infinities and NaN."""
+    import torch
+
+    from paper_2603_07156_b200 import _lib
+
+    rng = np.random.default_rng(17)
+    x = np.concatenate([rng.uniform(-750, 710, 500_000), rng.standard_normal(200_000) * 30,
+                        rng.uniform(-1e-3, 1e-3, 100_000), np.linspace(-709.0, -707.0, 20_001),
+                        np.linspace(707.0, 709.9, 20_001), -(2.0 ** np.arange(-1074, 11, dtype=np.float64)),
+                        np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, 709.782712893384, -745.1332191019412])])
+    xd = torch.from_numpy(x).cuda()
+    out = torch.empty(2 * x.size, dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib.otb_selftest_exp(xd.data_ptr(), x.size, out.data_ptr()))
+    got = out.cpu().numpy()
+    fast, ref = got[: x.size], got[x.size:]
+    same = (fast.view(np.uint64) == ref.view(np.uint64)) | (np.isnan(fast) & np.isnan(ref))
+    assert same.all(), (x[~same][:5], fast[~same][:5], ref[~same][:5])
+    with np.errstate(all="ignore"):
+        fin = np.isfinite(ref) & (ref > 1e-300)
+        assert np.max(np.abs(ref[fin] - np.exp(x[fin])) / np.spacing(np.exp(x[fin]))) <= 2.0
