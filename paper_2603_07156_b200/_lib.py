@@ -48,6 +48,11 @@ class TestOut(C.Structure):
     __test__ = False
 
 
+class InnerOut(C.Structure):
+    _fields_ = [("value0", dbl), ("grad_norm0", dbl), ("stepped", C.c_int), ("tested", C.c_int),
+                ("newton", NewtonOut), ("test", TestOut)]
+
+
 class WarmOut(C.Structure):
     _fields_ = [("sweeps", i64), ("err", dbl)]
 
@@ -84,6 +89,7 @@ SIGNATURES = {
     "otb_selftest_div": (C.c_int, [vp, i64, dbl, vp]),
     "otb_selftest_log": (C.c_int, [vp, i64, vp]),
     "otb_selftest_exp": (C.c_int, [vp, i64, vp]),
+    "otb_inner_iteration": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, dbl, dbl, vp, vp]),
     "otb_cg_trace": (C.c_int, [vp, vp, i64, C.POINTER(i64)]),
     "otb_prof_enable": (C.c_int, [vp, C.c_int]),
     "otb_prof_read": (C.c_int, [vp, C.POINTER(dbl), C.POINTER(i64), C.POINTER(dbl), C.c_int]),

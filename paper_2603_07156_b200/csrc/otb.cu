@@ -1259,6 +1259,29 @@ int otb_recover_round(otb_ctx* c, const double* logX, const double* gamma, doubl
   return do_round(c, logX, gamma, logX_out, recover, metrics, out);
 }
 
+int otb_inner_iteration(otb_ctx* c, const double* logX, const double* gamma_in, double* gamma_out,
+                        const otb_newton_params* p, int eval_first, double floor, double test_below,
+                        double* logX_out, otb_inner_out* out) {
+  TRY(require_bound(c));
+  if (!out) return fail(OTB_ERR_ARG, "out is null");
+  if (((uintptr_t)logX) % 256 != 0) return fail(OTB_ERR_ARG, "logX must be 256-byte aligned");
+  if (eval_first) TRY(do_eval(c, logX, gamma_in));                 // inner_newton.py:196
+  out->value0 = c->last_value;
+  out->grad_norm0 = c->last_gnorm;
+  out->stepped = 0;
+  out->tested = 0;
+  if (c->last_gnorm <= floor) return OTB_OK;                       // :205 gradient floor
+  TRY(otb_newton_step(c, logX, gamma_in, gamma_out, p, &out->newton));
+  out->stepped = 1;
+  if (test_below >= 0.0 && out->newton.grad_norm_after < test_below) {   // :239 pre-check, then the test
+    if (!logX_out || ((uintptr_t)logX_out) % 256 != 0)
+      return fail(OTB_ERR_ARG, "logX_out must be a 256-byte aligned buffer");
+    TRY(do_round(c, logX, gamma_out, logX_out, 1, 1, &out->test));
+    out->tested = 1;
+  }
+  return OTB_OK;
+}
+
 int otb_materialize_rounded(otb_ctx* c, double* out, int64_t ldo) {
   TRY(require_bound(c));
   if (!c->round_src) return fail(OTB_ERR_ARG, "no rounding performed yet");

@@ -127,16 +127,48 @@ def inner_solve(logplan: LogPlan, gamma0: DualState, problem: OtProblem, config:
                 g_cur[:n].copy_(s._vec(src)[:n])
     cand_t = out_plan if out_plan is not None else s.new_plan()
 
-    value, grad_norm = s.ops.eval(plan_t, g_cur)
     step_sizes: list[float] = []
     nnzs: list[int] = []
     cgs: list[int] = []
-    values: list[float] = [value]
     cg_total = 0
     stop = StopReason.MAX_INNER
     tested = None
     tests: list[tuple] = []
-    for v in range(1, config.max_inner + 1):
+    native = observer is None and not recenter_every and config.max_inner >= 1
+    if native:
+        # the loop body in native code (otb_inner_iteration): the initial
+        # evaluate, the floor stop, the step and the inexact test with no
+        # Python round trip between their kernels; same decisions, same order
+        test_below = mu_k if grad_target is None else -1.0
+        values: list[float] = []
+        for v in range(1, config.max_inner + 1):
+            r = s.ops.inner_iteration(plan_t, g_cur, g_nxt, config.armijo_sigma, config.armijo_beta,
+                                      config.cg_rel_tol, config.cg_max_iters, v == 1, floor, test_below, cand_t)
+            if v == 1:
+                value, grad_norm = float(r.value0), float(r.grad_norm0)
+                values.append(value)
+            if not r.stepped:
+                stop = StopReason.GRAD_FLOOR
+                break
+            nr = r.newton
+            g_cur, g_nxt = g_nxt, g_cur
+            value, grad_norm = float(nr.value_after), float(nr.grad_norm_after)
+            step_sizes.append(float(nr.t))
+            nnzs.append(int(nr.nnz))
+            cgs.append(int(nr.cg_iters))
+            values.append(value)
+            cg_total += int(nr.cg_iters)
+            if r.tested:
+                res = r.test
+                tests.append((v, grad_norm, float(res.bregman)))
+                if res.bregman <= scale * mu_k:
+                    stop = StopReason.INEXACT_CRITERION
+                    tested = res
+                    break
+    else:
+        value, grad_norm = s.ops.eval(plan_t, g_cur)
+        values = [value]
+    for v in range(1, 0 if native else config.max_inner + 1):
         if grad_norm <= floor:
             stop = StopReason.GRAD_FLOOR
             break

@@ -284,6 +284,19 @@ class Ops:
                                             gamma_out.data_ptr(), C.byref(p), C.byref(out)))
         return out
 
+    def inner_iteration(self, plan_t, gamma_in, gamma_out, sigma, beta, cg_rel_tol, cg_max_iters, eval_first,
+                        floor, test_below, out_plan):
+        """One iteration of inner_solve's loop in native code (otb_inner_iteration):
+        [eval], floor stop, Newton step, and the inexact test when the new
+        ||g|| < test_below (test_below < 0: never)."""
+        p = _lib.NewtonParams(float(sigma), float(beta), float(cg_rel_tol),
+                              0 if cg_max_iters is None else int(cg_max_iters), -1.0)
+        out = _lib.InnerOut()
+        _lib.check(_lib.lib.otb_inner_iteration(self.s.ctx, plan_t.data_ptr(), gamma_in.data_ptr(),
+                                                gamma_out.data_ptr(), C.byref(p), 1 if eval_first else 0,
+                                                float(floor), float(test_below), _ptr(out_plan), C.byref(out)))
+        return out
+
     def recover_round(self, plan_t, gamma_t, out_plan=None, recover=True, metrics=True):
         res = _lib.TestOut()
         _lib.check(_lib.lib.otb_recover_round(self.s.ctx, plan_t.data_ptr(), gamma_t.data_ptr(), _ptr(out_plan),
