@@ -57,8 +57,10 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_eval(Geom geo, 
         D.fetch(c, x);
         const int j = D.col(s, 0);
         const double2 gm = load_pair(io.gamma, j, D.c1);
-        if (j < D.c1) z[2 * s] = x.x + DIV(gm.x - c.x);
-        if (j + 1 < D.c1) z[2 * s + 1] = x.y + DIV(gm.y - c.y);
+        double q0, q1;
+        DIV.pair(gm.x - c.x, gm.y - c.y, q0, q1);
+        if (j < D.c1) z[2 * s] = x.x + q0;
+        if (j + 1 < D.c1) z[2 * s + 1] = x.y + q1;
         const double zm = z[2 * s] > z[2 * s + 1] ? z[2 * s] : z[2 * s + 1];   // DSETP + 2 FSEL (fmax: 4)
         mx = zm > mx ? zm : mx;
       }
@@ -95,10 +97,12 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_eval(Geom geo, 
         if (io.P != nullptr) {                    // semidual.py:82-83: shifted / row_sum
           const int j = D.col(s, 0);
           double* dst = io.P + (size_t)r * D.g.ld + j;
+          double p0, p1;
+          DS.pair(z[2 * s], z[2 * s + 1], p0, p1);
           if (j + 1 < D.c1) {
-            *reinterpret_cast<double2*>(dst) = make_double2(DS(z[2 * s]), DS(z[2 * s + 1]));
+            *reinterpret_cast<double2*>(dst) = make_double2(p0, p1);
           } else if (j < D.c1) {
-            dst[0] = DS(z[2 * s]);
+            dst[0] = p0;
           }
         }
       }
@@ -403,8 +407,10 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
             if (pairs) {
               if (k0 | k1) {
                 const int off = base + __popc((b0 | b1) & lt);
-                const double v0 = k0 ? (anc ? P[2 * s] : DK(P[2 * s])) : 0.0;
-                const double v1 = k1 ? (anc ? P[2 * s + 1] : DK(P[2 * s + 1])) : 0.0;
+                double n0, n1;   // sparsify.py:109-110: kept / kept_sum (the anchor row unnormalised)
+                DK.pair(P[2 * s], P[2 * s + 1], n0, n1);
+                const double v0 = k0 ? (anc ? P[2 * s] : n0) : 0.0;
+                const double v1 = k1 ? (anc ? P[2 * s + 1] : n1) : 0.0;
                 *reinterpret_cast<double2*>(io.vals + wbase + 2 * off) = make_double2(v0, v1);
                 if (k0) a2->x += ai * v0;
                 if (k1) a2->y += ai * v1;
@@ -499,14 +505,16 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_a(Geom geo
         double* dst = io.Xout + (size_t)r * D.g.ld + j;
         double l0 = x.x, l1 = x.y;   // the slice's log entries (candidate, or the plan as given)
         if (io.recover) {
+          double q0, q1;
+          DIV.pair(gm.x - c.x, gm.y - c.y, q0, q1);
           if (j < D.c1) {
-            const double raw = ((la + x.x) + DIV(gm.x - c.x)) - l;
+            const double raw = ((la + x.x) + q0) - l;
             bad |= (isnan(raw) || raw == INFINITY);
             l0 = fmax(raw, kLogFloor);
             dst[0] = l0;
           }
           if (j + 1 < D.c1) {
-            const double raw = ((la + x.y) + DIV(gm.y - c.y)) - l;
+            const double raw = ((la + x.y) + q1) - l;
             bad |= (isnan(raw) || raw == INFINITY);
             l1 = fmax(raw, kLogFloor);
             dst[1] = l1;
