@@ -839,8 +839,10 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_warm_zeta(Geom 
         cs[2 * s + 1] = c.y;
         const int j = D.col(s, 0);
         const double2 gm = load_pair(io.gamma, j, D.c1);
-        if (j < D.c1) mx = fmax(mx, x.x + DIV(gm.x - c.x));
-        if (j + 1 < D.c1) mx = fmax(mx, x.y + DIV(gm.y - c.y));
+        double q0, q1;
+        DIV.pair(gm.x - c.x, gm.y - c.y, q0, q1);
+        if (j < D.c1) mx = fmax(mx, x.x + q0);
+        if (j + 1 < D.c1) mx = fmax(mx, x.y + q1);
       }
     }
     double t[1] = {mx};
@@ -852,8 +854,16 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_warm_zeta(Geom 
       if (s < D.nsl) {
         const int j = D.col(s, 0);
         const double2 gm = load_pair(io.gamma, j, D.c1);
-        if (j < D.c1) se += exp((xs[2 * s] + DIV(gm.x - cs[2 * s])) - M);
-        if (j + 1 < D.c1) se += exp((xs[2 * s + 1] + DIV(gm.y - cs[2 * s + 1])) - M);
+        double q0, q1;
+        DIV.pair(gm.x - cs[2 * s], gm.y - cs[2 * s + 1], q0, q1);
+        bool ok = true;
+        double e0 = exp_fast((xs[2 * s] + q0) - M, ok), e1 = exp_fast((xs[2 * s + 1] + q1) - M, ok);
+        if (!ok) {
+          e0 = exp((xs[2 * s] + q0) - M);
+          e1 = exp((xs[2 * s + 1] + q1) - M);
+        }
+        if (j < D.c1) se += e0;
+        if (j + 1 < D.c1) se += e1;
       }
     }
     t[0] = se;
@@ -877,9 +887,16 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_warm_zeta(Geom 
       if (s < D.nsl) {
         const int j = D.col(s, 0);
         const double2 gm = load_pair(io.gamma, j, D.c1);
-        double e0 = 0.0, e1 = 0.0;
-        if (j < D.c1) e0 = exp(xs[2 * s] + DIV((zeta + gm.x) - cs[2 * s]));
-        if (j + 1 < D.c1) e1 = exp(xs[2 * s + 1] + DIV((zeta + gm.y) - cs[2 * s + 1]));
+        double q0, q1;
+        DIV.pair((zeta + gm.x) - cs[2 * s], (zeta + gm.y) - cs[2 * s + 1], q0, q1);
+        bool ok = true;
+        double e0 = exp_fast(xs[2 * s] + q0, ok), e1 = exp_fast(xs[2 * s + 1] + q1, ok);
+        if (!ok) {
+          e0 = exp(xs[2 * s] + q0);
+          e1 = exp(xs[2 * s + 1] + q1);
+        }
+        if (j >= D.c1) e0 = 0.0;
+        if (j + 1 >= D.c1) e1 = 0.0;
         double2* a2 = D.acc2(0, s);
         double2 v = *a2;
         v.x += e0;
@@ -929,8 +946,10 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_warm_gamma(Geom
         double2* m2 = D.acc2(0, s);
         double2* s2 = D.acc2(1, s);
         double2 m = *m2, sm = *s2;
+        double q0, q1;
+        DIV.pair(zi - c.x, zi - c.y, q0, q1);
         if (j < D.c1) {
-          const double tv = x.x + DIV(zi - c.x);
+          const double tv = x.x + q0;
           if (tv > m.x) {
             sm.x = sm.x * exp(m.x - tv) + 1.0;
             m.x = tv;
@@ -939,7 +958,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_warm_gamma(Geom
           }
         }
         if (j + 1 < D.c1) {
-          const double tv = x.y + DIV(zi - c.y);
+          const double tv = x.y + q1;
           if (tv > m.y) {
             sm.y = sm.y * exp(m.y - tv) + 1.0;
             m.y = tv;
