@@ -71,8 +71,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_eval(Geom geo, 
     D.reduce<1, kMax>(t);
     double M = t[0];
     if (D.g.cl > 1) {
-      double all[kMaxCluster * 4];
-      D.exchange<1>(t, all);
+      const double* all = D.exchange<1>(t);
       M = all[0];
       for (int q = 1; q < D.g.cl; ++q) M = fmax(M, all[q * 4]);
     }
@@ -278,8 +277,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
     int myoff = 0;                                     // offset of this window in the row
     if (D.g.cl > 1) {
       double v3[3] = {(double)need, ksum, (double)ecnt};
-      double all[kMaxCluster * 4];
-      D.template exchange<3>(v3, all);
+      const double* all = D.template exchange<3>(v3);
       double cs = 0.0, kss = 0.0, es = 0.0;
       for (int q = 0; q < D.g.cl; ++q) {
         if (q < D.cr) myoff += (int)all[q * 4];
@@ -314,8 +312,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
       jm = u[0];
       if (D.g.cl > 1) {
         double v2[2] = {pmax, jm};
-        double all[kMaxCluster * 4];
-        D.template exchange<2>(v2, all);
+        const double* all = D.template exchange<2>(v2);
         double bp = all[0], bj = all[1];
         for (int q = 1; q < D.g.cl; ++q) {
           if (all[q * 4] > bp || (all[q * 4] == bp && all[q * 4 + 1] < bj)) {
@@ -351,8 +348,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
     }
     if (D.g.cl > 1) {
       double v1[1] = {(double)start};
-      double all[kMaxCluster * 4];
-      D.template exchange<1>(v1, all);
+      const double* all = D.template exchange<1>(v1);
       start = (unsigned long long)all[0];
     }
     const bool ovf = (int64_t)(start + cnt_al) > io.cap;
@@ -871,8 +867,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_warm_zeta(Geom 
     double S = t[0];
     if (D.g.cl > 1) {
       double v2[2] = {M, S};
-      double all[kMaxCluster * 4];
-      D.exchange<2>(v2, all);
+      const double* all = D.exchange<2>(v2);
       double Mg = all[0];
       for (int q = 1; q < D.g.cl; ++q) Mg = fmax(Mg, all[q * 4]);
       double Sg = 0.0;

@@ -197,15 +197,12 @@ struct Dense {
     block_reduce<K, OP>(v, sm.slots, rphase, g.nt);
   }
 
-  // Exchange K (<=4) values among the cl CTAs of the cluster; out[q*4+k] is
-  // CTA q's value k.  No-op copy when cl == 1.  Consumer threads only.
+  // Exchange K (<=4) values among the cl (> 1) CTAs of the cluster.  Returns
+  // the shared-memory table: entry [q*4 + k] is CTA q's value k, readable
+  // until the exchange after next (two buffers alternate).  Consumer threads
+  // only.
   template <int K>
-  OTB_DEV void exchange(const double (&v)[K], double* out) {
-    if (g.cl == 1) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) out[k] = v[k];
-      return;
-    }
+  OTB_DEV const double* exchange(const double (&v)[K]) {
     const int q = xcount & 1;
     const uint32_t par = (uint32_t)((xcount >> 1) & 1);
     double* mine = sm.xbuf + (q * kMaxCluster + cr) * 4;
@@ -220,11 +217,8 @@ struct Dense {
       }
     }
     bar_sync(1, g.nt);
-    const double* src = sm.xbuf + q * kMaxCluster * 4;
-    for (int rk = 0; rk < g.cl; ++rk)
-#pragma unroll
-      for (int k = 0; k < K; ++k) out[rk * 4 + k] = src[rk * 4 + k];
     ++xcount;
+    return sm.xbuf + q * kMaxCluster * 4;
   }
 
   // Row-wide (cluster-wide) sum of a per-thread value.
@@ -232,8 +226,7 @@ struct Dense {
     double t[1] = {v};
     reduce<1, kSum>(t);
     if (g.cl == 1) return t[0];
-    double all[kMaxCluster * 4];
-    exchange<1>(t, all);
+    const double* all = exchange<1>(t);
     double s = 0.0;
     for (int q = 0; q < g.cl; ++q) s += all[q * 4];
     return s;
@@ -248,8 +241,7 @@ struct Dense {
       return;
     }
     const double t[2] = {s, mn};
-    double all[kMaxCluster * 4];
-    exchange<2>(t, all);
+    const double* all = exchange<2>(t);
     S = 0.0;
     MN = all[1];
     for (int q = 0; q < g.cl; ++q) S += all[q * 4];
@@ -259,8 +251,7 @@ struct Dense {
     double t[1] = {v};
     reduce<1, kMin>(t);
     if (g.cl == 1) return t[0];
-    double all[kMaxCluster * 4];
-    exchange<1>(t, all);
+    const double* all = exchange<1>(t);
     double s = all[0];
     for (int q = 1; q < g.cl; ++q) s = fmin(s, all[q * 4]);
     return s;
