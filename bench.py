@@ -45,7 +45,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK_GBS = 6650.0
-E2E_DEFAULT = 10
+E2E_DEFAULT = 30
 
 
 def parse():

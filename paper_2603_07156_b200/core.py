@@ -186,9 +186,17 @@ class LogPlan:
         out[:, :n].copy_(src, non_blocking=True)
         if ld > n:
             out[:, n:].zero_()
-        if check:
-            _check_plan_tensor(out[:, :n])
-            torch.clamp_min_(out[:, :n], LOG_FLOOR)
+        if check:   # core.py:141-145 in one native pass (count NaN/+inf, clamp at LOG_FLOOR)
+            import ctypes
+
+            from . import _lib
+
+            bad = ctypes.c_int64()
+            _lib.check(_lib.lib.otb_check_clamp_plan(out.data_ptr(), m, n, ld, float(LOG_FLOOR),
+                                                     ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream),
+                                                     ctypes.byref(bad)))
+            if bad.value:
+                raise InvalidCost("log plan contains NaN or +inf entries")
         self._dev = ("padded", out)
         return out
 

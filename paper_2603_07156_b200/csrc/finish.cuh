@@ -18,6 +18,7 @@ struct DevScalars {
   double row_sq, col_sq;               // KKT marginal residual sums of squares
   double warm_err;
   double drift;
+  double cnorm_sq;                     // ||C||_F^2 when the caller gave it as a device scalar
   double scratch[4];
   unsigned long long alloc;            // CSR bump allocator
   unsigned long long nnzc;             // kept entries of the last sparsify
@@ -406,6 +407,34 @@ __global__ void k_bm_export(const uint4* __restrict__ bm, int nq, int m_loc, con
 __global__ void k_selftest_log(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = log_fast(x[i]);
+}
+
+// core.py:141-145 on an uploaded log plan in one pass: count NaN / +inf
+// entries (InvalidCost) and clamp below at LOG_FLOOR (NaN stays NaN).
+__global__ void k_check_clamp(double* __restrict__ X, int64_t ld, int m, int n, double floor_v,
+                              unsigned long long* __restrict__ bad) {
+  unsigned long long nb = 0;
+  for (int r = blockIdx.x; r < m; r += gridDim.x) {   // one row per block step, columns by pairs
+    double* row = X + (int64_t)r * ld;
+    for (int j = 2 * threadIdx.x; j < n; j += 2 * blockDim.x) {
+      if (j + 1 < n) {
+        double2 v = *reinterpret_cast<double2*>(row + j);   // rows are 256-byte aligned, j even
+        nb += (v.x != v.x || v.x == INFINITY) + (v.y != v.y || v.y == INFINITY);
+        const bool c0 = v.x < floor_v, c1 = v.y < floor_v;
+        if (c0 || c1) {
+          v.x = c0 ? floor_v : v.x;
+          v.y = c1 ? floor_v : v.y;
+          *reinterpret_cast<double2*>(row + j) = v;
+        }
+      } else {
+        const double v = row[j];
+        nb += (v != v || v == INFINITY);
+        if (v < floor_v) row[j] = floor_v;
+      }
+    }
+  }
+  nb = (unsigned long long)warp_sum_i((int)nb);
+  if ((threadIdx.x & 31) == 0 && nb) atomicAdd(bad, nb);
 }
 
 // Test hook for exp_fast (common.cuh): out[i] = exp_fast(x_i) (exp() where

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -147,6 +148,7 @@ struct otb_ctx {
   // problem
   const double *C = nullptr, *a = nullptr, *b = nullptr, *log_a = nullptr, *log_b = nullptr;
   double eta = 0.0, norm_c = 0.0, norm_a = 0.0, norm_b = 0.0;
+  bool norm_c_dev = false;   // ||C|| from ds->cnorm_sq (otb_set_cost_norm_sq)
   int64_t anchor = -1;
   bool bound = false;
   // buffers
@@ -700,7 +702,7 @@ int do_round(otb_ctx* c, const double* X, const double* gamma, double* Xout, int
     out->deficit = h.deficit;
     out->bregman = h.s8[0] - h.s8[1] + h.sumx;   // feasibility.py:85
     out->objective = h.s8[2];
-    const double cscale = 1.0 + c->norm_c;
+    const double cscale = 1.0 + (c->norm_c_dev ? std::sqrt(h.cnorm_sq) : c->norm_c);
     const double row_res = std::sqrt(h.s8[7]) / (1.0 + c->norm_a);
     const double col_res = std::sqrt(h.col_sq) / (1.0 + c->norm_b);
     const double neg = std::sqrt(h.s8[4]) / (1.0 + std::sqrt(h.s8[3]));
@@ -1065,6 +1067,7 @@ int otb_bind(otb_ctx* c, const double* C, const double* a, const double* b, cons
   c->eta = eta;
   c->anchor = anchor_global;
   c->norm_c = norm_c;
+  c->norm_c_dev = false;
   c->norm_a = norm_a;
   c->norm_b = norm_b;
   c->bound = true;
@@ -1257,6 +1260,14 @@ int otb_recover_round(otb_ctx* c, const double* logX, const double* gamma, doubl
   if (recover && (!logX_out || ((uintptr_t)logX_out) % 256 != 0))
     return fail(OTB_ERR_ARG, "logX_out must be a 256-byte aligned buffer");
   return do_round(c, logX, gamma, logX_out, recover, metrics, out);
+}
+
+int otb_set_cost_norm_sq(otb_ctx* c, const double* norm_sq) {
+  if (!c) return fail(OTB_ERR_ARG, "null context");
+  if (!norm_sq) return fail(OTB_ERR_ARG, "null norm");
+  CUDA_TRY(cudaMemcpyAsync(&c->ds->cnorm_sq, norm_sq, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  c->norm_c_dev = true;
+  return OTB_OK;
 }
 
 int otb_inner_iteration(otb_ctx* c, const double* logX, const double* gamma_in, double* gamma_out,
@@ -1516,6 +1527,33 @@ int otb_scale_cost(double* C, int64_t m_loc, int64_t n, int64_t ld, double peak,
     CUDA_TRY(cudaGetLastError());
   }
   CUDA_TRY(cudaStreamSynchronize(st));
+  return OTB_OK;
+}
+
+// Counters of otb_check_clamp_plan: a ring of slots so that calls from
+// several host threads / streams never share one (no allocation per call).
+__device__ unsigned long long g_plan_bad[256];
+static std::atomic<unsigned> g_plan_slot{0};
+
+int otb_check_clamp_plan(double* X, int64_t m_loc, int64_t n, int64_t ld, double floor_v, void* stream,
+                         int64_t* bad_out) {
+  if (!X || !bad_out || ld < n || m_loc < 0 || n < 1) return fail(OTB_ERR_ARG, "bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  *bad_out = 0;
+  if (m_loc == 0) return OTB_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  unsigned long long* slots = nullptr;
+  CUDA_TRY(cudaGetSymbolAddress((void**)&slots, g_plan_bad));
+  unsigned long long* dbad = slots + (g_plan_slot.fetch_add(1) & 255u);
+  CUDA_TRY(cudaMemsetAsync(dbad, 0, sizeof(unsigned long long), st));
+  k_check_clamp<<<sms * 8, 256, 0, st>>>(X, ld, (int)m_loc, (int)n, floor_v, dbad);
+  CUDA_TRY(cudaGetLastError());
+  unsigned long long hb = 0;
+  CUDA_TRY(cudaMemcpyAsync(&hb, dbad, sizeof(hb), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *bad_out = (int64_t)hb;
   return OTB_OK;
 }
 

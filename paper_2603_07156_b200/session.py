@@ -16,6 +16,7 @@ HBM layout: C and every log plan are stored as
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -38,6 +39,19 @@ def _torch():
 
 def round_up(x: int, k: int) -> int:
     return (x + k - 1) // k * k
+
+
+_SIDE: dict = {}
+
+
+def _side_stream(dev):
+    """One upload stream per device (created once, not per session)."""
+    st = _SIDE.get(dev.index)
+    if st is None:
+        import torch
+
+        st = _SIDE[dev.index] = torch.cuda.Stream(dev)
+    return st
 
 
 class Session:
@@ -78,6 +92,24 @@ class Session:
         if adopt:
             sq = torch.linalg.vector_norm(self.C).reshape(1) ** 2
             self.norm_c = float(torch.sqrt(sq))
+        elif _is_torch(cost) and not cost.is_cuda and os.environ.get("OTB_C_SIDE", "1") != "0":
+            # host C: uploaded on a side stream, so that the caller's next
+            # upload (the log plan) shares the PCIe link with it; ||C|| stays on
+            # the device (otb_set_cost_norm_sq).  The first library call on
+            # this session makes the library stream wait for it (_ready).
+            side = _side_stream(dev)
+            side.wait_stream(torch.cuda.current_stream(dev))
+            with torch.cuda.stream(side):
+                self.C[:, :n].copy_(cost[rows], non_blocking=True)
+                sq = torch.linalg.vector_norm(self.C).reshape(1) ** 2   # ||C||_F^2 of the local rows
+                if comm is not None and comm.world > 1:
+                    import torch.distributed as dist
+
+                    dist.all_reduce(sq)
+                self._c_ready = torch.cuda.Event()
+                self._c_ready.record(side)
+            self._norm_sq = sq
+            self.norm_c = None
         elif _is_torch(cost):
             self.C[:, :n].copy_(cost[rows], non_blocking=True)
             sq = torch.linalg.vector_norm(self.C).reshape(1) ** 2   # ||C||_F^2 of the local rows
@@ -145,12 +177,23 @@ class Session:
             return
         _lib.check(_lib.lib.otb_bind(self.ctx, self.C.data_ptr(), self.a.data_ptr(), self.b.data_ptr(),
                                      self.log_a.data_ptr(), self.log_b.data_ptr(), eta, anchor,
-                                     self.norm_c, self.norm_a, self.norm_b))
+                                     0.0 if self.norm_c is None else self.norm_c, self.norm_a, self.norm_b))
+        if self.norm_c is None and getattr(self, "_c_ready", None) is None:
+            _lib.check(_lib.lib.otb_set_cost_norm_sq(self.ctx, self._norm_sq.data_ptr()))
         self.eta = eta
         self.anchor = anchor
 
+    def _ready(self):
+        """Make the current stream wait for the side-stream upload of C."""
+        ev = getattr(self, "_c_ready", None)
+        if ev is not None:
+            self.torch.cuda.current_stream(self.device).wait_event(ev)
+            self._c_ready = None
+            _lib.check(_lib.lib.otb_set_cost_norm_sq(self.ctx, self._norm_sq.data_ptr()))
+
     @property
     def ops(self) -> "Ops":
+        self._ready()
         return Ops(self)
 
     def plan(self, logplan):

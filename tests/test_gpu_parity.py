@@ -611,3 +611,27 @@ def test_fast_exp_is_cuda_exp(cuda):
     with np.errstate(all="ignore"):
         fin = np.isfinite(ref) & (ref > 1e-300)
         assert np.max(np.abs(ref[fin] - np.exp(x[fin])) / np.spacing(np.exp(x[fin]))) <= 2.0
+
+
+def test_host_tensor_log_plan_check_and_clamp_on_device(cuda):
+    """A LogPlan given as a host torch tensor is checked and clamped on the
+    device in one pass (otb_check_clamp_plan, core.py:141-145): NaN or +inf
+    raise InvalidCost; entries below LOG_FLOOR (and -inf) become LOG_FLOOR."""
+    import torch
+
+    P = _api()
+    from paper_2603_07156_b200 import errors
+    from paper_2603_07156_b200.core import LOG_FLOOR
+
+    rng = np.random.default_rng(3)
+    for bad_val in (np.nan, np.inf):
+        x = rng.standard_normal((37, 45))
+        x[5, 7] = bad_val
+        with pytest.raises(errors.InvalidCost):
+            P.LogPlan(torch.from_numpy(x).pin_memory()).device_padded(64, torch.device("cuda", 0))
+    x = rng.standard_normal((37, 45))
+    x[0, 0], x[3, 44], x[36, 1] = -np.inf, -3e6, LOG_FLOOR
+    t = P.LogPlan(torch.from_numpy(x).pin_memory()).device_padded(64, torch.device("cuda", 0))
+    got = t[:, :45].cpu().numpy()
+    want = np.maximum(x, LOG_FLOOR)
+    assert np.array_equal(got, want)
