@@ -99,6 +99,7 @@ class Session:
             # this session makes the library stream wait for it (_ready).
             side = _side_stream(dev)
             side.wait_stream(torch.cuda.current_stream(dev))
+            self.C.record_stream(side)   # the allocator must not reuse C before the upload ends
             with torch.cuda.stream(side):
                 self.C[:, :n].copy_(cost[rows], non_blocking=True)
                 sq = torch.linalg.vector_norm(self.C).reshape(1) ** 2   # ||C||_F^2 of the local rows
@@ -187,8 +188,10 @@ class Session:
         """Make the current stream wait for the side-stream upload of C."""
         ev = getattr(self, "_c_ready", None)
         if ev is not None:
-            self.torch.cuda.current_stream(self.device).wait_event(ev)
+            cur = self.torch.cuda.current_stream(self.device)
+            cur.wait_event(ev)
             self._c_ready = None
+            self._norm_sq.record_stream(cur)   # read by the library's copy on this stream
             _lib.check(_lib.lib.otb_set_cost_norm_sq(self.ctx, self._norm_sq.data_ptr()))
 
     @property
