@@ -955,7 +955,10 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
     otb_destroy(c);
     return st;
   }
-  c->chunk = rup(std::max<int64_t>(8192, 2 * n), kCsrAlign);
+  // CSR chunk per bump allocation: large enough that a CTA refills (two
+  // named barriers) every ~16 rows, not every ~2 (the slack, at most one
+  // chunk per CTA, is part of the capacity)
+  c->chunk = rup(std::max<int64_t>(8192, 16 * n), kCsrAlign);
   // first Newton steps keep 50-70% of P: start at 3/4
   int64_t init_cap =
       std::max<int64_t>((int64_t)1 << 20, m_loc * (rup(n, kCsrAlign)) * 3 / 4) + (int64_t)c->ncl * c->chunk;
