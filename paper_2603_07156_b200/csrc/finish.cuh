@@ -129,6 +129,30 @@ __global__ void k_trial(int n, const double* gamma, const double* dir, double t,
     out[j] = gamma[j] + t * dir[j];
 }
 
+// Slope g.dir (as k_dot) fused with the first Armijo trial gamma + t dir
+// (as k_trial): one pass over the three vectors, one launch less.
+__global__ void __launch_bounds__(256) k_dot_trial(int n, const double* x, const double* y, DevScalars* ds,
+                                                   double* bpart, double* out, const double* gamma, double t,
+                                                   double* trial) {
+  __shared__ double red[2][kMaxWarps * 4];
+  double s = 0.0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const double yj = y[j];
+    s = fma(x[j], yj, s);
+    trial[j] = gamma[j] + t * yj;
+  }
+  int ph = 0;
+  double tt[1] = {s};
+  block_reduce<1, kSum>(tt, &red[0][0], ph, blockDim.x);
+  if (threadIdx.x == 0) bpart[blockIdx.x] = tt[0];
+  if (last_block(&ds->cnt[CNT_DOT])) {
+    if (threadIdx.x < 32) {
+      const double v = warp_fixed_sum(bpart, gridDim.x, 1);
+      if (threadIdx.x == 0) *out = v;
+    }
+  }
+}
+
 // out = -v
 __global__ void k_neg(int n, const double* v, double* out) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) out[j] = -v[j];

@@ -574,10 +574,11 @@ int cg_iteration(otb_ctx* c, int64_t k, double* x) {
 // next stream synchronisation).  k_cg_fused returns at once when k_cg_init
 // already decided (rhs = 0, inconsistent system) or the CSR overflowed.
 int cg_fused_launch(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t max_iters, double* x,
-                    int64_t* rec) {
+                    int64_t* rec, const double* neg_of = nullptr) {
   const int n = (int)c->n;
+  // with neg_of the right-hand side -neg_of is formed here into c->rhs (rhs must be c->rhs)
   k_cg_init<<<c->colgrid, 256, 0, c->stream>>>(n, rhs, x, c->cg_r, c->cg_p[0], c->cg, c->bpart, shift, rel_tol,
-                                               (long long)max_iters);
+                                               (long long)max_iters, neg_of, neg_of ? c->rhs : nullptr);
   LAUNCH_CHECK();
   CgFusedArgs fa{csr_view(c), c->a,     c->d,  n,     c->fused_ng, c->eta, x,          rhs, c->cg_ap,
                  c->colpart,  c->scal, c->cg, c->bm, c->nq,       c->cg_trace, &c->ds->flags};
@@ -1204,12 +1205,11 @@ int otb_newton_step(otb_ctx* c, const double* logX, const double* gamma_in, doub
     for (int attempt = 0; attempt < 8 && !done; ++attempt) {
       int64_t sp_rec = -1, cg_rec = -1;
       TRY(sparsify_launch(c, logX, gamma_in, rho, &sp_rec));
-      k_neg<<<c->colgrid, 256, 0, c->stream>>>(n, c->g, c->rhs);   // inner_newton.py:117: (H + ||g|| I) d = -g
-      LAUNCH_CHECK();
-      TRY(cg_fused_launch(c, g0, c->rhs, p->cg_rel_tol, maxit, c->dir, &cg_rec));
-      k_dot<<<c->colgrid, 256, 0, c->stream>>>(n, c->g, c->dir, c->ds, c->bpart, &c->ds->slope);   // :118
-      LAUNCH_CHECK();
-      k_trial<<<c->colgrid, 256, 0, c->stream>>>(n, gamma_in, c->dir, 1.0, c->gtrial);
+      // inner_newton.py:117: (H + ||g|| I) d = -g  (k_cg_init forms rhs = -g)
+      TRY(cg_fused_launch(c, g0, c->rhs, p->cg_rel_tol, maxit, c->dir, &cg_rec, c->g));
+      // :118 slope = g . dir, with the t = 1 trial gamma_in + dir in the same pass
+      k_dot_trial<<<c->colgrid, 256, 0, c->stream>>>(n, c->g, c->dir, c->ds, c->bpart, &c->ds->slope, gamma_in, 1.0,
+                                                     c->gtrial);
       LAUNCH_CHECK();
       TRY(eval_launch(c, logX, c->gtrial));
       TRY(sync_scalars(c));

@@ -1026,13 +1026,17 @@ __global__ void __launch_bounds__(256) k_cg_update(int n, double* x, double* r, 
 }
 
 // krylov.py:51-67 set-up: x = 0, r = p = rhs, rs = r.r, stop target.
+// neg_of != nullptr: the right-hand side is -neg_of, written to rhs_out
+// (inner_newton.py:117's -g without a separate pass).
 __global__ void __launch_bounds__(256) k_cg_init(int n, const double* rhs, double* x, double* r, double* p0,
                                                  CgState* st, double* bpart, double shift, double rel_tol,
-                                                 long long max_iters) {
+                                                 long long max_iters, const double* neg_of = nullptr,
+                                                 double* rhs_out = nullptr) {
   __shared__ double red[2][kMaxWarps * 4];
   double sq = 0.0, sm = 0.0;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const double v = rhs[j];
+    const double v = (neg_of != nullptr) ? -neg_of[j] : rhs[j];
+    if (rhs_out != nullptr) rhs_out[j] = v;
     x[j] = 0.0;
     r[j] = v;
     p0[j] = v;
