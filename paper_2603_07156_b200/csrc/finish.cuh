@@ -34,19 +34,37 @@ enum CounterIdx {
 
 // out[j] = sum_c part[c*n + j]; out[n + k] = sum_c spart[c*sstride + k].
 // One block = 32 columns; the 8 warps split the partial rows (fixed order).
+// Single rank (nothing to all-reduce in between), the elementwise finish of
+// k_vec_post can be applied here (post = POST_COPY / POST_Y / POST_EC into
+// post_out) and scalar k also stored at sdst[k] — one launch instead of two
+// plus the scalar copies.  post < 0: plain column sums into out.
+struct ColPost {
+  int post;                // < 0: none
+  const double* b;
+  double* out;
+  double* sdst[2];         // optional destinations of scalars 0, 1
+};
 __global__ void __launch_bounds__(256) k_colreduce(const double* part, int nparts, int n, double* out,
                                                    const double* spart, int nspart, int sstride, int nscal,
-                                                   unsigned int* counter) {
+                                                   unsigned int* counter, ColPost cp) {
   __shared__ double red[8 * 32];
   const double s = reduce_partials32(part, nparts, n, blockIdx.x * 32, red);
   const int j = blockIdx.x * 32 + threadIdx.x;
-  if (threadIdx.x < 32 && j < n) out[j] = s;
+  if (threadIdx.x < 32 && j < n) {
+    if (cp.post < 0) out[j] = s;
+    else if (cp.post == 0) cp.out[j] = s;                                            // POST_COPY
+    else if (cp.post == 1) cp.out[j] = (s > 0.0) ? fmin(div_rn(cp.b[j], s), 1.0) : 1.0;   // POST_Y
+    else cp.out[j] = cp.b[j] - s;                                                     // POST_EC
+  }
   if (nscal > 0) {
     if (last_block(counter)) {
       if (threadIdx.x < 32) {
         for (int k = 0; k < nscal; ++k) {
           const double v = warp_fixed_sum(spart + k, nspart, sstride);
-          if (threadIdx.x == 0) out[n + k] = v;
+          if (threadIdx.x == 0) {
+            out[n + k] = v;
+            if (k < 2 && cp.sdst[k] != nullptr) *cp.sdst[k] = v;
+          }
         }
       }
     }

@@ -324,9 +324,10 @@ int sync_scalars(otb_ctx* c) {
   return OTB_OK;
 }
 
-int colreduce(otb_ctx* c, int nparts, const double* spart, int nspart, int sstride, int nscal) {
+int colreduce(otb_ctx* c, int nparts, const double* spart, int nspart, int sstride, int nscal,
+              ColPost cp = ColPost{-1, nullptr, nullptr, {nullptr, nullptr}}) {
   k_colreduce<<<c->col32, 256, 0, c->stream>>>(c->colpart, nparts, (int)c->n, c->sendbuf, spart, nspart, sstride,
-                                                 nscal, &c->ds->cnt[CNT_COLRED]);
+                                                 nscal, &c->ds->cnt[CNT_COLRED], cp);
   LAUNCH_CHECK();
   return OTB_OK;
 }
@@ -430,6 +431,10 @@ int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho
     LAUNCH_CHECK();
   }
   c->rowpre_valid = !bitmap;
+  if (c->nranks == 1) {   // d = column sums, written by the reduction itself
+    TRY(colreduce(c, c->ncl, nullptr, 0, 0, 0, ColPost{POST_COPY, c->b, c->d, {nullptr, nullptr}}));
+    return OTB_OK;
+  }
   TRY(colreduce(c, c->ncl, nullptr, 0, 0, 0));
   TRY(allreduce(c, c->sendbuf, (size_t)n, kNcclSum));
   k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_COPY, n, c->sendbuf, c->b, c->d, c->ds, c->bpart, nullptr);
@@ -649,13 +654,18 @@ int do_round(otb_ctx* c, const double* X, const double* gamma, double* Xout, int
     TRY(prof_begin(c, &e0));
     TRY(launch_dense(c, DK_TESTA, geo, &io));
     TRY(prof_end(c, PC_TESTA, e0, recover ? 24.0 * mn : 16.0 * mn));
-    TRY(colreduce(c, c->ncl, c->vpart, c->grid, 2, 2));
-    TRY(allreduce(c, c->sendbuf, (size_t)n + 2, kNcclSum));
-    k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_Y, n, c->sendbuf, c->b, c->yv, c->ds, c->bpart, nullptr);
-    LAUNCH_CHECK();
-    CUDA_TRY(cudaMemcpyAsync(&c->ds->sumx, c->sendbuf + n, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-    CUDA_TRY(cudaMemcpyAsync(&c->ds->scratch[1], c->sendbuf + n + 1, sizeof(double), cudaMemcpyDeviceToDevice,
-                             c->stream));
+    if (c->nranks == 1) {   // y and the two scalars straight from the reduction
+      TRY(colreduce(c, c->ncl, c->vpart, c->grid, 2, 2,
+                    ColPost{POST_Y, c->b, c->yv, {&c->ds->sumx, &c->ds->scratch[1]}}));
+    } else {
+      TRY(colreduce(c, c->ncl, c->vpart, c->grid, 2, 2));
+      TRY(allreduce(c, c->sendbuf, (size_t)n + 2, kNcclSum));
+      k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_Y, n, c->sendbuf, c->b, c->yv, c->ds, c->bpart, nullptr);
+      LAUNCH_CHECK();
+      CUDA_TRY(cudaMemcpyAsync(&c->ds->sumx, c->sendbuf + n, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+      CUDA_TRY(cudaMemcpyAsync(&c->ds->scratch[1], c->sendbuf + n + 1, sizeof(double), cudaMemcpyDeviceToDevice,
+                               c->stream));
+    }
   }
   const double* src = recover ? Xout : X;
   // pass B: F = (X z) y, e_r, e_c, deficit
@@ -669,11 +679,16 @@ int do_round(otb_ctx* c, const double* X, const double* gamma, double* Xout, int
     k_rows_post<<<c->colgrid, 256, 0, c->stream>>>(0, (int)c->m_loc, c->cl, c->rowpart, c->a, c->row0, c->er, c->ds,
                                                    c->bpart, &c->ds->scratch[2]);
     LAUNCH_CHECK();
-    TRY(colreduce(c, c->ncl, &c->ds->scratch[2], 1, 1, 1));
-    TRY(allreduce(c, c->sendbuf, (size_t)n + 1, kNcclSum));
-    k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_EC, n, c->sendbuf, c->b, c->ec, c->ds, c->bpart, nullptr);
-    LAUNCH_CHECK();
-    CUDA_TRY(cudaMemcpyAsync(&c->ds->deficit, c->sendbuf + n, sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    if (c->nranks == 1) {   // e_c and the deficit straight from the reduction
+      TRY(colreduce(c, c->ncl, &c->ds->scratch[2], 1, 1, 1, ColPost{POST_EC, c->b, c->ec, {&c->ds->deficit, nullptr}}));
+    } else {
+      TRY(colreduce(c, c->ncl, &c->ds->scratch[2], 1, 1, 1));
+      TRY(allreduce(c, c->sendbuf, (size_t)n + 1, kNcclSum));
+      k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_EC, n, c->sendbuf, c->b, c->ec, c->ds, c->bpart, nullptr);
+      LAUNCH_CHECK();
+      CUDA_TRY(cudaMemcpyAsync(&c->ds->deficit, c->sendbuf + n, sizeof(double), cudaMemcpyDeviceToDevice,
+                               c->stream));
+    }
   }
   // pass C: rank-one correction, Bregman divergence, objective, KKT sums
   {
