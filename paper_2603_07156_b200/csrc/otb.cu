@@ -1288,12 +1288,14 @@ int otb_set_cost_norm_sq(otb_ctx* c, const double* norm_sq) {
   return OTB_OK;
 }
 
-int otb_inner_iteration(otb_ctx* c, const double* logX, const double* gamma_in, double* gamma_out,
+int otb_inner_iteration(otb_ctx* c, const double* logX, double* gamma_in, double* gamma_out,
                         const otb_newton_params* p, int eval_first, double floor, double test_below,
-                        double* logX_out, otb_inner_out* out) {
+                        double* logX_out, const double* gamma_src, otb_inner_out* out) {
   TRY(require_bound(c));
   if (!out) return fail(OTB_ERR_ARG, "out is null");
   if (((uintptr_t)logX) % 256 != 0) return fail(OTB_ERR_ARG, "logX must be 256-byte aligned");
+  if (gamma_src && gamma_src != gamma_in)   // the caller's dual, copied into the working buffer
+    CUDA_TRY(cudaMemcpyAsync(gamma_in, gamma_src, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, c->stream));
   if (eval_first) TRY(do_eval(c, logX, gamma_in));                 // inner_newton.py:196
   out->value0 = c->last_value;
   out->grad_norm0 = c->last_gnorm;

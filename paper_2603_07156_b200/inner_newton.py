@@ -115,13 +115,18 @@ def inner_solve(logplan: LogPlan, gamma0: DualState, problem: OtProblem, config:
     scale = float(min(m, n)) if config.inner_scale is InnerScale.MIN_DIM else 1.0
     floor = GRAD_HARD_FLOOR if grad_target is None else max(grad_target, GRAD_HARD_FLOOR)
     plan_t = s.plan(logplan)
+    native = observer is None and not recenter_every and config.max_inner >= 1
+    g_src = None   # a device dual copied into g_cur by the first native call
     if gamma_bufs is None:
         g_cur, g_nxt = s._vec(gamma0.gamma), s.new_vec()
     else:
         g_cur, g_nxt = gamma_bufs
         if not (_is_device(gamma0.gamma) and gamma0.gamma.data_ptr() == g_cur.data_ptr()):
             src = gamma0.gamma
-            if _is_device(src):
+            if _is_device(src) and native and src.dtype == s.torch.float64 and src.is_contiguous() \
+                    and src.device == g_cur.device and src.numel() >= n:
+                g_src = src
+            elif _is_device(src):
                 g_cur[:n].copy_(src.reshape(-1)[:n])
             else:
                 g_cur[:n].copy_(s._vec(src)[:n])
@@ -134,7 +139,6 @@ def inner_solve(logplan: LogPlan, gamma0: DualState, problem: OtProblem, config:
     stop = StopReason.MAX_INNER
     tested = None
     tests: list[tuple] = []
-    native = observer is None and not recenter_every and config.max_inner >= 1
     if native:
         # the loop body in native code (otb_inner_iteration): the initial
         # evaluate, the floor stop, the step and the inexact test with no
@@ -143,7 +147,8 @@ def inner_solve(logplan: LogPlan, gamma0: DualState, problem: OtProblem, config:
         values: list[float] = []
         for v in range(1, config.max_inner + 1):
             r = s.ops.inner_iteration(plan_t, g_cur, g_nxt, config.armijo_sigma, config.armijo_beta,
-                                      config.cg_rel_tol, config.cg_max_iters, v == 1, floor, test_below, cand_t)
+                                      config.cg_rel_tol, config.cg_max_iters, v == 1, floor, test_below, cand_t,
+                                      g_src if v == 1 else None)
             if v == 1:
                 value, grad_norm = float(r.value0), float(r.grad_norm0)
                 values.append(value)

@@ -331,7 +331,7 @@ class Ops:
         return out
 
     def inner_iteration(self, plan_t, gamma_in, gamma_out, sigma, beta, cg_rel_tol, cg_max_iters, eval_first,
-                        floor, test_below, out_plan):
+                        floor, test_below, out_plan, gamma_src=None):
         """One iteration of inner_solve's loop in native code (otb_inner_iteration):
         [eval], floor stop, Newton step, and the inexact test when the new
         ||g|| < test_below (test_below < 0: never)."""
@@ -340,7 +340,8 @@ class Ops:
         out = _lib.InnerOut()
         _lib.check(_lib.lib.otb_inner_iteration(self.s.ctx, plan_t.data_ptr(), gamma_in.data_ptr(),
                                                 gamma_out.data_ptr(), C.byref(p), 1 if eval_first else 0,
-                                                float(floor), float(test_below), _ptr(out_plan), C.byref(out)))
+                                                float(floor), float(test_below), _ptr(out_plan), _ptr(gamma_src),
+                                                C.byref(out)))
         return out
 
     def recover_round(self, plan_t, gamma_t, out_plan=None, recover=True, metrics=True):
