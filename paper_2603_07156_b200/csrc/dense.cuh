@@ -151,6 +151,8 @@ struct SparsifyIO {
   int* flags;             // bit 1: capacity overflow
   uint4* bm;              // bitmap index [m_loc][nq] (sparse.cuh), or nullptr
   int nq;
+  const double* gnorm;    // non-null: rho = (eta ||g||) / mn from this device scalar (no host round trip)
+  double mn;
 };
 // With the bitmap index, a row's run holds column PAIRS (2l, 2l+1) with at
 // least one kept entry, 16 bytes each (the unkept one stored as 0.0), and
@@ -173,7 +175,8 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
   }
   __shared__ int tab[kTabInts];
   __shared__ unsigned long long chunk_base;
-  const double eta = io.eta, rho = io.rho;
+  const double eta = io.eta;
+  const double rho = io.gnorm != nullptr ? (eta * *io.gnorm) / io.mn : io.rho;   // inner_newton.py:112-114
   const Divider DIV(eta);
   const double log_rho = log(rho);
   const int nw = D.g.nt >> 5;

@@ -19,6 +19,7 @@ struct DevScalars {
   double warm_err;
   double drift;
   double cnorm_sq;                     // ||C||_F^2 when the caller gave it as a device scalar
+  double ev0[3];                       // value, ||g||, non-finite count of an eval not yet read by the host
   double scratch[4];
   unsigned long long alloc;            // CSR bump allocator
   unsigned long long nnzc;             // kept entries of the last sparsify

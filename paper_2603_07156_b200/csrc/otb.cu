@@ -403,7 +403,8 @@ int row_prefix(otb_ctx* c) {
 // bounds / row prefix where hess_apply needs them, Hessian diagonal.  The
 // kept count and the capacity flag land in c->ds; *rec is the profiling
 // record whose byte count needs nnz (or -1).
-int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho, int64_t* rec) {
+int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho, int64_t* rec,
+                    const double* gnorm_dev = nullptr) {
   const int n = (int)c->n;
   const int64_t anchor_local = (c->anchor >= c->row0 && c->anchor < c->row1) ? c->anchor - c->row0 : -1;
   // alloc, nnzc, flags are adjacent in DevScalars
@@ -414,7 +415,7 @@ int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho
   SparsifyIO io{gamma, c->a, c->eta, rho, anchor_local, c->rowM, c->rowS, c->lse, bitmap ? nullptr : c->cols,
                 c->vals, c->cap,
                 c->row_start, c->row_len, &c->ds->alloc, &c->ds->nnzc, c->chunk, c->colpart, &c->ds->flags,
-                bitmap ? c->bm : nullptr, c->nq};
+                bitmap ? c->bm : nullptr, c->nq, gnorm_dev, (double)c->m_glob * (double)c->n};
   cudaEvent_t e0 = nullptr;
   TRY(prof_begin(c, &e0));
   TRY(launch_dense(c, kind, geo, &io));
@@ -579,11 +580,11 @@ int cg_iteration(otb_ctx* c, int64_t k, double* x) {
 // next stream synchronisation).  k_cg_fused returns at once when k_cg_init
 // already decided (rhs = 0, inconsistent system) or the CSR overflowed.
 int cg_fused_launch(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t max_iters, double* x,
-                    int64_t* rec, const double* neg_of = nullptr) {
+                    int64_t* rec, const double* neg_of = nullptr, const double* shift_dev = nullptr) {
   const int n = (int)c->n;
   // with neg_of the right-hand side -neg_of is formed here into c->rhs (rhs must be c->rhs)
   k_cg_init<<<c->colgrid, 256, 0, c->stream>>>(n, rhs, x, c->cg_r, c->cg_p[0], c->cg, c->bpart, shift, rel_tol,
-                                               (long long)max_iters, neg_of, neg_of ? c->rhs : nullptr);
+                                               (long long)max_iters, neg_of, neg_of ? c->rhs : nullptr, shift_dev);
   LAUNCH_CHECK();
   CgFusedArgs fa{csr_view(c), c->a,     c->d,  n,     c->fused_ng, c->eta, x,          rhs, c->cg_ap,
                  c->colpart,  c->scal, c->cg, c->bm, c->nq,       c->cg_trace, &c->ds->flags};
@@ -1197,51 +1198,95 @@ int armijo(otb_ctx* c, const double* logX, const double* gamma_in, double v0, do
   return fail(OTB_ERR_LINESEARCH, "no Armijo step accepted after 200 trials");
 }
 
+// The Newton step with the persistent CG (cg_fused): sparsify, CG, slope and
+// the t = 1 trial are launched back to back and read with one host
+// synchronisation; then Armijo.  With `spec`, the eval at gamma_in was only
+// launched (its scalars saved in ds->ev0): rho and the CG shift are read on
+// the device, and the host learns L(gamma_in) and ||g|| at the same
+// synchronisation.  If that ||g|| is <= floor the step is discarded (the
+// eval at gamma_in is redone so that its row state is the cached one) and
+// *stepped = false.
+int newton_fused(otb_ctx* c, const double* logX, const double* gamma_in, const otb_newton_params* p, bool spec,
+                 double floor, double* v0, double* g0, double* rho, otb_cg_out* cgo, double* slope, double* t,
+                 int64_t* trials, bool* stepped) {
+  const int n = (int)c->n;
+  const int64_t maxit = (p->cg_max_iters > 0) ? p->cg_max_iters : 2 * c->n;
+  *stepped = false;
+  for (int attempt = 0; attempt < 8; ++attempt) {
+    int64_t sp_rec = -1, cg_rec = -1;
+    const double* gdev = spec ? &c->ds->ev0[1] : nullptr;
+    TRY(sparsify_launch(c, logX, gamma_in, spec ? 0.0 : *rho, &sp_rec, gdev));
+    // inner_newton.py:117: (H + ||g|| I) d = -g  (k_cg_init forms rhs = -g)
+    TRY(cg_fused_launch(c, spec ? 0.0 : *g0, c->rhs, p->cg_rel_tol, maxit, c->dir, &cg_rec, c->g, gdev));
+    // :118 slope = g . dir, with the t = 1 trial gamma_in + dir in the same pass
+    k_dot_trial<<<c->colgrid, 256, 0, c->stream>>>(n, c->g, c->dir, c->ds, c->bpart, &c->ds->slope, gamma_in, 1.0,
+                                                   c->gtrial);
+    LAUNCH_CHECK();
+    TRY(eval_launch(c, logX, c->gtrial));
+    TRY(sync_scalars(c));
+    if (spec) {   // the eval at gamma_in, now on the host
+      spec = false;
+      if (c->hs->ev0[2] != 0.0) {
+        c->have_eval = false;
+        return fail(OTB_ERR_NONFINITE, "row softmax produced non-finite values after stabilization");
+      }
+      *v0 = c->hs->ev0[0];
+      *g0 = c->hs->ev0[1];
+      *rho = c->eta * *g0 / ((double)c->m_glob * (double)c->n);   // inner_newton.py:112-114 (same bits)
+      if (*g0 <= floor) {                                          // :205 — nothing to step
+        TRY(do_eval(c, logX, gamma_in));
+        return OTB_OK;
+      }
+    }
+    bool redo = false;
+    TRY(sparsify_finish(c, sp_rec, &redo));
+    if (redo) {
+      TRY(do_eval(c, logX, gamma_in));   // the trial replaced the row state sparsify reads
+      continue;
+    }
+    c->have_eval = false;   // the row state is the trial's until eval_finish accepts it
+    TRY(cg_finish(c, cg_rec, cgo));
+    *slope = c->hs->slope;
+    TRY(eval_finish(c));
+    TRY(armijo(c, logX, gamma_in, *v0, *slope, p, true, t, trials));
+    *stepped = true;
+    return OTB_OK;
+  }
+  return fail(OTB_ERR_NOMEM, "CSR capacity could not be grown");
+}
+
+void fill_newton_out(const otb_ctx* c, double t, double slope, double rho, double v0, double g0,
+                     const otb_cg_out& cgo, int64_t trials, otb_newton_out* out) {
+  if (!out) return;
+  out->t = t;
+  out->slope = slope;
+  out->rho = rho;
+  out->value_before = v0;
+  out->value_after = c->last_value;
+  out->grad_norm_before = g0;
+  out->grad_norm_after = c->last_gnorm;
+  out->cg_iters = cgo.iters;
+  out->nnz = c->nnz;
+  out->trials = trials;
+  out->cg_residual = cgo.residual;
+}
+
 int otb_newton_step(otb_ctx* c, const double* logX, const double* gamma_in, double* gamma_out,
                     const otb_newton_params* p, otb_newton_out* out) {
   TRY(require_bound(c));
   if (!p) return fail(OTB_ERR_ARG, "null params");
   if (!c->have_eval) return fail(OTB_ERR_ARG, "otb_newton_step needs a preceding otb_eval at gamma_in");
   const int n = (int)c->n;
-  const double v0 = c->last_value, g0 = c->last_gnorm;
+  double v0 = c->last_value, g0 = c->last_gnorm;
   // inner_newton.py:112-114
-  const double rho = (p->rho_override >= 0.0) ? p->rho_override : c->eta * g0 / ((double)c->m_glob * (double)c->n);
+  double rho = (p->rho_override >= 0.0) ? p->rho_override : c->eta * g0 / ((double)c->m_glob * (double)c->n);
   const int64_t maxit = (p->cg_max_iters > 0) ? p->cg_max_iters : 2 * c->n;
   otb_cg_out cgo;
   double slope = 0.0, t = 1.0;
   int64_t trials = 0;
   if (c->cg_fused) {
-    // One host synchronisation for sparsify + CG + slope + the t = 1 trial:
-    // everything is launched back to back and the host reads the kept
-    // count, the capacity flag, the CG state, the slope and the trial's
-    // value together.  A CSR overflow (first call on a problem) grows the
-    // capacity, re-evaluates at gamma_in and repeats.
-    bool done = false;
-    for (int attempt = 0; attempt < 8 && !done; ++attempt) {
-      int64_t sp_rec = -1, cg_rec = -1;
-      TRY(sparsify_launch(c, logX, gamma_in, rho, &sp_rec));
-      // inner_newton.py:117: (H + ||g|| I) d = -g  (k_cg_init forms rhs = -g)
-      TRY(cg_fused_launch(c, g0, c->rhs, p->cg_rel_tol, maxit, c->dir, &cg_rec, c->g));
-      // :118 slope = g . dir, with the t = 1 trial gamma_in + dir in the same pass
-      k_dot_trial<<<c->colgrid, 256, 0, c->stream>>>(n, c->g, c->dir, c->ds, c->bpart, &c->ds->slope, gamma_in, 1.0,
-                                                     c->gtrial);
-      LAUNCH_CHECK();
-      TRY(eval_launch(c, logX, c->gtrial));
-      TRY(sync_scalars(c));
-      bool redo = false;
-      TRY(sparsify_finish(c, sp_rec, &redo));
-      if (redo) {
-        TRY(do_eval(c, logX, gamma_in));   // the trial replaced the row state sparsify reads
-        continue;
-      }
-      c->have_eval = false;   // the row state is the trial's until eval_finish accepts it
-      TRY(cg_finish(c, cg_rec, &cgo));
-      slope = c->hs->slope;
-      TRY(eval_finish(c));
-      done = true;
-    }
-    if (!done) return fail(OTB_ERR_NOMEM, "CSR capacity could not be grown");
-    TRY(armijo(c, logX, gamma_in, v0, slope, p, true, &t, &trials));
+    bool stepped = false;
+    TRY(newton_fused(c, logX, gamma_in, p, false, -1.0, &v0, &g0, &rho, &cgo, &slope, &t, &trials, &stepped));
   } else {
     TRY(do_sparsify(c, logX, gamma_in, rho));
     k_neg<<<c->colgrid, 256, 0, c->stream>>>(n, c->g, c->rhs);
@@ -1255,19 +1300,7 @@ int otb_newton_step(otb_ctx* c, const double* logX, const double* gamma_in, doub
   }
   // stream-ordered: the caller's later work on this stream sees gamma_out
   CUDA_TRY(cudaMemcpyAsync(gamma_out, c->gtrial, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
-  if (out) {
-    out->t = t;
-    out->slope = slope;
-    out->rho = rho;
-    out->value_before = v0;
-    out->value_after = c->last_value;
-    out->grad_norm_before = g0;
-    out->grad_norm_after = c->last_gnorm;
-    out->cg_iters = cgo.iters;
-    out->nnz = c->nnz;
-    out->trials = trials;
-    out->cg_residual = cgo.residual;
-  }
+  fill_newton_out(c, t, slope, rho, v0, g0, cgo, trials, out);
   return OTB_OK;
 }
 
@@ -1296,14 +1329,36 @@ int otb_inner_iteration(otb_ctx* c, const double* logX, double* gamma_in, double
   if (((uintptr_t)logX) % 256 != 0) return fail(OTB_ERR_ARG, "logX must be 256-byte aligned");
   if (gamma_src && gamma_src != gamma_in)   // the caller's dual, copied into the working buffer
     CUDA_TRY(cudaMemcpyAsync(gamma_in, gamma_src, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, c->stream));
-  if (eval_first) TRY(do_eval(c, logX, gamma_in));                 // inner_newton.py:196
-  out->value0 = c->last_value;
-  out->grad_norm0 = c->last_gnorm;
   out->stepped = 0;
   out->tested = 0;
-  if (c->last_gnorm <= floor) return OTB_OK;                       // :205 gradient floor
-  TRY(otb_newton_step(c, logX, gamma_in, gamma_out, p, &out->newton));
-  out->stepped = 1;
+  if (eval_first && c->cg_fused && p && p->rho_override < 0.0) {
+    // inner_newton.py:196 + the first step without a synchronisation in
+    // between: the eval is launched and its scalars kept on the device
+    TRY(eval_launch(c, logX, gamma_in));
+    c->p_valid = c->Pbuf != nullptr;   // the stored P is in stream order before sparsify reads it
+    CUDA_TRY(cudaMemcpyAsync(&c->ds->ev0[0], &c->ds->value, 2 * sizeof(double), cudaMemcpyDeviceToDevice,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(&c->ds->ev0[2], &c->ds->scratch[0], sizeof(double), cudaMemcpyDeviceToDevice,
+                             c->stream));
+    double v0 = 0.0, g0 = 0.0, rho = 0.0, slope = 0.0, t = 1.0;
+    int64_t trials = 0;
+    otb_cg_out cgo{};
+    bool stepped = false;
+    TRY(newton_fused(c, logX, gamma_in, p, true, floor, &v0, &g0, &rho, &cgo, &slope, &t, &trials, &stepped));
+    out->value0 = v0;
+    out->grad_norm0 = g0;
+    if (!stepped) return OTB_OK;                                   // :205 gradient floor
+    CUDA_TRY(cudaMemcpyAsync(gamma_out, c->gtrial, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, c->stream));
+    fill_newton_out(c, t, slope, rho, v0, g0, cgo, trials, &out->newton);
+    out->stepped = 1;
+  } else {
+    if (eval_first) TRY(do_eval(c, logX, gamma_in));               // inner_newton.py:196
+    out->value0 = c->last_value;
+    out->grad_norm0 = c->last_gnorm;
+    if (c->last_gnorm <= floor) return OTB_OK;                     // :205 gradient floor
+    TRY(otb_newton_step(c, logX, gamma_in, gamma_out, p, &out->newton));
+    out->stepped = 1;
+  }
   if (test_below >= 0.0 && out->newton.grad_norm_after < test_below) {   // :239 pre-check, then the test
     if (!logX_out || ((uintptr_t)logX_out) % 256 != 0)
       return fail(OTB_ERR_ARG, "logX_out must be a 256-byte aligned buffer");

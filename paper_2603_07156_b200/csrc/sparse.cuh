@@ -1031,7 +1031,7 @@ __global__ void __launch_bounds__(256) k_cg_update(int n, double* x, double* r, 
 __global__ void __launch_bounds__(256) k_cg_init(int n, const double* rhs, double* x, double* r, double* p0,
                                                  CgState* st, double* bpart, double shift, double rel_tol,
                                                  long long max_iters, const double* neg_of = nullptr,
-                                                 double* rhs_out = nullptr) {
+                                                 double* rhs_out = nullptr, const double* shift_dev = nullptr) {
   __shared__ double red[2][kMaxWarps * 4];
   double sq = 0.0, sm = 0.0;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
@@ -1056,15 +1056,16 @@ __global__ void __launch_bounds__(256) k_cg_init(int n, const double* rhs, doubl
       const double sum = warp_fixed_sum(bpart + 1, gridDim.x, 2);
       if (threadIdx.x == 0) {
         const double bnorm = sqrt(rs);
+        const double sh = shift_dev != nullptr ? *shift_dev : shift;   // ||g|| of an eval the host has not read
         st->rs = rs;
         st->bnorm = bnorm;
-        st->shift = shift;
+        st->shift = sh;
         st->target = rel_tol * bnorm;
         st->iters = 0;
         st->max_iters = max_iters;
         st->beta = 0.0;
         st->res = bnorm;
-        if (shift == 0.0 && fabs(sum) > 1e-12 * fmax(1.0, bnorm)) st->status = CG_INCONSISTENT;
+        if (sh == 0.0 && fabs(sum) > 1e-12 * fmax(1.0, bnorm)) st->status = CG_INCONSISTENT;
         else if (bnorm == 0.0) {
           st->status = CG_DONE;
           st->res = 0.0;
