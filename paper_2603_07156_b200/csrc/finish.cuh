@@ -107,6 +107,66 @@ __global__ void __launch_bounds__(256) k_eval_post(int n, const double* buf, con
   }
 }
 
+// Single rank: k_colreduce and k_eval_post in one kernel (one launch less per
+// eval) with k_eval_post's summation tree reproduced exactly, so the bits of
+// ||g|| and L are those of the two-kernel path: level 1 = xor tree over the
+// 32 columns of a block (a k_eval_post warp), level 2 = xor tree over 8
+// consecutive blocks (a k_eval_post block of 256 columns), level 3 =
+// warp_fixed_sum over those groups (k_eval_post's grid, colgrid groups).
+// Valid while colgrid * 256 >= n (one column per k_eval_post thread).
+__global__ void __launch_bounds__(256) k_colreduce_eval(const double* part, int nparts, int n, const double* spart,
+                                                        int nspart, const double* b, const double* gamma, double eta,
+                                                        double* g, DevScalars* ds, double* bpart, int colgrid) {
+  __shared__ double red[8 * 32];
+  __shared__ double l2[2][512];
+  const double s = reduce_partials32(part, nparts, n, blockIdx.x * 32, red);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < 32) {
+    const int j = blockIdx.x * 32 + lane;
+    double sq = 0.0, bg = 0.0;
+    if (j < n) {
+      const double gj = s - b[j];
+      g[j] = gj;
+      sq = fma(gj, gj, sq);
+      bg += (-b[j]) * gamma[j];
+    }
+    sq = warp_sum(sq);
+    bg = warp_sum(bg);
+    if (lane == 0) {
+      bpart[2 * blockIdx.x] = sq;
+      bpart[2 * blockIdx.x + 1] = bg;
+    }
+  }
+  if (last_block(&ds->cnt[CNT_EVALPOST])) {
+    const int nb = gridDim.x;
+    for (int B = warp; B < colgrid; B += 8) {   // level 2: groups of 8 blocks, xor tree as in block_reduce
+      const int k = 8 * B + lane;
+      double x0 = (lane < 8 && k < nb) ? bpart[2 * k] : 0.0;
+      double x1 = (lane < 8 && k < nb) ? bpart[2 * k + 1] : 0.0;
+      x0 = warp_sum(x0);
+      x1 = warp_sum(x1);
+      if (lane == 0) {
+        l2[0][B] = x0;
+        l2[1][B] = x1;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const double sqs = warp_fixed_sum(&l2[0][0], colgrid, 1);
+      const double bgs = warp_fixed_sum(&l2[1][0], colgrid, 1);
+      const double alse = warp_fixed_sum(spart, nspart, 2);       // as k_colreduce's scalars (stride 2)
+      const double nbad = warp_fixed_sum(spart + 1, nspart, 2);
+      if (threadIdx.x == 0) {
+        ds->scratch[0] = nbad;   // count of non-finite rows
+        ds->gnorm = sqrt(sqs);
+        ds->alse = alse;
+        ds->bgam = bgs;
+        ds->value = bgs + eta * alse;
+      }
+    }
+  }
+}
+
 // Dot product x.y into *out (fixed-order), e.g. slope = g.dir.
 __global__ void __launch_bounds__(256) k_dot(int n, const double* x, const double* y, DevScalars* ds,
                                              double* bpart, double* out) {

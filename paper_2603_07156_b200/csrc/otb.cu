@@ -349,6 +349,12 @@ int eval_launch(otb_ctx* c, const double* X, const double* gamma) {
   TRY(prof_begin(c, &e0));
   TRY(launch_dense(c, DK_EVAL, geo, &io));
   TRY(prof_end(c, PC_EVAL, e0, 16.0 * c->m_loc * n + 8.0 * c->m_loc + 24.0 * n));
+  if (c->nranks == 1 && (int64_t)c->colgrid * 256 >= n && c->colgrid <= 512) {
+    k_colreduce_eval<<<c->col32, 256, 0, c->stream>>>(c->colpart, c->ncl, n, c->vpart, c->ncl, c->b, gamma, c->eta,
+                                                      c->g, c->ds, c->bpart, c->colgrid);
+    LAUNCH_CHECK();
+    return OTB_OK;
+  }
   TRY(colreduce(c, c->ncl, c->vpart, c->ncl, 2, 2));
   TRY(allreduce(c, c->sendbuf, (size_t)n + 2, kNcclSum));
   k_eval_post<<<c->colgrid, 256, 0, c->stream>>>(n, c->sendbuf, c->b, gamma, c->eta, c->g, c->ds, c->bpart);
