@@ -167,6 +167,109 @@ __global__ void __launch_bounds__(256) k_colreduce_eval(const double* part, int 
   }
 }
 
+// Single rank: the finish of test pass B (mode 0) or C (mode 1) in one
+// kernel — blocks [0, col32) reduce the column partials (k_colreduce),
+// blocks [col32, col32 + colgrid) do k_rows_post's work with its own thread
+// mapping, and the last block combines — reproducing the summation trees of
+// k_rows_post, k_colreduce and k_vec_post(POST_COLRES) exactly (same bits).
+//   mode 0: er_i = a_i - rowsum_i; deficit = sum |er|; ec_j = b_j - colsum_j
+//   mode 1: s8[0..6] = CTA scalar totals, s8[7] = sum (rowsum_i - a_i)^2,
+//           col_sq = sum_j (colsum_j - b_j)^2
+struct TestFinishIO {
+  int mode;
+  const double* colpart;   // [nparts][n]
+  int nparts;
+  int n;
+  const double* b;
+  double* ec;              // mode 0
+  const double* rowpart;   // [m_loc][cl]
+  int m_loc, cl;
+  const double* a;
+  int64_t row0;
+  double* er;              // mode 0
+  const double* spart;     // mode 1: [nspart][8] CTA scalars
+  int nspart;
+  int col32, colgrid;
+  DevScalars* ds;
+  double* bpart;           // col32 + colgrid doubles
+};
+__global__ void __launch_bounds__(256) k_test_finish(TestFinishIO io) {
+  __shared__ double red[8 * 32];
+  __shared__ double red2[2][kMaxWarps * 4];
+  __shared__ double l2[512];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* bcol = io.bpart;
+  double* brow = io.bpart + io.col32;
+  if ((int)blockIdx.x < io.col32) {
+    const double s = reduce_partials32(io.colpart, io.nparts, io.n, blockIdx.x * 32, red);
+    if (threadIdx.x < 32) {
+      const int j = blockIdx.x * 32 + lane;
+      if (io.mode == 0) {
+        if (j < io.n) io.ec[j] = io.b[j] - s;   // feasibility.py:65
+      } else {
+        double sq = 0.0;
+        if (j < io.n) {
+          const double e = s - io.b[j];
+          sq = fma(e, e, sq);
+        }
+        sq = warp_sum(sq);
+        if (lane == 0) bcol[blockIdx.x] = sq;
+      }
+    }
+  } else {
+    const int rb = blockIdx.x - io.col32;
+    double s = 0.0;
+    for (int i = rb * blockDim.x + threadIdx.x; i < io.m_loc; i += io.colgrid * blockDim.x) {
+      double rs = 0.0;
+      for (int q = 0; q < io.cl; ++q) rs += io.rowpart[(size_t)i * io.cl + q];
+      const double ai = io.a[io.row0 + i];
+      if (io.mode == 0) {
+        const double e = ai - rs;
+        io.er[i] = e;
+        s += fabs(e);
+      } else {
+        const double e = rs - ai;
+        s = fma(e, e, s);
+      }
+    }
+    int ph = 0;
+    double t[1] = {s};
+    block_reduce<1, kSum>(t, &red2[0][0], ph, blockDim.x);
+    if (threadIdx.x == 0) brow[rb] = t[0];
+  }
+  if (last_block(&io.ds->cnt[CNT_ROWS])) {
+    if (io.mode == 1) {
+      for (int B = warp; B < io.colgrid; B += 8) {   // the column residual's level 2 (k_vec_post blocks)
+        const int k = 8 * B + lane;
+        double x = (lane < 8 && k < io.col32) ? bcol[k] : 0.0;
+        x = warp_sum(x);
+        if (lane == 0) l2[B] = x;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const double rows = warp_fixed_sum(brow, io.colgrid, 1);
+      if (io.mode == 0) {
+        if (threadIdx.x == 0) {
+          io.ds->scratch[2] = rows;
+          io.ds->deficit = rows;   // feasibility.py:66
+        }
+      } else {
+        const double colsq = warp_fixed_sum(l2, io.colgrid, 1);
+        double v[7];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) v[k] = warp_fixed_sum(io.spart + k, io.nspart, 8);
+        if (threadIdx.x == 0) {
+#pragma unroll
+          for (int k = 0; k < 7; ++k) io.ds->s8[k] = v[k];
+          io.ds->s8[7] = rows;
+          io.ds->col_sq = colsq;
+        }
+      }
+    }
+  }
+}
+
 // Dot product x.y into *out (fixed-order), e.g. slope = g.dir.
 __global__ void __launch_bounds__(256) k_dot(int n, const double* x, const double* y, DevScalars* ds,
                                              double* bpart, double* out) {

@@ -683,12 +683,16 @@ int do_round(otb_ctx* c, const double* X, const double* gamma, double* Xout, int
     TRY(prof_begin(c, &e0));
     TRY(launch_dense(c, DK_TESTB, geo, &io));
     TRY(prof_end(c, PC_TESTB, e0, 8.0 * mn));
-    k_rows_post<<<c->colgrid, 256, 0, c->stream>>>(0, (int)c->m_loc, c->cl, c->rowpart, c->a, c->row0, c->er, c->ds,
-                                                   c->bpart, &c->ds->scratch[2]);
-    LAUNCH_CHECK();
-    if (c->nranks == 1) {   // e_c and the deficit straight from the reduction
-      TRY(colreduce(c, c->ncl, &c->ds->scratch[2], 1, 1, 1, ColPost{POST_EC, c->b, c->ec, {&c->ds->deficit, nullptr}}));
+    if (c->nranks == 1 && c->colgrid <= 512) {   // rows, e_c and the deficit in one kernel
+      TestFinishIO fi{0,       c->colpart, c->ncl,          (int)n,     c->b,      c->ec,     c->rowpart,
+                      (int)c->m_loc, c->cl, c->a,           c->row0,    c->er,     nullptr,   0,
+                      c->col32, c->colgrid, c->ds,          c->bpart};
+      k_test_finish<<<c->col32 + c->colgrid, 256, 0, c->stream>>>(fi);
+      LAUNCH_CHECK();
     } else {
+      k_rows_post<<<c->colgrid, 256, 0, c->stream>>>(0, (int)c->m_loc, c->cl, c->rowpart, c->a, c->row0, c->er,
+                                                     c->ds, c->bpart, &c->ds->scratch[2]);
+      LAUNCH_CHECK();
       TRY(colreduce(c, c->ncl, &c->ds->scratch[2], 1, 1, 1));
       TRY(allreduce(c, c->sendbuf, (size_t)n + 1, kNcclSum));
       k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_EC, n, c->sendbuf, c->b, c->ec, c->ds, c->bpart, nullptr);
@@ -706,15 +710,23 @@ int do_round(otb_ctx* c, const double* X, const double* gamma, double* Xout, int
     TRY(prof_begin(c, &e0));
     TRY(launch_dense(c, kind, geo, &io));
     TRY(prof_end(c, PC_TESTC, e0, metrics ? 16.0 * mn : 8.0 * mn));
-    k_rows_post<<<c->colgrid, 256, 0, c->stream>>>(1, (int)c->m_loc, c->cl, c->rowpart, c->a, c->row0, nullptr,
-                                                   c->ds, c->bpart, c->vpart + 7);
-    LAUNCH_CHECK();
-    TRY(colreduce(c, c->ncl, c->vpart, c->grid, 8, 8));
-    TRY(allreduce(c, c->sendbuf, (size_t)n + 8, kNcclSum));
-    k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_COLRES, n, c->sendbuf, c->b, nullptr, c->ds, c->bpart,
-                                                  &c->ds->col_sq);
-    LAUNCH_CHECK();
-    CUDA_TRY(cudaMemcpyAsync(c->ds->s8, c->sendbuf + n, 8 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    if (c->nranks == 1 && c->colgrid <= 512) {   // rows, columns and the 8 scalars in one kernel
+      TestFinishIO fi{1,       c->colpart, c->ncl,          (int)n,     c->b,      nullptr,   c->rowpart,
+                      (int)c->m_loc, c->cl, c->a,           c->row0,    nullptr,   c->vpart,  c->grid,
+                      c->col32, c->colgrid, c->ds,          c->bpart};
+      k_test_finish<<<c->col32 + c->colgrid, 256, 0, c->stream>>>(fi);
+      LAUNCH_CHECK();
+    } else {
+      k_rows_post<<<c->colgrid, 256, 0, c->stream>>>(1, (int)c->m_loc, c->cl, c->rowpart, c->a, c->row0, nullptr,
+                                                     c->ds, c->bpart, c->vpart + 7);
+      LAUNCH_CHECK();
+      TRY(colreduce(c, c->ncl, c->vpart, c->grid, 8, 8));
+      TRY(allreduce(c, c->sendbuf, (size_t)n + 8, kNcclSum));
+      k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_COLRES, n, c->sendbuf, c->b, nullptr, c->ds, c->bpart,
+                                                    &c->ds->col_sq);
+      LAUNCH_CHECK();
+      CUDA_TRY(cudaMemcpyAsync(c->ds->s8, c->sendbuf + n, 8 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    }
   }
   TRY(sync_scalars(c));
   c->round_src = src;
