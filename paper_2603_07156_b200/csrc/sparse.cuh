@@ -731,8 +731,12 @@ OTB_DEV void hv_bitmap_partial(const Csr& A, const uint4* bm, const double* a, c
 // Staged variant of hv_bitmap_partial: the producer warp streams, the 512
 // consumer threads compute; `rg` persists across calls (ring position).
 template <int V>
-OTB_DEV void hv_staged_partial(const Csr& A, const uint4* bm, const double* a, const double* vsm, int n, int nq, int rb,
-                               int re, double* slots, StRing& rg, double* dst) {
+// upd (persistent CG): vsm holds the previous direction and the CG update
+// p = r + beta p (krylov.py:83) is done here, by the thread that owns the
+// column, instead of in a separate pass over all n.
+OTB_DEV void hv_staged_partial(const Csr& A, const uint4* bm, const double* a, double* vsm, int n, int nq, int rb,
+                               int re, double* slots, StRing& rg, double* dst, const double* rsm = nullptr,
+                               double beta = 0.0, bool upd = false) {
   constexpr int NQ = HvVar<V>::NQ, CW = HvVar<V>::CW;
   if (threadIdx.x >= CW * 32) {
     st_produce(A, bm, a, rb, re, nq, 0, CW * NQ, true, rg);
@@ -742,7 +746,15 @@ OTB_DEV void hv_staged_partial(const Csr& A, const uint4* bm, const double* a, c
 #pragma unroll
   for (int i = 0; i < 2 * NQ; ++i) {
     const int j = bm_col<CW>(i >> 1, i & 1);
-    vr[i] = (j < n) ? vsm[j] : 0.0;
+    double v = 0.0;
+    if (j < n) {
+      v = vsm[j];
+      if (upd) {
+        v = rsm[j] + beta * v;   // krylov.py:83
+        vsm[j] = v;
+      }
+    }
+    vr[i] = v;
     ar[i] = 0.0;
   }
   st_consume<NQ, false, CW>(rb, re, vr, ar, slots, rg, nullptr);
@@ -1162,7 +1174,7 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_cg_fused(CgFusedArgs 
     // ---- phase 1: the hess_apply partial row of this CTA
     double* dst = c.colpart + (size_t)b * n;
     if constexpr (HvVar<V>::kStaged) {
-      hv_staged_partial<V>(c.A, c.bm, c.a, psm, n, c.nq, rb, re, gslots, rg, dst);
+      hv_staged_partial<V>(c.A, c.bm, c.a, psm, n, c.nq, rb, re, gslots, rg, dst, rsm, beta, it > 0);
     } else if constexpr (HvVar<V>::kBitmap) {
       hv_bitmap_partial<V>(c.A, c.bm, c.a, psm, n, rb, re, gslots,
                           reinterpret_cast<unsigned char*>(gslots + 16 * 64), dst);
@@ -1259,10 +1271,12 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_cg_fused(CgFusedArgs 
       status = CG_MAXIT;
       break;
     }
-    for (int j = tid; j < n; j += nth) psm[j] = rsm[j] + beta * psm[j];   // krylov.py:83
+    if constexpr (!HvVar<V>::kStaged) {   // staged variants update p in the next hess_apply (owned columns)
+      for (int j = tid; j < n; j += nth) psm[j] = rsm[j] + beta * psm[j];   // krylov.py:83
+    }
     if (c.trace != nullptr && tid == 0 && it - 1 < kCgTraceIters)          // (it already counts this one)
       c.trace[((size_t)b * kCgTraceIters + (size_t)(it - 1)) * 6 + 5] = globaltimer();
-    __syncthreads();
+    if constexpr (!HvVar<V>::kStaged) __syncthreads();
   }
   if (b == 0 && tid == 0) {
     CgState* s = c.st;
