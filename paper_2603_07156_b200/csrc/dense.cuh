@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
   const int nw = D.g.nt >> 5;
   const unsigned lt = (1u << D.lane) - 1u;
   const bool pairs = io.bm != nullptr;
+  const int bq0 = (D.c0 >> 6) + D.warp, bqs = D.slice >> 6;   // word of slice 0, words per slice (64-col words)
   unsigned long long cur = 0, end = 0;
   unsigned long long kept = 0;
   int rowpar = 0;
@@ -358,6 +359,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
     if (ovf && D.tid == 0 && D.cr == 0) atomicOr(io.flags, 2);
     const double ai = __ldg(io.a + D.g.row0 + r);
     const unsigned long long wbase = start + (pairs ? 2 * myoff : myoff);
+    uint4* bmr = pairs ? io.bm + (size_t)r * io.nq : nullptr;   // the row's bitmap words
     const Divider DK(ksum);
     if (!ovf) {
       if (fallback) {
@@ -398,10 +400,8 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
             const unsigned b0 = bb0[s], b1 = bb1[s];
             const int base = pre[s] & 0xffff;
             const int j = D.col(s, 0);
-            if (io.bm != nullptr && D.lane == 0) {
-              const int cs = D.c0 + s * D.slice + 64 * D.warp;
-              if (cs < D.c1) io.bm[(size_t)r * io.nq + cs / 64] = make_uint4(b0, b1, (unsigned)(myoff + base), 0u);
-            }
+            if (bmr != nullptr && D.lane == 0 && D.c0 + s * D.slice + 64 * D.warp < D.c1)   // this warp's word
+              bmr[bq0 + s * bqs] = make_uint4(b0, b1, (unsigned)(myoff + base), 0u);
             double2* a2 = D.acc2(0, s);
             if (pairs) {
               if (k0 | k1) {
