@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_eval(Geom geo, 
     const double S = D.row_sum(se);
     const double ai = __ldg(io.a + D.g.row0 + r);
     const double w = ai / S;
+    double* Prow = io.P != nullptr ? io.P + (size_t)r * D.g.ld + D.col(0, 0) : nullptr;   // this thread's slice-0 pair
     const Divider DS(S);
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_eval(Geom geo, 
         *a2 = v;
         if (io.P != nullptr) {                    // semidual.py:82-83: shifted / row_sum
           const int j = D.col(s, 0);
-          double* dst = io.P + (size_t)r * D.g.ld + j;
+          double* dst = Prow + s * D.slice;
           double p0, p1;
           DS.pair(z[2 * s], z[2 * s + 1], p0, p1);
           if (j + 1 < D.c1) {
@@ -485,6 +486,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_a(Geom geo
     const int64_t gi = D.g.row0 + r;
     const double la = io.recover ? __ldg(io.log_a + gi) : 0.0;
     const double l = io.recover ? io.lse[r] : 0.0;
+    double* Xrow = io.Xout + (size_t)r * D.g.ld + D.col(0, 0);   // this thread's slice-0 pair of the row
     double xv[2 * NS];
     double rs = 0.0;
     double shmin = INFINITY;
@@ -501,7 +503,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_a(Geom geo
           if (j < D.c1) shmin = fmin(shmin, c.x - gm.x);
           if (j + 1 < D.c1) shmin = fmin(shmin, c.y - gm.y);
         }
-        double* dst = io.Xout + (size_t)r * D.g.ld + j;
+        double* dst = Xrow + s * D.slice;
         double l0 = x.x, l1 = x.y;   // the slice's log entries (candidate, or the plan as given)
         if (io.recover) {
           double q0, q1;
