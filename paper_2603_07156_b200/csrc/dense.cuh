@@ -84,7 +84,6 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_eval(Geom geo, 
     const double S = D.row_sum(se);
     const double ai = __ldg(io.a + D.g.row0 + r);
     const double w = ai / S;
-    double* Prow = io.P != nullptr ? io.P + (size_t)r * D.g.ld + D.col(0, 0) : nullptr;   // this thread's slice-0 pair
     const Divider DS(S);
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
@@ -96,7 +95,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_eval(Geom geo, 
         *a2 = v;
         if (io.P != nullptr) {                    // semidual.py:82-83: shifted / row_sum
           const int j = D.col(s, 0);
-          double* dst = Prow + s * D.slice;
+          double* dst = io.P + (size_t)r * D.g.ld + j;
           double p0, p1;
           DS.pair(z[2 * s], z[2 * s + 1], p0, p1);
           if (j + 1 < D.c1) {
