@@ -335,26 +335,29 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
     // Contiguous row run: cluster rank 0 bump-allocates from its current
     // chunk (state replicated in all of its consumer threads) and shares
     // the start with the other ranks of the cluster.
-    unsigned long long start = 0;
+    // The (cur, end) chunk state is the same in every rank of the cluster
+    // (cnt is the cluster-wide count), so only a refill needs rank 0's new
+    // chunk base sent to the others — about one row in ten at cfg5 instead
+    // of every row.
     const int sto = pairs ? 2 * cnt : cnt;   // stored doubles of the row
     const int cnt_al = (sto + 7) & ~7;      // runs start on 8-entry boundaries (vector loads in hess_apply)
-    if (D.cr == 0) {
-      if (cur + (unsigned long long)cnt_al > end) {
-        const unsigned long long want = (unsigned long long)max((int64_t)cnt_al, io.chunk);
+    if (cur + (unsigned long long)cnt_al > end) {
+      const unsigned long long want = (unsigned long long)max((int64_t)cnt_al, io.chunk);
+      if (D.cr == 0) {
         if (D.tid == 0) chunk_base = atomicAdd(io.alloc, want);
         bar_sync(1, D.g.nt);
         cur = chunk_base;
-        end = cur + want;
         bar_sync(1, D.g.nt);   // chunk_base may be rewritten next time
       }
-      start = cur;
-      cur += (unsigned long long)cnt_al;
+      if (D.g.cl > 1) {
+        double v1[1] = {(double)cur};
+        const double* all = D.template exchange<1>(v1);
+        cur = (unsigned long long)all[0];   // rank 0's base
+      }
+      end = cur + want;
     }
-    if (D.g.cl > 1) {
-      double v1[1] = {(double)start};
-      const double* all = D.template exchange<1>(v1);
-      start = (unsigned long long)all[0];
-    }
+    const unsigned long long start = cur;
+    cur += (unsigned long long)cnt_al;
     const bool ovf = (int64_t)(start + cnt_al) > io.cap;
     if (ovf && D.tid == 0 && D.cr == 0) atomicOr(io.flags, 2);
     const double ai = __ldg(io.a + D.g.row0 + r);
