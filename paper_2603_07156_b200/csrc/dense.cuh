@@ -14,6 +14,9 @@ constexpr int kMaxThreads = OTB_DENSE_MAXT;   // 512 consumers + 1 producer warp
 #define OTB_DENSE_MINB 1           // CTAs per SM the register allocation is sized for
 #endif
 constexpr int kTabInts = 2 * kMaxNS * 32;
+#ifndef OTB_ZETA_A_NS
+#define OTB_ZETA_A_NS 6   // rows of more than this many slices take the KKT c-transform from pass A
+#endif
 
 // ---------------------------------------------------------------- eval (K1)
 // semidual.py:51-100: logits = logX + (gamma - C)/eta, row max, shifted
@@ -482,7 +485,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_a(Geom geo
   double sumx = 0.0;
   int bad = 0;
   // wide rows (NS > 6) also reduce the c-transform for pass C (see k_test_c)
-  constexpr bool kCtr = NS > 6;
+  constexpr bool kCtr = NS > OTB_ZETA_A_NS;
   const bool ctr = kCtr && io.czeta != nullptr;
   for (int r = D.r0; r < D.r1; ++r) {
     const int64_t gi = D.g.row0 + r;
@@ -692,7 +695,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_c(Geom geo
   // C - gamma).  Up to 6 slices the row's f and C - gamma stay in registers
   // and zeta is reduced here; wider rows take zeta from pass A (k_test_a,
   // czeta) so that they do not spill.  Same values, same summation order.
-  constexpr bool kZetaFromA = NS > 6;
+  constexpr bool kZetaFromA = NS > OTB_ZETA_A_NS;
   constexpr int KR = (METRICS && !kZetaFromA) ? 2 * NS : 1;
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
   for (int r = D.r0; r < D.r1; ++r) {

@@ -656,7 +656,7 @@ int do_round(otb_ctx* c, const double* X, const double* gamma, double* Xout, int
   {
     Geom geo = make_geom(c, DK_TESTA, c->C, X);
     TestAIO io{gamma,  c->a,     c->log_a, c->lse, c->eta, Xout, c->zrow, c->colpart, c->vpart, recover,
-               (metrics && c->ns > 6) ? c->czeta : nullptr};   // k_test_c: wide rows take zeta from pass A
+               (metrics && c->ns > OTB_ZETA_A_NS) ? c->czeta : nullptr};   // k_test_c: wide rows take zeta from pass A
     cudaEvent_t e0 = nullptr;
     TRY(prof_begin(c, &e0));
     TRY(launch_dense(c, DK_TESTA, geo, &io));
