@@ -217,10 +217,11 @@ def test_baseline_config_end_to_end(cuda, idx):
 
 # ------------------------------------------------- oracle-checked seeded cases
 @pytest.mark.parametrize("m,n,eta", [(1, 5, 1e-2), (7, 1, 1e-2), (37, 29, 5e-2), (257, 131, 1e-2),
-                                     (64, 9000, 1e-2), (40, 16400, 1e-2), (9, 50001, 1e-2)])
+                                     (64, 9000, 1e-2), (40, 16400, 1e-2), (9, 50001, 1e-2), (24, 60000, 1e-2)])
 def test_step_pipeline_vs_oracle(cuda, m, n, eta):
-    """Ragged / odd / cluster-split (n > 8192) / atomic-scatter (n > 14398)
-    geometries: eval, one Newton step and the inexact test vs the oracle."""
+    """Ragged / odd / cluster-split (n > 10240; 60000 columns = clusters of 8)
+    / window-cluster geometries: eval, one Newton step and the inexact test
+    vs the oracle."""
     P = _api()
     from paper_2603_07156_b200 import instances
 
