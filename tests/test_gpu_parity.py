@@ -636,3 +636,43 @@ def test_host_tensor_log_plan_check_and_clamp_on_device(cuda):
     got = t[:, :45].cpu().numpy()
     want = np.maximum(x, LOG_FLOOR)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("mu_k,grad_target,max_inner", [(1e-3, None, 6), (1e-9, None, 3), (0.0, 1e-9, 8),
+                                                         (0.0, 1.0, 4)])
+def test_native_inner_iteration_equals_python_loop(cuda, mu_k, grad_target, max_inner):
+    """inner_solve's loop body runs natively (otb_inner_iteration: the first
+    step launched without waiting for the first eval, decisions in C) unless
+    an observer is given; both paths must give the same bits: dual,
+    candidate, Newton/CG counts, stop reason, objective — including the
+    inexact-test stop, max_inner, and the gradient-floor stop before any
+    step (grad_target = 1: the speculative step is discarded)."""
+    import torch
+
+    P = _api()
+    from paper_2603_07156_b200 import instances
+    from paper_2603_07156_b200.inner_newton import inner_solve
+    from paper_2603_07156_b200.sinkhorn import warm_start
+
+    C, a, b = instances.small_uniform(300, 257, 5)
+    eta = 1e-2
+    outs = []
+    for observe in (False, True):
+        prob = P.OtProblem(torch.from_numpy(C).cuda(), a, b)
+        cfg = P.SolverConfig(eta=eta, kkt_tol=1e-9, max_inner=max_inner)
+        X = P.LogPlan(O.product_log_plan(a, b))
+        gam, _ = warm_start(X, prob, eta, 1e-3, gamma0=np.zeros(257))
+        seen = []
+        gs, cand, rep = inner_solve(X, gam, prob, cfg, mu_k=mu_k, outer_k=0, grad_target=grad_target,
+                                    observer=(seen.append if observe else None))
+        g = gs.gamma.cpu().numpy() if hasattr(gs.gamma, "cpu") else np.asarray(gs.gamma)
+        outs.append((g.copy(), np.asarray(cand.log_entries).copy(), rep))
+    (g0, c0, r0), (g1, c1, r1) = outs
+    assert r0.newton_iters == r1.newton_iters and r0.cg_iters_total == r1.cg_iters_total
+    assert r0.stop_reason == r1.stop_reason
+    assert np.array_equal(g0.view(np.uint64), g1.view(np.uint64))
+    assert np.array_equal(c0.view(np.uint64), c1.view(np.uint64))
+    assert r0.objective == r1.objective and r0.kkt == r1.kkt and r0.bregman == r1.bregman
+    assert r0.values == r1.values and r0.step_sizes == r1.step_sizes
+    if grad_target == 1.0:
+        assert r0.newton_iters == 0
