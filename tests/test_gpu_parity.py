@@ -676,3 +676,24 @@ def test_native_inner_iteration_equals_python_loop(cuda, mu_k, grad_target, max_
     assert r0.values == r1.values and r0.step_sizes == r1.step_sizes
     if grad_target == 1.0:
         assert r0.newton_iters == 0
+
+
+@pytest.mark.parametrize("m,n", [(64, 16400), (24, 60000)])
+def test_cluster_paths_are_deterministic(cuda, m, n):
+    """Rows split over thread-block clusters (DSMEM exchanges, replicated
+    CSR chunk state) and window-cluster hess_apply: two runs of a Newton
+    step + inexact test give identical bits."""
+    P = _api()
+    from paper_2603_07156_b200 import instances
+    from paper_2603_07156_b200.inner_newton import inner_solve
+
+    C, a, b = instances.small_uniform(m, n, 2)
+    res = []
+    for _ in range(2):
+        prob = P.OtProblem(C, a, b)
+        cfg = P.SolverConfig(eta=1e-2, kkt_tol=1e-9, max_inner=2)
+        gs, cand, rep = inner_solve(P.LogPlan(O.product_log_plan(a, b)), P.DualState(np.zeros(n)), prob, cfg,
+                                    mu_k=1e-3, outer_k=0)
+        res.append((np.asarray(gs.gamma).copy(), rep.cg_iters_total, rep.objective, rep.bregman))
+    assert np.array_equal(res[0][0].view(np.uint64), res[1][0].view(np.uint64))
+    assert res[0][1:] == res[1][1:]
