@@ -116,7 +116,8 @@ __global__ void __launch_bounds__(256) k_eval_post(int n, const double* buf, con
 // Valid while colgrid * 256 >= n (one column per k_eval_post thread).
 __global__ void __launch_bounds__(256) k_colreduce_eval(const double* part, int nparts, int n, const double* spart,
                                                         int nspart, const double* b, const double* gamma, double eta,
-                                                        double* g, DevScalars* ds, double* bpart, int colgrid) {
+                                                        double* g, DevScalars* ds, double* bpart, int colgrid,
+                                                        bool save_ev0 = false) {
   __shared__ double red[8 * 32];
   __shared__ double l2[2][512];
   const double s = reduce_partials32(part, nparts, n, blockIdx.x * 32, red);
@@ -162,6 +163,11 @@ __global__ void __launch_bounds__(256) k_colreduce_eval(const double* part, int 
         ds->alse = alse;
         ds->bgam = bgs;
         ds->value = bgs + eta * alse;
+        if (save_ev0) {          // kept for a host read after later evals (otb_inner_iteration)
+          ds->ev0[0] = ds->value;
+          ds->ev0[1] = ds->gnorm;
+          ds->ev0[2] = nbad;
+        }
       }
     }
   }

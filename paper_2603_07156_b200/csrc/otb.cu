@@ -340,7 +340,7 @@ int require_bound(const otb_ctx* c) {
 
 // ------------------------------------------------------------- eval
 // Launch part of an eval (no host synchronisation).
-int eval_launch(otb_ctx* c, const double* X, const double* gamma) {
+int eval_launch(otb_ctx* c, const double* X, const double* gamma, bool save_ev0 = false) {
   const int n = (int)c->n;
   Geom geo = make_geom(c, DK_EVAL, c->C, X);
   EvalIO io{gamma, c->a, c->eta, c->rowM, c->rowS, c->lse, c->colpart, c->vpart, c->Pbuf};
@@ -351,7 +351,7 @@ int eval_launch(otb_ctx* c, const double* X, const double* gamma) {
   TRY(prof_end(c, PC_EVAL, e0, 16.0 * c->m_loc * n + 8.0 * c->m_loc + 24.0 * n));
   if (c->nranks == 1 && (int64_t)c->colgrid * 256 >= n && c->colgrid <= 512) {
     k_colreduce_eval<<<c->col32, 256, 0, c->stream>>>(c->colpart, c->ncl, n, c->vpart, c->ncl, c->b, gamma, c->eta,
-                                                      c->g, c->ds, c->bpart, c->colgrid);
+                                                      c->g, c->ds, c->bpart, c->colgrid, save_ev0);
     LAUNCH_CHECK();
     return OTB_OK;
   }
@@ -359,6 +359,12 @@ int eval_launch(otb_ctx* c, const double* X, const double* gamma) {
   TRY(allreduce(c, c->sendbuf, (size_t)n + 2, kNcclSum));
   k_eval_post<<<c->colgrid, 256, 0, c->stream>>>(n, c->sendbuf, c->b, gamma, c->eta, c->g, c->ds, c->bpart);
   LAUNCH_CHECK();
+  if (save_ev0) {
+    CUDA_TRY(cudaMemcpyAsync(&c->ds->ev0[0], &c->ds->value, 2 * sizeof(double), cudaMemcpyDeviceToDevice,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(&c->ds->ev0[2], &c->ds->scratch[0], sizeof(double), cudaMemcpyDeviceToDevice,
+                             c->stream));
+  }
   return OTB_OK;
 }
 
@@ -1194,15 +1200,15 @@ int otb_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t 
 // Armijo backtracking from t0 (whose trial eval is in c->hs when
 // `evaluated`), inner_newton.py:74-94.
 int armijo(otb_ctx* c, const double* logX, const double* gamma_in, double v0, double slope,
-           const otb_newton_params* p, bool evaluated, double* t_out, int64_t* trials_out) {
+           const otb_newton_params* p, bool evaluated, double* t_out, int64_t* trials_out, double* trial) {
   const int n = (int)c->n;
   double t = 1.0;
   int64_t trials = 0;
   for (int k = 0; k < 200; ++k) {
     if (!(evaluated && k == 0)) {
-      k_trial<<<c->colgrid, 256, 0, c->stream>>>(n, gamma_in, c->dir, t, c->gtrial);
+      k_trial<<<c->colgrid, 256, 0, c->stream>>>(n, gamma_in, c->dir, t, trial);
       LAUNCH_CHECK();
-      TRY(do_eval(c, logX, c->gtrial));
+      TRY(do_eval(c, logX, trial));
     }
     ++trials;
     if (c->last_value <= v0 + p->sigma * t * slope) {
@@ -1226,7 +1232,7 @@ int armijo(otb_ctx* c, const double* logX, const double* gamma_in, double v0, do
 // *stepped = false.
 int newton_fused(otb_ctx* c, const double* logX, const double* gamma_in, const otb_newton_params* p, bool spec,
                  double floor, double* v0, double* g0, double* rho, otb_cg_out* cgo, double* slope, double* t,
-                 int64_t* trials, bool* stepped) {
+                 int64_t* trials, bool* stepped, double* trial) {
   const int n = (int)c->n;
   const int64_t maxit = (p->cg_max_iters > 0) ? p->cg_max_iters : 2 * c->n;
   *stepped = false;
@@ -1238,9 +1244,9 @@ int newton_fused(otb_ctx* c, const double* logX, const double* gamma_in, const o
     TRY(cg_fused_launch(c, spec ? 0.0 : *g0, c->rhs, p->cg_rel_tol, maxit, c->dir, &cg_rec, c->g, gdev));
     // :118 slope = g . dir, with the t = 1 trial gamma_in + dir in the same pass
     k_dot_trial<<<c->colgrid, 256, 0, c->stream>>>(n, c->g, c->dir, c->ds, c->bpart, &c->ds->slope, gamma_in, 1.0,
-                                                   c->gtrial);
+                                                   trial);
     LAUNCH_CHECK();
-    TRY(eval_launch(c, logX, c->gtrial));
+    TRY(eval_launch(c, logX, trial));
     TRY(sync_scalars(c));
     if (spec) {   // the eval at gamma_in, now on the host
       spec = false;
@@ -1266,7 +1272,7 @@ int newton_fused(otb_ctx* c, const double* logX, const double* gamma_in, const o
     TRY(cg_finish(c, cg_rec, cgo));
     *slope = c->hs->slope;
     TRY(eval_finish(c));
-    TRY(armijo(c, logX, gamma_in, *v0, *slope, p, true, t, trials));
+    TRY(armijo(c, logX, gamma_in, *v0, *slope, p, true, t, trials, trial));
     *stepped = true;
     return OTB_OK;
   }
@@ -1302,9 +1308,12 @@ int otb_newton_step(otb_ctx* c, const double* logX, const double* gamma_in, doub
   otb_cg_out cgo;
   double slope = 0.0, t = 1.0;
   int64_t trials = 0;
+  // trials go straight into gamma_out unless it aliases gamma_in (backtracking re-reads gamma_in)
+  double* trial = (gamma_out != gamma_in) ? gamma_out : c->gtrial;
   if (c->cg_fused) {
     bool stepped = false;
-    TRY(newton_fused(c, logX, gamma_in, p, false, -1.0, &v0, &g0, &rho, &cgo, &slope, &t, &trials, &stepped));
+    TRY(newton_fused(c, logX, gamma_in, p, false, -1.0, &v0, &g0, &rho, &cgo, &slope, &t, &trials, &stepped,
+                     trial));
   } else {
     TRY(do_sparsify(c, logX, gamma_in, rho));
     k_neg<<<c->colgrid, 256, 0, c->stream>>>(n, c->g, c->rhs);
@@ -1314,10 +1323,11 @@ int otb_newton_step(otb_ctx* c, const double* logX, const double* gamma_in, doub
     LAUNCH_CHECK();
     TRY(sync_scalars(c));
     slope = c->hs->slope;
-    TRY(armijo(c, logX, gamma_in, v0, slope, p, false, &t, &trials));
+    TRY(armijo(c, logX, gamma_in, v0, slope, p, false, &t, &trials, trial));
   }
   // stream-ordered: the caller's later work on this stream sees gamma_out
-  CUDA_TRY(cudaMemcpyAsync(gamma_out, c->gtrial, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  if (trial != gamma_out)
+    CUDA_TRY(cudaMemcpyAsync(gamma_out, trial, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
   fill_newton_out(c, t, slope, rho, v0, g0, cgo, trials, out);
   return OTB_OK;
 }
@@ -1352,21 +1362,20 @@ int otb_inner_iteration(otb_ctx* c, const double* logX, double* gamma_in, double
   if (eval_first && c->cg_fused && p && p->rho_override < 0.0) {
     // inner_newton.py:196 + the first step without a synchronisation in
     // between: the eval is launched and its scalars kept on the device
-    TRY(eval_launch(c, logX, gamma_in));
+    TRY(eval_launch(c, logX, gamma_in, true));   // its L, ||g||, flag also kept in ds->ev0
     c->p_valid = c->Pbuf != nullptr;   // the stored P is in stream order before sparsify reads it
-    CUDA_TRY(cudaMemcpyAsync(&c->ds->ev0[0], &c->ds->value, 2 * sizeof(double), cudaMemcpyDeviceToDevice,
-                             c->stream));
-    CUDA_TRY(cudaMemcpyAsync(&c->ds->ev0[2], &c->ds->scratch[0], sizeof(double), cudaMemcpyDeviceToDevice,
-                             c->stream));
     double v0 = 0.0, g0 = 0.0, rho = 0.0, slope = 0.0, t = 1.0;
     int64_t trials = 0;
     otb_cg_out cgo{};
     bool stepped = false;
-    TRY(newton_fused(c, logX, gamma_in, p, true, floor, &v0, &g0, &rho, &cgo, &slope, &t, &trials, &stepped));
+    double* trial = (gamma_out != gamma_in) ? gamma_out : c->gtrial;
+    TRY(newton_fused(c, logX, gamma_in, p, true, floor, &v0, &g0, &rho, &cgo, &slope, &t, &trials, &stepped,
+                     trial));
     out->value0 = v0;
     out->grad_norm0 = g0;
     if (!stepped) return OTB_OK;                                   // :205 gradient floor
-    CUDA_TRY(cudaMemcpyAsync(gamma_out, c->gtrial, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, c->stream));
+    if (trial != gamma_out)
+      CUDA_TRY(cudaMemcpyAsync(gamma_out, trial, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, c->stream));
     fill_newton_out(c, t, slope, rho, v0, g0, cgo, trials, &out->newton);
     out->stepped = 1;
   } else {
