@@ -927,7 +927,9 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   }
   if (c->hv_mode == 0 || c->hv_mode == 2) {
     c->hv_grid = sms;
-    c->hv_nb = sms;
+    const char* env_cgg = std::getenv("OTB_CG_GRID");   // experiments: fewer hess_apply / CG CTAs
+    if (env_cgg && std::atoi(env_cgg) > 0) c->hv_grid = std::min(sms, std::atoi(env_cgg));
+    c->hv_nb = c->hv_grid;
     cudaError_t e = allow_max_smem(kHvFn[c->hv_var], device);
     if (e == cudaSuccess) e = allow_max_smem(kCgFn[c->hv_var], device);
     if (e != cudaSuccess) {
