@@ -124,10 +124,19 @@ class Session:
             self.norm_c = float(np.linalg.norm(cost))
         # marginals and their logs (numpy on the host: the reference's bits)
         self.a_host, self.b_host = a_h, b_h
-        self.a = torch.from_numpy(np.ascontiguousarray(a_h)).to(dev)
-        self.b = self._vec(b_h)
-        self.log_a = torch.from_numpy(np.log(a_h)).to(dev)
-        self.log_b = self._vec(np.log(b_h))
+        # one upload for the four vectors: [a | b | log a | log b], segments on
+        # 256-byte boundaries, b and log b zero-padded like _vec
+        ma, nb = round_up(m, 32), round_up(round_up(n, 2) + 16, 32)
+        pack = np.zeros(2 * ma + 2 * nb)
+        pack[:m] = a_h
+        pack[ma:ma + n] = b_h
+        pack[ma + nb:ma + nb + m] = np.log(a_h)
+        pack[2 * ma + nb:2 * ma + nb + n] = np.log(b_h)
+        vecs = torch.from_numpy(pack).to(dev)
+        self.a = vecs[:m]
+        self.b = vecs[ma:ma + round_up(n, 2) + 16]
+        self.log_a = vecs[ma + nb:ma + nb + m]
+        self.log_b = vecs[2 * ma + nb:2 * ma + nb + round_up(n, 2) + 16]
         self.norm_a = float(np.linalg.norm(a_h))
         self.norm_b = float(np.linalg.norm(b_h))
         self.default_anchor = int(np.argmax(a_h))             # sparsify.py:25-27
