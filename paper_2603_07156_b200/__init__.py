@@ -56,6 +56,18 @@ _LAZY = {
     "round_log_plan": "feasibility",
     "round_to_feasible": "feasibility",
     "kkt_residual": "feasibility",
+    "bregman_div": "feasibility",
+    "c_transform": "feasibility",
+    "gap": "feasibility",
+    "FeasiblePlan": "feasibility",
+    "KktReport": "feasibility",
+    "hessian_matvec_exact": "semidual",
+    "zeta_from_cache": "semidual",
+    "TwoDualState": "sinkhorn",
+    "scaled_plan_log": "sinkhorn",
+    "zeta_update": "sinkhorn",
+    "gamma_update": "sinkhorn",
+    "LocalGroup": "distributed",
     "warm_start": "sinkhorn",
     "Trajectory": "trajectory",
     "TrajectoryRecord": "trajectory",

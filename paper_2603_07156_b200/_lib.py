@@ -66,6 +66,10 @@ SIGNATURES = {
     "otb_set_stream": (C.c_int, [vp, vp]),
     "otb_nccl_get_unique_id": (C.c_int, [C.c_char_p, vp]),
     "otb_attach_nccl": (C.c_int, [vp, C.c_char_p, vp, C.c_int, C.c_int]),
+    "otb_group_create": (C.c_int, [C.POINTER(vp), C.c_int]),
+    "otb_group_destroy": (C.c_int, [vp]),
+    "otb_group_abort": (C.c_int, [vp]),
+    "otb_attach_group": (C.c_int, [vp, vp, C.c_int]),
     "otb_bind": (C.c_int, [vp, vp, vp, vp, vp, vp, dbl, i64, dbl, dbl, dbl]),
     "otb_eval": (C.c_int, [vp, vp, vp, vp, vp, C.POINTER(EvalOut)]),
     "otb_sparsify": (C.c_int, [vp, vp, vp, dbl, C.POINTER(i64)]),
@@ -93,6 +97,10 @@ SIGNATURES = {
     "otb_set_cost_norm_sq": (C.c_int, [vp, vp]),
     "otb_check_clamp_plan": (C.c_int, [vp, i64, i64, i64, dbl, vp, vp]),
     "otb_cg_trace": (C.c_int, [vp, vp, i64, C.POINTER(i64)]),
+    "otb_round_dense": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, i64, C.POINTER(dbl), vp]),
+    "otb_bregman_dense": (C.c_int, [vp, i64, vp, i64, i64, i64, C.POINTER(dbl), vp]),
+    "otb_kkt_dense": (C.c_int, [vp, i64, vp, i64, vp, vp, vp, i64, i64, vp, C.POINTER(dbl), vp]),
+    "otb_hessian_dense": (C.c_int, [vp, i64, i64, i64, vp, vp, dbl, vp, vp]),
     "otb_prof_enable": (C.c_int, [vp, C.c_int]),
     "otb_prof_read": (C.c_int, [vp, C.POINTER(dbl), C.POINTER(i64), C.POINTER(dbl), C.c_int]),
 }

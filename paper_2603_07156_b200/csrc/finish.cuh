@@ -21,6 +21,7 @@ struct DevScalars {
   double cnorm_sq;                     // ||C||_F^2 when the caller gave it as a device scalar
   double ev0[3];                       // value, ||g||, non-finite count of an eval not yet read by the host
   double scratch[4];
+  double sp_glob[2];                   // multi-rank sparsify: overflow on any rank, total kept entries
   unsigned long long alloc;            // CSR bump allocator
   unsigned long long nnzc;             // kept entries of the last sparsify
   int flags;
@@ -386,6 +387,39 @@ __global__ void __launch_bounds__(256) k_vec_post(int mode, int n, const double*
         if (threadIdx.x == 0) *out_s = v2;
       }
     }
+  }
+}
+
+// Local-group all-reduce (otb_attach_group): out = op over ranks 0..N-1, in
+// rank order, of the ranks' buffers (same device).  Every rank runs this on
+// its own stream after waiting for the others' events, so every rank gets
+// the same bits.
+constexpr int kMaxGroup = 16;
+struct LocalRed {
+  const double* src[kMaxGroup];
+  int nranks;
+  int op;            // 0 sum, 2 max (NCCL op codes)
+  int64_t count;
+  double* out;
+};
+__global__ void __launch_bounds__(256) k_local_reduce(LocalRed r) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < r.count; j += (int64_t)gridDim.x * blockDim.x) {
+    double t = r.src[0][j];
+    for (int q = 1; q < r.nranks; ++q) {
+      const double v = r.src[q][j];
+      t = (r.op == 2) ? fmax(t, v) : t + v;
+    }
+    r.out[j] = t;
+  }
+}
+
+// Multi-rank sparsify: [capacity-overflow flag, kept entries] as doubles
+// after the n column sums, so that the all-reduce of d also tells every rank
+// whether ANY rank must redo the pass (the collectives stay matched).
+__global__ void k_sparsify_scalars(const DevScalars* ds, double* dst) {
+  if (threadIdx.x == 0) {
+    dst[0] = (ds->flags & 2) ? 1.0 : 0.0;
+    dst[1] = (double)ds->nnzc;
   }
 }
 

@@ -11,11 +11,15 @@
 #include <cstdio>
 #include <cstdlib>
 #include <atomic>
+#include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
 #include "dense.cuh"
+#include "dense_api.cuh"
 #include "finish.cuh"
 #include "sparse.cuh"
 
@@ -112,13 +116,57 @@ const void* const kHvFn[kHvVariants] = HV_ROW(k_hv_grp);     // variant codes: s
 const void* const kCgFn[kHvVariants] = HV_ROW(k_cg_fused);
 
 enum ProfClass {
-  PC_EVAL = 0, PC_SPARSIFY, PC_HV, PC_CGVEC, PC_TESTA, PC_TESTB, PC_TESTC, PC_WARMZ, PC_WARMG, PC_CGFUSED, PC_N = 16
+  PC_EVAL = 0, PC_SPARSIFY, PC_HV, PC_CGVEC, PC_TESTA, PC_TESTB, PC_TESTC, PC_WARMZ, PC_WARMG, PC_CGFUSED,
+  PC_SKIP = 15,   // CG iterations launched past convergence (no-op kernels): not reported
+  PC_N = 16
 };
 
 constexpr int kCgBatch = 16;
 constexpr size_t kMaxDynSmem = 232448;  // 227 KB
 
 }  // namespace
+
+// Local group (otb_attach_group): the ranks of one process, one host thread
+// each.  A generation barrier with a timeout; `broken` releases everyone.
+struct otb_group {
+  int n = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  bool broken = false;
+  double timeout_s = 300.0;
+  const double* bufs[kMaxGroup] = {};
+  int64_t counts[kMaxGroup] = {};
+  int ops[kMaxGroup] = {};
+  cudaEvent_t ready[kMaxGroup] = {}, done[kMaxGroup] = {};
+  int devices[kMaxGroup] = {};
+
+  int barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    if (broken) return fail(OTB_ERR_NCCL, "local group broken (a rank failed or timed out)");
+    const uint64_t g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return OTB_OK;
+    }
+    const bool ok = cv.wait_for(lk, std::chrono::duration<double>(timeout_s), [&] { return gen != g || broken; });
+    if (!ok) {
+      broken = true;
+      cv.notify_all();
+      return fail(OTB_ERR_NCCL, "local group: barrier timed out (collective sequences of the ranks differ?)");
+    }
+    if (broken) return fail(OTB_ERR_NCCL, "local group broken (a rank failed or timed out)");
+    return OTB_OK;
+  }
+  void abort() {
+    std::lock_guard<std::mutex> lk(mu);
+    broken = true;
+    cv.notify_all();
+  }
+};
 
 struct otb_ctx {
   int device = 0;
@@ -176,7 +224,10 @@ struct otb_ctx {
   // NCCL
   Nccl nccl;
   NcclComm comm = nullptr;
+  otb_group* group = nullptr;   // local group (instead of NCCL)
+  double* lg_tmp = nullptr;     // its reduction target
   int nranks = 1, rank = 0;
+  int64_t nnz_glob = 0;         // kept entries over all ranks
   int64_t launches = 0;       // kernels launched by this context
   // profiling
   bool prof = false;
@@ -310,8 +361,44 @@ int launch_dense(otb_ctx* c, int kind, Geom geo, void* io) {
   return OTB_OK;
 }
 
+// Local group all-reduce: publish, barrier, wait for every rank's event,
+// fixed-order sum into lg_tmp, barrier (no rank overwrites its buffer while a
+// peer still reads it), copy back.
+int group_allreduce(otb_ctx* c, double* buf, size_t count, int op) {
+  otb_group* G = c->group;
+  const int r = c->rank, N = G->n;
+  if (count > (size_t)(rup(c->n, 2) + 16)) return fail(OTB_ERR_ARG, "local group all-reduce larger than its buffer");
+  G->bufs[r] = buf;
+  G->counts[r] = (int64_t)count;
+  G->ops[r] = op;
+  CUDA_TRY(cudaEventRecord(G->ready[r], c->stream));
+  TRY(G->barrier());
+  LocalRed lr{};
+  for (int q = 0; q < N; ++q) {
+    if (G->counts[q] != (int64_t)count || G->ops[q] != op) {
+      G->abort();
+      return fail(OTB_ERR_NCCL, "local group: ranks issued different all-reduces");
+    }
+    if (q != r) CUDA_TRY(cudaStreamWaitEvent(c->stream, G->ready[q], 0));
+    lr.src[q] = G->bufs[q];
+  }
+  lr.nranks = N;
+  lr.op = op;
+  lr.count = (int64_t)count;
+  lr.out = c->lg_tmp;
+  k_local_reduce<<<(int)std::min<int64_t>(cdiv((int64_t)count, 256), 2 * c->num_sms), 256, 0, c->stream>>>(lr);
+  LAUNCH_CHECK();
+  CUDA_TRY(cudaEventRecord(G->done[r], c->stream));
+  TRY(G->barrier());
+  for (int q = 0; q < N; ++q)
+    if (q != r) CUDA_TRY(cudaStreamWaitEvent(c->stream, G->done[q], 0));
+  CUDA_TRY(cudaMemcpyAsync(buf, c->lg_tmp, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  return OTB_OK;
+}
+
 int allreduce(otb_ctx* c, double* buf, size_t count, int op) {
   if (c->nranks <= 1) return OTB_OK;
+  if (c->group) return group_allreduce(c, buf, count, op);
   const int r = c->nccl.allReduce(buf, buf, count, kNcclFloat64, op, c->comm, c->stream);
   if (r != 0)
     return fail(OTB_ERR_NCCL, std::string("ncclAllReduce: ") + (c->nccl.getErrorString ? c->nccl.getErrorString(r) : "?"));
@@ -449,9 +536,14 @@ int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho
     return OTB_OK;
   }
   TRY(colreduce(c, c->ncl, nullptr, 0, 0, 0));
-  TRY(allreduce(c, c->sendbuf, (size_t)n, kNcclSum));
+  // [overflow flag, kept entries] ride along with d: a redo after a CSR
+  // overflow on ANY rank is then taken by every rank (matched collectives)
+  k_sparsify_scalars<<<1, 32, 0, c->stream>>>(c->ds, c->sendbuf + n);
+  LAUNCH_CHECK();
+  TRY(allreduce(c, c->sendbuf, (size_t)n + 2, kNcclSum));
   k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_COPY, n, c->sendbuf, c->b, c->d, c->ds, c->bpart, nullptr);
   LAUNCH_CHECK();
+  CUDA_TRY(cudaMemcpyAsync(c->ds->sp_glob, c->sendbuf + n, 2 * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   return OTB_OK;
 }
 
@@ -461,12 +553,15 @@ int sparsify_finish(otb_ctx* c, int64_t rec, bool* redo) {
   const int64_t nnz = (int64_t)c->hs->nnzc;
   if (rec >= 0 && rec < (int64_t)c->recs.size())
     c->recs[(size_t)rec].bytes = 16.0 * c->m_loc * c->n + 12.0 * nnz + 8.0 * (c->m_loc + 1);
-  *redo = (c->hs->flags & 2) != 0;
+  const bool mine = (c->hs->flags & 2) != 0;
+  *redo = c->nranks > 1 ? c->hs->sp_glob[0] != 0.0 : mine;
   if (*redo) {
+    if (!mine) return OTB_OK;   // another rank overflowed: same redo, nothing to grow here
     const int64_t need = (int64_t)c->hs->alloc + (int64_t)c->ncl * c->chunk;
     return grow_csr(c, need + need / 8);
   }
   c->nnz = nnz;
+  c->nnz_glob = c->nranks > 1 ? (int64_t)c->hs->sp_glob[1] : nnz;
   return OTB_OK;
 }
 
@@ -594,6 +689,8 @@ int cg_iteration(otb_ctx* c, int64_t k, double* x) {
 int cg_fused_launch(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t max_iters, double* x,
                     int64_t* rec, const double* neg_of = nullptr, const double* shift_dev = nullptr) {
   const int n = (int)c->n;
+  // the persistent CG reduces H v over its own rows only: single rank
+  if (c->nranks != 1) return fail(OTB_ERR_ARG, "internal: persistent CG launched with more than one rank");
   // with neg_of the right-hand side -neg_of is formed here into c->rhs (rhs must be c->rhs)
   k_cg_init<<<c->colgrid, 256, 0, c->stream>>>(n, rhs, x, c->cg_r, c->cg_p[0], c->cg, c->bpart, shift, rel_tol,
                                                (long long)max_iters, neg_of, neg_of ? c->rhs : nullptr, shift_dev);
@@ -645,10 +742,21 @@ int do_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t m
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   if (c->hcg->status == CG_INCONSISTENT) return cg_finish(c, -1, out);
   int64_t k = 0;
+  const size_t rec0 = c->recs.size();
   while (c->hcg->status == CG_RUN) {
     for (int j = 0; j < kCgBatch; ++j, ++k) TRY(cg_iteration(c, k, x));
     CUDA_TRY(cudaMemcpyAsync(c->hcg, c->cg, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
+  // profiling: the launches of a batch past convergence return at once;
+  // only the iterations that ran count (time and bytes)
+  if (c->prof) {
+    int64_t hv_seen = 0, vec_seen = 0;
+    for (size_t q = rec0; q < c->recs.size(); ++q) {
+      auto& r = c->recs[q];
+      if (r.cls == PC_HV && ++hv_seen > c->hcg->iters) r.cls = PC_SKIP;
+      if (r.cls == PC_CGVEC && ++vec_seen > c->hcg->iters) r.cls = PC_SKIP;
+    }
   }
   return cg_finish(c, -1, out);
 }
@@ -760,6 +868,29 @@ int do_round(otb_ctx* c, const double* X, const double* gamma, double* Xout, int
   return OTB_OK;
 }
 
+}  // namespace
+
+// ------------------------------------------------------------ dense drop-ins
+// (dense_api.cuh) Context-free, on `stream`; temporaries from the stream
+// allocator; host results after one synchronisation.
+namespace {
+struct DapiScratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  ~DapiScratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+  int get(double** p, size_t count) {
+    cudaError_t e = cudaMallocAsync((void**)p, std::max<size_t>(count, 1) * sizeof(double), st);
+    if (e != cudaSuccess) return fail(OTB_ERR_NOMEM, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+    ptrs.push_back(*p);
+    return OTB_OK;
+  }
+};
+int dapi_rows_grid(int64_t m) { return (int)std::max<int64_t>(1, std::min<int64_t>(m, 148 * 8)); }
+dim3 dapi_cols_grid(int64_t m, int64_t n) {
+  return dim3((unsigned)cdiv(n, kDapiThreads), (unsigned)std::max<int64_t>(1, std::min<int64_t>(m, kDapiRB)));
+}
 }  // namespace
 
 // ======================================================================
@@ -1049,7 +1180,7 @@ int otb_destroy(otb_ctx* c) {
                   (void*)c->cg_ap, (void*)c->cg_y, (void*)c->gtrial, (void*)c->yv, (void*)c->ec, (void*)c->Mloc,
                   (void*)c->Mglob, (void*)c->Sloc, (void*)c->row_start, (void*)c->rowpre, (void*)c->row_len, (void*)c->row_nnz,
                   (void*)c->cols, (void*)c->vals, (void*)c->ds, (void*)c->cg, (void*)c->scal, (void*)c->cta_rb,
-                  (void*)c->bm, (void*)c->Pbuf, (void*)c->cg_trace})
+                  (void*)c->bm, (void*)c->Pbuf, (void*)c->cg_trace, (void*)c->lg_tmp})
     if (p) cudaFree(p);
   if (c->hs) cudaFreeHost(c->hs);
   if (c->hcg) cudaFreeHost(c->hcg);
@@ -1095,6 +1226,57 @@ int otb_attach_nccl(otb_ctx* c, const char* nccl_path, const void* id128, int nr
   if (r != 0) return fail(OTB_ERR_NCCL, "ncclCommInitRank failed");
   c->nranks = nranks;
   c->rank = rank;
+  c->cg_fused = false;   // the persistent CG has no H v all-reduce (krylov.py:68-84 needs the global H v)
+  c->have_eval = false;
+  return OTB_OK;
+}
+
+int otb_group_create(otb_group** out, int nranks) {
+  if (!out) return fail(OTB_ERR_ARG, "out is null");
+  *out = nullptr;
+  if (nranks < 1 || nranks > kMaxGroup) return fail(OTB_ERR_ARG, "group size must be 1..16");
+  otb_group* g = new otb_group();
+  g->n = nranks;
+  const char* env = std::getenv("OTB_GROUP_TIMEOUT");
+  if (env && std::atof(env) > 0) g->timeout_s = std::atof(env);
+  *out = g;
+  return OTB_OK;
+}
+
+int otb_group_abort(otb_group* g) {
+  if (!g) return fail(OTB_ERR_ARG, "null group");
+  g->abort();
+  return OTB_OK;
+}
+
+int otb_group_destroy(otb_group* g) {
+  if (!g) return OTB_OK;
+  for (int q = 0; q < g->n; ++q) {
+    if (g->ready[q]) cudaEventDestroy(g->ready[q]);
+    if (g->done[q]) cudaEventDestroy(g->done[q]);
+  }
+  delete g;
+  return OTB_OK;
+}
+
+int otb_attach_group(otb_ctx* c, otb_group* g, int rank) {
+  if (!c || !g) return fail(OTB_ERR_ARG, "null context or group");
+  if (rank < 0 || rank >= g->n) return fail(OTB_ERR_ARG, "rank out of range");
+  if (c->comm || c->group) return fail(OTB_ERR_ARG, "context already attached");
+  CUDA_TRY(cudaSetDevice(c->device));
+  {
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (g->ready[rank]) return fail(OTB_ERR_ARG, "rank already attached");
+    CUDA_TRY(cudaEventCreateWithFlags(&g->ready[rank], cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&g->done[rank], cudaEventDisableTiming));
+    g->devices[rank] = c->device;
+  }
+  if (g->n > 1) TRY(dalloc(&c->lg_tmp, (size_t)(rup(c->n, 2) + 16)));
+  c->group = g;
+  c->nranks = g->n;
+  c->rank = rank;
+  if (g->n > 1) c->cg_fused = false;
+  c->have_eval = false;
   return OTB_OK;
 }
 
@@ -1292,7 +1474,7 @@ void fill_newton_out(const otb_ctx* c, double t, double slope, double rho, doubl
   out->grad_norm_before = g0;
   out->grad_norm_after = c->last_gnorm;
   out->cg_iters = cgo.iters;
-  out->nnz = c->nnz;
+  out->nnz = c->nnz_glob;   // all ranks' kept entries (the reference's nnz of the global P_rho)
   out->trials = trials;
   out->cg_residual = cgo.residual;
 }
@@ -1658,6 +1840,107 @@ int otb_check_clamp_plan(double* X, int64_t m_loc, int64_t n, int64_t ld, double
   CUDA_TRY(cudaMemcpyAsync(&hb, dbad, sizeof(hb), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   *bad_out = (int64_t)hb;
+  return OTB_OK;
+}
+
+
+int otb_round_dense(const double* x, int64_t m, int64_t n, int64_t ldx, const double* a, const double* b, double* out,
+                    int64_t ldo, double* deficit_out, void* stream) {
+  if (!x || !a || !b || !out || m < 1 || n < 1 || ldx < n || ldo < n) return fail(OTB_ERR_ARG, "bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DapiScratch S{st, {}};
+  double *z, *y, *er, *ec, *part, *def;
+  TRY(S.get(&z, m));
+  TRY(S.get(&y, n));
+  TRY(S.get(&er, m));
+  TRY(S.get(&ec, n));
+  const dim3 cg = dapi_cols_grid(m, n);
+  TRY(S.get(&part, (size_t)cg.y * n));
+  TRY(S.get(&def, 1));
+  const int rg = dapi_rows_grid(m), vg = (int)cdiv(n, kDapiThreads);
+  k_dapi_rows<<<rg, kDapiThreads, 0, st>>>(x, ldx, (int)m, (int)n, nullptr, nullptr, a, 1, z);       // :56-58
+  k_dapi_cols<<<cg, kDapiThreads, 0, st>>>(x, ldx, (int)m, (int)n, z, nullptr, part);                 // :60
+  k_dapi_colfinish<<<vg, kDapiThreads, 0, st>>>(part, (int)cg.y, (int)n, b, 1, y);                   // :61-62
+  k_dapi_rows<<<rg, kDapiThreads, 0, st>>>(x, ldx, (int)m, (int)n, z, y, a, 2, er);                   // :64
+  k_dapi_cols<<<cg, kDapiThreads, 0, st>>>(x, ldx, (int)m, (int)n, z, y, part);
+  k_dapi_colfinish<<<vg, kDapiThreads, 0, st>>>(part, (int)cg.y, (int)n, b, 2, ec);                  // :65
+  k_dapi_vsum<<<1, kDapiThreads, 0, st>>>(er, (int)m, 0, def);                                         // :66
+  k_dapi_round_out<<<148 * 8, 256, 0, st>>>(x, ldx, (int)m, (int)n, z, y, er, ec, def, out, ldo);     // :67-68
+  CUDA_TRY(cudaGetLastError());
+  double h = 0.0;
+  CUDA_TRY(cudaMemcpyAsync(&h, def, sizeof h, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (deficit_out) *deficit_out = h;
+  return OTB_OK;
+}
+
+int otb_bregman_dense(const double* x, int64_t ldx, const double* logy, int64_t ldy, int64_t m, int64_t n,
+                      double* result, void* stream) {
+  if (!x || !logy || !result || m < 1 || n < 1 || ldx < n || ldy < n) return fail(OTB_ERR_ARG, "bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DapiScratch S{st, {}};
+  double *rows3, *tot;
+  TRY(S.get(&rows3, 3 * (size_t)m));
+  TRY(S.get(&tot, 3));
+  k_dapi_bregman<<<dapi_rows_grid(m), kDapiThreads, 0, st>>>(x, ldx, logy, ldy, (int)m, (int)n, rows3);
+  k_dapi_rowstats<<<1, 96, 0, st>>>(rows3, (int)m, 3, nullptr, tot);
+  CUDA_TRY(cudaGetLastError());
+  double h[3];
+  CUDA_TRY(cudaMemcpyAsync(h, tot, sizeof h, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  *result = h[0] - h[1] + h[2];   // feasibility.py:85: terms.sum() - x.sum() + exp(log_y).sum()
+  return OTB_OK;
+}
+
+int otb_kkt_dense(const double* x, int64_t ldx, const double* C, int64_t ldc, const double* gamma, const double* a,
+                  const double* b, int64_t m, int64_t n, double* zeta_out, double* sums8, void* stream) {
+  if (!x || !C || !gamma || !a || !b || !sums8 || m < 1 || n < 1 || ldx < n || ldc < n)
+    return fail(OTB_ERR_ARG, "bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DapiScratch S{st, {}};
+  double *zeta = zeta_out, *rows6, *tot, *part, *cs;
+  if (!zeta) TRY(S.get(&zeta, m));
+  TRY(S.get(&rows6, 6 * (size_t)m));
+  TRY(S.get(&tot, 8));
+  const dim3 cg = dapi_cols_grid(m, n);
+  TRY(S.get(&part, (size_t)cg.y * n));
+  TRY(S.get(&cs, n));
+  k_dapi_kkt<<<dapi_rows_grid(m), kDapiThreads, 0, st>>>(x, ldx, C, ldc, gamma, (int)m, (int)n, zeta, rows6);
+  k_dapi_rowstats<<<1, 224, 0, st>>>(rows6, (int)m, 6, a, tot);   // tot[0..5] sums, tot[6] = sum (rowsum - a)^2
+  k_dapi_cols<<<cg, kDapiThreads, 0, st>>>(x, ldx, (int)m, (int)n, nullptr, nullptr, part);
+  k_dapi_colfinish<<<(int)cdiv(n, kDapiThreads), kDapiThreads, 0, st>>>(part, (int)cg.y, (int)n, b, 0, cs);
+  k_dapi_sqdiff<<<1, kDapiThreads, 0, st>>>(cs, b, (int)n, tot + 7);
+  CUDA_TRY(cudaGetLastError());
+  double h[8];
+  CUDA_TRY(cudaMemcpyAsync(h, tot, sizeof h, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  // [row_res_sq, col_res_sq, neg_sq, x_sq, dslack_sq, comp, <C,x>, sum x]
+  sums8[0] = h[6];
+  sums8[1] = h[7];
+  sums8[2] = h[1];
+  sums8[3] = h[2];
+  sums8[4] = h[3];
+  sums8[5] = h[4];
+  sums8[6] = h[5];
+  sums8[7] = h[0];
+  return OTB_OK;
+}
+
+int otb_hessian_dense(const double* P, int64_t ld, int64_t m, int64_t n, const double* a, const double* v, double eta,
+                      double* out, void* stream) {
+  if (!P || !a || !v || !out || m < 1 || n < 1 || ld < n || !(eta > 0.0)) return fail(OTB_ERR_ARG, "bad arguments");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DapiScratch S{st, {}};
+  double *w, *p0, *p1;
+  TRY(S.get(&w, m));
+  const dim3 cg = dapi_cols_grid(m, n);
+  TRY(S.get(&p0, (size_t)cg.y * n));
+  TRY(S.get(&p1, (size_t)cg.y * n));
+  k_dapi_rowdot<<<dapi_rows_grid(m), kDapiThreads, 0, st>>>(P, ld, (int)m, (int)n, v, a, w);
+  k_dapi_cols2<<<cg, kDapiThreads, 0, st>>>(P, ld, (int)m, (int)n, a, w, p0, p1);
+  k_dapi_hv_out<<<(int)cdiv(n, kDapiThreads), kDapiThreads, 0, st>>>(p0, p1, (int)cg.y, (int)n, v, eta, out);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(st));
   return OTB_OK;
 }
 

@@ -207,10 +207,8 @@ def device_cost(points: PointInstance, device, rows: tuple[int, int] | None = No
     if points.normalised:
         p = peak.value
         if comm is not None and getattr(comm, "world", 1) > 1:
-            import torch.distributed as dist
-
             t = torch.tensor([p], dtype=torch.float64, device=device)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            comm.all_reduce_(t, op="max")
             p = float(t.item())
         _lib.check(_lib.lib.otb_scale_cost(buf.data_ptr(), r1 - r0, n, ld, p, C.c_void_p(stream)))
     return buf[:, :n] if ld > n else buf

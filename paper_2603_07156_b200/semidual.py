@@ -100,3 +100,23 @@ def zeta_from_cache(cache: RowSoftmaxCache, problem: OtProblem, eta: float) -> n
     z = s.new_vec(s.m_loc)
     s.ops.zeta_from_lse(z)
     return z[: s.m_loc].cpu().numpy()
+
+
+def hessian_matvec_exact(cache: RowSoftmaxCache, problem: OtProblem, eta: float, v) -> np.ndarray:
+    """semidual.py:103-114 — (diag(P^T a) - P^T diag(a) P) v / eta with the
+    dense P of ``cache`` (materialised in HBM, then otb_hessian_dense: row
+    dots P v, column sums P^T a and P^T (a P v), one output pass)."""
+    import ctypes as C
+
+    from . import _lib
+
+    s = cache.session
+    s.ops.eval(cache.plan_t, cache.gamma_t)          # re-arm the row statistics
+    P = s.ops.materialize_p(cache.plan_t, cache.gamma_t)
+    vd = s._vec(v)
+    out = s.new_vec()
+    m_loc, n = s.m_loc, s.n
+    a_loc = s.a[s.row_begin:s.row_end]
+    _lib.check(_lib.lib.otb_hessian_dense(P.data_ptr(), n, m_loc, n, a_loc.data_ptr(), vd.data_ptr(), float(eta),
+                                          out.data_ptr(), C.c_void_p(s.torch.cuda.current_stream().cuda_stream)))
+    return out[:n].cpu().numpy()

@@ -104,9 +104,7 @@ class Session:
                 self.C[:, :n].copy_(cost[rows], non_blocking=True)
                 sq = torch.linalg.vector_norm(self.C).reshape(1) ** 2   # ||C||_F^2 of the local rows
                 if comm is not None and comm.world > 1:
-                    import torch.distributed as dist
-
-                    dist.all_reduce(sq)
+                    comm.all_reduce_(sq)
                 self._c_ready = torch.cuda.Event()
                 self._c_ready.record(side)
             self._norm_sq = sq
@@ -115,9 +113,7 @@ class Session:
             self.C[:, :n].copy_(cost[rows], non_blocking=True)
             sq = torch.linalg.vector_norm(self.C).reshape(1) ** 2   # ||C||_F^2 of the local rows
             if comm is not None and comm.world > 1:
-                import torch.distributed as dist
-
-                dist.all_reduce(sq)
+                comm.all_reduce_(sq)
             self.norm_c = float(torch.sqrt(sq))
         else:
             self.C[:, :n].copy_(torch.from_numpy(np.ascontiguousarray(cost[rows])))

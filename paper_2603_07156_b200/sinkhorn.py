@@ -12,7 +12,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .core import LogPlan, OtProblem
+from .core import LogPlan, OtProblem, host
 from .semidual import DualState
 from .session import session_for
 
@@ -44,3 +44,51 @@ def warm_start(logplan: LogPlan, problem: OtProblem, eta: float, warm_tol: float
     if device_in:
         return DualState(gamma_buf[:n], generation=generation), zeta_buf[: s.m_loc]
     return DualState(gamma_buf[:n].cpu().numpy(), generation=generation), zeta_buf[: s.m_loc].cpu().numpy()
+
+
+# ------------------------------------------- single updates (sinkhorn.py:26-58)
+class TwoDualState:
+    """sinkhorn.py:26-35 — column dual gamma and row dual zeta."""
+
+    def __init__(self, gamma, zeta):
+        self.gamma = np.asarray(host(gamma), dtype=np.float64)
+        self.zeta = np.asarray(host(zeta), dtype=np.float64)
+
+
+def _two_dual_tensors(s, state):
+    g = s._vec(state.gamma)
+    z = s._vec(state.zeta, s.m_loc)
+    return g, z
+
+
+def scaled_plan_log(logplan: LogPlan, state: TwoDualState, problem: OtProblem, eta: float) -> np.ndarray:
+    """sinkhorn.py:41-43 — log X + (zeta_i + gamma_j - C_ij) / eta, one
+    device pass (otb_scaled_plan).  Entries below LOG_FLOOR come back
+    clamped to it (the device writes a LogPlan); NaN / +inf raise
+    InvalidCost."""
+    s = session_for(problem, eta)
+    plan_t = s.plan(logplan)
+    g, z = _two_dual_tensors(s, state)
+    out = s.new_plan()
+    s.ops.scaled_plan(plan_t, g, z, out)
+    return out[:, : s.n].cpu().numpy()
+
+
+def zeta_update(logplan: LogPlan, state: TwoDualState, problem: OtProblem, eta: float) -> TwoDualState:
+    """sinkhorn.py:46-51 — zeta = eta (log a - LSE_j(log X + (gamma - C)/eta)),
+    the row pass of otb_sinkhorn_zeta."""
+    s = session_for(problem, eta)
+    plan_t = s.plan(logplan)
+    g, z = _two_dual_tensors(s, state)
+    s.ops.sinkhorn_zeta(plan_t, g, z)
+    return TwoDualState(state.gamma, z[: s.m_loc].cpu().numpy())
+
+
+def gamma_update(logplan: LogPlan, state: TwoDualState, problem: OtProblem, eta: float) -> TwoDualState:
+    """sinkhorn.py:54-58 — gamma = eta (log b - LSE_i(log X + (zeta - C)/eta)),
+    the column pass of otb_sinkhorn_gamma."""
+    s = session_for(problem, eta)
+    plan_t = s.plan(logplan)
+    g, z = _two_dual_tensors(s, state)
+    s.ops.sinkhorn_gamma(plan_t, g, z)
+    return TwoDualState(g[: s.n].cpu().numpy(), state.zeta)

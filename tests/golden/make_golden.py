@@ -208,12 +208,66 @@ def config_scalars():
     (HERE / "config_scalars.json").write_text(json.dumps(out, indent=1))
 
 
+def dense_cases():
+    """Kernel-level drop-ins on dense LINEAR matrices (feasibility.py:44-127,
+    semidual.py:103-114, sinkhorn.py:41-58): an infeasible x with negative
+    entries for kkt_residual (certified as given), round_to_feasible of a
+    nonnegative infeasible x, bregman_div, c_transform, gap, the exact Hessian
+    product and single Sinkhorn updates."""
+    for i, (kind, m, n, seed, eta) in enumerate([("uniform", 23, 17, 0, 1e-2), ("square", 40, 33, 1, 5e-2),
+                                                 ("spherical", 9, 50, 2, 1e-2)]):
+        p = problem(kind, m, n, seed)
+        rng = np.random.default_rng(seed + 50)
+        x = rng.random((m, n)) * (2.0 / (m * n))                 # nonnegative, marginals off
+        xneg = x - 0.3 / (m * n)                                  # some negative entries
+        lp = core.LogPlan(core.initial_plan(p).log_entries + 0.3 * rng.normal(size=(m, n)))
+        g = perturbed_gamma(n, seed, 0.1)
+        z0 = rng.normal(size=m) * 0.01
+        rounded = feasibility.round_to_feasible(x, p.source_marginal, p.target_marginal)
+        rep = feasibility.kkt_residual(xneg, g, p.cost, p.source_marginal, p.target_marginal)
+        cache = semidual.compute_p(lp, semidual.DualState(g), p, eta)
+        v = rng.normal(size=n)
+        hv = semidual.hessian_matvec_exact(cache, p, eta, v)
+        st = sinkhorn.TwoDualState(gamma=g, zeta=z0)
+        zu = sinkhorn.zeta_update(lp, st, p, eta)
+        gu = sinkhorn.gamma_update(lp, st, p, eta)
+        spl = sinkhorn.scaled_plan_log(lp, st, p, eta)
+        save(f"dense_{i}", C=p.cost, a=p.source_marginal, b=p.target_marginal, x=x, xneg=xneg, logY=lp.log_entries,
+             gamma=g, zeta0=z0, eta=eta, v=v, rounded=rounded.entries, bregman=feasibility.bregman_div(x, lp),
+             kkt=np.array([rep.delta_p, rep.delta_d, rep.delta_c, rep.delta_kkt]), zeta_used=rep.zeta_used,
+             c_transform=feasibility.c_transform(g, p.cost), gap=feasibility.gap(rounded, p.cost, 0.01),
+             hv=hv, zeta_upd=zu.zeta, gamma_upd=gu.gamma, scaled_log=spl)
+
+
+def config_seeds():
+    """BASELINE configs 1 and 2 at seeds 1 and 2, and config 3 (seed 0)
+    truncated at max_outer=2: the reference's scalars per outer."""
+    out = {}
+    jobs = [(1, 1, None), (1, 2, None), (2, 1, None), (2, 2, None), (3, 0, 2)]
+    for idx, seed, max_outer in jobs:
+        inst = instances.config(idx, seed)
+        p = core.OtProblem(inst.cost, inst.a, inst.b)
+        kw = {} if max_outer is None else {"max_outer": max_outer}
+        res = bregman_outer.ibsn_solve(p, core.SolverConfig(eta=inst.eta, kkt_tol=inst.kkt_tol, **kw))
+        last = res.trajectory.records[-1]
+        out[f"cfg{idx}_seed{seed}" + ("" if max_outer is None else f"_outer{max_outer}")] = dict(
+            objective=res.objective, kkt=res.kkt, outer_iters=res.outer_iters, max_outer=max_outer,
+            newton_total=last.inner_total, cg_total=last.cg_total,
+            objectives=[r.objective for r in res.trajectory.records],
+            kkts=[r.kkt for r in res.trajectory.records],
+            inner_totals=[r.inner_total for r in res.trajectory.records],
+            cg_totals=[r.cg_total for r in res.trajectory.records])
+        print(idx, seed, out[list(out)[-1]]["objective"], flush=True)
+        (HERE / "config_seeds.json").write_text(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["eval", "sparsify", "newton", "rounding", "candidate", "warm", "inner", "solve",
                              "eot", "ibsink", "configs"]
     fns = {"eval": eval_cases, "sparsify": sparsify_cases, "newton": newton_cases, "rounding": rounding_cases,
            "candidate": candidate_cases, "warm": warm_cases, "inner": inner_cases, "solve": solve_cases,
-           "eot": eot_cases, "ibsink": ibsink_cases, "configs": config_scalars}
+           "eot": eot_cases, "ibsink": ibsink_cases, "configs": config_scalars, "dense": dense_cases,
+           "seeds": config_seeds}
     for w in which:
         fns[w]()
         print("done", w)

@@ -1,0 +1,187 @@
+"""The row-sharded (multi-rank) path on ONE GPU, through a libotb local group.
+
+``distributed.LocalGroup(world)`` runs ``world`` ranks as host threads of one
+process, one libotb context and one CUDA stream each, with disjoint row
+shards (``row_range``).  Their all-reduces — the same call sites as the NCCL
+path: gradient column sums (semidual.py:98-100), d and every CG iteration's
+H v (sparsify.py:143-153, krylov.py:68-84), the rounding column sums
+(feasibility.py:56-66), the warm-start gamma sweep max/sum (sinkhorn.py:54-58)
+— are a fixed-order device sum over the ranks.  The sharded result must match
+the one-rank result to the BASELINE tolerance: |d<C,X>|/<C,X> <= 1e-8, equal
+outer and Newton counts, CG totals within 5% (reduction orders differ, so CG
+can move by a few iterations, as between 1 and 8 BLAS threads in the
+reference).
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _api():
+    import paper_2603_07156_b200 as P
+
+    return P
+
+
+def _solve_sharded(inst, world, cfg):
+    import torch
+
+    P = _api()
+    from paper_2603_07156_b200.distributed import LocalGroup
+
+    grp = LocalGroup(world)
+    try:
+        def body(r, comm):
+            prob = P.OtProblem(inst.cost, inst.a, inst.b)
+            res = P.ibsn_solve(prob, cfg, comm=comm)
+            info = res._session.info()
+            rounded = res.rounded_plan            # local rows of the rounded plan
+            gam = np.asarray(res.gamma)
+            return res, info, rounded, gam
+
+        out = grp.run(body)
+        torch.cuda.synchronize()
+        return out
+    finally:
+        grp.close()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_config1_solve_sharded_matches_one_rank(cuda, world):
+    P = _api()
+    inst = P.instances.config(1, 0)
+    cfg = P.SolverConfig(eta=inst.eta, kkt_tol=inst.kkt_tol)
+    one = P.ibsn_solve(P.OtProblem(inst.cost, inst.a, inst.b), cfg)
+    outs = _solve_sharded(inst, world, cfg)
+    for r, (res, info, rounded, gam) in enumerate(outs):
+        assert info["nranks"] == world and info["rank"] == r
+        assert info["cg_fused"] == 0            # the persistent CG is single-rank
+        assert res.outer_iters == one.outer_iters
+        assert res.newton_iters == one.newton_iters
+        assert abs(res.cg_iters - one.cg_iters) <= 0.05 * one.cg_iters
+        assert abs(res.objective - one.objective) <= 1e-8 * abs(one.objective)
+        assert res.kkt < cfg.kkt_tol
+        # the replicated dual is bitwise identical on every rank
+        assert np.array_equal(gam, np.asarray(outs[0][3]))
+    # the shards of the rounded plan form an exactly feasible plan
+    X = np.concatenate([o[2] for o in outs], axis=0)
+    assert X.shape == inst.cost.shape
+    assert np.max(np.abs(X.sum(axis=1) - inst.a)) <= 1e-12
+    assert np.max(np.abs(X.sum(axis=0) - inst.b)) <= 1e-12
+    assert abs(float((inst.cost * X).sum()) - one.objective) <= 1e-8 * abs(one.objective)
+
+
+def test_config2_solve_two_ranks(cuda):
+    P = _api()
+    inst = P.instances.config(2, 0)
+    cfg = P.SolverConfig(eta=inst.eta, kkt_tol=inst.kkt_tol)
+    one = P.ibsn_solve(P.OtProblem(inst.cost, inst.a, inst.b), cfg)
+    outs = _solve_sharded(inst, 2, cfg)
+    for res, info, _, _ in outs:
+        assert info["cg_fused"] == 0
+        assert (res.outer_iters, res.newton_iters) == (one.outer_iters, one.newton_iters)
+        assert abs(res.cg_iters - one.cg_iters) <= 0.05 * one.cg_iters
+        assert abs(res.objective - one.objective) <= 1e-8 * abs(one.objective)
+
+
+def _inner_sharded(C, a, b, lx, g0, eta, world, max_inner=1):
+    """inner_solve(max_inner) with the rows of (C, log X) sharded."""
+    P = _api()
+    from paper_2603_07156_b200.distributed import LocalGroup
+
+    grp = LocalGroup(world)
+    try:
+        def body(r, comm):
+            r0, r1 = comm.row_range(C.shape[0])
+            prob = P.OtProblem(C, a, b)
+            cfg = P.SolverConfig(eta=eta, kkt_tol=1e-9, max_inner=max_inner)
+            st, cand, rep = P.inner_solve(P.LogPlan(lx[r0:r1]), P.DualState(g0), prob, cfg, mu_k=1e3,
+                                          outer_k=0, comm=comm)
+            return np.asarray(st.gamma)[: C.shape[1]].copy(), rep
+        return grp.run(body)
+    finally:
+        grp.close()
+
+
+def _inner_one(C, a, b, lx, g0, eta, max_inner=1):
+    P = _api()
+    cfg = P.SolverConfig(eta=eta, kkt_tol=1e-9, max_inner=max_inner)
+    st, cand, rep = P.inner_solve(P.LogPlan(lx), P.DualState(g0), P.OtProblem(C, a, b), cfg, mu_k=1e3, outer_k=0)
+    return np.asarray(st.gamma)[: C.shape[1]], rep
+
+
+def test_newton_step_window_cluster_geometry_two_ranks(cuda):
+    """n = 16384 (config 4's column count): the window-cluster hess_apply
+    (hv_mode 3) and the cluster-split dense passes, rows sharded over 2."""
+    from oracle import otb_oracle as O
+    P = _api()
+    rng = np.random.default_rng(11)
+    m, n, eta = 96, 16384, 1e-2
+    x = rng.random((m, 3))
+    y = rng.random((n, 3))
+    C = ((x[:, None, :] - y[None, :, :]) ** 2).sum(-1)
+    C /= C.max()
+    a = np.full(m, 1.0 / m)
+    b = np.full(n, 1.0 / n)
+    lx = O.product_log_plan(a, b)
+    g0, _, _ = O.warm_start(lx, C, a, b, eta, 1e-3)
+    g1, r1 = _inner_one(C, a, b, lx, g0, eta, max_inner=2)
+    outs = _inner_sharded(C, a, b, lx, g0, eta, 2, max_inner=2)
+    for g2, r2 in outs:
+        assert r2.newton_iters == r1.newton_iters
+        assert all(abs(x - y) <= 1 for x, y in zip(r2.cg_iters, r1.cg_iters))
+        assert r2.nnz == r1.nnz                 # global kept count, all-reduced
+        assert np.max(np.abs(g2 - g1)) <= 1e-9 * max(1.0, np.abs(g1).max())
+        assert r2.objective == pytest.approx(r1.objective, rel=1e-10)
+    assert np.array_equal(outs[0][0], outs[1][0])
+
+
+def test_csr_overflow_on_one_rank_only(cuda, monkeypatch):
+    """Rank 0's rows keep (almost) every entry, rank 1's few: only rank 0
+    outgrows the initial CSR capacity.  The overflow flag rides with the d
+    all-reduce, so both ranks redo the pass and the collectives stay matched
+    (a rank-local redo would deadlock the group / NCCL)."""
+    from oracle import otb_oracle as O
+    P = _api()
+    rng = np.random.default_rng(5)
+    m, n, eta = 64, 512, 1e-2
+    C = np.empty((m, n))
+    C[: m // 2] = 0.5 + 1e-4 * rng.random((m // 2, n))   # flat rows: P ~ uniform, all kept
+    C[m // 2:] = rng.random((m - m // 2, n))              # varied rows: sparse P
+    a = rng.random(m) + 0.1
+    a /= a.sum()
+    b = rng.random(n) + 0.1
+    b /= b.sum()
+    lx = O.product_log_plan(a, b)
+    g0, _, _ = O.warm_start(lx, C, a, b, eta, 1e-3)
+    g1, r1 = _inner_one(C, a, b, lx, g0, eta)
+    # contexts created from here on start with a tiny CSR (entries)
+    monkeypatch.setenv("OTB_CSR_CAP0", str(m * n // 4))
+    outs = _inner_sharded(C, a, b, lx, g0, eta, 2)
+    for g2, r2 in outs:
+        assert r2.nnz == r1.nnz
+        assert abs(r2.cg_iters[0] - r1.cg_iters[0]) <= 1
+        assert np.max(np.abs(g2 - g1)) <= 1e-9 * max(1.0, np.abs(g1).max())
+
+
+def test_group_mismatch_fails_loudly(cuda):
+    """A rank that raises breaks the group: the others leave their barrier
+    with an error instead of hanging."""
+    P = _api()
+    from paper_2603_07156_b200.distributed import LocalGroup
+
+    inst = P.instances.config(1, 0)
+    grp = LocalGroup(2)
+    try:
+        def body(r, comm):
+            if r == 1:
+                raise RuntimeError("rank 1 gives up")
+            prob = P.OtProblem(inst.cost, inst.a, inst.b)
+            return P.ibsn_solve(prob, P.SolverConfig(eta=inst.eta, kkt_tol=inst.kkt_tol), comm=comm)
+
+        with pytest.raises(RuntimeError, match="rank 1 gives up"):
+            grp.run(body, timeout=120)
+    finally:
+        grp.close()

@@ -1,6 +1,9 @@
 """Summarise an `ncu --set full` report into profiles/.
 
-    python tools/ncu_summary.py REPORT.ncu-rep OUT_DIR [config_key]
+    python tools/ncu_summary.py REPORT.ncu-rep|RAW.csv OUT_DIR [config_key]
+
+(RAW.csv = `ncu -i REPORT --page raw --csv` made on the GPU box when the
+report itself is too large to copy back.)
 
 Writes OUT_DIR/ncu_full_summary.csv (one row per captured launch: duration,
 DRAM bytes read/written, achieved DRAM GB/s, issue-slot use, pipe shares,
@@ -17,7 +20,7 @@ import subprocess
 import sys
 
 CLASS = {"k_cg_fused": "cg_fused", "k_eval": "eval", "k_sparsify": "sparsify", "k_test_a": "test_a",
-         "k_test_b": "test_b", "k_test_c": "test_c", "k_hv_grp": "hess_apply", "k_warm_zeta": "warm_zeta",
+         "k_test_b": "test_b", "k_test_c": "test_c", "k_hv_grp": "hess_apply", "k_hv_wc": "hess_apply", "k_warm_zeta": "warm_zeta",
          "k_warm_gamma": "warm_gamma"}
 
 KEYS = [("gpu__time_duration.sum", "duration_us", 1e-3),
@@ -42,8 +45,11 @@ def to_mb(v, unit):
 def main():
     rep, out_dir = sys.argv[1], sys.argv[2]
     key = sys.argv[3] if len(sys.argv) > 3 else "cfg2"
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--kernel-name-base", "function"],
-                         capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):
+        raw = open(rep).read()
+    else:
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--kernel-name-base", "function"],
+                             capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     out_rows = []
@@ -83,7 +89,8 @@ def main():
     os.makedirs(out_dir, exist_ok=True)
     fields = ["id", "kernel", "duration_us", "dram_read_MB", "dram_write_MB", "dram_GBps"] + \
         [lab for _, lab, _ in KEYS if lab not in ("duration_us", "dram_read_MB", "dram_write_MB")] + ["top_stalls"]
-    with open(os.path.join(out_dir, "ncu_full_summary.csv"), "w", newline="") as f:
+    out_name = os.environ.get("NCU_SUMMARY_NAME", "ncu_full_summary.csv")
+    with open(os.path.join(out_dir, out_name), "w", newline="") as f:
         w = csv.DictWriter(f, fieldnames=fields)
         w.writeheader()
         for row in out_rows:
