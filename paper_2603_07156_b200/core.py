@@ -26,8 +26,40 @@ def _is_torch(x) -> bool:
     return type(x).__module__.startswith("torch")
 
 
+class RowShardCost:
+    """The rows [row0, row0 + rows.shape[0]) of an m x n cost matrix, held
+    on this rank's GPU (multi-GPU runs build only their own rows: config 5's
+    C is 20 GB).  ``OtProblem(RowShardCost(...), a, b)`` has the GLOBAL shape
+    (m, n); a session created with the matching row range (distributed
+    ``row_range``) uses the local tensor in place.  ``rows`` may be a padded
+    view (stride (ld, 1))."""
+
+    def __init__(self, rows, row0: int, m: int):
+        if not (_is_torch(rows) and rows.dim() == 2):
+            raise ShapeMismatch("RowShardCost needs a 2-D torch tensor of local rows")
+        if not 0 <= row0 <= row0 + rows.shape[0] <= m:
+            raise ShapeMismatch("row shard outside the matrix")
+        self.rows = rows
+        self.row0 = int(row0)
+        self.m = int(m)
+
+    @property
+    def shape(self) -> tuple[int, int]:
+        return (self.m, int(self.rows.shape[1]))
+
+    @property
+    def ndim(self) -> int:
+        return 2
+
+    @property
+    def is_cuda(self) -> bool:
+        return bool(self.rows.is_cuda)
+
+
 def _as_float_array(x, ndim: int):
     """core.py:30-34; torch tensors are kept (as contiguous float64)."""
+    if isinstance(x, RowShardCost):
+        return x
     if _is_torch(x):
         import torch
 
@@ -256,6 +288,8 @@ def validate(problem: OtProblem) -> None:
         raise ShapeMismatch(f"source marginal has length {a.shape[0]}, cost has {m} rows")
     if b.shape[0] != n:
         raise ShapeMismatch(f"target marginal has length {b.shape[0]}, cost has {n} columns")
+    if isinstance(cost, RowShardCost):   # each rank checks its own rows
+        cost = cost.rows
     if _is_torch(cost):
         import torch
 

@@ -114,6 +114,21 @@ const void* const kDenseFn[DK_COUNT][kMaxNS + 1] = {
   }
 const void* const kHvFn[kHvVariants] = HV_ROW(k_hv_grp);     // variant codes: sparse.cuh HvVar
 const void* const kCgFn[kHvVariants] = HV_ROW(k_cg_fused);
+const void* const kWcFn[kMaxNQ + 1] = {nullptr,           (const void*)k_hv_wc<1>, (const void*)k_hv_wc<2>,
+                                       (const void*)k_hv_wc<3>, (const void*)k_hv_wc<4>, (const void*)k_hv_wc<5>,
+                                       (const void*)k_hv_wc<6>, (const void*)k_hv_wc<7>, (const void*)k_hv_wc<8>};
+int wc_stage_bytes(int nqw) {
+  switch (nqw) {
+    case 1: return WcGeo<1>::kStage;
+    case 2: return WcGeo<2>::kStage;
+    case 3: return WcGeo<3>::kStage;
+    case 4: return WcGeo<4>::kStage;
+    case 5: return WcGeo<5>::kStage;
+    case 6: return WcGeo<6>::kStage;
+    case 7: return WcGeo<7>::kStage;
+    default: return WcGeo<8>::kStage;
+  }
+}
 
 enum ProfClass {
   PC_EVAL = 0, PC_SPARSIFY, PC_HV, PC_CGVEC, PC_TESTA, PC_TESTB, PC_TESTC, PC_WARMZ, PC_WARMG, PC_CGFUSED,
@@ -275,8 +290,8 @@ cudaError_t allow_max_smem(const void* fn, int device) {
 
 size_t dense_smem(const otb_ctx* c, int kind, int nstage) {
   const size_t slice = 2 * (size_t)c->nt;
-  const size_t dbl = (size_t)nstage * kNmat[kind] * slice + (size_t)kNacc[kind] * c->ns * slice + 2 * kMaxWarps * 4 + 2 * 8 * 4;
-  return dbl * 8 + (2 * (size_t)nstage + 2) * 8 + 64 * 4;
+  const size_t dbl = (size_t)nstage * kNmat[kind] * slice + (size_t)kNacc[kind] * c->ns * slice + 2 * kMaxWarps * 4 + kXb * 8 * 4;
+  return dbl * 8 + (2 * (size_t)nstage + kXb) * 8 + 64 * 4;
 }
 
 Geom make_geom(const otb_ctx* c, int kind, const double* m0, const double* m1) {
@@ -618,7 +633,7 @@ int run_hv(otb_ctx* c, const double* v_src, const double* r, const double* p_pre
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(c->hv_grid);
       cfg.blockDim = dim3(kStThreads);
-      cfg.dynamicSmemBytes = kWcSmemBytes;
+      cfg.dynamicSmemBytes = c->hv_smem;
       cfg.stream = c->stream;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -627,7 +642,7 @@ int run_hv(otb_ctx* c, const double* v_src, const double* r, const double* p_pre
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      CUDA_TRY(cudaLaunchKernelExC(&cfg, (const void*)k_hv_wc, args));
+      CUDA_TRY(cudaLaunchKernelExC(&cfg, kWcFn[c->hv_var], args));
     } else {
       CUDA_TRY(cudaLaunchKernel(kHvFn[c->hv_var], dim3(c->hv_grid), dim3(c->hv_threads), args, c->hv_smem,
                                 c->stream));
@@ -924,8 +939,61 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   c->num_sms = sms;
   // dense geometry: cluster size, column window, slices, threads
+  // Cluster size: any cl <= 8 whose window fits one CTA (<= kMaxNS slices),
+  // chosen for the least time per row block: rows per co-resident cluster x
+  // (slices per CTA + the cost of the row exchanges, ~2 slices).  Clusters
+  // must fit in a GPC, so the co-resident count is queried: e.g. n = 50000
+  // gets cl = 5 (26 clusters, 130 SMs) instead of cl = 8 (15 clusters,
+  // 120 SMs).  OTB_DENSE_CL forces the size.
   int cl = 1;
-  while (cdiv(n, cl) > 2 * 512 * kMaxNS && cl < kMaxCluster) cl *= 2;
+  {
+    const char* env_cl = std::getenv("OTB_DENSE_CL");
+    const int force_cl = env_cl ? std::atoi(env_cl) : 0;
+    double best = 1e300;
+    for (int q = 1; q <= kMaxCluster; ++q) {
+      if (force_cl > 0 && q != force_cl) continue;
+      const int64_t colw_q = rup(cdiv(n, q), q > 1 ? 64 : 2);
+      if (cdiv(colw_q, 1024) > kMaxNS) continue;
+      const int ns_q = (int)std::max<int64_t>(1, cdiv(colw_q, 1024));
+      const int nt_q = (int)std::max<int64_t>(32, rup(cdiv(colw_q, 2 * ns_q), 32));
+      int fit = sms / q;
+      if (q > 1) {
+        c->nt = nt_q;
+        c->ns = ns_q;
+        int st = 8;
+        while (st > 2 && dense_smem(c, DK_EVAL, st) > kMaxDynSmem - 1024) --st;
+        const void* fn = kDenseFn[DK_EVAL][ns_q];
+        int nclus = 0;
+        if (allow_max_smem(fn, device) == cudaSuccess) {
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3((unsigned)(q * (sms / q)));
+          cfg.blockDim = dim3((unsigned)(nt_q + 32));
+          cfg.dynamicSmemBytes = dense_smem(c, DK_EVAL, st);
+          cudaLaunchAttribute attr[1];
+          attr[0].id = cudaLaunchAttributeClusterDimension;
+          attr[0].val.clusterDim.x = (unsigned)q;
+          attr[0].val.clusterDim.y = 1;
+          attr[0].val.clusterDim.z = 1;
+          cfg.attrs = attr;
+          cfg.numAttrs = 1;
+          if (cudaOccupancyMaxActiveClusters(&nclus, fn, &cfg) != cudaSuccess) nclus = 0;
+        }
+        cudaGetLastError();
+        if (nclus < 1) continue;
+        fit = std::min(fit, nclus);
+      }
+      const int64_t ncl_q = std::max<int64_t>(1, std::min<int64_t>(fit, c->m_loc));
+      const double cost = (double)cdiv(c->m_loc, ncl_q) * (ns_q + (q > 1 ? 2.0 : 0.0));
+      if (cost < best * (1.0 - 1e-9)) {
+        best = cost;
+        cl = q;
+      }
+    }
+    if (best >= 1e300) {
+      delete c;
+      return fail(OTB_ERR_ARG, "no dense cluster geometry fits this n");
+    }
+  }
   c->cl = cl;
   c->colw = (int)rup(cdiv(n, cl), cl > 1 ? 64 : 2);   // cluster windows start on 64-column words
   int ns = (int)std::min<int64_t>(kMaxNS, std::max<int64_t>(1, cdiv(c->colw, 1024)));
@@ -1020,40 +1088,65 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
     }
   }
   // n > 8192 and too wide for the group accumulators (hv_mode 1): window
-  // clusters of W = ceil(n / 4096) CTAs (bitmap words per row = 64 W), when
-  // the device runs such a cluster (OTB_HV_WC=1 forces them for any n > 8192)
-  const int nwin = (int)cdiv(n, kWinCols);
+  // clusters (sparse.cuh k_hv_wc<NQ>): W CTAs of 1024 NQ columns each,
+  // W = ceil(n / (1024 NQ)) <= 16.  NQ is chosen for the least work per SM:
+  // rows per co-resident cluster x window width (clusters must fit in a GPC,
+  // so e.g. clusters of 13 leave a third of the SMs idle).  OTB_HV_NQ forces
+  // NQ; OTB_HV_WC=1 uses the window clusters for any n > 8192.
   const char* env_wc = std::getenv("OTB_HV_WC");
   const bool want_wc = (c->hv_mode == 1 || (env_wc && std::atoi(env_wc) == 1)) && c->hv_mode != 2;
-  if (want_wc && nwin >= 2 && nwin <= 16 && !(env_bm && std::atoi(env_bm) == 0) &&
-      !(env_wc && std::atoi(env_wc) == 0) && !(env_hv && std::atoi(env_hv) == 1)) {
-    cudaError_t e = allow_max_smem((const void*)k_hv_wc, device);
-    if (e == cudaSuccess && nwin > 8)
-      e = cudaFuncSetAttribute((const void*)k_hv_wc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    int nclusters = 0;
-    if (e == cudaSuccess) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)(nwin * (sms / nwin)));
-      cfg.blockDim = dim3(kStThreads);
-      cfg.dynamicSmemBytes = kWcSmemBytes;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = (unsigned)nwin;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      cfg.attrs = attr;
-      cfg.numAttrs = 1;
-      e = cudaOccupancyMaxActiveClusters(&nclusters, (const void*)k_hv_wc, &cfg);
+  if (want_wc && n > 8192 && !(env_bm && std::atoi(env_bm) == 0) && !(env_wc && std::atoi(env_wc) == 0) &&
+      !(env_hv && std::atoi(env_hv) == 1)) {
+    const char* env_nq = std::getenv("OTB_HV_NQ");
+    const int force_nq = env_nq ? std::atoi(env_nq) : 0;
+    double best = 1e300;
+    int best_nq = 0, best_w = 0, best_ncl = 0, best_s = 0;
+    for (int nqw = 1; nqw <= kMaxNQ; ++nqw) {
+      if (force_nq > 0 && nqw != force_nq) continue;
+      const int W = (int)cdiv(n, 1024 * nqw);
+      if (W < 2 || W > kWcMaxW) continue;
+      const void* fn = kWcFn[nqw];
+      const int stage = wc_stage_bytes(nqw);
+      const int S = (int)std::min<int64_t>(4, (int64_t)(kMaxDynSmem - 8192 - 8192 * nqw) / (stage + 16));
+      if (S < 2) continue;
+      cudaError_t e = allow_max_smem(fn, device);
+      if (e == cudaSuccess && W > 8) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      int nclusters = 0;
+      if (e == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(W * (sms / W)));
+        cfg.blockDim = dim3(kStThreads);
+        cfg.dynamicSmemBytes = wc_smem_bytes(nqw, stage, S);
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)W;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg);
+      }
+      cudaGetLastError();
+      if (e != cudaSuccess || nclusters < 1) continue;
+      nclusters = std::min(nclusters, sms / W);
+      const double cost = (double)nqw / nclusters;   // rows per cluster x window width
+      if (cost < best * (1.0 - 1e-9)) {
+        best = cost;
+        best_nq = nqw;
+        best_w = W;
+        best_ncl = nclusters;
+        best_s = S;
+      }
     }
-    cudaGetLastError();
-    if (e == cudaSuccess && nclusters >= 1) {
+    if (best_nq > 0) {
       c->hv_mode = 3;
-      c->hv_win = nwin;
-      c->nq = 64 * nwin;
-      c->hv_ng = 0;
-      c->hv_smem = kWcSmemBytes;
-      c->hv_nb = std::min(nclusters, sms / nwin);
-      c->hv_grid = c->hv_nb * nwin;
+      c->hv_var = best_nq;
+      c->hv_win = best_w;
+      c->nq = 16 * best_nq * best_w;   // bitmap words per row
+      c->hv_ng = best_s;               // ring stages
+      c->hv_smem = wc_smem_bytes(best_nq, wc_stage_bytes(best_nq), best_s);
+      c->hv_nb = best_ncl;
+      c->hv_grid = best_ncl * best_w;
     }
   }
   if (c->hv_mode == 0 || c->hv_mode == 2) {

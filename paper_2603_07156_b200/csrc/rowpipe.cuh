@@ -26,6 +26,7 @@
 namespace otb {
 
 constexpr int kMaxCluster = 8;
+constexpr int kXb = 4;       // cluster exchange buffers (rotating; >= 3 needed, see exchange())
 constexpr int kMaxNS = 10;   // 1024-column slices per CTA: one CTA per row up to n = 10240
 
 struct Geom {
@@ -48,17 +49,17 @@ struct SmemMap {
   double* ring;      // nstage * nmat * 2nt
   double* acc;       // nacc * ns * 2nt
   double* slots;     // 2 * kMaxWarps * 4
-  double* xbuf;      // 2 * 8 * 4
+  double* xbuf;      // kXb * 8 * 4
   uint64_t* full;    // nstage
   uint64_t* empty;   // nstage
-  uint64_t* xbar;    // 2
+  uint64_t* xbar;    // kXb
   int* misc;         // 64 ints
 };
 
 OTB_DEV size_t smem_bytes_for(const Geom& g, int nmat) {
   size_t slice = 2 * (size_t)g.nt;
-  size_t d = (size_t)g.nstage * nmat * slice + (size_t)g.nacc * g.ns * slice + 2 * kMaxWarps * 4 + 2 * 8 * 4;
-  return d * 8 + (2 * (size_t)g.nstage + 2) * 8 + 64 * 4;
+  size_t d = (size_t)g.nstage * nmat * slice + (size_t)g.nacc * g.ns * slice + 2 * kMaxWarps * 4 + kXb * 8 * 4;
+  return d * 8 + (2 * (size_t)g.nstage + kXb) * 8 + 64 * 4;
 }
 
 OTB_DEV SmemMap carve(const Geom& g, int nmat, unsigned char* base) {
@@ -72,12 +73,12 @@ OTB_DEV SmemMap carve(const Geom& g, int nmat, unsigned char* base) {
   s.slots = p;
   p += 2 * kMaxWarps * 4;
   s.xbuf = p;
-  p += 2 * 8 * 4;
+  p += kXb * 8 * 4;
   uint64_t* b = reinterpret_cast<uint64_t*>(p);
   s.full = b;
   s.empty = b + g.nstage;
   s.xbar = b + 2 * g.nstage;
-  s.misc = reinterpret_cast<int*>(b + 2 * g.nstage + 2);
+  s.misc = reinterpret_cast<int*>(b + 2 * g.nstage + kXb);
   return s;
 }
 
@@ -126,9 +127,13 @@ struct Dense {
         mbar_init(&sm.full[s], 1);
         mbar_init(&sm.empty[s], g.nt / 32);
       }
-      mbar_init(&sm.xbar[0], g.cl);
-      mbar_init(&sm.xbar[1], g.cl);
+      // exchange buffers: one local arrival + 32 bytes (4 doubles) from every
+      // CTA of the cluster per use (st.async complete_tx), armed here for the
+      // first kXb exchanges and re-armed by the receiver after each one
+      for (int q = 0; q < kXb; ++q) mbar_init(&sm.xbar[q], 1);
       fence_mbar_init();
+      if (g.cl > 1)
+        for (int q = 0; q < kXb; ++q) mbar_arrive_expect_tx(&sm.xbar[q], 32u * (uint32_t)g.cl);
     }
     // zero accumulators (consumer-owned slots only, but any thread may do it)
     const int na = g.nacc * g.ns * slice;
@@ -198,26 +203,30 @@ struct Dense {
   }
 
   // Exchange K (<=4) values among the cl (> 1) CTAs of the cluster.  Returns
-  // the shared-memory table: entry [q*4 + k] is CTA q's value k, readable
-  // until the exchange after next (two buffers alternate).  Consumer threads
-  // only.
+  // the shared-memory table: entry [q*4 + k] is CTA q's value k.  Every
+  // value goes out as st.async (async proxy) completing 32 bytes per CTA on
+  // the peer's buffer barrier, so the wait is a cta-scope one (no L1
+  // invalidation, unlike a cluster-scope acquire).  Buffers rotate over
+  // kXb = 4: a peer can write buffer x mod 4 again only at exchange x + 4,
+  // i.e. after this CTA sent exchange x + 3, which its warp 0 does only after
+  // the block reduction that precedes it — by then every thread has finished
+  // reading table x (read right after exchange x returns).  The table is
+  // readable until the next block reduction.  Consumer threads only.
   template <int K>
   OTB_DEV const double* exchange(const double (&v)[K]) {
-    const int q = xcount & 1;
-    const uint32_t par = (uint32_t)((xcount >> 1) & 1);
+    static_assert(K >= 1 && K <= 4, "exchange of 1..4 values");
+    const int q = xcount & (kXb - 1);
+    const uint32_t par = (uint32_t)((xcount / kXb) & 1);
     double* mine = sm.xbuf + (q * kMaxCluster + cr) * 4;
     if (warp == 0 && lane < g.cl) {   // lane rk serves cluster rank rk: the remote ops go out in parallel
       const uint32_t dst = mapa(smem_u32(mine), (uint32_t)lane);
-#pragma unroll
-      for (int k = 0; k < K; ++k) st_cluster_f64(dst + 8u * k, v[k]);
-      mbar_arrive_remote(mapa(smem_u32(&sm.xbar[q]), (uint32_t)lane));
+      const uint32_t bar = mapa(smem_u32(&sm.xbar[q]), (uint32_t)lane);
+      st_async_v2f64(dst, v[0], K > 1 ? v[K > 1 ? 1 : 0] : 0.0, bar);
+      st_async_v2f64(dst + 16u, K > 2 ? v[K > 2 ? 2 : 0] : 0.0, K > 3 ? v[K > 3 ? 3 : 0] : 0.0, bar);
     }
-    if (tid == 0) {
-      while (!mbar_try_wait_cluster(&sm.xbar[q], par)) {
-      }
-    }
-    bar_sync(1, g.nt);
+    mbar_wait(&sm.xbar[q], par);   // every consumer thread: the async-proxy data is then visible to it
     ++xcount;
+    if (tid == 0) mbar_arrive_expect_tx(&sm.xbar[q], 32u * (uint32_t)g.cl);   // re-arm for exchange + kXb
     return sm.xbuf + q * kMaxCluster * 4;
   }
 

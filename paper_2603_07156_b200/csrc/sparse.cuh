@@ -831,60 +831,262 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_hv_grp(HvArgs h) {
   }
 }
 
-// Window-cluster hess_apply for n > 8192: a cluster of W = ceil(n / 4096)
-// CTAs shares one row block; CTA rank q owns the 4096 columns of window q
-// (bitmap words [64 q, 64 q + 64), NQ = 4 words per warp, v and the
-// accumulator in registers).  Each CTA's producer warp stages its window's
-// words and value segment of every row (TMA), the row dots of each batch are
-// completed across the windows by ClusterDots (DSMEM), so every value is
-// read once, nothing is scattered through atomics and the result is
-// deterministic.  Partial rows go to colpart[cluster][n].
-constexpr int kWinCols = 4096;
-constexpr int kWcStages = 3;
-constexpr size_t kWcSmemBytes = 16 * 64 * 8 + kWcStages * (size_t)kStBytes + 2 * kWcStages * 8;
+// Window-cluster hess_apply for n > 8192 (configs 4-5): a cluster of W
+// CTAs shares one row block; CTA rank q owns window q = bitmap words
+// [WW q, WW (q + 1)) of every row, WW = 16 NQ words = 1024 NQ columns (NQ
+// words per consumer warp, v and the accumulator in registers).  W and NQ are
+// chosen at context creation so the clusters that are co-resident cover the
+// most SMs per window column (otb.cu, hv geometry).
+//
+// The row dot of row k needs all W windows' partials, so a plain schedule
+// (dots, exchange, update) stalls every row on the slowest CTA of the
+// cluster.  Here the exchange is decoupled by D rows:
+//   step k: (a) issue the global (L2) loads of row k-D's values at the pair
+//               positions saved when its dots were formed,
+//           (b) row k from the TMA ring: partial dots from shared memory,
+//               pair positions saved (uint16, registers), stage released,
+//               CTA sum, partial sent to every peer (DSMEM + remote arrive),
+//           (c) receive row k-D's W partials (window order), apply
+//               a_r * dot_r * P_rj to the owned columns.
+// Row k-D's values were brought to the SM by TMA D rows earlier, so the
+// re-read is an L2 hit; HBM sees each value once.  The ring holds only the
+// rows in flight (loads + dots); the exchange waits hold no stage.  Rows are
+// applied in order, partials summed in window order: deterministic.
+constexpr int kWcD = 4;                  // exchange lookahead (rows)                  // exchange lookahead (rows)                  // exchange lookahead (rows)                  // exchange lookahead (rows)                  // exchange lookahead (rows)                  // exchange lookahead (rows)
+constexpr int kWcX = 2 * kWcD + 2;       // exchange buffers (>= 2 D + 1: see the note in wc_consume)
+constexpr int kWcMaxW = 16;
+constexpr int kWcHdr = 32;
 
+template <int NQ>
+struct WcGeo {
+  static constexpr int WW = 16 * NQ;                  // words per window
+  static constexpr int kVals = 1024 * NQ + 8;         // staged values per row (window + zero pair + slack)
+  static constexpr int kZero = 1024 * NQ;             // zero pair (never a copy target)
+  static constexpr int kStage = WW * 16 + kWcHdr + kVals * 8;
+  static constexpr int kVsm = 1024 * NQ * 8;          // the window of v
+};
+
+struct WcHdr {
+  long long st;      // row_start of the row (doubles)
+  double ar;         // a_r
+  int base;          // stage value index of the row's pair 0 (= -2 off(first word))
+  int pad[3];
+};
+
+__host__ __device__ inline size_t wc_smem_bytes(int nqw, int stage_bytes, int S) {
+  return (size_t)1024 * nqw * 8 + (size_t)S * stage_bytes + 2 * (size_t)S * 8;
+}
+
+template <int NQ>
+OTB_DEV void wc_produce(const Csr& A, const uint4* bm, const double* a, int rb, int re, int stride, int woff,
+                        bool last_window, unsigned char* ring, uint64_t* full, uint64_t* empty, int S) {
+  using G = WcGeo<NQ>;
+  const int lane = threadIdx.x & 31;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int g0 = rb; g0 < re; g0 += 32) {
+    const int r = g0 + lane;
+    long long st = 0, src = 0;
+    int cnt = 0, base = 0;
+    double ar = 0.0;
+    if (r < re) {
+      st = A.row_start[r];
+      const int fo = (woff > 0) ? 2 * (int)bm[(size_t)r * stride + woff].z : 0;
+      const int lo = last_window ? A.row_len[r] : 2 * (int)bm[(size_t)r * stride + woff + G::WW].z;
+      src = st + fo;                     // even: runs start on 8-entry boundaries, offsets count pairs
+      cnt = max(lo - fo, 0);
+      base = -fo;
+      ar = a[A.row0 + r];
+    }
+    const int rows = min(32, re - g0);
+    for (int k = 0; k < rows; ++k) {
+      const long long kst = __shfl_sync(0xffffffffu, st, k);
+      const long long ksrc = __shfl_sync(0xffffffffu, src, k);
+      const int kcnt = __shfl_sync(0xffffffffu, cnt, k);
+      const int kbase = __shfl_sync(0xffffffffu, base, k);
+      const double kar = __shfl_sync(0xffffffffu, ar, k);
+      if (lane == 0) {
+        mbar_wait(&empty[stage], phase ^ 1u);
+        unsigned char* sp = ring + (size_t)stage * G::kStage;
+        WcHdr* h = reinterpret_cast<WcHdr*>(sp + G::WW * 16);
+        double* vdst = reinterpret_cast<double*>(sp + G::WW * 16 + kWcHdr);
+        h->st = kst;
+        h->ar = kar;
+        h->base = kbase;
+        mbar_arrive_expect_tx(&full[stage], (uint32_t)kcnt * 8u + (uint32_t)G::WW * 16u);
+        if (kcnt > 0) bulk_g2s(vdst, A.vals + ksrc, (uint32_t)kcnt * 8u, &full[stage]);
+        bulk_g2s(sp, bm + (size_t)(g0 + k) * stride + woff, (uint32_t)G::WW * 16u, &full[stage]);
+      }
+      if (++stage == S) {
+        stage = 0;
+        phase ^= 1u;
+      }
+    }
+  }
+}
+
+// Consumers (512 threads).  Exchange buffer safety: a CTA at dot row k has
+// received row k-D, so every peer has sent row >= k-D and (being at dot row
+// >= k-D) has received rows <= k-2D-1... a sender of row k reuses buffer
+// k % X, last used for row k-X; with X >= 2D+1 every CTA has consumed row k-X
+// before any peer can send row k.
+template <int NQ>
+OTB_DEV void wc_consume(int cnt, const double* __restrict__ vals, const double* vsm, double (&acc)[2 * NQ],
+                        unsigned char* ring, uint64_t* full, uint64_t* empty, int S, double* xbuf, uint64_t* xbar,
+                        int W, int cr, double* slots, WcHdr* hring) {
+  using G = WcGeo<NQ>;
+  constexpr int D = kWcD;
+  constexpr int NI = (NQ + 1) / 2;   // uint32 words of packed uint16 pair positions per row
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lb = 1u << lane, lt = lb - 1u;
+  int stage = 0, rphase = 0;
+  uint32_t phase = 0;
+  uint32_t pidx[D][NI];
+#pragma unroll
+  for (int j = 0; j < D; ++j)
+#pragma unroll
+    for (int i = 0; i < NI; ++i) pidx[j][i] = 0xffffffffu;
+  for (int k0 = 0; k0 < cnt + D; k0 += D) {
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const int k = k0 + j, ku = k - D;
+      // (a) row ku: loads of its values from L2 (positions saved in slot j)
+      double e[2 * NQ];
+      double ar_u = 0.0;
+      const bool upd = ku >= 0 && ku < cnt;
+      if (upd) {
+        const WcHdr hu = hring[ku % (D + 1)];
+        ar_u = hu.ar;
+        const double* vr = vals + hu.st;
+#pragma unroll
+        for (int t = 0; t < NQ; ++t) {
+          const uint32_t p = (pidx[j][t >> 1] >> (16 * (t & 1))) & 0xffffu;
+          double2 x = make_double2(0.0, 0.0);
+          if (p != 0xffffu) x = __ldg(reinterpret_cast<const double2*>(vr + 2 * (int)p));
+          e[2 * t] = x.x;
+          e[2 * t + 1] = x.y;
+        }
+      }
+      // (b) row k: partial dots from the staged window, positions saved
+      if (k < cnt) {
+        mbar_wait(&full[stage], phase);
+        const unsigned char* sp = ring + (size_t)stage * G::kStage;
+        const uint4* words = reinterpret_cast<const uint4*>(sp);
+        const WcHdr* h = reinterpret_cast<const WcHdr*>(sp + G::WW * 16);
+        const double* sv = reinterpret_cast<const double*>(sp + G::WW * 16 + kWcHdr);
+        const int base = h->base;
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < NI; ++i) pidx[j][i] = 0xffffffffu;
+#pragma unroll
+        for (int t = 0; t < NQ; ++t) {
+          const uint4 wd = words[warp + 16 * t];
+          const unsigned pm = bm_pairs(wd);
+          const int P = (int)wd.z + __popc(pm & lt);   // pair index in the row run
+          const bool kp = (pm & lb) != 0u;
+          const int idx = kp ? base + 2 * P : G::kZero;
+          const double2 x = *reinterpret_cast<const double2*>(sv + idx);
+          const double2 vv = *reinterpret_cast<const double2*>(vsm + bm_col<16>(t, 0));
+          d0 = fma(x.x, vv.x, d0);
+          d1 = fma(x.y, vv.y, d1);
+          if (kp) pidx[j][t >> 1] = (pidx[j][t >> 1] & ~(0xffffu << (16 * (t & 1)))) | ((uint32_t)P << (16 * (t & 1)));
+        }
+        if (threadIdx.x == 0) hring[k % (D + 1)] = *h;
+        mbar_arrive(&empty[stage]);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1u;
+        }
+        double dt[1] = {d0 + d1};
+        block_reduce<1, kSum>(dt, slots, rphase, kStConsumers);
+        if (threadIdx.x < W) {   // thread q serves peer q, in parallel
+          const int q = k % kWcX;
+          st_async_f64(mapa(smem_u32(xbuf + q * kWcMaxW + cr), (uint32_t)threadIdx.x), dt[0],
+                       mapa(smem_u32(&xbar[q]), (uint32_t)threadIdx.x));
+        }
+      }
+      // (c) row ku: the W partials in window order, then the update
+      if (upd) {
+        const int q = ku % kWcX;
+        const uint32_t par = (uint32_t)((ku / kWcX) & 1);
+        mbar_wait(&xbar[q], par);
+        double dot = 0.0;
+        for (int rk = 0; rk < W; ++rk) dot += xbuf[q * kWcMaxW + rk];
+        // re-arm buffer q for row ku + X once every consumer has read it (the
+        // next block reduction is that barrier; peers cannot send row ku + X
+        // before this CTA has sent row ku + X - D, i.e. after this point)
+        if (threadIdx.x == 0) mbar_arrive_expect_tx(&xbar[q], 8u * (uint32_t)W);
+        const double w = ar_u * dot;   // sparsify.py:153: weights * pv
+#pragma unroll
+        for (int i = 0; i < 2 * NQ; ++i) acc[i] = fma(e[i], w, acc[i]);
+      }
+    }
+  }
+}
+
+template <int NQ>
 __global__ void __launch_bounds__(kStThreads, 1) k_hv_wc(HvArgs h) {
-  extern __shared__ __align__(16) double hsm[];
-  __shared__ double xbuf[kXBufs * 16 * 4];
-  __shared__ uint64_t xbar[kXBufs];
+  using G = WcGeo<NQ>;
+  extern __shared__ __align__(16) unsigned char wsm[];
+  __shared__ double xbuf[kWcX * kWcMaxW];
+  __shared__ uint64_t xbar[kWcX];
+  __shared__ double slots[2 * kMaxWarps * 4];
+  __shared__ WcHdr hring[kWcD + 1];
   const int W = h.nwin;
+  const int S = h.ng;   // ring stages (HvArgs.ng reused)
   const int cr = (int)cluster_ctarank(), cid = blockIdx.x / W, ncl = gridDim.x / W;
-  StRing rg = st_ring(reinterpret_cast<unsigned char*>(hsm + 16 * 64), kWcStages);
+  double* vsm = reinterpret_cast<double*>(wsm);            // [1024 NQ] the window of v
+  unsigned char* ring = wsm + (size_t)G::kVsm;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)S * G::kStage);
+  uint64_t* empty = full + S;
   if (threadIdx.x == 0) {
-    for (int q = 0; q < kXBufs; ++q) mbar_init(&xbar[q], W);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kStConsumers);
+    }
+    for (int q = 0; q < kWcX; ++q) mbar_init(&xbar[q], 1);
     fence_mbar_init();
+    // exchange buffer q expects W partials (st.async, 8 bytes each) per use;
+    // armed here for rows 0..X-1, re-armed by the receiver after each use
+    for (int q = 0; q < kWcX; ++q) mbar_arrive_expect_tx(&xbar[q], 8u * (uint32_t)W);
+  }
+  if (threadIdx.x < S * 2) {   // the zero pair of every stage
+    double* sv = reinterpret_cast<double*>(ring + (size_t)(threadIdx.x >> 1) * G::kStage + G::WW * 16 + kWcHdr);
+    sv[G::kZero + (threadIdx.x & 1)] = 0.0;
   }
   __syncwarp();
   cluster_sync_all();
   if (h.st == nullptr || h.st->status == CG_RUN) {   // same decision in every CTA
-    const int n = h.n, cb = kWinCols * cr;
+    const int n = h.n, cb = 64 * G::WW * cr;
     int rb, re;
     cta_rows(h.A, cid, ncl, rb, re);
     if (threadIdx.x >= kStConsumers) {
-      st_produce(h.A, h.bm, h.a, rb, re, h.nq, 64 * cr, 64, cr + 1 == W, rg);
+      wc_produce<NQ>(h.A, h.bm, h.a, rb, re, h.nq, G::WW * cr, cr + 1 == W, ring, full, empty, S);
     } else {
+      // the window of v in shared memory (registers hold the accumulator and
+      // the values in flight); p = r + beta p by the column's owner (krylov.py:83)
       const double beta = h.update ? h.st->beta : 0.0;
-      double vr[8], ar[8];
+      double ar[2 * NQ];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int j = cb + bm_col<16>(i >> 1, i & 1);
+      for (int i = 0; i < 2 * NQ; ++i) {
+        const int jl = bm_col<16>(i >> 1, i & 1), j = cb + jl;
         double v = 0.0;
         if (j < n) {
           if (h.update) {
-            v = h.r[j] + beta * h.p_prev[j];      // krylov.py:83
+            v = h.r[j] + beta * h.p_prev[j];
             if (cid == 0) h.p_cur[j] = v;
           } else {
             v = h.v_src[j];
           }
         }
-        vr[i] = v;
+        vsm[jl] = v;
         ar[i] = 0.0;
       }
-      ClusterDots cx{xbuf, xbar, W, cr, 0, 0, kStConsumers};
-      st_consume<4, true>(rb, re, vr, ar, hsm, rg, &cx);
+      bar_sync(1, kStConsumers);
+      wc_consume<NQ>(re - rb, h.A.vals, vsm, ar, ring, full, empty, S, xbuf, xbar, W, cr, slots, hring);
       double* dst = h.colpart + (size_t)cid * n;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < 2 * NQ; ++i) {
         const int j = cb + bm_col<16>(i >> 1, i & 1);
         if (j < n) dst[j] = ar[i];
       }

@@ -21,7 +21,7 @@ import os
 import numpy as np
 
 from . import _lib
-from .core import OtProblem, _is_torch, host
+from .core import OtProblem, RowShardCost, _is_torch, host
 from .errors import ShapeMismatch
 
 _SESSION_ATTR = "_otb_sessions"
@@ -80,8 +80,15 @@ class Session:
         # padded local rows of C (a CUDA cost that already has this layout —
         # e.g. instances.device_cost with ld — is used in place, not copied)
         rows = slice(self.row_begin, self.row_end)
+        if isinstance(cost, RowShardCost):
+            if (cost.row0, cost.row0 + cost.rows.shape[0]) != (self.row_begin, self.row_end):
+                raise ShapeMismatch("RowShardCost rows do not match this rank's row range")
+            cost, rows = cost.rows, slice(0, self.m_loc)
+            local_rows = True
+        else:
+            local_rows = self.m_loc == m
         adopt = (_is_torch(cost) and cost.is_cuda and cost.device == dev and cost.dtype == f64
-                 and cost.stride() == (self.ld, 1) and self.m_loc == m and cost.storage_offset() == 0
+                 and cost.stride() == (self.ld, 1) and local_rows and cost.storage_offset() == 0
                  and cost.untyped_storage().nbytes() >= self.m_loc * self.ld * 8)
         if adopt:
             self.C = torch.as_strided(cost, (self.m_loc, self.ld), (self.ld, 1))
@@ -90,7 +97,9 @@ class Session:
             if self.ld > n:
                 self.C[:, n:].zero_()
         if adopt:
-            sq = torch.linalg.vector_norm(self.C).reshape(1) ** 2
+            sq = torch.linalg.vector_norm(self.C).reshape(1) ** 2   # ||C||_F^2 of the local rows
+            if comm is not None and comm.world > 1 and self.m_loc < m:
+                comm.all_reduce_(sq)
             self.norm_c = float(torch.sqrt(sq))
         elif _is_torch(cost) and not cost.is_cuda and os.environ.get("OTB_C_SIDE", "1") != "0":
             # host C: uploaded on a side stream, so that the caller's next

@@ -51,7 +51,8 @@ def _solve_sharded(inst, world, cfg):
 @pytest.mark.parametrize("world", [2, 4])
 def test_config1_solve_sharded_matches_one_rank(cuda, world):
     P = _api()
-    inst = P.instances.config(1, 0)
+    from paper_2603_07156_b200 import instances
+    inst = instances.config(1, 0)
     cfg = P.SolverConfig(eta=inst.eta, kkt_tol=inst.kkt_tol)
     one = P.ibsn_solve(P.OtProblem(inst.cost, inst.a, inst.b), cfg)
     outs = _solve_sharded(inst, world, cfg)
@@ -75,7 +76,8 @@ def test_config1_solve_sharded_matches_one_rank(cuda, world):
 
 def test_config2_solve_two_ranks(cuda):
     P = _api()
-    inst = P.instances.config(2, 0)
+    from paper_2603_07156_b200 import instances
+    inst = instances.config(2, 0)
     cfg = P.SolverConfig(eta=inst.eta, kkt_tol=inst.kkt_tol)
     one = P.ibsn_solve(P.OtProblem(inst.cost, inst.a, inst.b), cfg)
     outs = _solve_sharded(inst, 2, cfg)
@@ -172,7 +174,8 @@ def test_group_mismatch_fails_loudly(cuda):
     P = _api()
     from paper_2603_07156_b200.distributed import LocalGroup
 
-    inst = P.instances.config(1, 0)
+    from paper_2603_07156_b200 import instances
+    inst = instances.config(1, 0)
     grp = LocalGroup(2)
     try:
         def body(r, comm):
