@@ -1,34 +1,48 @@
 #!/usr/bin/env python
 """Benchmark of the IBSN inner loop on B200 (driver contract: one JSON line).
 
-Metric: Newton inner iterations per second.  One *step* is one inner
-iteration of ``inner_solve`` on BASELINE config 2 (64x64 grid histograms,
-m = n = 4096, eta = 1e-2; ``--config`` selects another), started from the
-same state every step — the product plan X^0 = a b^T after the outer-0
-warm start — through the public API ``inner_solve(..., max_inner=1,
-mu_k=1e3)``: eval of the current dual, sparsify, device CG, Armijo line
-search, candidate recovery, rounding, Bregman inexact test and KKT metrics.
+Metric (BASELINE.json): Newton inner iterations per second, OT solve time to
+tol, kernel HBM GB/s vs peak.  Workload: BASELINE config 5 by default — the
+largest configuration that fits one GPU (m = n = 50000, C and X 20 GB each,
+points uniform in [0,1]^2, C normalised, eta = 1e-2, tol 1e-6), seeded
+synthetic data built on the GPU bit-identically to the host numpy recipe
+(tests: test_device_cost_construction_is_bitwise_numpy).  ``--config``
+selects another configuration.
 
-Lines reported:
-  value      steps/s with inputs resident in HBM, CUDA events, max over ranks
-  e2e        the same call with pinned HOST inputs (C, log X, marginals,
-             dual copied in, dual + candidate plan copied out, every step)
-  roofline   the dominant kernel (by time share, from a profiled pass of the
-             same steps): algorithmic bytes / event-timed duration vs the
-             measured HBM copy peak of MEASURED_PEAKS.json
-  cpu_baseline  the CPU oracle (numpy port of the reference) on a bounded
-             sample of the same step, rank 0 at N=1
-  solve      OT solve time to tol (full ibsn_solve, device-resident inputs)
+One *step* = one inner iteration of ``inner_solve`` started from the same
+state every step — the product plan X^0 = a b^T after the outer-0 warm start —
+through the public API ``inner_solve(..., max_inner=1, mu_k=1e3)``: eval of
+the current dual, sparsify, device CG, Armijo line search, candidate
+recovery, rounding, Bregman inexact test and KKT metrics.
 
-``--impl reference`` times the reference's CPU algorithm (the oracle port;
-the reference is pure Python/numpy) on the same workload, rank 0 only.
+Keys of the line:
+  value         steps/s with inputs resident in HBM (CUDA events, max over ranks)
+  e2e           the same public call with pinned HOST C, log X, marginals and
+                dual: every step copies them in (40 GB at config 5) and reads
+                the dual and report scalars back
+  roofline      the dominant kernel (time share of a profiled pass of the same
+                steps): algorithmic bytes / CUDA-event launch time vs the
+                measured HBM copy peak; per_kernel lists every kernel class
+                with its fraction and the ncu DRAM bytes (profiles/traffic.json)
+  cpu_baseline  the reference itself (otibsn from baseline/_ref) on the box's
+                host cores, on a bounded sample of the same step (a row sample
+                for configs 4-5, scaled to Newton it/s), rank 0 at N = 1
+  solve         OT solve time to tol: ibsn_solve from device-resident inputs
+  secondary     configs 2 and 3 (value + solve) when the default config runs
+
+Multi-GPU (torchrun, one rank per GPU): rows sharded over the ranks, each rank
+builds only its own rows of C on its GPU; the length-n vectors are combined by
+NCCL all-reduce inside libotb.  The problem is fixed: ``"scaling": "strong"``.
+
+``--impl reference`` times the reference's CPU implementation (oracle/cpu_step.py:
+otibsn itself from baseline/_ref, else the numpy port) on the same config,
+metric and unit, rank 0 only, all host threads for BLAS.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import sys
 import threading
@@ -45,21 +59,26 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK_GBS = 6650.0
-E2E_DEFAULT = 30
+DEFAULT_CONFIG = 5
+CG_ITERS_HINT = {1: 196, 2: 32, 3: 23, 4: 28, 5: 33}   # GPU arm's CG iterations per step (row-sample size)
+METRIC = "newton_inner_iterations_per_s"
+UNIT = "newton_it/s"
+STEP = "inner_solve(max_inner=1, mu_k=1e3) from the outer-0 warm-started state"
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--config", type=int, default=DEFAULT_CONFIG)
     p.add_argument("--seed", type=int, default=0)
-    p.add_argument("--e2e-steps", type=int, default=E2E_DEFAULT)
-    p.add_argument("--cpu-sample", type=float, default=15.0, help="seconds of CPU oracle work (cpu_baseline)")
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--cpu-sample", type=float, default=15.0, help="seconds of CPU reference work (cpu_baseline)")
     p.add_argument("--no-solve", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--secondary", default=None, help="comma list of extra configs (default 2,3 with config 5)")
     return p.parse_args()
 
 
@@ -72,9 +91,13 @@ def peaks():
         return HBM_FALLBACK_GBS, "fallback", {}
 
 
-def workload_name(idx, inst):
-    m, n = len(inst.a), len(inst.b)
-    return f"{inst.name}: m={m} n={n} eta={inst.eta} tol={inst.kkt_tol}"
+def config_dict(idx, pts):
+    """The ``config`` object, identical in both arms."""
+    m, n = len(pts.a), len(pts.b)
+    return {"workload": f"BASELINE config {idx}: {pts.name}: m={m} n={n} eta={pts.eta} tol={pts.kkt_tol}",
+            "step": STEP,
+            "l2": f"inputs larger than L2 (C + log X = {2 * 8 * m * n / 1e6:.0f} MB > 126 MB)"
+            if 16 * m * n > 126e6 else f"C + log X = {2 * 8 * m * n / 1e6:.0f} MB (L2-resident)"}
 
 
 # ----------------------------------------------------------------- clocks
@@ -130,83 +153,255 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-# ------------------------------------------------------------- CPU oracle
-def oracle_state(inst):
-    from oracle import otb_oracle as O
+# --------------------------------------------------------- CPU reference
+def cpu_measure(idx, pts, steps, warmup, budget_s, full_cost=None):
+    """Time the CPU step (oracle/cpu_step.py) -> (Newton it/s, description, kind)."""
+    from oracle import cpu_step
 
-    a, b, C = inst.a, inst.b, inst.cost
-    lx = O.product_log_plan(a, b)
-    g0, _, _ = O.warm_start(lx, C, a, b, inst.eta, 1e-3)
-    return lx, g0
-
-
-def oracle_step(inst, lx, g0):
-    """The bench step on the CPU oracle: inner_solve(max_inner=1, mu_k=1e3)."""
-    from oracle import otb_oracle as O
-
-    m, n = inst.cost.shape
-    r = O.inner(lx, inst.cost, inst.a, inst.b, g0, inst.eta, 1e3, float(min(m, n)), max_inner=1)
-    # inner() rounds and tests; the bench step also reports the KKT metrics
-    O.kkt(r.rounded, r.gamma, inst.cost, inst.a, inst.b)
-    return r
-
-
-def cpu_baseline(inst, budget_s):
-    lx, g0 = oracle_state(inst)
+    st, scale = cpu_step.make_step(pts, full_cost=full_cost, cg_iters=CG_ITERS_HINT.get(idx, 32),
+                                   budget_s=budget_s)
+    for _ in range(warmup):
+        st.step()
     t0 = time.perf_counter()
-    done = 0
-    while True:
-        oracle_step(inst, lx, g0)
-        done += 1
-        el = time.perf_counter() - t0
-        if el >= budget_s or done >= 50:
-            break
-    cores = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
-    return {"value": done / el, "unit": "newton_it/s", "cores": cores, "kind": "port",
-            "sample": f"{done} bench steps (one inner Newton iteration + inexact test each) of {inst.name} "
-                      f"in {el:.1f} s; numpy restatement of the reference (oracle/otb_oracle.py), "
-                      f"BLAS threads={cores}, elementwise numpy single-threaded"}
+    for _ in range(steps):
+        st.step()
+    el = time.perf_counter() - t0
+    per_step = el / steps * scale
+    return 1.0 / per_step, st.describe(steps, el), st.kind
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from oracle import cpu_step
     from paper_2603_07156_b200 import instances
 
-    inst = instances.config(args.config, args.seed)
-    lx, g0 = oracle_state(inst)
-    for _ in range(args.warmup):
-        oracle_step(inst, lx, g0)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        oracle_step(inst, lx, g0)
-    el = time.perf_counter() - t0
-    v = args.steps / el
-    cores = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+    pts = instances.config_points(args.config, args.seed)
+    budget = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    value, sample, kind = cpu_measure(args.config, pts, args.steps, args.warmup, budget)
+    cores = cpu_step.blas_threads()
     line = {
-        "impl": "reference", "metric": "newton_inner_iterations_per_s", "value": v, "unit": "newton_it/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name(args.config, inst), "step": "inner_solve(max_inner=1, mu_k=1e3)"},
-        "cpu_baseline": {"value": v, "unit": "newton_it/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} timed steps after {args.warmup} warm-up steps"},
-        "e2e": {"value": v, "unit": "newton_it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(args.config, pts),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample + f"; BLAS threads {cores} (numpy ufuncs and scipy sparse "
+                                           f"products are single-threaded)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------- our arm
-def run_ours(args):
+class Resident:
+    """Device-resident problem + the warm-started state of the bench step."""
+
+    def __init__(self, idx, seed, dev, comm, world, rank):
+        import torch
+
+        from paper_2603_07156_b200 import instances
+        from paper_2603_07156_b200.core import LogPlan, OtProblem, RowShardCost, SolverConfig
+        from paper_2603_07156_b200.distributed import row_range
+        from paper_2603_07156_b200.session import session_for
+        from paper_2603_07156_b200.sinkhorn import warm_start
+
+        self.pts = pts = instances.config_points(idx, seed)
+        self.m, self.n = m, n = len(pts.a), len(pts.b)
+        self.ld = ld = (n + 31) // 32 * 32
+        self.r0, self.r1 = row_range(m, rank, world)
+        # C on the GPU: this rank's rows only, bit-identical to the host recipe
+        local = instances.device_cost(pts, dev, rows=(self.r0, self.r1), ld=ld, comm=comm)
+        self.cost_local = local
+        cost = RowShardCost(local, self.r0, m) if world > 1 else local
+        self.prob = OtProblem(cost, pts.a, pts.b)
+        self.cfg = SolverConfig(eta=pts.eta, kkt_tol=pts.kkt_tol, max_inner=1)
+        self.s = s = session_for(self.prob, pts.eta, comm)
+        self.X0 = s.new_plan()
+        s.ops.init_plan(self.X0)
+        self.lp0 = LogPlan.from_padded(self.X0, n)
+        gst, _ = warm_start(self.lp0, self.prob, pts.eta, self.cfg.warm_tol,
+                            gamma0=torch.zeros(n, dtype=torch.float64, device=dev), comm=comm)
+        self.g0 = gst.gamma.clone()
+        self.out_plan = s.new_plan()
+        self.bufs = (s.new_vec(), s.new_vec())
+        self.comm = comm
+
+    def step(self):
+        from paper_2603_07156_b200.inner_newton import inner_solve
+        from paper_2603_07156_b200.semidual import DualState
+
+        return inner_solve(self.lp0, DualState(self.g0), self.prob, self.cfg, mu_k=1e3, outer_k=0, session=self.s,
+                           out_plan=self.out_plan, gamma_bufs=self.bufs)
+
+
+def timed_steps(res, steps, warmup, world, dev, local):
     import torch
     import torch.distributed as dist
 
-    from paper_2603_07156_b200 import instances
-    from paper_2603_07156_b200.core import LogPlan, OtProblem, SolverConfig
+    for _ in range(max(warmup, 3)):
+        _, _, rep = res.step()
+    torch.cuda.synchronize()
+    l0 = res.s.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev0.record()
+        for _ in range(steps):
+            _, _, rep = res.step()
+        ev1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms, res.s.launches() - l0, rep, clocks.summary()
+
+
+def roofline(res, idx, steps):
+    """Profiled pass of the same steps: per-kernel-class CUDA-event times on
+    the library's stream, algorithmic bytes, fraction of the
+    measured HBM peak, ncu DRAM bytes per launch from profiles/traffic.json."""
+    s = res.s
+    s.prof_enable(True)
+    for _ in range(max(2, min(steps, 5))):
+        res.step()
+    prof = s.prof_read(reset=True)
+    s.prof_enable(False)
+    hbm, peak_kind, _ = peaks()
+    traffic = {}
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"cfg{idx}", {})
+        except Exception:
+            traffic = {}
+    total_ms = sum(v["ms"] for v in prof.values())
+    per = {}
+    for k, v in prof.items():
+        if not v["launches"]:
+            continue
+        us = 1e3 * v["ms"] / v["launches"]
+        bpl = v["bytes"] / v["launches"]
+        gbs = bpl / (us * 1e-6) / 1e9 if us > 0 else 0.0
+        tr = traffic.get(k)
+        per[k] = {"us_per_launch": us, "launches": v["launches"], "bytes_per_launch": bpl, "GB/s": gbs,
+                  "frac": gbs / hbm, "share": v["ms"] / total_ms if total_ms else 0.0,
+                  "traffic": tr, "dram_GB/s": (tr / (us * 1e-6) / 1e9) if (tr and us > 0) else None}
+    dom = max(per, key=lambda k: per[k]["share"])
+    d = per[dom]
+    return {"bound": "hbm", "kernel": dom, "achieved": d["GB/s"], "peak": hbm, "unit": "GB/s", "frac": d["frac"],
+            "peak_kind": peak_kind, "traffic": d["traffic"], "bytes_per_launch": d["bytes_per_launch"],
+            "us_per_launch": d["us_per_launch"], "time_share": d["share"], "per_kernel": per}
+
+
+def e2e_measure(res, steps, world, dev, comm):
+    """inner_solve through the public API with pinned HOST inputs: every step
+    copies C, log X (local rows), the marginals and the dual in, and reads the
+    dual and the report scalars back.  The resident step's buffers are freed
+    first (the e2e call allocates its own device copies, like a user's)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_07156_b200.core import LogPlan, OtProblem, RowShardCost
     from paper_2603_07156_b200.inner_newton import inner_solve
     from paper_2603_07156_b200.semidual import DualState
-    from paper_2603_07156_b200.session import session_for
-    from paper_2603_07156_b200.sinkhorn import warm_start
+
+    n, m, ml = res.n, res.m, res.r1 - res.r0
+    C_pin = torch.empty((ml, n), dtype=torch.float64, pin_memory=True)
+    C_pin.copy_(res.cost_local[:, :n])
+    lx_pin = torch.empty((ml, n), dtype=torch.float64, pin_memory=True)
+    lx_pin.copy_(torch.from_numpy(np.log(res.pts.a[res.r0:res.r1]))[:, None]
+                 + torch.from_numpy(np.log(res.pts.b))[None, :])
+    lx_pin.clamp_(min=-1e6)
+    g_pin = res.g0[:n].cpu().pin_memory()
+    a, b = res.pts.a, res.pts.b
+    cfg = res.cfg
+    # free the resident step (its session, plans, CSR) before the e2e copies
+    for attr in ("out_plan", "X0", "bufs", "lp0"):
+        setattr(res, attr, None)
+    res.s.close()
+    res.s = None
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+    def one():
+        # a sharded host cost is wrapped like the device one: rows of this rank
+        cost = C_pin if world == 1 else RowShardCost(C_pin, res.r0, m)
+        hprob = OtProblem(cost, a, b)
+        gs, cand, rep = inner_solve(LogPlan(lx_pin), DualState(g_pin), hprob, cfg, mu_k=1e3, outer_k=0, comm=comm)
+        return np.asarray(gs.gamma).sum() + rep.objective + rep.kkt
+
+    one()                     # first call: context creation, pinned staging
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([el], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    return {"value": steps / el, "unit": UNIT, "h2d_bytes_per_step": int(8 * ml * n * 2 + 8 * (m + 2 * n)),
+            "d2h_bytes_per_step": int(8 * n + 8 * 16), "steps": steps,
+            "path": "inner_solve(LogPlan(pinned host log X), DualState(pinned host), OtProblem(pinned host C), "
+                    "max_inner=1): H2D of C, log X, marginals, dual; D2H of the dual and the report scalars"}
+
+
+def solve_measure(prob, pts, comm, world, warm):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2603_07156_b200.bregman_outer import ibsn_solve
+    from paper_2603_07156_b200.core import SolverConfig
+
+    full = SolverConfig(eta=pts.eta, kkt_tol=pts.kkt_tol)
+    if warm:
+        ibsn_solve(prob, full, comm=comm)   # session + CSR capacity growth
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    r = ibsn_solve(prob, full, comm=comm)
+    e1.record()
+    torch.cuda.synchronize()
+    sec = e0.elapsed_time(e1) / 1e3
+    return {"time_s": sec, "outer": r.outer_iters, "newton": r.newton_iters, "cg": r.cg_iters,
+            "warm_sweeps": r.warm_sweeps, "objective": r.objective, "kkt": r.kkt,
+            "newton_it_per_s": r.newton_iters / sec if sec > 0 else None,
+            "from": "device-resident C; ibsn_solve(OtProblem, SolverConfig(eta, kkt_tol)) to kkt < tol"}
+
+
+def secondary(idx, seed, dev, steps):
+    """Value + solve of a smaller config in the same process (N = 1)."""
+    import torch
+
+    res = Resident(idx, seed, dev, None, 1, 0)
+    ms, launches, rep, _ = timed_steps(res, steps, 3, 1, dev, dev.index)
+    roof = roofline(res, idx, steps)
+    out = {"config": config_dict(idx, res.pts), "value": steps / (ms / 1e3), "ms_per_step": ms / steps,
+           "cg_iters_per_step": rep.cg_iters[-1] if rep.cg_iters else 0,
+           "roofline": {k: roof[k] for k in ("kernel", "achieved", "frac", "traffic")},
+           "solve": solve_measure(res.prob, res.pts, None, 1, warm=True)}
+    res.s.close()
+    del res
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -220,170 +415,54 @@ def run_ours(args):
 
         comm = RowComm()
 
-    pts = instances.config_points(args.config, args.seed)
-    m, n = len(pts.a), len(pts.b)
-    # configs 4-5 (C is 8.6 / 20 GB): C built on the GPU, bit-identical to the
-    # host recipe (instances.device_cost), no m x n host array; those runs
-    # skip the CPU arm, the e2e line (unless --e2e-steps is given) and the solve
-    big = m * n >= 5e8
-    if big:
-        inst = instances.Instance(pts.name, None, pts.a, pts.b, pts.eta, pts.kkt_tol)
-        cost_dev = instances.device_cost(pts, dev, rows=None, ld=(n + 31) // 32 * 32)
-    else:
-        inst = pts.build()
-        cost_dev = torch.from_numpy(inst.cost).to(dev)
-    cfg = SolverConfig(eta=inst.eta, kkt_tol=inst.kkt_tol, max_inner=1)
-    prob = OtProblem(cost_dev, inst.a, inst.b)
-    s = session_for(prob, inst.eta, comm)
-    X0 = s.new_plan()
-    s.ops.init_plan(X0)
-    lp0 = LogPlan.from_padded(X0, n)
-    gst, _ = warm_start(lp0, prob, inst.eta, cfg.warm_tol, gamma0=torch.zeros(n, dtype=torch.float64, device=dev),
-                        comm=comm)
-    g0 = gst.gamma.clone()
-    out_plan = s.new_plan()
-    bufs = (s.new_vec(), s.new_vec())
-
-    def step():
-        return inner_solve(lp0, DualState(g0), prob, cfg, mu_k=1e3, outer_k=0, session=s, out_plan=out_plan,
-                           gamma_bufs=bufs)
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    nwarm = max(args.warmup, 3)
-    for _ in range(nwarm):
-        _, _, rep = step()
-    torch.cuda.synchronize()
-    l0 = s.launches()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
-        barrier()
-        torch.cuda.synchronize()
-        ev0.record()
-        for _ in range(args.steps):
-            _, _, rep = step()
-        ev1.record()
-        torch.cuda.synchronize()
-        barrier()
-    ms = ev0.elapsed_time(ev1)
-    launches = s.launches() - l0
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    res = Resident(args.config, args.seed, dev, comm, world, rank)
+    m, n = res.m, res.n
+    shard = [res.r0, res.r1]
+    ms, launches, rep, clocks = timed_steps(res, args.steps, args.warmup, world, dev, local)
     value = args.steps / (ms / 1e3)
+    geometry = res.s.info()
     nnz = rep.nnz[-1] if rep.nnz else 0
     cg_its = rep.cg_iters[-1] if rep.cg_iters else 0
-
-    # profiled pass (same steps) -> per-kernel durations for the roofline
-    s.prof_enable(True)
-    for _ in range(max(3, min(args.steps, 10))):
-        step()
-    prof = s.prof_read(reset=True)
-    s.prof_enable(False)
-    hbm, peak_kind, _ = peaks()
-    dom = max(prof, key=lambda k: prof[k]["ms"])
-    d = prof[dom]
-    per_launch_bytes = d["bytes"] / max(d["launches"], 1)
-    per_launch_ms = d["ms"] / max(d["launches"], 1)
-    achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9 if per_launch_ms > 0 else 0.0
-    total_ms = sum(v["ms"] for v in prof.values())
-    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "peak_kind": peak_kind, "traffic": None,
-            "bytes_per_launch": per_launch_bytes, "us_per_launch": per_launch_ms * 1e3,
-            "time_share": d["ms"] / total_ms if total_ms else None,
-            "per_kernel": {k: {"us_per_launch": 1e3 * v["ms"] / max(v["launches"], 1),
-                               "launches": v["launches"],
-                               "GB/s": (v["bytes"] / (v["ms"] * 1e-3) / 1e9) if v["ms"] else 0.0,
-                               "share": v["ms"] / total_ms if total_ms else 0.0}
-                           for k, v in prof.items() if v["launches"]}}
-    traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(traffic_file):
-        try:
-            tr = json.load(open(traffic_file)).get(f"cfg{args.config}", {}).get(dom)
-            roof["traffic"] = tr
-        except Exception:
-            pass
-
-    # end to end through the public API with pinned host buffers
-    m_loc = s.m_loc
-    e2e = None
-    if big and args.e2e_steps == E2E_DEFAULT:
-        args.e2e_steps = 0
-    host_cost = (inst.cost if inst.cost is not None else cost_dev.cpu().numpy()) if args.e2e_steps > 0 else None
-    C_pin = torch.from_numpy(np.ascontiguousarray(host_cost)).pin_memory() if host_cost is not None else None
-    e2e_steps = args.e2e_steps
-    if e2e_steps > 0:
-        lx_host = np.log(inst.a)[s.row_begin:s.row_end, None] + np.log(inst.b)[None, :]
-        lx_pin = torch.from_numpy(np.maximum(lx_host, -1e6)).pin_memory()
-        g_pin = g0[:n].cpu().pin_memory()
-    torch.cuda.synchronize()
-
-    if e2e_steps > 0:
-        def e2e_step():
-            # inputs from pinned host memory every step; the step's result read back
-            # to the host: the dual (n doubles) and the report's objective / kkt.
-            # The candidate plan stays in HBM, as ibsn_solve keeps it.
-            hprob = OtProblem(C_pin, inst.a, inst.b)
-            gs, cand, rep = inner_solve(LogPlan(lx_pin), DualState(g_pin), hprob, cfg, mu_k=1e3, outer_k=0, comm=comm)
-            return np.asarray(gs.gamma).sum() + rep.objective + rep.kkt
-
-        for _ in range(nwarm):      # first call pays context creation and pinned-buffer allocation
-            e2e_step()
-        torch.cuda.synchronize()
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            e2e_step()
-        torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
-        e2e = {"value": e2e_steps / e2e_s, "unit": "newton_it/s",
-               "h2d_bytes_per_step": int(8 * m_loc * n * 2 + 8 * (m + 2 * n)),
-               "d2h_bytes_per_step": int(8 * n + 8 * 16),
-               "path": "inner_solve(LogPlan(pinned host), DualState(pinned host), OtProblem(pinned host C), "
-                       "max_inner=1): H2D of C, log X, marginals, dual; D2H of the dual and the report scalars "
-                       "(the candidate plan stays in HBM, as in ibsn_solve)"}
+    roof = roofline(res, args.config, args.steps)
 
     solve = None
-    if not args.no_solve and not big:
-        from paper_2603_07156_b200.bregman_outer import ibsn_solve
+    if not args.no_solve:
+        solve = solve_measure(res.prob, res.pts, comm, world, warm=m * n < 5e8)
+    e2e = e2e_measure(res, args.e2e_steps, world, dev, comm) if args.e2e_steps > 0 else None
 
-        sprob = OtProblem(torch.from_numpy(inst.cost).to(dev), inst.a, inst.b)
-        full = SolverConfig(eta=inst.eta, kkt_tol=inst.kkt_tol)
-        ibsn_solve(sprob, full, comm=comm)   # warm (session + capacity growth)
-        torch.cuda.synchronize()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        res = ibsn_solve(sprob, full, comm=comm)
-        e1.record()
-        torch.cuda.synchronize()
-        solve = {"time_s": e0.elapsed_time(e1) / 1e3, "outer": res.outer_iters, "newton": res.newton_iters,
-                 "cg": res.cg_iters, "warm_sweeps": res.warm_sweeps, "objective": res.objective, "kkt": res.kkt,
-                 "newton_it_per_s": res.newton_iters / (e0.elapsed_time(e1) / 1e3)}
+    sec = {}
+    sec_list = args.secondary if args.secondary is not None else ("2,3" if args.config == DEFAULT_CONFIG else "")
+    if world == 1 and sec_list:
+        del res
+        torch.cuda.empty_cache()
+        for s_idx in [int(x) for x in sec_list.split(",") if x.strip()]:
+            sec[f"config{s_idx}"] = secondary(s_idx, args.seed, dev, 10)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu and not big:
-        cpu = cpu_baseline(inst, args.cpu_sample)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import cpu_step
+        from paper_2603_07156_b200 import instances
+
+        pts = instances.config_points(args.config, args.seed)
+        v, sample, kind = cpu_measure(args.config, pts, 1, 0, args.cpu_sample)
+        cpu = {"value": v, "unit": UNIT, "cores": cpu_step.blas_threads(), "kind": kind,
+               "sample": sample + " (BLAS threads as stated; numpy ufuncs and scipy sparse products are "
+                                  "single-threaded)"}
 
     if rank == 0:
+        from paper_2603_07156_b200.instances import config_points
+
+        pts = config_points(args.config, args.seed)
         line = {
-            "metric": "newton_inner_iterations_per_s", "value": value, "unit": "newton_it/s", "n_gpus": world,
-            "steps": args.steps, "warmup": nwarm, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(args.config, inst),
-                       "step": "inner_solve(max_inner=1, mu_k=1e3) from the outer-0 warm-started state",
-                       "l2": f"inputs larger than L2 (C + log X = {2 * 8 * m * n / 1e6:.0f} MB > 126 MB)",
-                       "nnz": nnz, "density": nnz / (m * n), "cg_iters_per_step": cg_its,
-                       "geometry": s.info()},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clocks.summary(), "solve": solve,
+            "config": config_dict(args.config, pts),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "solve": solve,
+            "details": {"nnz": nnz, "density": nnz / (m * n), "cg_iters_per_step": cg_its, "geometry": geometry,
+                        "row_shard": shard if world > 1 else None},
+            "secondary": sec or None,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -156,6 +156,9 @@ struct SparsifyIO {
   int nq;
   const double* gnorm;    // non-null: rho = (eta ||g||) / mn from this device scalar (no host round trip)
   double mn;
+  double* dense;          // non-null: P_rho written DENSE (local rows x ld, 0 where dropped) instead of
+                          // the row runs; may alias the P being streamed (each element is read before
+                          // its own thread overwrites it)
 };
 // With the bitmap index, a row's run holds column PAIRS (2l, 2l+1) with at
 // least one kept entry, 16 bytes each (the unkept one stored as 0.0), and
@@ -334,6 +337,45 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
       cnt = 1;
       ecnt = 1;
       myoff = 0;
+    }
+    if (io.dense != nullptr) {
+      // dense P_rho (hess_apply window kernels at high density): the same
+      // values as the runs, 0.0 where dropped, d accumulated in the same order
+      const double ai = __ldg(io.a + D.g.row0 + r);
+      double* drow = io.dense + (size_t)r * D.g.ld;
+      const Divider DK(ksum);
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        if (s < D.nsl) {
+          const int j = D.col(s, 0);
+          double v0, v1;
+          bool k0, k1;
+          if (fallback) {
+            k0 = j == jbest && P[2 * s] >= 0.0;
+            k1 = j + 1 == jbest && P[2 * s + 1] >= 0.0;
+            v0 = k0 ? 1.0 : 0.0;
+            v1 = k1 ? 1.0 : 0.0;
+          } else {
+            k0 = (keep >> (2 * s)) & 1u;
+            k1 = (keep >> (2 * s + 1)) & 1u;
+            double n0, n1;   // sparsify.py:109-110: kept / kept_sum (the anchor row unnormalised)
+            DK.pair(P[2 * s], P[2 * s + 1], n0, n1);
+            v0 = k0 ? (anc ? P[2 * s] : n0) : 0.0;
+            v1 = k1 ? (anc ? P[2 * s + 1] : n1) : 0.0;
+          }
+          if (j + 1 < D.c1) {
+            *reinterpret_cast<double2*>(drow + j) = make_double2(v0, v1);
+          } else if (j < D.c1) {
+            drow[j] = v0;
+          }
+          double2* a2 = D.acc2(0, s);
+          if (k0) a2->x += ai * v0;
+          if (k1) a2->y += ai * v1;
+        }
+      }
+      if (D.tid == 0 && D.cr == 0) kept += ecnt;
+      rowpar ^= 1;
+      continue;
     }
     // Contiguous row run: cluster rank 0 bump-allocates from its current
     // chunk (state replicated in all of its consumer threads) and shares

@@ -649,6 +649,45 @@ __global__ void k_bm_export(const uint4* __restrict__ bm, int nq, int m_loc, con
   }
 }
 
+// CSR export of a dense P_rho (window-cluster dense mode): a row's kept
+// entries are its nonzeros (kept values are > 0), except the anchor row,
+// stored whole like the reference's anchor_row (zeros included).
+__global__ void k_dense_rownnz(const double* __restrict__ Pr, int64_t ld, int m_loc, int n, int64_t anchor_local,
+                               int* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < m_loc; r += (gridDim.x * blockDim.x) >> 5) {
+    int k = 0;
+    if (r == anchor_local) {
+      k = n;
+    } else {
+      for (int j = lane; j < n; j += 32) k += Pr[(size_t)r * ld + j] != 0.0;
+      for (int o = 16; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+    }
+    if (lane == 0) cnt[r] = k;
+  }
+}
+
+__global__ void k_dense_export(const double* __restrict__ Pr, int64_t ld, int m_loc, int n, int64_t anchor_local,
+                               const int64_t* __restrict__ rowpre, int32_t* __restrict__ out_cols,
+                               double* __restrict__ out_vals) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < m_loc; r += (gridDim.x * blockDim.x) >> 5) {
+    int64_t o = rowpre[r];
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + lane;
+      const double v = j < n ? Pr[(size_t)r * ld + j] : 0.0;
+      const bool k = j < n && (r == anchor_local || v != 0.0);
+      const unsigned b = __ballot_sync(0xffffffffu, k);
+      if (k) {
+        out_cols[o + __popc(b & lt)] = j;
+        out_vals[o + __popc(b & lt)] = v;
+      }
+      o += __popc(b);
+    }
+  }
+}
+
 // Test hook for log_fast (common.cuh).
 __global__ void k_selftest_log(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

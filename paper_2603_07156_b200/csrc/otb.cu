@@ -114,9 +114,13 @@ const void* const kDenseFn[DK_COUNT][kMaxNS + 1] = {
   }
 const void* const kHvFn[kHvVariants] = HV_ROW(k_hv_grp);     // variant codes: sparse.cuh HvVar
 const void* const kCgFn[kHvVariants] = HV_ROW(k_cg_fused);
-const void* const kWcFn[kMaxNQ + 1] = {nullptr,           (const void*)k_hv_wc<1>, (const void*)k_hv_wc<2>,
-                                       (const void*)k_hv_wc<3>, (const void*)k_hv_wc<4>, (const void*)k_hv_wc<5>,
-                                       (const void*)k_hv_wc<6>, (const void*)k_hv_wc<7>, (const void*)k_hv_wc<8>};
+#define WC_ROW(D)                                                                                     \
+  {                                                                                                   \
+    nullptr, (const void*)k_hv_wc<1, D>, (const void*)k_hv_wc<2, D>, (const void*)k_hv_wc<3, D>,     \
+        (const void*)k_hv_wc<4, D>, (const void*)k_hv_wc<5, D>, (const void*)k_hv_wc<6, D>,           \
+        (const void*)k_hv_wc<7, D>, (const void*)k_hv_wc<8, D>                                        \
+  }
+const void* const kWcFn[2][kMaxNQ + 1] = {WC_ROW(false), WC_ROW(true)};   // [dense P_rho][NQ]
 int wc_stage_bytes(int nqw) {
   switch (nqw) {
     case 1: return WcGeo<1>::kStage;
@@ -200,6 +204,9 @@ struct otb_ctx {
   double* Pbuf = nullptr;    // P of the last eval (local rows x ld), streamed by sparsify
   unsigned long long* cg_trace = nullptr;   // OTB_CG_TRACE=1: phase stamps of the fused CG
   bool p_valid = false;
+  bool rho_dense = false;    // the last sparsify wrote P_rho dense into Pbuf (window-cluster hess_apply)
+  int dense_policy = -1;     // OTB_HV_DENSE: 0 never, 1 always, -1 by the last kept density
+  double last_density = 0.0; // kept entries / (m_loc n) of the last sparsify
   bool rowpre_valid = false;
   size_t hv_smem = 0;
   bool cg_fused = false;     // persistent cooperative CG available (1 rank, smem hv)
@@ -526,13 +533,24 @@ int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho
   const int kind = c->p_valid ? DK_SPARSP : DK_SPARSIFY;
   Geom geo = c->p_valid ? make_geom(c, DK_SPARSP, c->Pbuf, nullptr) : make_geom(c, DK_SPARSIFY, c->C, X);
   const bool bitmap = c->hv_mode == 2 || c->hv_mode == 3;   // hess_apply reads the bitmap, not the columns
+  // window-cluster hess_apply: dense P_rho (written over the stored P) when
+  // most pairs are kept — a fixed position per value instead of bitmap
+  // offsets; the products are bitwise the same (dropped entries are 0.0 and
+  // every thread sums the same columns in the same order)
+  const char* env_hd = std::getenv("OTB_HV_DENSE");   // read per call: an experiment / test knob
+  c->dense_policy = env_hd ? (std::atoi(env_hd) > 0 ? 1 : 0) : -1;
+  const bool dense = c->hv_mode == 3 && c->Pbuf != nullptr &&
+                     (c->dense_policy == 1 || (c->dense_policy < 0 && c->last_density >= kDenseRhoMin));
   SparsifyIO io{gamma, c->a, c->eta, rho, anchor_local, c->rowM, c->rowS, c->lse, bitmap ? nullptr : c->cols,
                 c->vals, c->cap,
                 c->row_start, c->row_len, &c->ds->alloc, &c->ds->nnzc, c->chunk, c->colpart, &c->ds->flags,
-                bitmap ? c->bm : nullptr, c->nq, gnorm_dev, (double)c->m_glob * (double)c->n};
+                bitmap ? c->bm : nullptr, c->nq, gnorm_dev, (double)c->m_glob * (double)c->n,
+                dense ? c->Pbuf : nullptr};
+  c->rho_dense = dense;
   cudaEvent_t e0 = nullptr;
   TRY(prof_begin(c, &e0));
   TRY(launch_dense(c, kind, geo, &io));
+  if (dense) c->p_valid = false;   // Pbuf now holds P_rho
   *rec = c->prof ? (int64_t)c->recs.size() : -1;
   TRY(prof_end(c, PC_SPARSIFY, e0, 0.0));
   // the row prefix (CSR export, nnz-balanced bounds) only where it is used
@@ -577,6 +595,7 @@ int sparsify_finish(otb_ctx* c, int64_t rec, bool* redo) {
   }
   c->nnz = nnz;
   c->nnz_glob = c->nranks > 1 ? (int64_t)c->hs->sp_glob[1] : nnz;
+  c->last_density = (double)nnz / std::max(1.0, (double)c->m_loc * (double)c->n);
   return OTB_OK;
 }
 
@@ -626,7 +645,8 @@ int run_hv(otb_ctx* c, const double* v_src, const double* r, const double* p_pre
   cudaEvent_t e0 = nullptr;
   if (c->hv_mode != 1) {
     HvArgs h{csr_view(c), c->a, n, c->hv_ng, v_src, r, p_prev, p_cur, update, st, c->colpart, c->bm, c->nq,
-             c->hv_win};
+             c->hv_win, c->ld};
+    if (c->hv_mode == 3 && c->rho_dense) h.A.vals = c->Pbuf;
     TRY(prof_begin(c, &e0));
     void* args[1] = {&h};
     if (c->hv_mode == 3) {
@@ -642,7 +662,7 @@ int run_hv(otb_ctx* c, const double* v_src, const double* r, const double* p_pre
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      CUDA_TRY(cudaLaunchKernelExC(&cfg, kWcFn[c->hv_var], args));
+      CUDA_TRY(cudaLaunchKernelExC(&cfg, kWcFn[c->rho_dense ? 1 : 0][c->hv_var], args));
     } else {
       CUDA_TRY(cudaLaunchKernel(kHvFn[c->hv_var], dim3(c->hv_grid), dim3(c->hv_threads), args, c->hv_smem,
                                 c->stream));
@@ -1105,12 +1125,15 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
       if (force_nq > 0 && nqw != force_nq) continue;
       const int W = (int)cdiv(n, 1024 * nqw);
       if (W < 2 || W > kWcMaxW) continue;
-      const void* fn = kWcFn[nqw];
+      const void* fn = kWcFn[0][nqw];
       const int stage = wc_stage_bytes(nqw);
       const int S = (int)std::min<int64_t>(4, (int64_t)(kMaxDynSmem - 8192 - 8192 * nqw) / (stage + 16));
       if (S < 2) continue;
       cudaError_t e = allow_max_smem(fn, device);
+      if (e == cudaSuccess) e = allow_max_smem(kWcFn[1][nqw], device);
       if (e == cudaSuccess && W > 8) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e == cudaSuccess && W > 8)
+        e = cudaFuncSetAttribute(kWcFn[1][nqw], cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       int nclusters = 0;
       if (e == cudaSuccess) {
         cudaLaunchConfig_t cfg = {};
@@ -1211,7 +1234,10 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   // P of the eval, so that sparsify streams one matrix and does no exp
   // (OTB_STORE_P=0: sparsify recomputes P from C and log X)
   const char* env_p = std::getenv("OTB_STORE_P");
-  if (st == OTB_OK && !(env_p && std::atoi(env_p) == 0)) st = dalloc(&c->Pbuf, (size_t)m_loc * ld);
+  if (st == OTB_OK && !(env_p && std::atoi(env_p) == 0)) {
+    st = dalloc(&c->Pbuf, (size_t)m_loc * ld);
+    if (st == OTB_OK) cudaMemset(c->Pbuf, 0, sizeof(double) * (size_t)m_loc * ld);   // padding columns stay 0
+  }
   const char* env_tr = std::getenv("OTB_CG_TRACE");
   if (st == OTB_OK && env_tr && std::atoi(env_tr) == 1) {
     const size_t cnt = (size_t)c->hv_grid * kCgTraceIters * 6;
@@ -1424,6 +1450,27 @@ int otb_sparsify(otb_ctx* c, const double* logX, const double* gamma, double rho
 int otb_csr_export(otb_ctx* c, int64_t* row_ptr, int32_t* cols, double* vals, double* d) {
   TRY(require_bound(c));
   const bool bitmap = c->hv_mode == 2 || c->hv_mode == 3;   // pair-layout runs, columns in the bitmap words
+  if (c->hv_mode == 3 && c->rho_dense) {   // dense P_rho: nonzeros per row (every entry of the anchor row)
+    const int64_t anchor_local = (c->anchor >= c->row0 && c->anchor < c->row1) ? c->anchor - c->row0 : -1;
+    if (!c->row_nnz) TRY(dalloc(&c->row_nnz, c->m_loc));
+    k_dense_rownnz<<<c->num_sms * 8, 256, 0, c->stream>>>(c->Pbuf, c->ld, (int)c->m_loc, (int)c->n, anchor_local,
+                                                           c->row_nnz);
+    LAUNCH_CHECK();
+    k_row_prefix<<<1, 1024, 0, c->stream>>>(c->row_nnz, (int)c->m_loc, c->rowpre);
+    LAUNCH_CHECK();
+    if (row_ptr)
+      CUDA_TRY(cudaMemcpyAsync(row_ptr, c->rowpre, sizeof(int64_t) * (c->m_loc + 1), cudaMemcpyDeviceToDevice,
+                               c->stream));
+    if (cols && vals) {
+      k_dense_export<<<c->num_sms * 8, 256, 0, c->stream>>>(c->Pbuf, c->ld, (int)c->m_loc, (int)c->n, anchor_local,
+                                                            c->rowpre, cols, vals);
+      LAUNCH_CHECK();
+    }
+    c->rowpre_valid = false;
+    if (d) CUDA_TRY(cudaMemcpyAsync(d, c->d, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return OTB_OK;
+  }
   if (!c->rowpre_valid && (row_ptr || (cols && vals))) {
     if (bitmap) {
       if (!c->row_nnz) TRY(dalloc(&c->row_nnz, c->m_loc));

@@ -783,6 +783,7 @@ struct HvArgs {
   const uint4* bm;         // bitmap index (NQ > 0)
   int nq;
   int nwin;                // window-cluster variant: CTAs per cluster
+  int64_t ld;              // window-cluster dense mode: row stride of the dense P_rho (A.vals)
 };
 
 // Standalone hess_apply partials (multi-rank CG iterations, otb_hess_apply).
@@ -852,6 +853,7 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_hv_grp(HvArgs h) {
 // re-read is an L2 hit; HBM sees each value once.  The ring holds only the
 // rows in flight (loads + dots); the exchange waits hold no stage.  Rows are
 // applied in order, partials summed in window order: deterministic.
+constexpr double kDenseRhoMin = 0.5;   // kept density above which sparsify writes P_rho dense (OTB_HV_DENSE)
 constexpr int kWcD = 4;                  // exchange lookahead (rows)                  // exchange lookahead (rows)                  // exchange lookahead (rows)                  // exchange lookahead (rows)                  // exchange lookahead (rows)                  // exchange lookahead (rows)
 constexpr int kWcX = 2 * kWcD + 2;       // exchange buffers (>= 2 D + 1: see the note in wc_consume)
 constexpr int kWcMaxW = 16;
@@ -877,9 +879,13 @@ __host__ __device__ inline size_t wc_smem_bytes(int nqw, int stage_bytes, int S)
   return (size_t)1024 * nqw * 8 + (size_t)S * stage_bytes + 2 * (size_t)S * 8;
 }
 
-template <int NQ>
+// DENSE: the rows are the dense P_rho of sparsify's dense mode (vals = its
+// base, row stride ld): the window is copied as is (no words), and a value's
+// position is its column.
+template <int NQ, bool DENSE>
 OTB_DEV void wc_produce(const Csr& A, const uint4* bm, const double* a, int rb, int re, int stride, int woff,
-                        bool last_window, unsigned char* ring, uint64_t* full, uint64_t* empty, int S) {
+                        bool last_window, unsigned char* ring, uint64_t* full, uint64_t* empty, int S,
+                        int64_t ld, int wcols) {
   using G = WcGeo<NQ>;
   const int lane = threadIdx.x & 31;
   int stage = 0;
@@ -890,12 +896,19 @@ OTB_DEV void wc_produce(const Csr& A, const uint4* bm, const double* a, int rb, 
     int cnt = 0, base = 0;
     double ar = 0.0;
     if (r < re) {
-      st = A.row_start[r];
-      const int fo = (woff > 0) ? 2 * (int)bm[(size_t)r * stride + woff].z : 0;
-      const int lo = last_window ? A.row_len[r] : 2 * (int)bm[(size_t)r * stride + woff + G::WW].z;
-      src = st + fo;                     // even: runs start on 8-entry boundaries, offsets count pairs
-      cnt = max(lo - fo, 0);
-      base = -fo;
+      if constexpr (DENSE) {
+        st = (long long)r * ld + 64LL * woff;   // window start (column 64 woff)
+        src = st;
+        cnt = wcols;
+        base = 0;
+      } else {
+        st = A.row_start[r];
+        const int fo = (woff > 0) ? 2 * (int)bm[(size_t)r * stride + woff].z : 0;
+        const int lo = last_window ? A.row_len[r] : 2 * (int)bm[(size_t)r * stride + woff + G::WW].z;
+        src = st + fo;                     // even: runs start on 8-entry boundaries, offsets count pairs
+        cnt = max(lo - fo, 0);
+        base = -fo;
+      }
       ar = a[A.row0 + r];
     }
     const int rows = min(32, re - g0);
@@ -913,9 +926,9 @@ OTB_DEV void wc_produce(const Csr& A, const uint4* bm, const double* a, int rb, 
         h->st = kst;
         h->ar = kar;
         h->base = kbase;
-        mbar_arrive_expect_tx(&full[stage], (uint32_t)kcnt * 8u + (uint32_t)G::WW * 16u);
+        mbar_arrive_expect_tx(&full[stage], (uint32_t)kcnt * 8u + (DENSE ? 0u : (uint32_t)G::WW * 16u));
         if (kcnt > 0) bulk_g2s(vdst, A.vals + ksrc, (uint32_t)kcnt * 8u, &full[stage]);
-        bulk_g2s(sp, bm + (size_t)(g0 + k) * stride + woff, (uint32_t)G::WW * 16u, &full[stage]);
+        if (!DENSE) bulk_g2s(sp, bm + (size_t)(g0 + k) * stride + woff, (uint32_t)G::WW * 16u, &full[stage]);
       }
       if (++stage == S) {
         stage = 0;
@@ -930,10 +943,12 @@ OTB_DEV void wc_produce(const Csr& A, const uint4* bm, const double* a, int rb, 
 // >= k-D) has received rows <= k-2D-1... a sender of row k reuses buffer
 // k % X, last used for row k-X; with X >= 2D+1 every CTA has consumed row k-X
 // before any peer can send row k.
-template <int NQ>
+template <int NQ, bool DENSE>
 OTB_DEV void wc_consume(int cnt, const double* __restrict__ vals, const double* vsm, double (&acc)[2 * NQ],
                         unsigned char* ring, uint64_t* full, uint64_t* empty, int S, double* xbuf, uint64_t* xbar,
-                        int W, int cr, double* slots, WcHdr* hring) {
+                        int W, int cr, double* slots, WcHdr* hring, int lim) {
+  // lim (DENSE): columns of this window inside the matrix (the last window's
+  // tail is neither staged nor loaded)
   using G = WcGeo<NQ>;
   constexpr int D = kWcD;
   constexpr int NI = (NQ + 1) / 2;   // uint32 words of packed uint16 pair positions per row
@@ -960,9 +975,13 @@ OTB_DEV void wc_consume(int cnt, const double* __restrict__ vals, const double* 
         const double* vr = vals + hu.st;
 #pragma unroll
         for (int t = 0; t < NQ; ++t) {
-          const uint32_t p = (pidx[j][t >> 1] >> (16 * (t & 1))) & 0xffffu;
           double2 x = make_double2(0.0, 0.0);
-          if (p != 0xffffu) x = __ldg(reinterpret_cast<const double2*>(vr + 2 * (int)p));
+          if constexpr (DENSE) {
+            if (bm_col<16>(t, 0) < lim) x = __ldg(reinterpret_cast<const double2*>(vr + bm_col<16>(t, 0)));
+          } else {
+            const uint32_t p = (pidx[j][t >> 1] >> (16 * (t & 1))) & 0xffffu;
+            if (p != 0xffffu) x = __ldg(reinterpret_cast<const double2*>(vr + 2 * (int)p));
+          }
           e[2 * t] = x.x;
           e[2 * t + 1] = x.y;
         }
@@ -978,8 +997,18 @@ OTB_DEV void wc_consume(int cnt, const double* __restrict__ vals, const double* 
         double d0 = 0.0, d1 = 0.0;
 #pragma unroll
         for (int i = 0; i < NI; ++i) pidx[j][i] = 0xffffffffu;
+        if constexpr (DENSE) {
 #pragma unroll
-        for (int t = 0; t < NQ; ++t) {
+          for (int t = 0; t < NQ; ++t) {
+            const int jl = bm_col<16>(t, 0);
+            const double2 x = jl < lim ? *reinterpret_cast<const double2*>(sv + jl) : make_double2(0.0, 0.0);
+            const double2 vv = *reinterpret_cast<const double2*>(vsm + jl);
+            d0 = fma(x.x, vv.x, d0);
+            d1 = fma(x.y, vv.y, d1);
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < (DENSE ? 0 : NQ); ++t) {
           const uint4 wd = words[warp + 16 * t];
           const unsigned pm = bm_pairs(wd);
           const int P = (int)wd.z + __popc(pm & lt);   // pair index in the row run
@@ -1024,7 +1053,7 @@ OTB_DEV void wc_consume(int cnt, const double* __restrict__ vals, const double* 
   }
 }
 
-template <int NQ>
+template <int NQ, bool DENSE>
 __global__ void __launch_bounds__(kStThreads, 1) k_hv_wc(HvArgs h) {
   using G = WcGeo<NQ>;
   extern __shared__ __align__(16) unsigned char wsm[];
@@ -1061,7 +1090,8 @@ __global__ void __launch_bounds__(kStThreads, 1) k_hv_wc(HvArgs h) {
     int rb, re;
     cta_rows(h.A, cid, ncl, rb, re);
     if (threadIdx.x >= kStConsumers) {
-      wc_produce<NQ>(h.A, h.bm, h.a, rb, re, h.nq, G::WW * cr, cr + 1 == W, ring, full, empty, S);
+      wc_produce<NQ, DENSE>(h.A, h.bm, h.a, rb, re, h.nq, G::WW * cr, cr + 1 == W, ring, full, empty, S, h.ld,
+                            min(1024 * NQ, (int)(h.ld - 64LL * G::WW * cr)));
     } else {
       // the window of v in shared memory (registers hold the accumulator and
       // the values in flight); p = r + beta p by the column's owner (krylov.py:83)
@@ -1083,7 +1113,8 @@ __global__ void __launch_bounds__(kStThreads, 1) k_hv_wc(HvArgs h) {
         ar[i] = 0.0;
       }
       bar_sync(1, kStConsumers);
-      wc_consume<NQ>(re - rb, h.A.vals, vsm, ar, ring, full, empty, S, xbuf, xbar, W, cr, slots, hring);
+      wc_consume<NQ, DENSE>(re - rb, h.A.vals, vsm, ar, ring, full, empty, S, xbuf, xbar, W, cr, slots, hring,
+                            min(1024 * NQ, (int)(h.ld - 64LL * G::WW * cr)));
       double* dst = h.colpart + (size_t)cid * n;
 #pragma unroll
       for (int i = 0; i < 2 * NQ; ++i) {

@@ -36,3 +36,22 @@ def test_our_arm_needs_a_gpu():
     res = _run(["--steps", "1", "--warmup", "0", "--no-cpu", "--no-solve"])
     assert res.returncode != 0
     assert "CUDA" in (res.stderr + res.stdout) or "GPU" in (res.stderr + res.stdout)
+
+
+def test_cpu_row_sample_step_runs_the_reference():
+    """The configs-4/5 CPU baseline: a row sample of one step through the
+    reference's own functions (otibsn), K CG products exactly."""
+    from oracle import cpu_step
+    from paper_2603_07156_b200 import instances as I
+
+    pts = I.uniform2d_points(3000, 2500, 1)
+
+    def rows(k):
+        return I.normalise(I.sq_dist(pts.x[:k], pts.y))
+
+    st = cpu_step.RowSampleStep(rows, pts.a, pts.b, pts.eta, 3000, 5, 40)
+    st.step()
+    assert st.kind in ("reference", "port")
+    if os.path.isdir("/root/reference/pkg/src"):
+        assert st.kind == "reference"
+    assert "rows 0..40 of 3000" in st.describe(1, 1.0)

@@ -697,3 +697,44 @@ def test_cluster_paths_are_deterministic(cuda, m, n):
         res.append((np.asarray(gs.gamma).copy(), rep.cg_iters_total, rep.objective, rep.bregman))
     assert np.array_equal(res[0][0].view(np.uint64), res[1][0].view(np.uint64))
     assert res[0][1:] == res[1][1:]
+
+
+@pytest.mark.parametrize("m,n", [(120, 16400), (70, 50001), (33, 9000)])
+def test_dense_rho_equals_bitmap_rho(cuda, monkeypatch, m, n):
+    """Window-cluster hess_apply over a DENSE P_rho (sparsify's dense mode,
+    OTB_HV_DENSE=1) and over the bitmap-indexed pair runs (OTB_HV_DENSE=0):
+    the same CSR, H v bitwise equal (dropped entries are 0.0 and every thread
+    sums the same columns in the same order), and a 2-step inner solve gives
+    the same bits.  (9000 columns forces the window clusters with OTB_HV_WC.)"""
+    P = _api()
+    from paper_2603_07156_b200 import instances
+    from paper_2603_07156_b200.inner_newton import inner_solve
+
+    monkeypatch.setenv("OTB_HV_WC", "1")
+    C, a, b = instances.small_uniform(m, n, 9 + n)
+    lx = O.product_log_plan(a, b)
+    rng = np.random.default_rng(n)
+    gam = rng.standard_normal(n) * 1e-3
+    v = rng.standard_normal(n)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("OTB_HV_DENSE", mode)
+        prob = P.OtProblem(C, a, b)
+        eta = 1e-2
+        cache = P.compute_p(P.LogPlan(lx), P.DualState(gam), prob, eta)
+        rho = eta * float(np.linalg.norm(P.semidual_gradient(cache, prob))) / (m * n)
+        sp = P.sparsify_p(cache, rho, int(np.argmax(a)))
+        op = P.SparseHessianOp(sp)
+        hv = op.matvec(v)
+        info = cache.session.info()
+        cfg = P.SolverConfig(eta=eta, kkt_tol=1e-9, max_inner=2)
+        gs, cand, rep = inner_solve(P.LogPlan(lx), P.DualState(np.zeros(n)), P.OtProblem(C, a, b), cfg,
+                                    mu_k=1e-3, outer_k=0)
+        out[mode] = (sp, hv, np.asarray(gs.gamma).copy(), rep.cg_iters_total, rep.objective, info)
+    assert out["0"][5]["hv_mode"] == 3 and out["1"][5]["hv_mode"] == 3
+    s0, s1 = out["0"][0], out["1"][0]
+    assert np.array_equal(s0.row_offsets, s1.row_offsets) and np.array_equal(s0.col_indices, s1.col_indices)
+    assert np.array_equal(s0.values, s1.values) and np.array_equal(s0.anchor_row, s1.anchor_row)
+    assert np.array_equal(out["0"][1].view(np.uint64), out["1"][1].view(np.uint64))
+    assert np.array_equal(out["0"][2].view(np.uint64), out["1"][2].view(np.uint64))
+    assert out["0"][3:5] == out["1"][3:5]
