@@ -249,6 +249,53 @@ def conjugate_gradient(apply_h, shift, rhs, rel_tol=1e-10, max_iters=None):
     return x, k, float(np.sqrt(rr))
 
 
+def jacobi_inverse(h: SparseHessian, shift):
+    """Extension (no reference counterpart; the reference's CG is plain):
+    1 / diag(H_rho + shift I), diag(H_rho)_j = (d_j - sum_i a_i P_rho[i,j]^2)/eta."""
+    p = h.rows.dense()
+    q = (p * p).T @ h.a
+    dj = (h.d - q) / h.eta + shift
+    return np.where(dj > 0.0, 1.0 / np.where(dj > 0.0, dj, 1.0), 1.0)
+
+
+def preconditioned_cg(apply_h, shift, rhs, minv, rel_tol=1e-10, max_iters=None):
+    """Jacobi PCG on (H + shift I) x = rhs from x0 = 0: z = minv r, the
+    same stopping test on ||r|| as krylov.py:79-82 (extension)."""
+    rhs = np.asarray(rhs, dtype=np.float64)
+    n = rhs.size
+    cap = 2 * n if max_iters is None else max_iters
+    bnorm = float(np.linalg.norm(rhs))
+    x = np.zeros(n)
+    if bnorm == 0.0:
+        return x, 0, 0.0
+    r = rhs.copy()
+    z = minv * r
+    d = z.copy()
+    rz = float(r @ z)
+    rr = float(r @ r)
+    goal = rel_tol * bnorm
+    k = 0
+    for _ in range(cap):
+        hd = apply_h(d) + shift * d
+        curv = float(d @ hd)
+        if curv <= 0.0:
+            if math.sqrt(rr) <= goal:
+                break
+            raise OracleError("NotPositiveDefinite", f"curvature {curv:.3g}")
+        alpha = rz / curv
+        x += alpha * d
+        r -= alpha * hd
+        k += 1
+        rr = float(r @ r)
+        if math.sqrt(rr) <= goal:
+            break
+        z = minv * r
+        rz_new = float(r @ z)
+        d = z + (rz_new / rz) * d
+        rz = rz_new
+    return x, k, float(np.sqrt(rr))
+
+
 # --------------------------------------------------------------------------
 # feasibility  (feasibility.py)
 # --------------------------------------------------------------------------

@@ -70,6 +70,7 @@ SIGNATURES = {
     "otb_group_destroy": (C.c_int, [vp]),
     "otb_group_abort": (C.c_int, [vp]),
     "otb_attach_group": (C.c_int, [vp, vp, C.c_int]),
+    "otb_set_cg_precond": (C.c_int, [vp, C.c_int]),
     "otb_bind": (C.c_int, [vp, vp, vp, vp, vp, vp, dbl, i64, dbl, dbl, dbl]),
     "otb_eval": (C.c_int, [vp, vp, vp, vp, vp, C.POINTER(EvalOut)]),
     "otb_sparsify": (C.c_int, [vp, vp, vp, dbl, C.POINTER(i64)]),

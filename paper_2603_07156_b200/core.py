@@ -126,6 +126,10 @@ class SolverConfig:
     armijo_beta: float = 0.8
     seed: int = 0
     log_inner_kkt: bool = False
+    # extension (not in the reference, which runs plain CG): None = plain CG
+    # (krylov.py, the parity default) or "jacobi" = Jacobi-preconditioned CG
+    # on the same Newton systems with the same stopping test
+    cg_preconditioner: str | None = None
 
     def __post_init__(self):
         for name in ("eta", "mu0", "mu_floor", "warm_tol", "kkt_tol", "cg_rel_tol"):
@@ -137,6 +141,8 @@ class SolverConfig:
         for name in ("max_outer", "max_inner"):
             if getattr(self, name) < 1:
                 raise ValueError(f"{name} must be at least 1")
+        if self.cg_preconditioner not in (None, "jacobi"):
+            raise ValueError("cg_preconditioner must be None or 'jacobi'")
 
 
 class LogPlan:

@@ -156,6 +156,7 @@ struct SparsifyIO {
   int nq;
   const double* gnorm;    // non-null: rho = (eta ||g||) / mn from this device scalar (no host round trip)
   double mn;
+  double* colpart2;       // non-null (Jacobi PCG): [ncl][n] partial of q = (P_rho o P_rho)^T a, accumulator 1
   double* dense;          // non-null: P_rho written DENSE (local rows x ld, 0 where dropped) instead of
                           // the row runs; may alias the P being streamed (each element is read before
                           // its own thread overwrites it)
@@ -371,6 +372,11 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
           double2* a2 = D.acc2(0, s);
           if (k0) a2->x += ai * v0;
           if (k1) a2->y += ai * v1;
+          if (io.colpart2 != nullptr) {   // Jacobi diagonal of P_rho^T diag(a) P_rho
+            double2* q2 = D.acc2(1, s);
+            if (k0) q2->x += ai * (v0 * v0);
+            if (k1) q2->y += ai * (v1 * v1);
+          }
         }
       }
       if (D.tid == 0 && D.cr == 0) kept += ecnt;
@@ -424,6 +430,11 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
             double2* a2 = D.acc2(0, k >> 1);
             if (k & 1) a2->y += ai * 1.0;
             else a2->x += ai * 1.0;
+            if (io.colpart2 != nullptr) {
+              double2* q2 = D.acc2(1, k >> 1);
+              if (k & 1) q2->y += ai * (1.0 * 1.0);
+              else q2->x += ai * (1.0 * 1.0);
+            }
           }
         }
         if (io.bm != nullptr && D.lane == 0) {
@@ -461,6 +472,11 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
                 *reinterpret_cast<double2*>(io.vals + wbase + 2 * off) = make_double2(v0, v1);
                 if (k0) a2->x += ai * v0;
                 if (k1) a2->y += ai * v1;
+                if (io.colpart2 != nullptr) {
+                  double2* q2 = D.acc2(1, s);
+                  if (k0) q2->x += ai * (v0 * v0);
+                  if (k1) q2->y += ai * (v1 * v1);
+                }
               }
               continue;
             }
@@ -470,12 +486,14 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
               if (io.cols != nullptr) io.cols[wbase + off] = (uint16_t)j;
               io.vals[wbase + off] = v;
               a2->x += ai * v;
+              if (io.colpart2 != nullptr) D.acc2(1, s)->x += ai * (v * v);
             }
             if (k1) {
               const double v = anc ? P[2 * s + 1] : DK(P[2 * s + 1]);
               if (io.cols != nullptr) io.cols[wbase + off + k0] = (uint16_t)(j + 1);
               io.vals[wbase + off + k0] = v;
               a2->y += ai * v;
+              if (io.colpart2 != nullptr) D.acc2(1, s)->y += ai * (v * v);
             }
           }
         }
@@ -491,6 +509,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
   if (D.tid == 0 && D.cr == 0 && kept) atomicAdd(io.nnzc, kept);
   bar_sync(1, D.g.nt);
   D.store_acc(0, io.colpart + (size_t)D.cid * D.g.n);
+  if (io.colpart2 != nullptr) D.store_acc(1, io.colpart2 + (size_t)D.cid * D.g.n);
   D.finish();
 }
 

@@ -207,6 +207,8 @@ struct otb_ctx {
   bool rho_dense = false;    // the last sparsify wrote P_rho dense into Pbuf (window-cluster hess_apply)
   int dense_policy = -1;     // OTB_HV_DENSE: 0 never, 1 always, -1 by the last kept density
   double last_density = 0.0; // kept entries / (m_loc n) of the last sparsify
+  int precond = 0;           // CG preconditioner: 0 none (the reference's plain CG), 1 Jacobi
+  double *jq = nullptr, *minv = nullptr, *zv = nullptr, *colpart2 = nullptr;   // PCG vectors
   bool rowpre_valid = false;
   size_t hv_smem = 0;
   bool cg_fused = false;     // persistent cooperative CG available (1 rank, smem hv)
@@ -295,9 +297,14 @@ cudaError_t allow_max_smem(const void* fn, int device) {
   return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
 }
 
+// Jacobi PCG: sparsify also accumulates q = (P_rho o P_rho)^T a (accumulator 1)
+int nacc_of(const otb_ctx* c, int kind) {
+  return ((kind == DK_SPARSIFY || kind == DK_SPARSP) && c->precond) ? 2 : kNacc[kind];
+}
+
 size_t dense_smem(const otb_ctx* c, int kind, int nstage) {
   const size_t slice = 2 * (size_t)c->nt;
-  const size_t dbl = (size_t)nstage * kNmat[kind] * slice + (size_t)kNacc[kind] * c->ns * slice + 2 * kMaxWarps * 4 + kXb * 8 * 4;
+  const size_t dbl = (size_t)nstage * kNmat[kind] * slice + (size_t)nacc_of(c, kind) * c->ns * slice + 2 * kMaxWarps * 4 + kXb * 8 * 4;
   return dbl * 8 + (2 * (size_t)nstage + kXb) * 8 + 64 * 4;
 }
 
@@ -314,7 +321,7 @@ Geom make_geom(const otb_ctx* c, int kind, const double* m0, const double* m1) {
   g.cl = c->cl;
   g.colw = c->colw;
   g.nstage = c->nstage[kind];
-  g.nacc = kNacc[kind];
+  g.nacc = nacc_of(c, kind);
   return g;
 }
 
@@ -545,7 +552,7 @@ int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho
                 c->vals, c->cap,
                 c->row_start, c->row_len, &c->ds->alloc, &c->ds->nnzc, c->chunk, c->colpart, &c->ds->flags,
                 bitmap ? c->bm : nullptr, c->nq, gnorm_dev, (double)c->m_glob * (double)c->n,
-                dense ? c->Pbuf : nullptr};
+                c->precond ? c->colpart2 : nullptr, dense ? c->Pbuf : nullptr};
   c->rho_dense = dense;
   cudaEvent_t e0 = nullptr;
   TRY(prof_begin(c, &e0));
@@ -564,6 +571,12 @@ int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho
     LAUNCH_CHECK();
   }
   c->rowpre_valid = !bitmap;
+  if (c->precond) {   // q = (P_rho o P_rho)^T a for the Jacobi diagonal, summed over ranks
+    k_colreduce<<<c->col32, 256, 0, c->stream>>>(c->colpart2, c->ncl, n, c->jq, nullptr, 0, 0, 0,
+                                                   &c->ds->cnt[CNT_COLRED], ColPost{-1, nullptr, nullptr, {nullptr, nullptr}});
+    LAUNCH_CHECK();
+    TRY(allreduce(c, c->jq, (size_t)n, kNcclSum));
+  }
   if (c->nranks == 1) {   // d = column sums, written by the reduction itself
     TRY(colreduce(c, c->ncl, nullptr, 0, 0, 0, ColPost{POST_COPY, c->b, c->d, {nullptr, nullptr}}));
     return OTB_OK;
@@ -705,13 +718,15 @@ int cg_iteration(otb_ctx* c, int64_t k, double* x) {
   double* pc = c->cg_p[k & 1];
   double* pp = c->cg_p[(k + 1) & 1];
   HvResult hr;
-  TRY(run_hv(c, pc, c->cg_r, pp, pc, k > 0 ? 1 : 0, c->cg, &hr));
+  // p = r + beta p (plain CG) or z + beta p (PCG) inside the hess_apply launch
+  TRY(run_hv(c, pc, c->precond ? c->zv : c->cg_r, pp, pc, k > 0 ? 1 : 0, c->cg, &hr));
   cudaEvent_t e0 = nullptr;
   TRY(prof_begin(c, &e0));
   CgApArgs a{n, hr.colpart, hr.nparts, hr.yatomic, hr.ysum, c->d, pc, c->eta, c->cg_ap, c->cg, c->bpart};
   k_cg_ap<<<c->col32, 256, 0, c->stream>>>(a);
   LAUNCH_CHECK();
-  k_cg_update<<<c->colgrid, 256, 0, c->stream>>>(n, x, c->cg_r, pc, c->cg_ap, c->cg, c->bpart);
+  k_cg_update<<<c->colgrid, 256, 0, c->stream>>>(n, x, c->cg_r, pc, c->cg_ap, c->cg, c->bpart,
+                                                  c->precond ? c->minv : nullptr, c->precond ? c->zv : nullptr);
   LAUNCH_CHECK();
   TRY(prof_end(c, PC_CGVEC, e0, 8.0 * 9 * n));
   return OTB_OK;
@@ -764,14 +779,16 @@ int cg_finish(otb_ctx* c, int64_t rec, otb_cg_out* out) {
 
 int do_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t max_iters, double* x, otb_cg_out* out) {
   const int n = (int)c->n;
-  if (c->cg_fused) {
+  if (c->cg_fused && !c->precond) {
     int64_t rec = -1;
     TRY(cg_fused_launch(c, shift, rhs, rel_tol, max_iters, x, &rec));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     return cg_finish(c, rec, out);
   }
+  const PcgInit pc = c->precond ? PcgInit{c->d, c->jq, c->eta, c->minv, c->zv}
+                                : PcgInit{nullptr, nullptr, 1.0, nullptr, nullptr};
   k_cg_init<<<c->colgrid, 256, 0, c->stream>>>(n, rhs, x, c->cg_r, c->cg_p[0], c->cg, c->bpart, shift, rel_tol,
-                                               (long long)max_iters);
+                                               (long long)max_iters, nullptr, nullptr, nullptr, pc);
   LAUNCH_CHECK();
   CUDA_TRY(cudaMemcpyAsync(c->hcg, c->cg, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -1037,9 +1054,14 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   if (env_cps) per_sm = std::max(1, std::min(4, std::atoi(env_cps)));
   c->ncl = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)(sms * per_sm) / cl, c->m_loc));
   c->grid = c->ncl * cl;
+  // ring depth: 8 stages unless OTB_DENSE_NSTAGE caps it (a shallower ring
+  // leaves more of the SM's 256 KB to L1, where the CTA's window of gamma is
+  // re-read every row)
+  const char* env_ns = std::getenv("OTB_DENSE_NSTAGE");
+  const int max_stage = env_ns ? std::max(2, std::min(8, std::atoi(env_ns))) : 8;
   for (int k = 0; k < DK_COUNT; ++k) {
     const size_t budget = kMaxDynSmem / per_sm - kStaticSmem[k] - 1024;
-    int st = 8;
+    int st = max_stage;
     while (st > 2 && dense_smem(c, k, st) > budget) --st;
     c->nstage[k] = st;
     c->smem[k] = dense_smem(c, k, st);
@@ -1048,6 +1070,10 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
       return fail(OTB_ERR_ARG, "dense geometry does not fit shared memory");
     }
     cudaError_t e = allow_max_smem(kDenseFn[k][c->ns], device);
+    if (e == cudaSuccess && env_ns) {   // carve only what the ring needs: the rest is L1
+      const int pct = (int)std::min<int64_t>(100, cdiv(100 * (int64_t)(c->smem[k] + kStaticSmem[k] + 1024), 233472));
+      e = cudaFuncSetAttribute(kDenseFn[k][c->ns], cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    }
     if (e != cudaSuccess) {
       delete c;
       return fail(OTB_ERR_CUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
@@ -1299,7 +1325,8 @@ int otb_destroy(otb_ctx* c) {
                   (void*)c->cg_ap, (void*)c->cg_y, (void*)c->gtrial, (void*)c->yv, (void*)c->ec, (void*)c->Mloc,
                   (void*)c->Mglob, (void*)c->Sloc, (void*)c->row_start, (void*)c->rowpre, (void*)c->row_len, (void*)c->row_nnz,
                   (void*)c->cols, (void*)c->vals, (void*)c->ds, (void*)c->cg, (void*)c->scal, (void*)c->cta_rb,
-                  (void*)c->bm, (void*)c->Pbuf, (void*)c->cg_trace, (void*)c->lg_tmp})
+                  (void*)c->bm, (void*)c->Pbuf, (void*)c->cg_trace, (void*)c->lg_tmp, (void*)c->jq,
+                  (void*)c->minv, (void*)c->zv, (void*)c->colpart2})
     if (p) cudaFree(p);
   if (c->hs) cudaFreeHost(c->hs);
   if (c->hcg) cudaFreeHost(c->hcg);
@@ -1346,6 +1373,31 @@ int otb_attach_nccl(otb_ctx* c, const char* nccl_path, const void* id128, int nr
   c->nranks = nranks;
   c->rank = rank;
   c->cg_fused = false;   // the persistent CG has no H v all-reduce (krylov.py:68-84 needs the global H v)
+  c->have_eval = false;
+  return OTB_OK;
+}
+
+int otb_set_cg_precond(otb_ctx* c, int kind) {
+  if (!c) return fail(OTB_ERR_ARG, "null context");
+  if (kind != 0 && kind != 1) return fail(OTB_ERR_ARG, "preconditioner kind must be 0 (none) or 1 (Jacobi)");
+  if (kind == c->precond) return OTB_OK;
+  if (kind == 1 && !c->jq) {
+    const size_t nv = (size_t)rup(c->n, 2) + 16;
+    TRY(dalloc(&c->jq, nv));
+    TRY(dalloc(&c->minv, nv));
+    TRY(dalloc(&c->zv, nv));
+    TRY(dalloc(&c->colpart2, (size_t)c->ncl * c->n));
+  }
+  c->precond = kind;
+  // the sparsify passes carry a second accumulator: re-size their rings
+  for (int k : {(int)DK_SPARSIFY, (int)DK_SPARSP}) {
+    const size_t budget = kMaxDynSmem - kStaticSmem[k] - 1024;
+    int st = 8;
+    while (st > 2 && dense_smem(c, k, st) > budget) --st;
+    if (dense_smem(c, k, st) > budget) return fail(OTB_ERR_ARG, "PCG accumulator does not fit shared memory");
+    c->nstage[k] = st;
+    c->smem[k] = dense_smem(c, k, st);
+  }
   c->have_eval = false;
   return OTB_OK;
 }
@@ -1634,7 +1686,7 @@ int otb_newton_step(otb_ctx* c, const double* logX, const double* gamma_in, doub
   int64_t trials = 0;
   // trials go straight into gamma_out unless it aliases gamma_in (backtracking re-reads gamma_in)
   double* trial = (gamma_out != gamma_in) ? gamma_out : c->gtrial;
-  if (c->cg_fused) {
+  if (c->cg_fused && !c->precond) {
     bool stepped = false;
     TRY(newton_fused(c, logX, gamma_in, p, false, -1.0, &v0, &g0, &rho, &cgo, &slope, &t, &trials, &stepped,
                      trial));
@@ -1683,7 +1735,7 @@ int otb_inner_iteration(otb_ctx* c, const double* logX, double* gamma_in, double
     CUDA_TRY(cudaMemcpyAsync(gamma_in, gamma_src, sizeof(double) * c->n, cudaMemcpyDeviceToDevice, c->stream));
   out->stepped = 0;
   out->tested = 0;
-  if (eval_first && c->cg_fused && p && p->rho_override < 0.0) {
+  if (eval_first && c->cg_fused && !c->precond && p && p->rho_override < 0.0) {
     // inner_newton.py:196 + the first step without a synchronisation in
     // between: the eval is launched and its scalars kept on the device
     TRY(eval_launch(c, logX, gamma_in, true));   // its L, ||g||, flag also kept in ds->ev0

@@ -42,8 +42,9 @@ enum CgStatus { CG_RUN = 0, CG_DONE = 1, CG_NOTPD = 2, CG_MAXIT = 3, CG_INCONSIS
 struct CgState {
   double rs, curv, alpha, beta, target, bnorm, shift, res;
   long long iters, max_iters;
-  int status, pad;
+  int status, precond;     // precond: Jacobi PCG (z = r / diag(H_rho + shift I)), else plain CG
   unsigned int cnt[4];
+  double rz;               // PCG: r . z
 };
 
 constexpr int kCsrAlign = 8;   // row runs start on 8-entry boundaries
@@ -1227,7 +1228,7 @@ __global__ void __launch_bounds__(256) k_cg_ap(CgApArgs c) {
           s->status = (sqrt(s->rs) <= s->target) ? CG_DONE : CG_NOTPD;
           s->res = sqrt(s->rs);
         } else {
-          s->alpha = s->rs / curv;
+          s->alpha = (s->precond ? s->rz : s->rs) / curv;
         }
       }
     }
@@ -1235,33 +1236,47 @@ __global__ void __launch_bounds__(256) k_cg_ap(CgApArgs c) {
 }
 
 // krylov.py:76-84: x += alpha p, r -= alpha ap, convergence test, beta.
+// PCG (minv != nullptr): z = minv r, beta = (r.z)_new / (r.z); the stopping
+// test stays on ||r|| (krylov.py:79-82), so plain and preconditioned CG
+// stop at the same residual.
 __global__ void __launch_bounds__(256) k_cg_update(int n, double* x, double* r, const double* p, const double* ap,
-                                                   CgState* st, double* bpart) {
+                                                   CgState* st, double* bpart, const double* minv = nullptr,
+                                                   double* z = nullptr) {
   if (st->status != CG_RUN) return;
   __shared__ double red[2][kMaxWarps * 4];
   const double alpha = st->alpha;
-  double part = 0.0;
+  double part = 0.0, pz = 0.0;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     x[j] = x[j] + alpha * p[j];
     const double rj = r[j] - alpha * ap[j];
     r[j] = rj;
     part = fma(rj, rj, part);
+    if (minv != nullptr) {
+      const double zj = rj * minv[j];
+      z[j] = zj;
+      pz = fma(rj, zj, pz);
+    }
   }
   int ph = 0;
-  double t[1] = {part};
-  block_reduce<1, kSum>(t, &red[0][0], ph, blockDim.x);
-  if (threadIdx.x == 0) bpart[blockIdx.x] = t[0];
+  double t[2] = {part, pz};
+  block_reduce<2, kSum>(t, &red[0][0], ph, blockDim.x);
+  if (threadIdx.x == 0) {
+    bpart[2 * blockIdx.x] = t[0];
+    bpart[2 * blockIdx.x + 1] = t[1];
+  }
   if (last_block(&st->cnt[1])) {
     if (threadIdx.x < 32) {
-      const double rsn = warp_fixed_sum(bpart, gridDim.x, 1);
+      const double rsn = warp_fixed_sum(bpart, gridDim.x, 2);
+      const double rzn = warp_fixed_sum(bpart + 1, gridDim.x, 2);
       if (threadIdx.x == 0) {
         st->iters += 1;
         if (sqrt(rsn) <= st->target) {
           st->rs = rsn;
           st->status = CG_DONE;
         } else {
-          st->beta = rsn / st->rs;
+          st->beta = st->precond ? rzn / st->rz : rsn / st->rs;
           st->rs = rsn;
+          st->rz = rzn;
           if (st->iters >= st->max_iters) st->status = CG_MAXIT;
         }
         st->res = sqrt(st->rs);
@@ -1273,33 +1288,59 @@ __global__ void __launch_bounds__(256) k_cg_update(int n, double* x, double* r, 
 // krylov.py:51-67 set-up: x = 0, r = p = rhs, rs = r.r, stop target.
 // neg_of != nullptr: the right-hand side is -neg_of, written to rhs_out
 // (inner_newton.py:117's -g without a separate pass).
+// PCG (pc.q != nullptr): the Jacobi preconditioner of H_rho + shift I,
+// minv_j = 1 / ((d_j - q_j) / eta + shift) with q = (P_rho o P_rho)^T a
+// (diag of P_rho^T diag(a) P_rho), z = minv r, p0 = z, rz = r.z.
+struct PcgInit {
+  const double* d;
+  const double* q;     // nullptr: plain CG (the reference's krylov.py)
+  double eta;
+  double* minv;
+  double* z;
+};
 __global__ void __launch_bounds__(256) k_cg_init(int n, const double* rhs, double* x, double* r, double* p0,
                                                  CgState* st, double* bpart, double shift, double rel_tol,
                                                  long long max_iters, const double* neg_of = nullptr,
-                                                 double* rhs_out = nullptr, const double* shift_dev = nullptr) {
+                                                 double* rhs_out = nullptr, const double* shift_dev = nullptr,
+                                                 PcgInit pc = PcgInit{nullptr, nullptr, 1.0, nullptr, nullptr}) {
   __shared__ double red[2][kMaxWarps * 4];
-  double sq = 0.0, sm = 0.0;
+  double sq = 0.0, sm = 0.0, rzp = 0.0;
+  const double sh0 = shift_dev != nullptr ? *shift_dev : shift;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const double v = (neg_of != nullptr) ? -neg_of[j] : rhs[j];
     if (rhs_out != nullptr) rhs_out[j] = v;
     x[j] = 0.0;
     r[j] = v;
-    p0[j] = v;
+    if (pc.q != nullptr) {
+      const double dj = div_rn(pc.d[j] - pc.q[j], pc.eta) + sh0;
+      const double mi = dj > 0.0 ? div_rn(1.0, dj) : 1.0;
+      pc.minv[j] = mi;
+      const double zj = v * mi;
+      pc.z[j] = zj;
+      p0[j] = zj;
+      rzp = fma(v, zj, rzp);
+    } else {
+      p0[j] = v;
+    }
     sq = fma(v, v, sq);
     sm += v;
   }
   int ph = 0;
-  double t[2] = {sq, sm};
-  block_reduce<2, kSum>(t, &red[0][0], ph, blockDim.x);
+  double t[4] = {sq, sm, rzp, 0.0};
+  block_reduce<4, kSum>(t, &red[0][0], ph, blockDim.x);
   if (threadIdx.x == 0) {
-    bpart[2 * blockIdx.x] = t[0];
-    bpart[2 * blockIdx.x + 1] = t[1];
+    bpart[4 * blockIdx.x] = t[0];
+    bpart[4 * blockIdx.x + 1] = t[1];
+    bpart[4 * blockIdx.x + 2] = t[2];
   }
   if (last_block(&st->cnt[2])) {
     if (threadIdx.x < 32) {
-      const double rs = warp_fixed_sum(bpart, gridDim.x, 2);
-      const double sum = warp_fixed_sum(bpart + 1, gridDim.x, 2);
+      const double rs = warp_fixed_sum(bpart, gridDim.x, 4);
+      const double sum = warp_fixed_sum(bpart + 1, gridDim.x, 4);
+      const double rz = warp_fixed_sum(bpart + 2, gridDim.x, 4);
       if (threadIdx.x == 0) {
+        st->precond = pc.q != nullptr;
+        st->rz = rz;
         const double bnorm = sqrt(rs);
         const double sh = shift_dev != nullptr ? *shift_dev : shift;   // ||g|| of an eval the host has not read
         st->rs = rs;

@@ -110,6 +110,7 @@ def inner_solve(logplan: LogPlan, gamma0: DualState, problem: OtProblem, config:
     of the reference API never pass them.
     """
     s = session if session is not None else session_for(problem, config.eta, comm)
+    s.set_precond(getattr(config, "cg_preconditioner", None))
     m, n = s.m, s.n
     eta = config.eta
     scale = float(min(m, n)) if config.inner_scale is InnerScale.MIN_DIM else 1.0

@@ -185,6 +185,14 @@ class Session:
     def new_plan(self):
         return self.torch.empty((self.m_loc, self.ld), dtype=self.torch.float64, device=self.device)
 
+    def set_precond(self, kind: str | None):
+        """CG preconditioner of this context: None (plain CG) or "jacobi"."""
+        code = {None: 0, "jacobi": 1}[kind]
+        if getattr(self, "_precond", 0) != code:
+            _lib.check(_lib.lib.otb_set_cg_precond(self.ctx, code))
+            self._precond = code
+            self._last_sparsify = None
+
     def bind(self, eta: float, anchor: int | None = None):
         eta = float(eta)
         anchor = self.default_anchor if anchor is None else int(anchor)
@@ -252,6 +260,8 @@ class Session:
         if self.ctx:
             pool = _CTX_POOL.setdefault(self._pool_key, []) if self._pool_key is not None else None
             if pool is not None and len(pool) < _POOL_DEPTH:
+                if getattr(self, "_precond", 0):
+                    _lib.lib.otb_set_cg_precond(self.ctx, 0)   # pooled contexts start plain
                 pool.append(self.ctx)
             else:
                 _lib.lib.otb_destroy(self.ctx)

@@ -738,3 +738,53 @@ def test_dense_rho_equals_bitmap_rho(cuda, monkeypatch, m, n):
     assert np.array_equal(out["0"][1].view(np.uint64), out["1"][1].view(np.uint64))
     assert np.array_equal(out["0"][2].view(np.uint64), out["1"][2].view(np.uint64))
     assert out["0"][3:5] == out["1"][3:5]
+
+
+@pytest.mark.parametrize("m,n", [(90, 70), (300, 4100), (64, 16400)])
+def test_jacobi_pcg_matches_oracle(cuda, m, n):
+    """cg_solve(preconditioner="jacobi") (extension; the reference's CG is
+    plain): the device PCG direction and iteration count match the oracle's
+    Jacobi PCG (diag(H_rho) = (d - (P_rho o P_rho)^T a)/eta accumulated by
+    sparsify), it solves the same system as plain CG, and needs fewer
+    iterations."""
+    P = _api()
+    from paper_2603_07156_b200 import instances
+
+    C, a, b = instances.small_uniform(m, n, 3 + n)
+    prob = P.OtProblem(C, a, b)
+    eta = 1e-2
+    lx = O.product_log_plan(a, b)
+    rng = np.random.default_rng(m)
+    gam = rng.standard_normal(n) * 1e-3
+    cache = P.compute_p(P.LogPlan(lx), P.DualState(gam), prob, eta)
+    grad = P.semidual_gradient(cache, prob)
+    gn = float(np.linalg.norm(grad))
+    rho = eta * gn / (m * n)
+    op = P.SparseHessianOp(P.sparsify_p(cache, rho, int(np.argmax(a))))
+    x0, it0, _ = P.cg_solve(op, gn, -grad, 1e-10)
+    x1, it1, res1 = P.cg_solve(op, gn, -grad, 1e-10, preconditioner="jacobi")
+    Pm, _ = O.softmax_rows(lx, C, gam, eta)
+    H = O.SparseHessian(O.threshold_rows(Pm, rho, int(np.argmax(a))), a, eta)
+    xr, itr, _ = O.preconditioned_cg(H.matvec, gn, -grad, O.jacobi_inverse(H, gn), 1e-10)
+    assert abs(it1 - itr) <= 1
+    assert rel(x1, xr) <= 1e-8
+    assert rel(x1, x0) <= 1e-7            # the same Newton direction
+    assert it1 <= it0
+    x2, it2, _ = P.cg_solve(op, gn, -grad, 1e-10)   # back to plain: the reference's iterates
+    assert it2 == it0 and np.array_equal(x2, x0)
+
+
+def test_jacobi_pcg_solve_same_answer(cuda):
+    """ibsn_solve with SolverConfig(cg_preconditioner="jacobi") on BASELINE
+    config 1: the same outer / Newton counts and objective (<= 1e-8) as the
+    plain-CG solve (the parity default), with fewer CG iterations in total."""
+    P = _api()
+    from paper_2603_07156_b200 import instances
+
+    inst = instances.config(1, 0)
+    plain = P.ibsn_solve(P.OtProblem(inst.cost, inst.a, inst.b), P.SolverConfig(eta=inst.eta, kkt_tol=inst.kkt_tol))
+    pcg = P.ibsn_solve(P.OtProblem(inst.cost, inst.a, inst.b),
+                       P.SolverConfig(eta=inst.eta, kkt_tol=inst.kkt_tol, cg_preconditioner="jacobi"))
+    assert (pcg.outer_iters, pcg.newton_iters) == (plain.outer_iters, plain.newton_iters)
+    assert abs(pcg.objective - plain.objective) <= 1e-8 * abs(plain.objective)
+    assert pcg.cg_iters < plain.cg_iters

@@ -189,3 +189,19 @@ def test_oracle_ibsink_matches_reference(name):
     assert [r["inner_total"] for r in recs] == list(g["inner_total"])
     assert obj == pytest.approx(float(g["objective"]), rel=1e-12)
     assert np.max(np.abs(rounded - g["rounded"])) <= 1e-12
+
+
+def test_oracle_jacobi_pcg_solves_the_system():
+    """The oracle's Jacobi PCG (extension) reaches the same solution as the
+    oracle's plain CG (pinned to the reference's krylov.py) on a golden
+    sparsify case, in no more iterations."""
+    g = golden("sparsify_1")
+    C, a, b, lx, gam, eta = g["C"], g["a"], g["b"], g["logX"], g["gamma"], float(g["eta"])
+    P, _ = O.softmax_rows(lx, C, gam, eta)
+    H = O.SparseHessian(O.threshold_rows(P, float(g["rho"]), int(g["anchor"])), a, eta)
+    grad = O.gradient(P, a, b)
+    gn = float(np.linalg.norm(grad))
+    x0, k0, _ = O.conjugate_gradient(H.matvec, gn, -grad, 1e-10)
+    x1, k1, _ = O.preconditioned_cg(H.matvec, gn, -grad, O.jacobi_inverse(H, gn), 1e-10)
+    assert np.max(np.abs(x1 - x0)) <= 1e-8 * np.max(np.abs(x0))
+    assert k1 <= k0
