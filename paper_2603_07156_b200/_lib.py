@@ -15,7 +15,9 @@ from pathlib import Path
 
 from . import errors
 
-LIB_PATH = Path(__file__).resolve().parent / "libotb.so"
+# OTB_LIB: an alternative build of the library (experiments: variants compiled
+# with different -D knobs side by side)
+LIB_PATH = Path(os.environ.get("OTB_LIB") or (Path(__file__).resolve().parent / "libotb.so"))
 
 i64 = C.c_int64
 dbl = C.c_double

@@ -208,6 +208,7 @@ struct otb_ctx {
   int dense_policy = -1;     // OTB_HV_DENSE: 0 never, 1 always, -1 by the last kept density
   double last_density = 0.0; // kept entries / (m_loc n) of the last sparsify
   int precond = 0;           // CG preconditioner: 0 none (the reference's plain CG), 1 Jacobi
+  bool force_post = false;   // OTB_FORCE_EVAL_POST=1 (tests): the multi-rank eval finish on one rank
   double *jq = nullptr, *minv = nullptr, *zv = nullptr, *colpart2 = nullptr;   // PCG vectors
   bool rowpre_valid = false;
   size_t hv_smem = 0;
@@ -465,7 +466,7 @@ int eval_launch(otb_ctx* c, const double* X, const double* gamma, bool save_ev0 
   TRY(prof_begin(c, &e0));
   TRY(launch_dense(c, DK_EVAL, geo, &io));
   TRY(prof_end(c, PC_EVAL, e0, 16.0 * c->m_loc * n + 8.0 * c->m_loc + 24.0 * n));
-  if (c->nranks == 1 && (int64_t)c->colgrid * 256 >= n && c->colgrid <= 512) {
+  if (c->nranks == 1 && (int64_t)c->colgrid * 256 >= n && c->colgrid <= 512 && !c->force_post) {
     k_colreduce_eval<<<c->col32, 256, 0, c->stream>>>(c->colpart, c->ncl, n, c->vpart, c->ncl, c->b, gamma, c->eta,
                                                       c->g, c->ds, c->bpart, c->colgrid, save_ev0);
     LAUNCH_CHECK();
@@ -1264,6 +1265,8 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
     st = dalloc(&c->Pbuf, (size_t)m_loc * ld);
     if (st == OTB_OK) cudaMemset(c->Pbuf, 0, sizeof(double) * (size_t)m_loc * ld);   // padding columns stay 0
   }
+  const char* env_fp = std::getenv("OTB_FORCE_EVAL_POST");
+  c->force_post = env_fp && std::atoi(env_fp) == 1;
   const char* env_tr = std::getenv("OTB_CG_TRACE");
   if (st == OTB_OK && env_tr && std::atoi(env_tr) == 1) {
     const size_t cnt = (size_t)c->hv_grid * kCgTraceIters * 6;

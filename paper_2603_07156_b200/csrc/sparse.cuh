@@ -939,6 +939,73 @@ OTB_DEV void wc_produce(const Csr& A, const uint4* bm, const double* a, int rb, 
   }
 }
 
+// Dense P_rho consumers, values KEPT in registers: row k's window values
+// are read from the stage once (dots), kept in a register slot, and applied
+// to the accumulator when row k's full dot arrives D rows later — no second
+// read of the values at all (HBM and L2 see each value once).  D = 1: the
+// exchange of row k overlaps the dots of row k+1; two register slots of
+// 2 NQ doubles.  Same per-thread sums and row order as wc_consume: the same
+// bits.
+template <int NQ>
+OTB_DEV void wc_consume_keep(int cnt, const double* vsm, double (&acc)[2 * NQ], unsigned char* ring, uint64_t* full,
+                             uint64_t* empty, int S, double* xbuf, uint64_t* xbar, int W, int cr, double* slots,
+                             WcHdr* hring) {
+  using G = WcGeo<NQ>;
+  constexpr int D = 1;
+  const int lane = threadIdx.x & 31;
+  int stage = 0, rphase = 0;
+  uint32_t phase = 0;
+  double kv[D + 1][2 * NQ];
+  double kar[D + 1];
+  for (int k0 = 0; k0 < cnt + D; k0 += D + 1) {
+#pragma unroll
+    for (int j = 0; j <= D; ++j) {
+      const int k = k0 + j, ku = k - D;
+      if (k < cnt) {   // dots of row k; its values stay in slot j
+        mbar_wait(&full[stage], phase);
+        const unsigned char* sp = ring + (size_t)stage * G::kStage;
+        const WcHdr* h = reinterpret_cast<const WcHdr*>(sp + G::WW * 16);
+        const double* sv = reinterpret_cast<const double*>(sp + G::WW * 16 + kWcHdr);
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int t = 0; t < NQ; ++t) {
+          const double2 x = *reinterpret_cast<const double2*>(sv + bm_col<16>(t, 0));
+          const double2 vv = *reinterpret_cast<const double2*>(vsm + bm_col<16>(t, 0));
+          kv[j][2 * t] = x.x;
+          kv[j][2 * t + 1] = x.y;
+          d0 = fma(x.x, vv.x, d0);
+          d1 = fma(x.y, vv.y, d1);
+        }
+        kar[j] = h->ar;
+        mbar_arrive(&empty[stage]);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1u;
+        }
+        double dt[1] = {d0 + d1};
+        block_reduce<1, kSum>(dt, slots, rphase, kStConsumers);
+        if (threadIdx.x < W) {
+          const int q = k % kWcX;
+          st_async_f64(mapa(smem_u32(xbuf + q * kWcMaxW + cr), (uint32_t)threadIdx.x), dt[0],
+                       mapa(smem_u32(&xbar[q]), (uint32_t)threadIdx.x));
+        }
+      }
+      if (ku >= 0 && ku < cnt) {   // row ku (slot (j + 1) mod (D + 1)): full dot, then the update
+        const int ju = (j + 1) % (D + 1);   // static after unrolling
+        const int q = ku % kWcX;
+        mbar_wait(&xbar[q], (uint32_t)((ku / kWcX) & 1));
+        double dot = (lane < W) ? xbuf[q * kWcMaxW + lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        if (threadIdx.x == 0) mbar_arrive_expect_tx(&xbar[q], 8u * (uint32_t)W);
+        const double w = kar[ju] * dot;   // sparsify.py:153: weights * pv
+#pragma unroll
+        for (int i = 0; i < 2 * NQ; ++i) acc[i] = fma(kv[ju][i], w, acc[i]);
+      }
+    }
+  }
+}
+
 // Consumers (512 threads).  Exchange buffer safety: a CTA at dot row k has
 // received row k-D, so every peer has sent row >= k-D and (being at dot row
 // >= k-D) has received rows <= k-2D-1... a sender of row k reuses buffer
@@ -950,6 +1017,7 @@ OTB_DEV void wc_consume(int cnt, const double* __restrict__ vals, const double* 
                         int W, int cr, double* slots, WcHdr* hring, int lim) {
   // lim (DENSE): columns of this window inside the matrix (the last window's
   // tail is neither staged nor loaded)
+  const bool wfull = lim >= 1024 * NQ;
   using G = WcGeo<NQ>;
   constexpr int D = kWcD;
   constexpr int NI = (NQ + 1) / 2;   // uint32 words of packed uint16 pair positions per row
@@ -974,17 +1042,36 @@ OTB_DEV void wc_consume(int cnt, const double* __restrict__ vals, const double* 
         const WcHdr hu = hring[ku % (D + 1)];
         ar_u = hu.ar;
         const double* vr = vals + hu.st;
+        if constexpr (DENSE) {
+          if (wfull) {   // fixed positions: no per-value test outside the last window
 #pragma unroll
-        for (int t = 0; t < NQ; ++t) {
-          double2 x = make_double2(0.0, 0.0);
-          if constexpr (DENSE) {
-            if (bm_col<16>(t, 0) < lim) x = __ldg(reinterpret_cast<const double2*>(vr + bm_col<16>(t, 0)));
+            for (int t = 0; t < NQ; ++t) {
+#ifdef OTB_HV_NO_REREAD   // experiment: timing without the L2 re-read (wrong results)
+              const double2 x = make_double2(0.0, 0.0);
+#else
+              const double2 x = __ldg(reinterpret_cast<const double2*>(vr + bm_col<16>(t, 0)));
+#endif
+              e[2 * t] = x.x;
+              e[2 * t + 1] = x.y;
+            }
           } else {
+#pragma unroll
+            for (int t = 0; t < NQ; ++t) {
+              double2 x = make_double2(0.0, 0.0);
+              if (bm_col<16>(t, 0) < lim) x = __ldg(reinterpret_cast<const double2*>(vr + bm_col<16>(t, 0)));
+              e[2 * t] = x.x;
+              e[2 * t + 1] = x.y;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int t = 0; t < NQ; ++t) {
+            double2 x = make_double2(0.0, 0.0);
             const uint32_t p = (pidx[j][t >> 1] >> (16 * (t & 1))) & 0xffffu;
             if (p != 0xffffu) x = __ldg(reinterpret_cast<const double2*>(vr + 2 * (int)p));
+            e[2 * t] = x.x;
+            e[2 * t + 1] = x.y;
           }
-          e[2 * t] = x.x;
-          e[2 * t + 1] = x.y;
         }
       }
       // (b) row k: partial dots from the staged window, positions saved
@@ -998,12 +1085,11 @@ OTB_DEV void wc_consume(int cnt, const double* __restrict__ vals, const double* 
         double d0 = 0.0, d1 = 0.0;
 #pragma unroll
         for (int i = 0; i < NI; ++i) pidx[j][i] = 0xffffffffu;
-        if constexpr (DENSE) {
+        if constexpr (DENSE) {   // (the stage tail past the matrix was zeroed at start)
 #pragma unroll
           for (int t = 0; t < NQ; ++t) {
-            const int jl = bm_col<16>(t, 0);
-            const double2 x = jl < lim ? *reinterpret_cast<const double2*>(sv + jl) : make_double2(0.0, 0.0);
-            const double2 vv = *reinterpret_cast<const double2*>(vsm + jl);
+            const double2 x = *reinterpret_cast<const double2*>(sv + bm_col<16>(t, 0));
+            const double2 vv = *reinterpret_cast<const double2*>(vsm + bm_col<16>(t, 0));
             d0 = fma(x.x, vv.x, d0);
             d1 = fma(x.y, vv.y, d1);
           }
@@ -1040,8 +1126,12 @@ OTB_DEV void wc_consume(int cnt, const double* __restrict__ vals, const double* 
         const int q = ku % kWcX;
         const uint32_t par = (uint32_t)((ku / kWcX) & 1);
         mbar_wait(&xbar[q], par);
-        double dot = 0.0;
-        for (int rk = 0; rk < W; ++rk) dot += xbuf[q * kWcMaxW + rk];
+        // the W partials: lane rk loads partial rk, then a xor butterfly —
+        // every lane of every warp and every CTA of the cluster forms the
+        // same tree (each step pairs the same two values), so the same bits
+        double dot = (lane < W) ? xbuf[q * kWcMaxW + lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
         // re-arm buffer q for row ku + X once every consumer has read it (the
         // next block reduction is that barrier; peers cannot send row ku + X
         // before this CTA has sent row ku + X - D, i.e. after this point)
@@ -1084,6 +1174,14 @@ __global__ void __launch_bounds__(kStThreads, 1) k_hv_wc(HvArgs h) {
     double* sv = reinterpret_cast<double*>(ring + (size_t)(threadIdx.x >> 1) * G::kStage + G::WW * 16 + kWcHdr);
     sv[G::kZero + (threadIdx.x & 1)] = 0.0;
   }
+  if (DENSE) {   // the last window's stage tail (past the matrix) reads as 0.0
+    const int lim = min(1024 * NQ, (int)(h.ld - 64LL * G::WW * cr));
+    if (lim < 1024 * NQ)
+      for (int i = threadIdx.x; i < S * (1024 * NQ - lim); i += blockDim.x) {
+        const int st = i / (1024 * NQ - lim), col = lim + i % (1024 * NQ - lim);
+        reinterpret_cast<double*>(ring + (size_t)st * G::kStage + G::WW * 16 + kWcHdr)[col] = 0.0;
+      }
+  }
   __syncwarp();
   cluster_sync_all();
   if (h.st == nullptr || h.st->status == CG_RUN) {   // same decision in every CTA
@@ -1114,8 +1212,11 @@ __global__ void __launch_bounds__(kStThreads, 1) k_hv_wc(HvArgs h) {
         ar[i] = 0.0;
       }
       bar_sync(1, kStConsumers);
-      wc_consume<NQ, DENSE>(re - rb, h.A.vals, vsm, ar, ring, full, empty, S, xbuf, xbar, W, cr, slots, hring,
-                            min(1024 * NQ, (int)(h.ld - 64LL * G::WW * cr)));
+      if constexpr (DENSE)
+        wc_consume_keep<NQ>(re - rb, vsm, ar, ring, full, empty, S, xbuf, xbar, W, cr, slots, hring);
+      else
+        wc_consume<NQ, DENSE>(re - rb, h.A.vals, vsm, ar, ring, full, empty, S, xbuf, xbar, W, cr, slots, hring,
+                              min(1024 * NQ, (int)(h.ld - 64LL * G::WW * cr)));
       double* dst = h.colpart + (size_t)cid * n;
 #pragma unroll
       for (int i = 0; i < 2 * NQ; ++i) {

@@ -788,3 +788,37 @@ def test_jacobi_pcg_solve_same_answer(cuda):
     assert (pcg.outer_iters, pcg.newton_iters) == (plain.outer_iters, plain.newton_iters)
     assert abs(pcg.objective - plain.objective) <= 1e-8 * abs(plain.objective)
     assert pcg.cg_iters < plain.cg_iters
+
+
+def test_speculative_step_with_eval_post_fallback(cuda, monkeypatch):
+    """OTB_FORCE_EVAL_POST=1 makes a single rank finish its evals with the
+    multi-rank kernels (k_colreduce + k_eval_post, and for the speculative
+    first step of the native inner iteration the ev0 scalars copied by
+    cudaMemcpyAsync).  Same bits as the fused single-rank finish, and the
+    native loop equals the Python loop on that path too."""
+    import torch
+
+    P = _api()
+    from paper_2603_07156_b200 import instances
+    from paper_2603_07156_b200.inner_newton import inner_solve
+    from paper_2603_07156_b200.sinkhorn import warm_start
+
+    C, a, b = instances.small_uniform(301, 259, 6)   # a shape no pooled context has
+    eta = 1e-2
+    outs = []
+    for force, observe in (("0", False), ("1", False), ("1", True)):
+        monkeypatch.setenv("OTB_FORCE_EVAL_POST", force)
+        from paper_2603_07156_b200 import session as S
+        S._CTX_POOL.clear()                              # contexts read the knob when created
+        prob = P.OtProblem(torch.from_numpy(C).cuda(), a, b)
+        cfg = P.SolverConfig(eta=eta, kkt_tol=1e-9, max_inner=4)
+        X = P.LogPlan(O.product_log_plan(a, b))
+        gam, _ = warm_start(X, prob, eta, 1e-3, gamma0=np.zeros(259))
+        seen = []
+        gs, cand, rep = inner_solve(X, gam, prob, cfg, mu_k=1e-3, outer_k=0,
+                                    observer=(seen.append if observe else None))
+        g = gs.gamma.cpu().numpy() if hasattr(gs.gamma, "cpu") else np.asarray(gs.gamma)
+        outs.append((g.copy(), rep.newton_iters, rep.cg_iters_total, rep.objective, rep.values))
+    for o in outs[1:]:
+        assert np.array_equal(o[0].view(np.uint64), outs[0][0].view(np.uint64))
+        assert o[1:] == outs[0][1:]

@@ -8,7 +8,8 @@
 #include "../paper_2603_07156_b200/csrc/common.cuh"
 using namespace otb;
 
-__global__ void k_tma(const double* src, size_t per_cta_bytes, int stage_bytes, int S, double* sink, int spin) {
+__global__ void k_tma(const double* src, size_t per_cta_bytes, int stage_bytes, int S, double* sink, int spin,
+                      int chunks = 1) {
   extern __shared__ __align__(128) unsigned char sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)S * stage_bytes);
   uint64_t* empty = full + S;
@@ -27,7 +28,10 @@ __global__ void k_tma(const double* src, size_t per_cta_bytes, int stage_bytes, 
       for (int k = 0; k < nseg; ++k) {
         mbar_wait(&empty[st], ph ^ 1u);
         mbar_arrive_expect_tx(&full[st], stage_bytes);
-        bulk_g2s(sm + (size_t)st * stage_bytes, base + (size_t)k * stage_bytes, stage_bytes, &full[st]);
+        const int cb = stage_bytes / chunks;
+        for (int q = 0; q < chunks; ++q)
+          bulk_g2s(sm + (size_t)st * stage_bytes + (size_t)q * cb, base + (size_t)k * stage_bytes + (size_t)q * cb, cb,
+                   &full[st]);
         if (++st == S) { st = 0; ph ^= 1u; }
       }
     }
@@ -77,6 +81,24 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     printf("TMA  cta/sm=%d stage=%2dKB S=%2d inflight=%3dKB/SM : %7.0f GB/s  err=%s\n", blocks_per_sm, stage_kb, S,
            stage_kb * S * blocks_per_sm, per * grid / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+  }
+  // large stages (one row window per stage, as the window-cluster hess_apply), 1 or several copies each
+  for (int grid_sms : {135, 148})
+  for (int stage_kb : {48, 64}) for (int S : {2, 3, 4}) for (int chunks : {1, 4, 12}) {
+    const int stage = stage_kb * 1024;
+    const size_t smem = (size_t)S * stage + 2 * S * 8;
+    if (smem > 227 * 1024) continue;
+    cudaFuncSetAttribute(k_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = grid_sms;
+    const size_t per = (total / grid) / stage * stage;
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(e0);
+      k_tma<<<grid, 512 + 32, smem>>>(src, per, stage, S, sink, 0, chunks);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+    }
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("TMA  ctas=%d stage=%2dKB S=%d copies/stage=%2d : %7.0f GB/s  err=%s\n", grid, stage_kb, S, chunks,
+           per * grid / (ms * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
   }
   for (int bpsm : {1, 2, 4, 8}) for (int th : {256, 512, 1024}) {
     for (int rep = 0; rep < 2; ++rep) {
