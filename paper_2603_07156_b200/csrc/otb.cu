@@ -209,6 +209,13 @@ struct otb_ctx {
   double last_density = 0.0; // kept entries / (m_loc n) of the last sparsify
   int precond = 0;           // CG preconditioner: 0 none (the reference's plain CG), 1 Jacobi
   bool force_post = false;   // OTB_FORCE_EVAL_POST=1 (tests): the multi-rank eval finish on one rank
+  // CUDA graphs of a 16-iteration CG batch (per-iteration path): [0] the
+  // first batch of a solve (k = 0 has no direction update), [1] the others
+  bool cg_graph = true;      // OTB_CG_GRAPH=0: eager launches
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t cg_exec[2] = {nullptr, nullptr};
+  unsigned char cg_key[2][160] = {};
+  int64_t cg_batch_launches[2] = {0, 0};
   double *jq = nullptr, *minv = nullptr, *zv = nullptr, *colpart2 = nullptr;   // PCG vectors
   bool rowpre_valid = false;
   size_t hv_smem = 0;
@@ -733,6 +740,67 @@ int cg_iteration(otb_ctx* c, int64_t k, double* x) {
   return OTB_OK;
 }
 
+// Everything a captured CG batch bakes in: the argument blocks of its
+// kernels (pointers, eta, kernel variant) and the solution vector.
+void cg_graph_key(const otb_ctx* c, const double* x, unsigned char* key) {
+  std::memset(key, 0, 160);
+  const void* ptrs[14] = {x,      c->vals,  c->cols,   c->Pbuf,  c->a,  c->d,     c->bm,
+                          c->row_start, c->row_len, c->cta_rb, c->minv, c->zv, c->colpart, c->sendbuf};
+  std::memcpy(key, ptrs, sizeof ptrs);
+  const int ints[6] = {c->rho_dense ? 1 : 0, c->precond, c->hv_mode, c->hv_var, c->nranks, c->hv_ng};
+  std::memcpy(key + sizeof ptrs, ints, sizeof ints);
+  std::memcpy(key + sizeof ptrs + sizeof ints, &c->eta, sizeof(double));
+}
+
+// kCgBatch iterations from iteration k0: replayed from a CUDA graph (one
+// launch, the NCCL all-reduces inside it on the multi-rank path) unless
+// profiling, a local group (its all-reduce synchronises host threads) or
+// OTB_CG_GRAPH=0; the graph is captured on first use and again whenever an
+// argument it bakes in changes (CSR regrown, dense/bitmap mode, eta).
+int cg_batch(otb_ctx* c, int64_t k0, double* x) {
+  if (c->prof || c->group || !c->cg_graph) {
+    for (int j = 0; j < kCgBatch; ++j) TRY(cg_iteration(c, k0 + j, x));
+    return OTB_OK;
+  }
+  const int which = k0 == 0 ? 0 : 1;   // batches start at even k: the same p-buffer parity
+  unsigned char key[160];
+  cg_graph_key(c, x, key);
+  if (!c->cg_exec[which] || std::memcmp(key, c->cg_key[which], sizeof key) != 0) {
+    if (c->cg_exec[which]) {
+      cudaGraphExecDestroy(c->cg_exec[which]);
+      c->cg_exec[which] = nullptr;
+    }
+    if (!c->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+    cudaStream_t saved = c->stream;
+    const int64_t l0 = c->launches;
+    c->stream = c->cap_stream;
+    CUDA_TRY(cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal));
+    int st = OTB_OK;
+    for (int j = 0; j < kCgBatch && st == OTB_OK; ++j) st = cg_iteration(c, k0 + j, x);
+    cudaGraph_t g = nullptr;
+    const cudaError_t ee = cudaStreamEndCapture(c->cap_stream, &g);
+    c->stream = saved;
+    const int64_t captured = c->launches - l0;
+    c->launches = l0;   // captured, not launched
+    if (st != OTB_OK) {
+      if (g) cudaGraphDestroy(g);
+      return st;
+    }
+    if (ee != cudaSuccess) return fail(OTB_ERR_CUDA, std::string("CG graph capture: ") + cudaGetErrorString(ee));
+    const cudaError_t ei = cudaGraphInstantiate(&c->cg_exec[which], g, 0);
+    cudaGraphDestroy(g);
+    if (ei != cudaSuccess) {
+      c->cg_exec[which] = nullptr;
+      return fail(OTB_ERR_CUDA, std::string("CG graph instantiate: ") + cudaGetErrorString(ei));
+    }
+    std::memcpy(c->cg_key[which], key, sizeof key);
+    c->cg_batch_launches[which] = captured;
+  }
+  CUDA_TRY(cudaGraphLaunch(c->cg_exec[which], c->stream));
+  c->launches += c->cg_batch_launches[which];
+  return OTB_OK;
+}
+
 // The whole CG loop as one cooperative launch (k_cg_fused), after
 // k_cg_init; the state is copied to c->hcg asynchronously (read it after the
 // next stream synchronisation).  k_cg_fused returns at once when k_cg_init
@@ -797,7 +865,8 @@ int do_cg(otb_ctx* c, double shift, const double* rhs, double rel_tol, int64_t m
   int64_t k = 0;
   const size_t rec0 = c->recs.size();
   while (c->hcg->status == CG_RUN) {
-    for (int j = 0; j < kCgBatch; ++j, ++k) TRY(cg_iteration(c, k, x));
+    TRY(cg_batch(c, k, x));
+    k += kCgBatch;
     CUDA_TRY(cudaMemcpyAsync(c->hcg, c->cg, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
   }
@@ -1265,6 +1334,8 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
     st = dalloc(&c->Pbuf, (size_t)m_loc * ld);
     if (st == OTB_OK) cudaMemset(c->Pbuf, 0, sizeof(double) * (size_t)m_loc * ld);   // padding columns stay 0
   }
+  const char* env_cgg2 = std::getenv("OTB_CG_GRAPH");
+  c->cg_graph = !(env_cgg2 && std::atoi(env_cgg2) == 0);
   const char* env_fp = std::getenv("OTB_FORCE_EVAL_POST");
   c->force_post = env_fp && std::atoi(env_fp) == 1;
   const char* env_tr = std::getenv("OTB_CG_TRACE");
@@ -1339,6 +1410,9 @@ int otb_destroy(otb_ctx* c) {
     cudaEventDestroy(r.e1);
   }
   for (auto e : c->pool) cudaEventDestroy(e);
+  for (auto& e : c->cg_exec)
+    if (e) cudaGraphExecDestroy(e);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->comm && c->nccl.commDestroy) c->nccl.commDestroy(c->comm);
   delete c;
   return OTB_OK;

@@ -822,3 +822,36 @@ def test_speculative_step_with_eval_post_fallback(cuda, monkeypatch):
     for o in outs[1:]:
         assert np.array_equal(o[0].view(np.uint64), outs[0][0].view(np.uint64))
         assert o[1:] == outs[0][1:]
+
+
+@pytest.mark.parametrize("m,n,env", [(130, 16400, None), (97, 3000, "OTB_CG_FUSED")])
+def test_cg_graph_batches_equal_eager_launches(cuda, monkeypatch, m, n, env):
+    """The per-iteration CG path (multi-rank, window clusters, PCG, or the
+    persistent CG switched off) replays each 16-iteration batch from a CUDA
+    graph (OTB_CG_GRAPH, default on); eager launches (OTB_CG_GRAPH=0) give
+    the same bits: Newton direction, CG iteration count, residual."""
+    P = _api()
+    from paper_2603_07156_b200 import instances
+    from paper_2603_07156_b200 import session as S
+
+    if env:
+        monkeypatch.setenv(env, "0")
+    C, a, b = instances.small_uniform(m, n, 21 + n)
+    lx = O.product_log_plan(a, b)
+    gam = np.random.default_rng(m).standard_normal(n) * 1e-3
+    out = []
+    for graph in ("1", "0"):
+        monkeypatch.setenv("OTB_CG_GRAPH", graph)
+        S._CTX_POOL.clear()                               # contexts read the knobs when created
+        prob = P.OtProblem(C, a, b)
+        eta = 1e-2
+        cache = P.compute_p(P.LogPlan(lx), P.DualState(gam), prob, eta)
+        grad = P.semidual_gradient(cache, prob)
+        gn = float(np.linalg.norm(grad))
+        op = P.SparseHessianOp(P.sparsify_p(cache, eta * gn / (m * n), int(np.argmax(a))))
+        x, it, res = P.cg_solve(op, gn, -grad, 1e-10)
+        assert cache.session.info()["cg_fused"] == 0
+        out.append((x, it, res))
+    assert out[0][1] == out[1][1] and out[0][1] > 16          # more than one batch
+    assert np.array_equal(out[0][0].view(np.uint64), out[1][0].view(np.uint64))
+    assert out[0][2] == out[1][2]
