@@ -168,6 +168,87 @@ struct SparsifyIO {
 // come in long runs (cfg2: 40 columns on average), so pairs cost ~1.5% more
 // bytes than single entries.  Without it, runs hold the kept entries.
 
+// Dense P_rho row (window-cluster hess_apply at high density): the same
+// values as the runs, 0.0 where dropped, d (and the PCG diagonal)
+// accumulated in the same order.  A row with nothing kept keeps its first
+// argmax with value 1 (sparsify.py:103-107), as in the run path.
+template <int NS, class DT>
+OTB_DEV void sparsify_dense_row(DT& D, const SparsifyIO& io, int r, bool anc, double (&P)[2 * NS], unsigned skip,
+                                unsigned keep, double ksum, int kcnt, const Divider& DS, unsigned long long& kept) {
+  int jbest = -1;
+  const bool fallback = !anc && kcnt == 0;
+  if (fallback) {
+#pragma unroll
+    for (int k = 0; k < 2 * NS; ++k)
+      if ((skip >> k) & 1u) P[k] = DS(exp(P[k]));   // skipped entries take part in the argmax
+    double pm = -1.0;
+#pragma unroll
+    for (int k = 0; k < 2 * NS; ++k) pm = fmax(pm, P[k]);
+    double u[1] = {pm};
+    D.template reduce<1, kMax>(u);
+    const double pmax = u[0];
+    double jm = 1e300;
+#pragma unroll
+    for (int k = 0; k < 2 * NS; ++k)
+      if (P[k] >= 0.0 && P[k] == pmax) jm = fmin(jm, (double)D.col(k >> 1, k & 1));
+    u[0] = jm;
+    D.template reduce<1, kMin>(u);
+    jm = u[0];
+    if (D.g.cl > 1) {
+      double v2[2] = {pmax, jm};
+      const double* all = D.template exchange<2>(v2);
+      double bp = all[0], bj = all[1];
+      for (int q = 1; q < D.g.cl; ++q) {
+        if (all[q * 4] > bp || (all[q * 4] == bp && all[q * 4 + 1] < bj)) {
+          bp = all[q * 4];
+          bj = all[q * 4 + 1];
+        }
+      }
+      jm = bj;
+    }
+    jbest = (int)jm;
+    kcnt = 1;
+  }
+  const double ai = __ldg(io.a + D.g.row0 + r);
+  double* drow = io.dense + (size_t)r * D.g.ld;
+  const Divider DK(ksum);
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    if (s < D.nsl) {
+      const int j = D.col(s, 0);
+      double v0, v1;
+      bool k0, k1;
+      if (fallback) {
+        k0 = j == jbest && P[2 * s] >= 0.0;
+        k1 = j + 1 == jbest && P[2 * s + 1] >= 0.0;
+        v0 = k0 ? 1.0 : 0.0;
+        v1 = k1 ? 1.0 : 0.0;
+      } else {
+        k0 = (keep >> (2 * s)) & 1u;
+        k1 = (keep >> (2 * s + 1)) & 1u;
+        double n0, n1;   // sparsify.py:109-110: kept / kept_sum (the anchor row unnormalised)
+        DK.pair(P[2 * s], P[2 * s + 1], n0, n1);
+        v0 = k0 ? (anc ? P[2 * s] : n0) : 0.0;
+        v1 = k1 ? (anc ? P[2 * s + 1] : n1) : 0.0;
+      }
+      if (j + 1 < D.c1) {
+        *reinterpret_cast<double2*>(drow + j) = make_double2(v0, v1);
+      } else if (j < D.c1) {
+        drow[j] = v0;
+      }
+      double2* a2 = D.acc2(0, s);
+      if (k0) a2->x += ai * v0;
+      if (k1) a2->y += ai * v1;
+      if (io.colpart2 != nullptr) {   // Jacobi diagonal of P_rho^T diag(a) P_rho
+        double2* q2 = D.acc2(1, s);
+        if (k0) q2->x += ai * (v0 * v0);
+        if (k1) q2->y += ai * (v1 * v1);
+      }
+    }
+  }
+  if (D.tid == 0 && D.cr == 0) kept += kcnt;
+}
+
 // FROMP: stream the P stored by the eval of the same gamma (one matrix, no
 // exp / division) instead of recomputing it from C and log X.
 template <int NS, bool FROMP>
@@ -189,6 +270,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
   const int nw = D.g.nt >> 5;
   const unsigned lt = (1u << D.lane) - 1u;
   const bool pairs = io.bm != nullptr;
+  const bool dmode = io.dense != nullptr;   // dense P_rho output (uniform over the grid)
   const int bq0 = (D.c0 >> 6) + D.warp, bqs = D.slice >> 6;   // word of slice 0, words per slice (64-col words)
   unsigned long long cur = 0, end = 0;
   unsigned long long kept = 0;
@@ -244,7 +326,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
         }
       }
       bb0[s] = bb1[s] = 0u;
-      if (s < D.nsl) {
+      if (s < D.nsl && !dmode) {   // dense P_rho needs no run layout: no ballots, no scan
         bb0[s] = __ballot_sync(0xffffffffu, (keep >> (2 * s)) & 1u);
         bb1[s] = __ballot_sync(0xffffffffu, (keep >> (2 * s + 1)) & 1u);
         // packed count of the warp's chunk: stored units (pairs, or entries) | entries << 16
@@ -252,6 +334,26 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
         const int ents = __popc(bb0[s]) + __popc(bb1[s]);
         if (D.lane == 0) tb[s * 32 + D.warp] = (pairs ? __popc(bb0[s] | bb1[s]) : ents) | (ents << 16);
       }
+    }
+    if (dmode) {
+      // kept sum and kept count of the row: one block reduction of both
+      // (per-value trees as in the run path, so the same ksum bits), one
+      // cluster exchange
+      double t2[2] = {ks, (double)__popc(keep)};
+      D.template reduce<2, kSum>(t2);
+      double ksum = t2[0], kcnt = t2[1];
+      if (D.g.cl > 1) {
+        const double* all = D.template exchange<2>(t2);
+        ksum = 0.0;
+        kcnt = 0.0;
+        for (int q = 0; q < D.g.cl; ++q) {
+          ksum += all[q * 4];
+          kcnt += all[q * 4 + 1];
+        }
+      }
+      sparsify_dense_row<NS>(D, io, r, anc, P, skip, keep, ksum, (int)kcnt, DS, kept);
+      rowpar ^= 1;
+      continue;
     }
     double t[1] = {ks};
     D.template reduce<1, kSum>(t);   // barrier also publishes tb
@@ -338,50 +440,6 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom g
       cnt = 1;
       ecnt = 1;
       myoff = 0;
-    }
-    if (io.dense != nullptr) {
-      // dense P_rho (hess_apply window kernels at high density): the same
-      // values as the runs, 0.0 where dropped, d accumulated in the same order
-      const double ai = __ldg(io.a + D.g.row0 + r);
-      double* drow = io.dense + (size_t)r * D.g.ld;
-      const Divider DK(ksum);
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        if (s < D.nsl) {
-          const int j = D.col(s, 0);
-          double v0, v1;
-          bool k0, k1;
-          if (fallback) {
-            k0 = j == jbest && P[2 * s] >= 0.0;
-            k1 = j + 1 == jbest && P[2 * s + 1] >= 0.0;
-            v0 = k0 ? 1.0 : 0.0;
-            v1 = k1 ? 1.0 : 0.0;
-          } else {
-            k0 = (keep >> (2 * s)) & 1u;
-            k1 = (keep >> (2 * s + 1)) & 1u;
-            double n0, n1;   // sparsify.py:109-110: kept / kept_sum (the anchor row unnormalised)
-            DK.pair(P[2 * s], P[2 * s + 1], n0, n1);
-            v0 = k0 ? (anc ? P[2 * s] : n0) : 0.0;
-            v1 = k1 ? (anc ? P[2 * s + 1] : n1) : 0.0;
-          }
-          if (j + 1 < D.c1) {
-            *reinterpret_cast<double2*>(drow + j) = make_double2(v0, v1);
-          } else if (j < D.c1) {
-            drow[j] = v0;
-          }
-          double2* a2 = D.acc2(0, s);
-          if (k0) a2->x += ai * v0;
-          if (k1) a2->y += ai * v1;
-          if (io.colpart2 != nullptr) {   // Jacobi diagonal of P_rho^T diag(a) P_rho
-            double2* q2 = D.acc2(1, s);
-            if (k0) q2->x += ai * (v0 * v0);
-            if (k1) q2->y += ai * (v1 * v1);
-          }
-        }
-      }
-      if (D.tid == 0 && D.cr == 0) kept += ecnt;
-      rowpar ^= 1;
-      continue;
     }
     // Contiguous row run: cluster rank 0 bump-allocates from its current
     // chunk (state replicated in all of its consumer threads) and shares

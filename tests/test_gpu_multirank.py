@@ -188,3 +188,54 @@ def test_group_mismatch_fails_loudly(cuda):
             grp.run(body, timeout=120)
     finally:
         grp.close()
+
+
+def test_row_shard_cost_bench_step_two_ranks(cuda):
+    """bench.py's sharded set-up on a local group: each rank builds ONLY its
+    rows of C on the GPU (instances.device_cost with a row range, the peak
+    max-reduced over the ranks), wraps them in RowShardCost (the session uses
+    them in place), warm-starts and runs the bench step.  The result equals
+    the one-rank step on the full C."""
+    import torch
+
+    P = _api()
+    from paper_2603_07156_b200 import instances
+    from paper_2603_07156_b200.core import LogPlan, RowShardCost
+    from paper_2603_07156_b200.distributed import LocalGroup
+    from paper_2603_07156_b200.session import session_for
+    from paper_2603_07156_b200.sinkhorn import warm_start
+
+    pts = instances.uniform2d_points(1500, 1300, 3)
+    m, n = 1500, 1300
+    ld = (n + 31) // 32 * 32
+    dev = torch.device("cuda", 0)
+
+    def step(cost, comm, r0=0, r1=m):
+        prob = P.OtProblem(cost, pts.a, pts.b)
+        cfg = P.SolverConfig(eta=pts.eta, kkt_tol=pts.kkt_tol, max_inner=1)
+        s = session_for(prob, pts.eta, comm)
+        X = s.new_plan()
+        s.ops.init_plan(X)
+        lp = LogPlan.from_padded(X, n)
+        g, _ = warm_start(lp, prob, pts.eta, cfg.warm_tol, gamma0=torch.zeros(n, dtype=torch.float64, device=dev),
+                          comm=comm)
+        st, cand, rep = P.inner_solve(lp, g, prob, cfg, mu_k=1e3, outer_k=0, comm=comm)
+        return st.gamma[:n].cpu().numpy(), rep
+
+    g1, r1 = step(instances.device_cost(pts, dev, ld=ld), None)
+    grp = LocalGroup(2)
+    try:
+        def body(r, comm):
+            a0, a1 = comm.row_range(m)
+            local = instances.device_cost(pts, dev, rows=(a0, a1), ld=ld, comm=comm)
+            return step(RowShardCost(local, a0, m), comm, a0, a1)
+
+        outs = grp.run(body)
+    finally:
+        grp.close()
+    for g2, r2 in outs:
+        assert r2.newton_iters == r1.newton_iters == 1
+        assert abs(r2.cg_iters[0] - r1.cg_iters[0]) <= 1
+        assert np.max(np.abs(g2 - g1)) <= 1e-9 * max(1.0, np.abs(g1).max())
+        assert r2.objective == pytest.approx(r1.objective, rel=1e-10)
+        assert r2.kkt == pytest.approx(r1.kkt, rel=1e-6)
