@@ -286,8 +286,6 @@ struct Dense {
 
 // Loads gamma-like column vectors as pairs (bounds-checked at n).
 OTB_DEV double2 load_pair(const double* v, int j, int lim) {
-  // j is even: one 16-byte load when the pair is inside and v is 16-byte aligned
-  if (j + 1 < lim && (reinterpret_cast<uintptr_t>(v) & 15u) == 0u) return __ldg(reinterpret_cast<const double2*>(v + j));
   double2 r;
   r.x = (j < lim) ? __ldg(v + j) : 0.0;
   r.y = (j + 1 < lim) ? __ldg(v + j + 1) : 0.0;
