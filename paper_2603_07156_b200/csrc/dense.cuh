@@ -35,38 +35,41 @@ struct EvalIO {
   double* P;            // optional: P = shifted / row_sum (local rows x ld), read by sparsify
 };
 
+// Streams (C, log X, gamma) with no producer warp (Dense<3, true>: 16
+// consumer warps, 128 registers): gamma's window slice comes through the
+// TMA ring with the two matrices, so no consumer waits on a global load.
+// gamma is padded with -inf past n, so the masked columns of a partial last
+// slice (stale but finite C, log X) give z = -inf: no per-element masks in
+// the row max, and only the P store of that slice is masked.  Exps: CUDA's
+// fast path, branch-free per pair; a pair with an argument outside
+// (-708.4, 708.4) (subnormal or zero result, -inf, NaN) is redone with exp().
+constexpr int kSelfThreads = 512;
 template <int NS>
-__global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_eval(Geom geo, EvalIO io) {
+__global__ void __launch_bounds__(kSelfThreads, 1) k_eval(Geom geo, EvalIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
-  Dense<2> D;
+  Dense<3, true> D;
   D.setup(geo, smem);
-  if (D.producer) {
-    D.produce();
-    D.finish();
-    return;
-  }
-  const double eta = io.eta;
-  const Divider DIV(eta);
+  const Divider DIV(io.eta);
+  const int nsl = D.nsl;
+  const bool tail = D.tail;
+  // valid columns of the thread's pair in the last slice (tail only)
+  const int lastv = D.c1 - (D.c0 + (nsl - 1) * D.slice) - 2 * D.tid;
   double alse = 0.0, nbad = 0.0;
   for (int r = D.r0; r < D.r1; ++r) {
     double z[2 * NS];
     double mx = -INFINITY;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      z[2 * s] = -INFINITY;
-      z[2 * s + 1] = -INFINITY;
-      if (s < D.nsl) {
-        double2 c, x;
-        D.fetch(c, x);
-        const int j = D.col(s, 0);
-        const double2 gm = load_pair(io.gamma, j, D.c1);
+      if (s < nsl) {
+        double2 c, x, gm;
+        D.fetch3(c, x, gm);
         double q0, q1;
-        DIV.pair(gm.x - c.x, gm.y - c.y, q0, q1);
-        if (j < D.c1) z[2 * s] = x.x + q0;
-        if (j + 1 < D.c1) z[2 * s + 1] = x.y + q1;
-        const double zm = z[2 * s] > z[2 * s + 1] ? z[2 * s] : z[2 * s + 1];   // DSETP + 2 FSEL (fmax: 4)
+        DIV.pair(gm.x - c.x, gm.y - c.y, q0, q1);   // semidual.py:52
+        z[2 * s] = x.x + q0;
+        z[2 * s + 1] = x.y + q1;
+        const double zm = z[2 * s] > z[2 * s + 1] ? z[2 * s] : z[2 * s + 1];
         mx = zm > mx ? zm : mx;
-      }
+      }   // z of slices >= nsl is never read
     }
     // row max over the whole row (cluster-wide when the row is split), so
     // that exp(z - M) is the reference's shifted value bit for bit
@@ -78,32 +81,44 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_eval(Geom geo, 
       M = all[0];
       for (int q = 1; q < D.g.cl; ++q) M = fmax(M, all[q * 4]);
     }
+    // semidual.py:81: exp(logits - row_max)
     double se = 0.0;
 #pragma unroll
-    for (int k = 0; k < 2 * NS; ++k) {
-      z[k] = exp(z[k] - M);
-      se += z[k];
+    for (int s = 0; s < NS; ++s) {
+      if (s < nsl) {
+        const double x0 = z[2 * s] - M, x1 = z[2 * s + 1] - M;
+        bool ok = true;
+        double e0 = exp_fast(x0, ok), e1 = exp_fast(x1, ok);
+        if (!ok) {
+          e0 = exp(x0);
+          e1 = exp(x1);
+        }
+        z[2 * s] = e0;
+        z[2 * s + 1] = e1;
+        se += e0;
+        se += e1;
+      }
     }
     const double S = D.row_sum(se);
     const double ai = __ldg(io.a + D.g.row0 + r);
     const double w = ai / S;
     const Divider DS(S);
+    double* Prow = io.P != nullptr ? io.P + (size_t)r * D.g.ld + D.col(0, 0) : nullptr;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      if (s < D.nsl) {
+      if (s < nsl) {
         double2* a2 = D.acc2(0, s);
         double2 v = *a2;
         v.x = fma(w, z[2 * s], v.x);
         v.y = fma(w, z[2 * s + 1], v.y);
         *a2 = v;
-        if (io.P != nullptr) {                    // semidual.py:82-83: shifted / row_sum
-          const int j = D.col(s, 0);
-          double* dst = io.P + (size_t)r * D.g.ld + j;
+        if (Prow != nullptr) {                    // semidual.py:82-83: shifted / row_sum
           double p0, p1;
           DS.pair(z[2 * s], z[2 * s + 1], p0, p1);
-          if (j + 1 < D.c1) {
+          double* dst = Prow + s * D.slice;
+          if (s < nsl - 1 || !tail || lastv > 1) {
             *reinterpret_cast<double2*>(dst) = make_double2(p0, p1);
-          } else if (j < D.c1) {
+          } else if (lastv > 0) {
             dst[0] = p0;
           }
         }

@@ -88,9 +88,12 @@ int load_nccl(const char* path, Nccl& api) {
 enum DenseKind {
   DK_EVAL = 0, DK_SPARSIFY, DK_TESTA, DK_TESTB, DK_TESTC0, DK_TESTC1, DK_WARMZ, DK_WARMG, DK_SPARSP, DK_COUNT
 };
-const int kNmat[DK_COUNT] = {2, 2, 2, 1, 1, 2, 2, 2, 1};
+const int kNmat[DK_COUNT] = {3, 2, 2, 1, 1, 2, 2, 2, 1};   // eval: C, log X and gamma
 const int kNacc[DK_COUNT] = {1, 1, 1, 1, 1, 1, 1, 2, 1};
 const int kStaticSmem[DK_COUNT] = {0, (int)(kTabInts * 4 + 16), 0, 0, 0, 0, 0, 0, (int)(kTabInts * 4 + 16)};
+// kinds whose CTA has no producer warp (Dense<NMAT, true>: the consumers refill the ring)
+const bool kSelfFeed[DK_COUNT] = {true, false, false, false, false, false, false, false, false};
+int dense_block(int kind, int nt) { return nt + (kSelfFeed[kind] ? 0 : 32); }
 
 #define NS_ROW(K)                                                                                   \
   { nullptr, (const void*)K<1>, (const void*)K<2>, (const void*)K<3>, (const void*)K<4>,             \
@@ -237,6 +240,7 @@ struct otb_ctx {
   double *colpart = nullptr, *vpart = nullptr, *sendbuf = nullptr, *bpart = nullptr;
   double *g = nullptr, *d = nullptr, *rhs = nullptr, *dir = nullptr, *cg_r = nullptr, *cg_p[2] = {nullptr, nullptr};
   double *cg_ap = nullptr, *cg_y = nullptr, *gtrial = nullptr, *yv = nullptr, *ec = nullptr;
+  double* gev = nullptr;      // aligned copy of a caller's gamma for the eval's TMA stream
   double *Mloc = nullptr, *Mglob = nullptr, *Sloc = nullptr;
   int64_t *row_start = nullptr, *rowpre = nullptr;
   int* row_len = nullptr;        // stored doubles of each row run
@@ -320,6 +324,7 @@ Geom make_geom(const otb_ctx* c, int kind, const double* m0, const double* m1) {
   Geom g;
   g.mat0 = m0;
   g.mat1 = m1;
+  g.vec = nullptr;
   g.ld = c->ld;
   g.m_loc = (int)c->m_loc;
   g.n = (int)c->n;
@@ -382,7 +387,7 @@ int launch_dense(otb_ctx* c, int kind, Geom geo, void* io) {
   const void* fn = kDenseFn[kind][geo.ns];
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)c->grid);
-  cfg.blockDim = dim3((unsigned)(geo.nt + 32));
+  cfg.blockDim = dim3((unsigned)dense_block(kind, geo.nt));
   cfg.dynamicSmemBytes = c->smem[kind];
   cfg.stream = c->stream;
   cudaLaunchAttribute attr[1];
@@ -466,7 +471,14 @@ int require_bound(const otb_ctx* c) {
 // Launch part of an eval (no host synchronisation).
 int eval_launch(otb_ctx* c, const double* X, const double* gamma, bool save_ev0 = false) {
   const int n = (int)c->n;
+  // gamma is streamed by TMA with the rows, a whole slice at a time: it is
+  // copied into gev, whose padding past n holds -inf (set at creation)
+  if (gamma != c->gev) {
+    CUDA_TRY(cudaMemcpyAsync(c->gev, gamma, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+    gamma = c->gev;
+  }
   Geom geo = make_geom(c, DK_EVAL, c->C, X);
+  geo.vec = gamma;
   EvalIO io{gamma, c->a, c->eta, c->rowM, c->rowS, c->lse, c->colpart, c->vpart, c->Pbuf};
   c->p_valid = false;
   cudaEvent_t e0 = nullptr;
@@ -1074,7 +1086,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
         if (allow_max_smem(fn, device) == cudaSuccess) {
           cudaLaunchConfig_t cfg = {};
           cfg.gridDim = dim3((unsigned)(q * (sms / q)));
-          cfg.blockDim = dim3((unsigned)(nt_q + 32));
+          cfg.blockDim = dim3((unsigned)dense_block(DK_EVAL, nt_q));
           cfg.dynamicSmemBytes = dense_smem(c, DK_EVAL, st);
           cudaLaunchAttribute attr[1];
           attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1119,6 +1131,10 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   }
   c->ns = ns;
   c->nt = std::max(nt, 32);
+  // cluster windows are whole slices, so that only the LAST CTA of a cluster
+  // can end on a partial slice (whose masked columns lie past n, where the
+  // eval's gamma stream is -inf)
+  if (cl > 1) c->colw = 2 * c->nt * c->ns;
   int per_sm = 1;
   const char* env_cps = std::getenv("OTB_DENSE_CTAS_PER_SM");
   if (env_cps) per_sm = std::max(1, std::min(4, std::atoi(env_cps)));
@@ -1157,7 +1173,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
     for (int k = 0; k < DK_COUNT; ++k) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3((unsigned)c->grid);
-      cfg.blockDim = dim3((unsigned)(c->nt + 32));
+      cfg.blockDim = dim3((unsigned)dense_block(k, c->nt));
       cfg.dynamicSmemBytes = c->smem[k];
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1320,6 +1336,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   for (double** p : {&c->g, &c->d, &c->rhs, &c->dir, &c->cg_r, &c->cg_p[0], &c->cg_p[1], &c->cg_ap, &c->cg_y,
                      &c->gtrial, &c->yv, &c->ec, &c->Mloc, &c->Mglob, &c->Sloc})
     A(p, nv);
+  A(&c->gev, (size_t)n + 2 * c->nt + 64);   // + one slice of -inf padding
   if (st == OTB_OK) st = dalloc(&c->row_start, m_loc);
   if (st == OTB_OK) st = dalloc(&c->rowpre, m_loc + 1);
   if (st == OTB_OK) st = dalloc(&c->row_len, m_loc);
@@ -1377,6 +1394,10 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   cudaMemset(c->cg, 0, sizeof(CgState));
   cudaMemset(c->cg_y, 0, sizeof(double) * nv);
   cudaMemset(c->row_len, 0, sizeof(int) * m_loc);
+  {   // the eval's gamma stream: -inf past n (masked columns of a partial slice give z = -inf)
+    const std::vector<double> ninf((size_t)2 * c->nt + 64, -INFINITY);
+    cudaMemcpy(c->gev + n, ninf.data(), ninf.size() * sizeof(double), cudaMemcpyHostToDevice);
+  }
   if (c->bm) cudaMemset(c->bm, 0, sizeof(uint4) * m_loc * c->nq);
   cudaMemset(c->rowpre, 0, sizeof(int64_t) * (m_loc + 1));
   cudaError_t e = cudaDeviceSynchronize();
@@ -1397,7 +1418,7 @@ int otb_destroy(otb_ctx* c) {
                   (void*)c->colpart, (void*)c->vpart, (void*)c->sendbuf, (void*)c->bpart, (void*)c->g, (void*)c->d,
                   (void*)c->rhs, (void*)c->dir, (void*)c->cg_r, (void*)c->cg_p[0], (void*)c->cg_p[1],
                   (void*)c->cg_ap, (void*)c->cg_y, (void*)c->gtrial, (void*)c->yv, (void*)c->ec, (void*)c->Mloc,
-                  (void*)c->Mglob, (void*)c->Sloc, (void*)c->row_start, (void*)c->rowpre, (void*)c->row_len, (void*)c->row_nnz,
+                  (void*)c->Mglob, (void*)c->Sloc, (void*)c->gev, (void*)c->row_start, (void*)c->rowpre, (void*)c->row_len, (void*)c->row_nnz,
                   (void*)c->cols, (void*)c->vals, (void*)c->ds, (void*)c->cg, (void*)c->scal, (void*)c->cta_rb,
                   (void*)c->bm, (void*)c->Pbuf, (void*)c->cg_trace, (void*)c->lg_tmp, (void*)c->jq,
                   (void*)c->minv, (void*)c->zv, (void*)c->colpart2})

@@ -32,6 +32,8 @@ constexpr int kMaxNS = 10;   // 1024-column slices per CTA: one CTA per row up t
 struct Geom {
   const double* mat0;   // first streamed matrix (row-major, ld)
   const double* mat1;   // second streamed matrix or nullptr
+  const double* vec;    // NMAT = 3: a row-invariant length-n vector (gamma) streamed as the third
+                        // array of every stage (16-byte aligned; one double past n readable)
   int64_t ld;           // leading dimension (doubles)
   int m_loc;            // local rows
   int n;                // columns
@@ -83,7 +85,17 @@ OTB_DEV SmemMap carve(const Geom& g, int nmat, unsigned char* base) {
 }
 
 // Per-CTA context of a dense pass.
-template <int NMAT>
+//
+// SELF = false: a producer warp (threads nt..nt+31) streams the ring; the
+// consumers release a stage on its `empty` barrier.
+// SELF = true: no producer warp (the CTA is the nt consumer threads, 16
+// warps at 512: 128 registers instead of 96).  Thread 0 issues the first
+// nstage slices; afterwards the LAST warp to finish reading a stage refills
+// it with the slice nstage positions ahead: every warp's lane 0 adds to the
+// stage's arrival counter (acq_rel), the one that completes the round
+// (count = rounds * nwarps - 1 before it) fences the async proxy and issues
+// the bulk copies.  Every thread advances the same refill cursor.
+template <int NMAT, bool SELF = false>
 struct Dense {
   Geom g;
   SmemMap sm;
@@ -101,6 +113,11 @@ struct Dense {
   uint32_t phase;
   int rphase;    // block-reduce slot parity
   int xcount;    // DSMEM exchanges done
+  bool tail;     // the window's last slice is partial (columns >= c1 masked)
+  // SELF: refill cursor (row, slice) of the slice nstage positions ahead of
+  // the one being consumed, and the ring rounds completed
+  int fr, fs;
+  uint32_t rounds;
 
   OTB_DEV void setup(const Geom& geo, unsigned char* smem) {
     g = geo;
@@ -108,7 +125,7 @@ struct Dense {
     tid = threadIdx.x;
     lane = tid & 31;
     warp = tid >> 5;
-    producer = tid >= g.nt;
+    producer = SELF ? false : tid >= g.nt;
     cr = (g.cl > 1) ? (int)cluster_ctarank() : 0;
     cid = blockIdx.x / g.cl;
     ncl = gridDim.x / g.cl;
@@ -118,14 +135,19 @@ struct Dense {
     c1 = min(c0 + g.colw, g.n);
     slice = 2 * g.nt;
     nsl = (c1 > c0) ? (c1 - c0 + slice - 1) / slice : 0;
+    tail = nsl > 0 && (c1 - c0) < nsl * slice;
     stage = 0;
     phase = 0;
     rphase = 0;
     xcount = 0;
+    rounds = 1;
+    fr = r0 + (nsl > 0 ? g.nstage / nsl : 0);
+    fs = nsl > 0 ? g.nstage % nsl : 0;
     if (tid == 0) {
       for (int s = 0; s < g.nstage; ++s) {
         mbar_init(&sm.full[s], 1);
-        mbar_init(&sm.empty[s], g.nt / 32);
+        if (!SELF) mbar_init(&sm.empty[s], g.nt / 32);
+        if (SELF) sm.misc[s] = 0;
       }
       // exchange buffers: one local arrival + 32 bytes (4 doubles) from every
       // CTA of the cluster per use (st.async complete_tx), armed here for the
@@ -138,6 +160,25 @@ struct Dense {
     // zero accumulators (consumer-owned slots only, but any thread may do it)
     const int na = g.nacc * g.ns * slice;
     for (int i = tid; i < na; i += blockDim.x) sm.acc[i] = 0.0;
+    if (SELF) {
+      // the ring too: a partial last slice leaves stale columns in its stage,
+      // which must be finite (NMAT = 3 masks them through the vector's -inf
+      // padding)
+      const int nr = g.nstage * NMAT * slice;
+      for (int i = tid; i < nr; i += blockDim.x) sm.ring[i] = 0.0;
+      fence_proxy_async();
+      __syncthreads();
+      if (tid == 0 && nsl > 0) {
+        int rr = r0, ss = 0;
+        for (int k = 0; k < g.nstage && rr < r1; ++k) {
+          issue(k, rr, ss);
+          if (++ss == nsl) {
+            ss = 0;
+            ++rr;
+          }
+        }
+      }
+    }
     if (g.cl > 1) {
       __syncwarp();
       cluster_sync_all();
@@ -148,28 +189,61 @@ struct Dense {
 
   OTB_DEV double* stage_buf(int st, int mat) const { return sm.ring + ((size_t)st * NMAT + mat) * slice; }
 
-  OTB_DEV void advance() {
-    if (++stage == g.nstage) {
-      stage = 0;
-      phase ^= 1u;
-    }
+  // Bulk copies of slice (r, s) of the window into stage st.  The vector
+  // (NMAT = 3) is copied as a full slice: its padding past n holds -inf.
+  OTB_DEV void issue(int st, int r, int s) {
+    int cols = min(slice, c1 - c0 - s * slice);
+    cols = (cols + 1) & ~1;
+    const uint32_t bytes = (uint32_t)cols * 8u;
+    const uint32_t vbytes = (uint32_t)slice * 8u;
+    mbar_arrive_expect_tx(&sm.full[st], bytes * (NMAT > 2 ? 2 : NMAT) + (NMAT > 2 ? vbytes : 0u));
+    const size_t off = (size_t)r * g.ld + c0 + (size_t)s * slice;
+    bulk_g2s(stage_buf(st, 0), g.mat0 + off, bytes, &sm.full[st]);
+    if (NMAT > 1) bulk_g2s(stage_buf(st, 1), g.mat1 + off, bytes, &sm.full[st]);
+    if (NMAT > 2) bulk_g2s(stage_buf(st, 2), g.vec + c0 + (size_t)s * slice, vbytes, &sm.full[st]);
   }
 
   // Producer: stream every (row, slice) of this CTA's window.
   OTB_DEV void produce() {
-    if (lane != 0) return;
+    if (SELF || lane != 0) return;
     for (int r = r0; r < r1; ++r) {
       for (int s = 0; s < nsl; ++s) {
         mbar_wait(&sm.empty[stage], phase ^ 1u);
-        int cols = min(slice, c1 - c0 - s * slice);
-        cols = (cols + 1) & ~1;
-        const uint32_t bytes = (uint32_t)cols * 8u;
-        mbar_arrive_expect_tx(&sm.full[stage], bytes * NMAT);
-        const size_t off = (size_t)r * g.ld + c0 + (size_t)s * slice;
-        bulk_g2s(stage_buf(stage, 0), g.mat0 + off, bytes, &sm.full[stage]);
-        if (NMAT > 1) bulk_g2s(stage_buf(stage, 1), g.mat1 + off, bytes, &sm.full[stage]);
+        issue(stage, r, s);
         advance();
       }
+    }
+  }
+
+  // Releases the stage just read (consumer side, all threads of the warp).
+  OTB_DEV void release() {
+    __syncwarp();
+    if (!SELF) {
+      if (lane == 0) mbar_arrive(&sm.empty[stage]);
+    } else {
+      if (lane == 0) {
+        uint32_t old;
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                     : "=r"(old)
+                     : "r"(smem_u32(&sm.misc[stage]))
+                     : "memory");
+        if (old == rounds * (uint32_t)(g.nt >> 5) - 1u && fr < r1) {   // last reader of this round
+          fence_proxy_async();
+          issue(stage, fr, fs);
+        }
+      }
+      if (++fs == nsl) {
+        fs = 0;
+        ++fr;
+      }
+    }
+  }
+
+  OTB_DEV void advance() {
+    if (++stage == g.nstage) {
+      stage = 0;
+      phase ^= 1u;
+      ++rounds;
     }
   }
 
@@ -187,8 +261,18 @@ struct Dense {
       const double2* b1 = reinterpret_cast<const double2*>(stage_buf(stage, 1));
       v1 = b1[tid];
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[stage]);
+    release();
+    advance();
+  }
+
+  // The same for three arrays (NMAT = 3: the two matrices and the vector).
+  OTB_DEV void fetch3(double2& v0, double2& v1, double2& v2) {
+    static_assert(NMAT == 3, "fetch3 needs three streamed arrays");
+    mbar_wait(&sm.full[stage], phase);
+    v0 = reinterpret_cast<const double2*>(stage_buf(stage, 0))[tid];
+    v1 = reinterpret_cast<const double2*>(stage_buf(stage, 1))[tid];
+    v2 = reinterpret_cast<const double2*>(stage_buf(stage, 2))[tid];
+    release();
     advance();
   }
 
