@@ -35,19 +35,20 @@ struct EvalIO {
   double* P;            // optional: P = shifted / row_sum (local rows x ld), read by sparsify
 };
 
-// Streams (C, log X, gamma) with no producer warp (Dense<3, true>: 16
+// Streams (C, log X, gamma) with no producer warp (Dense<3, true, 1>: 16
 // consumer warps, 128 registers): gamma's window slice comes through the
 // TMA ring with the two matrices, so no consumer waits on a global load.
-// gamma is padded with -inf past n, so the masked columns of a partial last
-// slice (stale but finite C, log X) give z = -inf: no per-element masks in
-// the row max, and only the P store of that slice is masked.  Exps: CUDA's
+// gamma is padded with -1e300 past n, so the masked columns of a partial
+// last slice (stale but finite C, log X) give z = -1e302 and exp() = 0: no
+// per-element masks in the row max, and only the P store of that slice is
+// masked.  Exps: CUDA's
 // fast path, branch-free per pair; a pair with an argument outside
 // (-708.4, 708.4) (subnormal or zero result, -inf, NaN) is redone with exp().
 constexpr int kSelfThreads = 512;
 template <int NS>
 __global__ void __launch_bounds__(kSelfThreads, 1) k_eval(Geom geo, EvalIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
-  Dense<3, true> D;
+  Dense<3, true, 1> D;
   D.setup(geo, smem);
   const Divider DIV(io.eta);
   const int nsl = D.nsl;
@@ -604,20 +605,20 @@ struct TestAIO {
   double* czeta;     // metrics: c-transform zeta_i = min_j (C_ij - gamma_j) per row (feasibility.py:103), or nullptr
 };
 
+// No producer warp (Dense<3, true, 1>: 128 registers); gamma streamed with
+// (C, log X) through the ring (-1e300 padding past n).  Only the last slice
+// of a partial window is masked (candidate store, exp of the plan as given).
 template <int NS>
-__global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_a(Geom geo, TestAIO io) {
+__global__ void __launch_bounds__(kSelfThreads, 1) k_test_a(Geom geo, TestAIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
-  Dense<2> D;
+  Dense<3, true, 1> D;
   D.setup(geo, smem);
-  if (D.producer) {
-    D.produce();
-    D.finish();
-    return;
-  }
-  const double eta = io.eta;
-  const Divider DIV(eta);
+  const int nsl = D.nsl;
+  const bool tail = D.tail;
+  const int lastv = D.c1 - (D.c0 + (nsl - 1) * D.slice) - 2 * D.tid;   // valid columns of the last pair
+  const Divider DIV(io.eta);
   double sumx = 0.0;
-  int bad = 0;
+  bool bad = false;
   // wide rows (NS > 6) also reduce the c-transform for pass C (see k_test_c)
   constexpr bool kCtr = NS > OTB_ZETA_A_NS;
   const bool ctr = kCtr && io.czeta != nullptr;
@@ -631,33 +632,27 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_a(Geom geo
     double shmin = INFINITY;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      xv[2 * s] = 0.0;
-      xv[2 * s + 1] = 0.0;
-      if (s < D.nsl) {
-        double2 c, x;
-        D.fetch(c, x);
-        const int j = D.col(s, 0);
-        const double2 gm = load_pair(io.gamma, j, D.c1);
+      if (s < nsl) {
+        double2 c, x, gm;
+        D.fetch3(c, x, gm);
+        const bool part = tail && s == nsl - 1;
         if (kCtr && ctr) {   // the slack's c-transform for pass C's KKT metrics
-          if (j < D.c1) shmin = fmin(shmin, c.x - gm.x);
-          if (j + 1 < D.c1) shmin = fmin(shmin, c.y - gm.y);
+          shmin = fmin(shmin, c.x - gm.x);
+          shmin = fmin(shmin, c.y - gm.y);
         }
-        double* dst = Xrow + s * D.slice;
         double l0 = x.x, l1 = x.y;   // the slice's log entries (candidate, or the plan as given)
-        if (io.recover) {
+        if (io.recover) {            // inner_newton.py:160-167, core.py:141-145
           double q0, q1;
           DIV.pair(gm.x - c.x, gm.y - c.y, q0, q1);
-          if (j < D.c1) {
-            const double raw = ((la + x.x) + q0) - l;
-            bad |= (isnan(raw) || raw == INFINITY);
-            l0 = fmax(raw, kLogFloor);
+          const double raw0 = ((la + x.x) + q0) - l, raw1 = ((la + x.y) + q1) - l;
+          bad |= isnan(raw0) || raw0 == INFINITY || isnan(raw1) || raw1 == INFINITY;
+          l0 = fmax(raw0, kLogFloor);
+          l1 = fmax(raw1, kLogFloor);
+          double* dst = Xrow + s * D.slice;
+          if (!part || lastv > 1) {
+            *reinterpret_cast<double2*>(dst) = make_double2(l0, l1);
+          } else if (lastv > 0) {
             dst[0] = l0;
-          }
-          if (j + 1 < D.c1) {
-            const double raw = ((la + x.y) + q1) - l;
-            bad |= (isnan(raw) || raw == INFINITY);
-            l1 = fmax(raw, kLogFloor);
-            dst[1] = l1;
           }
         }
         bool ok = true;   // both exps branch-free (exp() only when out of range)
@@ -666,9 +661,13 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_a(Geom geo
           e0 = exp(l0);
           e1 = exp(l1);
         }
-        if (j < D.c1) xv[2 * s] = e0;
-        if (j + 1 < D.c1) xv[2 * s + 1] = e1;
-        rs += xv[2 * s] + xv[2 * s + 1];
+        if (part) {
+          e0 = lastv > 0 ? e0 : 0.0;
+          e1 = lastv > 1 ? e1 : 0.0;
+        }
+        xv[2 * s] = e0;
+        xv[2 * s + 1] = e1;
+        rs += e0 + e1;
       }
     }
     double rsum;
@@ -680,10 +679,10 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_a(Geom geo
       rsum = D.row_sum(rs);
     }
     const double ai = __ldg(io.a + gi);
-    const double z = (rsum > 0.0) ? fmin(div_rn(ai, rsum), 1.0) : 1.0;
+    const double z = (rsum > 0.0) ? fmin(div_rn(ai, rsum), 1.0) : 1.0;   // feasibility.py:56-58
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      if (s < D.nsl) {
+      if (s < nsl) {
         double2* a2 = D.acc2(0, s);
         double2 v = *a2;
         v.x = v.x + xv[2 * s] * z;
@@ -696,7 +695,7 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_a(Geom geo
       sumx += rsum;
     }
   }
-  double bv[1] = {(double)bad};
+  double bv[1] = {bad ? 1.0 : 0.0};
   D.reduce<1, kSum>(bv);
   D.store_acc(0, io.colpart + (size_t)D.cid * D.g.n);
   if (D.tid == 0) {
@@ -715,82 +714,52 @@ struct TestBIO {
   double* colpart;   // [ncl][n]
 };
 
+// No producer warp (Dense<2, true, 1>: 128 registers), y streamed through
+// the ring with the candidate rows (zero padding past n: a partial last
+// slice's masked columns give f = 0), column sums in registers (no shared
+// accumulator: the ring takes the whole shared memory).
 template <int NS>
-__global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_b(Geom geo, TestBIO io) {
+__global__ void __launch_bounds__(kSelfThreads, 1) k_test_b(Geom geo, TestBIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
-  Dense<1> D;
+  Dense<2, true, 1> D;
   D.setup(geo, smem);
-  if (D.producer) {
-    D.produce();
-    D.finish();
-    return;
-  }
+  const int nsl = D.nsl;
+  double acc[2 * NS];
+#pragma unroll
+  for (int k = 0; k < 2 * NS; ++k) acc[k] = 0.0;
   for (int r = D.r0; r < D.r1; ++r) {
     const double z = io.zrow[r];
     double rs = 0.0;
-    if constexpr (NS <= 6) {
-      // the row's slices first (barrier waits are control flow), then all
-      // its exps branch-free so that their FMA chains overlap
-      double xs[2 * NS], ex[2 * NS];
 #pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        xs[2 * s] = xs[2 * s + 1] = 0.0;
-        if (s < D.nsl) {
-          double2 x, unused;
-          D.fetch(x, unused);
-          xs[2 * s] = x.x;
-          xs[2 * s + 1] = x.y;
+    for (int s = 0; s < NS; ++s) {
+      if (s < nsl) {
+        double2 v[2];   // candidate log entries, y
+        D.fetchn(v);
+        bool ok = true;
+        double e0 = exp_fast(v[0].x, ok), e1 = exp_fast(v[0].y, ok);
+        if (!ok) {
+          e0 = exp(v[0].x);
+          e1 = exp(v[0].y);
         }
-      }
-      bool ok = true;
-#pragma unroll
-      for (int k = 0; k < 2 * NS; ++k) ex[k] = exp_fast(xs[k], ok);
-      if (!ok) {
-#pragma unroll
-        for (int k = 0; k < 2 * NS; ++k) ex[k] = exp(xs[k]);
-      }
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        if (s < D.nsl) {
-          const int j = D.col(s, 0);
-          const double2 yy = load_pair(io.y, j, D.c1);
-          double f0 = 0.0, f1 = 0.0;
-          if (j < D.c1) f0 = (ex[2 * s] * z) * yy.x;
-          if (j + 1 < D.c1) f1 = (ex[2 * s + 1] * z) * yy.y;
-          rs += f0 + f1;
-          double2* a2 = D.acc2(0, s);
-          double2 v = *a2;
-          v.x += f0;
-          v.y += f1;
-          *a2 = v;
-        }
-      }
-    } else {   // wide rows: registers are short; one slice at a time
-#pragma unroll
-      for (int s = 0; s < NS; ++s) {
-        if (s < D.nsl) {
-          double2 x, unused;
-          D.fetch(x, unused);
-          const int j = D.col(s, 0);
-          const double2 yy = load_pair(io.y, j, D.c1);
-          double f0 = 0.0, f1 = 0.0;
-          if (j < D.c1) f0 = (exp(x.x) * z) * yy.x;
-          if (j + 1 < D.c1) f1 = (exp(x.y) * z) * yy.y;
-          rs += f0 + f1;
-          double2* a2 = D.acc2(0, s);
-          double2 v = *a2;
-          v.x += f0;
-          v.y += f1;
-          *a2 = v;
-        }
+        const double f0 = (e0 * z) * v[1].x, f1 = (e1 * z) * v[1].y;   // feasibility.py:65
+        rs += f0 + f1;
+        acc[2 * s] += f0;
+        acc[2 * s + 1] += f1;
       }
     }
     double t[1] = {rs};
     D.reduce<1, kSum>(t);
     if (D.tid == 0) io.rowpart[(size_t)r * D.g.cl + D.cr] = t[0];
   }
-  bar_sync(1, D.g.nt);
-  D.store_acc(0, io.colpart + (size_t)D.cid * D.g.n);
+  double* dst = io.colpart + (size_t)D.cid * D.g.n;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    if (s < nsl) {
+      const int j = D.col(s, 0);
+      if (j < D.c1) dst[j] = acc[2 * s];
+      if (j + 1 < D.c1) dst[j + 1] = acc[2 * s + 1];
+    }
+  }
   D.finish();
 }
 
@@ -813,16 +782,18 @@ struct TestCIO {
   const double* czeta;   // METRICS: row c-transform from pass A
 };
 
+// No producer warp (Dense<.., true, ..>: 128 registers); y, e_c and (with
+// METRICS) gamma streamed through the ring with the rows (X [, C], y, e_c
+// [, gamma]); their padding past n (0, 0, -1e300) makes a partial last
+// slice's masked columns contribute nothing (f = 0, slack = +1e300 > 0), so
+// there are no per-element masks; column sums in registers.
 template <int NS, bool METRICS>
-__global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_c(Geom geo, TestCIO io) {
+__global__ void __launch_bounds__(kSelfThreads, 1) k_test_c(Geom geo, TestCIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
-  Dense<METRICS ? 2 : 1> D;
+  constexpr int NM = METRICS ? 2 : 1, NA = NM + (METRICS ? 3 : 2);
+  Dense<NA, true, NA - NM> D;
   D.setup(geo, smem);
-  if (D.producer) {
-    D.produce();
-    D.finish();
-    return;
-  }
+  const int nsl = D.nsl;
   const double deficit = *io.deficit;
   const Divider DD(deficit);
   // The slack needs the row c-transform zeta (feasibility.py:103, row min of
@@ -832,6 +803,9 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_c(Geom geo
   constexpr bool kZetaFromA = NS > OTB_ZETA_A_NS;
   constexpr int KR = (METRICS && !kZetaFromA) ? 2 * NS : 1;
   double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+  double cacc[2 * NS];
+#pragma unroll
+  for (int k = 0; k < 2 * NS; ++k) cacc[k] = 0.0;
   for (int r = D.r0; r < D.r1; ++r) {
     const double z = io.zrow[r];
     const double e_r = io.er[r];
@@ -841,75 +815,62 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_c(Geom geo
     double rs = 0.0;
 #pragma unroll
     for (int s = 0; s < NS; ++s) {
-      if constexpr (KR > 1) {
-        fk[2 * s] = fk[2 * s + 1] = 0.0;
-        shk[2 * s] = shk[2 * s + 1] = 0.0;
-      }
-      if (s < D.nsl) {
-        double2 x, c;
-        D.fetch(x, c);
-        const int j = D.col(s, 0);
-        const double2 yy = load_pair(io.y, j, D.c1);
-        const double2 ee = load_pair(io.ec, j, D.c1);
-        double2 gm = make_double2(0.0, 0.0);
-        if constexpr (METRICS) gm = load_pair(io.gamma, j, D.c1);
-        double f2[2] = {0.0, 0.0};
+      if (s < nsl) {
+        double2 v[NA];
+        D.fetchn(v);
+        const double2 x = v[0];
+        const double2 yy = v[NM], ee = v[NM + 1];
         bool ok = true;   // both exps of the slice branch-free (exp() only when out of range)
         double ex2[2] = {exp_fast(x.x, ok), exp_fast(x.y, ok)};
         if (!ok) {
           ex2[0] = exp(x.x);
           ex2[1] = exp(x.y);
         }
+        double f2[2];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          if (j + e < D.c1) {
-            const double xl = e ? x.y : x.x;
-            double fv = (ex2[e] * z) * (e ? yy.y : yy.x);
-            if (deficit > 0.0) fv = fv + DD(e_r * (e ? ee.y : ee.x));
-            f2[e] = fv;
-            if (fv > 0.0) acc[0] += fv * (log_fast(fv) - xl);   // feasibility.py:84
-            acc[1] += fv;
-            rs += fv;
-            if constexpr (METRICS) {
-              const double cv = e ? c.y : c.x;
-              acc[2] += cv * fv;
-              acc[3] += fv * fv;
-              const double fm = fmin(fv, 0.0);
-              acc[4] += fm * fm;
-              const double shv = cv - (e ? gm.y : gm.x);
-              if constexpr (kZetaFromA) {
-                const double sl = shv - zeta_a;
-                const double sm = fmin(sl, 0.0);
-                acc[5] += sm * sm;
-                acc[6] += fv * sl;
-              } else {
-                fk[2 * s + e] = fv;
-                shk[2 * s + e] = shv;
-                shmin = fmin(shmin, shv);
-              }
+          const double xl = e ? x.y : x.x;
+          double fv = (ex2[e] * z) * (e ? yy.y : yy.x);              // feasibility.py:65
+          if (deficit > 0.0) fv = fv + DD(e_r * (e ? ee.y : ee.x));   // feasibility.py:67-68
+          f2[e] = fv;
+          if (fv > 0.0) acc[0] += fv * (log_fast(fv) - xl);   // feasibility.py:84
+          acc[1] += fv;
+          rs += fv;
+          if constexpr (METRICS) {
+            const double cv = e ? v[1].y : v[1].x;
+            const double gv = e ? v[NM + 2].y : v[NM + 2].x;
+            acc[2] += cv * fv;
+            acc[3] += fv * fv;
+            const double fm = fmin(fv, 0.0);
+            acc[4] += fm * fm;
+            const double shv = cv - gv;
+            if constexpr (kZetaFromA) {
+              const double sl = shv - zeta_a;
+              const double sm = fmin(sl, 0.0);
+              acc[5] += sm * sm;
+              acc[6] += fv * sl;
+            } else {
+              fk[2 * s + e] = fv;
+              shk[2 * s + e] = shv;
+              shmin = fmin(shmin, shv);
             }
           }
         }
-        double2* a2 = D.acc2(0, s);
-        double2 v = *a2;
-        v.x += f2[0];
-        v.y += f2[1];
-        *a2 = v;
+        cacc[2 * s] += f2[0];
+        cacc[2 * s + 1] += f2[1];
       }
     }
     if constexpr (KR > 1) {
       const double zeta = D.row_min(shmin);
 #pragma unroll
       for (int s = 0; s < NS; ++s) {
-        if (s < D.nsl) {
+        if (s < nsl) {
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            if (D.col(s, e) < D.c1) {
-              const double sl = shk[2 * s + e] - zeta;
-              const double sm = fmin(sl, 0.0);
-              acc[5] += sm * sm;
-              acc[6] += fk[2 * s + e] * sl;
-            }
+            const double sl = shk[2 * s + e] - zeta;
+            const double sm = fmin(sl, 0.0);
+            acc[5] += sm * sm;
+            acc[6] += fk[2 * s + e] * sl;
           }
         }
       }
@@ -934,8 +895,15 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_test_c(Geom geo
     sp[6] = w3[2];
     sp[7] = 0.0;
   }
-  bar_sync(1, D.g.nt);
-  D.store_acc(0, io.colpart + (size_t)D.cid * D.g.n);
+  double* dst = io.colpart + (size_t)D.cid * D.g.n;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    if (s < nsl) {
+      const int j = D.col(s, 0);
+      if (j < D.c1) dst[j] = cacc[2 * s];
+      if (j + 1 < D.c1) dst[j + 1] = cacc[2 * s + 1];
+    }
+  }
   D.finish();
 }
 

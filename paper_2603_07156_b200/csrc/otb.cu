@@ -88,12 +88,15 @@ int load_nccl(const char* path, Nccl& api) {
 enum DenseKind {
   DK_EVAL = 0, DK_SPARSIFY, DK_TESTA, DK_TESTB, DK_TESTC0, DK_TESTC1, DK_WARMZ, DK_WARMG, DK_SPARSP, DK_COUNT
 };
-const int kNmat[DK_COUNT] = {3, 2, 2, 1, 1, 2, 2, 2, 1};   // eval: C, log X and gamma
-const int kNacc[DK_COUNT] = {1, 1, 1, 1, 1, 1, 1, 2, 1};
+// streamed arrays: eval and test_a C, log X, gamma; test_b X, y; test_c X, y, e_c (+ C, gamma with
+// the metrics)
+const int kNmat[DK_COUNT] = {3, 2, 3, 2, 3, 5, 2, 2, 1};
+const int kNacc[DK_COUNT] = {1, 1, 1, 0, 0, 0, 1, 2, 1};   // shared accumulators (test_b, test_c: registers)
 const int kStaticSmem[DK_COUNT] = {0, (int)(kTabInts * 4 + 16), 0, 0, 0, 0, 0, 0, (int)(kTabInts * 4 + 16)};
 // kinds whose CTA has no producer warp (Dense<NMAT, true>: the consumers refill the ring)
-const bool kSelfFeed[DK_COUNT] = {true, false, false, false, false, false, false, false, false};
+const bool kSelfFeed[DK_COUNT] = {true, false, true, true, true, true, false, false, false};
 int dense_block(int kind, int nt) { return nt + (kSelfFeed[kind] ? 0 : 32); }
+constexpr int kMaxStageSelf = 16;   // ring depth cap of the self-fed kinds (misc holds their counters)
 
 #define NS_ROW(K)                                                                                   \
   { nullptr, (const void*)K<1>, (const void*)K<2>, (const void*)K<3>, (const void*)K<4>,             \
@@ -324,7 +327,7 @@ Geom make_geom(const otb_ctx* c, int kind, const double* m0, const double* m1) {
   Geom g;
   g.mat0 = m0;
   g.mat1 = m1;
-  g.vec = nullptr;
+  g.vec[0] = g.vec[1] = g.vec[2] = nullptr;
   g.ld = c->ld;
   g.m_loc = (int)c->m_loc;
   g.n = (int)c->n;
@@ -478,7 +481,7 @@ int eval_launch(otb_ctx* c, const double* X, const double* gamma, bool save_ev0 
     gamma = c->gev;
   }
   Geom geo = make_geom(c, DK_EVAL, c->C, X);
-  geo.vec = gamma;
+  geo.vec[0] = gamma;
   EvalIO io{gamma, c->a, c->eta, c->rowM, c->rowS, c->lse, c->colpart, c->vpart, c->Pbuf};
   c->p_valid = false;
   cudaEvent_t e0 = nullptr;
@@ -903,6 +906,9 @@ int do_round(otb_ctx* c, const double* X, const double* gamma, double* Xout, int
   // pass A: candidate + row scaling + column sums
   {
     Geom geo = make_geom(c, DK_TESTA, c->C, X);
+    if (gamma != nullptr && gamma != c->gev)   // streamed with the rows: the padded copy (-1e300 past n)
+      CUDA_TRY(cudaMemcpyAsync(c->gev, gamma, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+    geo.vec[0] = c->gev;
     TestAIO io{gamma,  c->a,     c->log_a, c->lse, c->eta, Xout, c->zrow, c->colpart, c->vpart, recover,
                (metrics && c->ns > OTB_ZETA_A_NS) ? c->czeta : nullptr};   // k_test_c: wide rows take zeta from pass A
     cudaEvent_t e0 = nullptr;
@@ -926,6 +932,7 @@ int do_round(otb_ctx* c, const double* X, const double* gamma, double* Xout, int
   // pass B: F = (X z) y, e_r, e_c, deficit
   {
     Geom geo = make_geom(c, DK_TESTB, src, nullptr);
+    geo.vec[0] = c->yv;   // zero padding past n
     TestBIO io{c->zrow, c->yv, c->rowpart, c->colpart};
     cudaEvent_t e0 = nullptr;
     TRY(prof_begin(c, &e0));
@@ -953,6 +960,13 @@ int do_round(otb_ctx* c, const double* X, const double* gamma, double* Xout, int
   {
     const int kind = metrics ? DK_TESTC1 : DK_TESTC0;
     Geom geo = make_geom(c, kind, src, metrics ? c->C : nullptr);
+    geo.vec[0] = c->yv;   // zero padding past n
+    geo.vec[1] = c->ec;   // zero padding past n
+    if (metrics) {        // -1e300 padding past n
+      if (gamma != nullptr && gamma != c->gev)
+        CUDA_TRY(cudaMemcpyAsync(c->gev, gamma, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+      geo.vec[2] = c->gev;
+    }
     TestCIO io{c->zrow, c->yv, c->er, c->ec, &c->ds->deficit, gamma, c->rowpart, c->colpart, c->vpart, c->czeta};
     cudaEvent_t e0 = nullptr;
     TRY(prof_begin(c, &e0));
@@ -1147,7 +1161,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   const int max_stage = env_ns ? std::max(2, std::min(8, std::atoi(env_ns))) : 8;
   for (int k = 0; k < DK_COUNT; ++k) {
     const size_t budget = kMaxDynSmem / per_sm - kStaticSmem[k] - 1024;
-    int st = max_stage;
+    int st = kSelfFeed[k] && !env_ns ? kMaxStageSelf : max_stage;   // the self-fed kinds: as deep as fits
     while (st > 2 && dense_smem(c, k, st) > budget) --st;
     c->nstage[k] = st;
     c->smem[k] = dense_smem(c, k, st);
@@ -1334,9 +1348,11 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   A(&c->bpart, 4 * (size_t)std::max(c->colgrid, c->col32) + 64);
   A(&c->scal, 2 * (size_t)c->hv_grid + 16);
   for (double** p : {&c->g, &c->d, &c->rhs, &c->dir, &c->cg_r, &c->cg_p[0], &c->cg_p[1], &c->cg_ap, &c->cg_y,
-                     &c->gtrial, &c->yv, &c->ec, &c->Mloc, &c->Mglob, &c->Sloc})
+                     &c->gtrial, &c->Mloc, &c->Mglob, &c->Sloc})
     A(p, nv);
+  A(&c->ec, (size_t)n + 2 * c->nt + 64);    // + one slice of zero padding (test_c streams e_c)
   A(&c->gev, (size_t)n + 2 * c->nt + 64);   // + one slice of -inf padding
+  A(&c->yv, (size_t)n + 2 * c->nt + 64);    // + one slice of zero padding (test_b streams y)
   if (st == OTB_OK) st = dalloc(&c->row_start, m_loc);
   if (st == OTB_OK) st = dalloc(&c->rowpre, m_loc + 1);
   if (st == OTB_OK) st = dalloc(&c->row_len, m_loc);
@@ -1394,9 +1410,13 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   cudaMemset(c->cg, 0, sizeof(CgState));
   cudaMemset(c->cg_y, 0, sizeof(double) * nv);
   cudaMemset(c->row_len, 0, sizeof(int) * m_loc);
-  {   // the eval's gamma stream: -inf past n (masked columns of a partial slice give z = -inf)
-    const std::vector<double> ninf((size_t)2 * c->nt + 64, -INFINITY);
-    cudaMemcpy(c->gev + n, ninf.data(), ninf.size() * sizeof(double), cudaMemcpyHostToDevice);
+  {   // padding of the vectors the dense passes stream past n, so that the masked
+      // columns of a partial last slice drop out: gamma -1e300 (eval: z = -1e302,
+      // exp = 0; test_c: slack +1e300 > 0), y and e_c 0 (f = 0)
+    const std::vector<double> pad((size_t)2 * c->nt + 64, -1e300);
+    cudaMemcpy(c->gev + n, pad.data(), pad.size() * sizeof(double), cudaMemcpyHostToDevice);
+    cudaMemset(c->yv, 0, sizeof(double) * ((size_t)n + 2 * c->nt + 64));
+    cudaMemset(c->ec, 0, sizeof(double) * ((size_t)n + 2 * c->nt + 64));
   }
   if (c->bm) cudaMemset(c->bm, 0, sizeof(uint4) * m_loc * c->nq);
   cudaMemset(c->rowpre, 0, sizeof(int64_t) * (m_loc + 1));

@@ -32,8 +32,9 @@ constexpr int kMaxNS = 10;   // 1024-column slices per CTA: one CTA per row up t
 struct Geom {
   const double* mat0;   // first streamed matrix (row-major, ld)
   const double* mat1;   // second streamed matrix or nullptr
-  const double* vec;    // NMAT = 3: a row-invariant length-n vector (gamma) streamed as the third
-                        // array of every stage (16-byte aligned; one double past n readable)
+  const double* vec[3]; // NV row-invariant length-n vectors (gamma, y, ...) streamed as the last NV
+                        // arrays of every stage, a whole slice each: 16-byte aligned, with at least
+                        // one slice of padding past n (its value chosen so masked columns drop out)
   int64_t ld;           // leading dimension (doubles)
   int m_loc;            // local rows
   int n;                // columns
@@ -95,8 +96,10 @@ OTB_DEV SmemMap carve(const Geom& g, int nmat, unsigned char* base) {
 // stage's arrival counter (acq_rel), the one that completes the round
 // (count = rounds * nwarps - 1 before it) fences the async proxy and issues
 // the bulk copies.  Every thread advances the same refill cursor.
-template <int NMAT, bool SELF = false>
+template <int NMAT, bool SELF = false, int NV = 0>
 struct Dense {
+  static_assert(NV >= 0 && NV <= 3 && NMAT - NV >= 1 && NMAT - NV <= 2, "1-2 matrices and 0-3 vectors");
+  static constexpr int NM = NMAT - NV;   // streamed matrices
   Geom g;
   SmemMap sm;
   int tid, lane, warp;
@@ -162,7 +165,7 @@ struct Dense {
     for (int i = tid; i < na; i += blockDim.x) sm.acc[i] = 0.0;
     if (SELF) {
       // the ring too: a partial last slice leaves stale columns in its stage,
-      // which must be finite (NMAT = 3 masks them through the vector's -inf
+      // which must be finite (the kernels mask them through the vectors'
       // padding)
       const int nr = g.nstage * NMAT * slice;
       for (int i = tid; i < nr; i += blockDim.x) sm.ring[i] = 0.0;
@@ -189,18 +192,20 @@ struct Dense {
 
   OTB_DEV double* stage_buf(int st, int mat) const { return sm.ring + ((size_t)st * NMAT + mat) * slice; }
 
-  // Bulk copies of slice (r, s) of the window into stage st.  The vector
-  // (NMAT = 3) is copied as a full slice: its padding past n holds -inf.
+  // Bulk copies of slice (r, s) of the window into stage st: the matrices'
+  // columns inside the window, the vectors as a whole slice (their padding
+  // past n covers a partial last slice).
   OTB_DEV void issue(int st, int r, int s) {
     int cols = min(slice, c1 - c0 - s * slice);
     cols = (cols + 1) & ~1;
     const uint32_t bytes = (uint32_t)cols * 8u;
     const uint32_t vbytes = (uint32_t)slice * 8u;
-    mbar_arrive_expect_tx(&sm.full[st], bytes * (NMAT > 2 ? 2 : NMAT) + (NMAT > 2 ? vbytes : 0u));
+    mbar_arrive_expect_tx(&sm.full[st], bytes * NM + vbytes * NV);
     const size_t off = (size_t)r * g.ld + c0 + (size_t)s * slice;
     bulk_g2s(stage_buf(st, 0), g.mat0 + off, bytes, &sm.full[st]);
-    if (NMAT > 1) bulk_g2s(stage_buf(st, 1), g.mat1 + off, bytes, &sm.full[st]);
-    if (NMAT > 2) bulk_g2s(stage_buf(st, 2), g.vec + c0 + (size_t)s * slice, vbytes, &sm.full[st]);
+    if (NM > 1) bulk_g2s(stage_buf(st, 1), g.mat1 + off, bytes, &sm.full[st]);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) bulk_g2s(stage_buf(st, NM + v), g.vec[v] + c0 + (size_t)s * slice, vbytes, &sm.full[st]);
   }
 
   // Producer: stream every (row, slice) of this CTA's window.
@@ -265,15 +270,21 @@ struct Dense {
     advance();
   }
 
-  // The same for three arrays (NMAT = 3: the two matrices and the vector).
-  OTB_DEV void fetch3(double2& v0, double2& v1, double2& v2) {
-    static_assert(NMAT == 3, "fetch3 needs three streamed arrays");
+  // The same for every streamed array (matrices first, then vectors).
+  OTB_DEV void fetchn(double2 (&v)[NMAT]) {
     mbar_wait(&sm.full[stage], phase);
-    v0 = reinterpret_cast<const double2*>(stage_buf(stage, 0))[tid];
-    v1 = reinterpret_cast<const double2*>(stage_buf(stage, 1))[tid];
-    v2 = reinterpret_cast<const double2*>(stage_buf(stage, 2))[tid];
+#pragma unroll
+    for (int k = 0; k < NMAT; ++k) v[k] = reinterpret_cast<const double2*>(stage_buf(stage, k))[tid];
     release();
     advance();
+  }
+  OTB_DEV void fetch3(double2& v0, double2& v1, double2& v2) {
+    static_assert(NMAT == 3, "fetch3 needs three streamed arrays");
+    double2 v[3];
+    fetchn(v);
+    v0 = v[0];
+    v1 = v[1];
+    v2 = v[2];
   }
 
   // Accumulator slots of this thread for slice s (double2 at acc[k]).

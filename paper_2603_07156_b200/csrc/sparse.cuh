@@ -855,7 +855,7 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_hv_grp(HvArgs h) {
 // rows in flight (loads + dots); the exchange waits hold no stage.  Rows are
 // applied in order, partials summed in window order: deterministic.
 constexpr double kDenseRhoMin = 0.5;   // kept density above which sparsify writes P_rho dense (OTB_HV_DENSE)
-constexpr int kWcD = 4;                  // exchange lookahead (rows)                  // exchange lookahead (rows)                  // exchange lookahead (rows)                  // exchange lookahead (rows)                  // exchange lookahead (rows)                  // exchange lookahead (rows)
+constexpr int kWcD = 4;                  // exchange lookahead (rows)
 constexpr int kWcX = 2 * kWcD + 2;       // exchange buffers (>= 2 D + 1: see the note in wc_consume)
 constexpr int kWcMaxW = 16;
 constexpr int kWcHdr = 32;
@@ -939,6 +939,35 @@ OTB_DEV void wc_produce(const Csr& A, const uint4* bm, const double* a, int rb, 
   }
 }
 
+// The CTA's partial of row k's dot, sent to the W peers.  Every warp sums
+// its lanes, writes the warp partial to slot buffer k mod 8 and ARRIVES on
+// named barrier 2 + (k mod 8); only the row's reducer warp (k mod 16) waits
+// there and forms the CTA partial with the same tree as block_reduce (the
+// same bits), its lanes q < W sending it to peer q.  The other 15 warps go
+// straight on to the next row.  Reuse of buffer / barrier k mod 8 at row
+// k + 8: a warp at the dots of row k + 8 has done the update of row
+// k + 8 - D (D <= 4), which needed row k's full dot, i.e. row k's reducer
+// has read its slots and passed its barrier.
+constexpr int kWcNB = 8;
+OTB_DEV void wc_send_partial(double v, int k, double* slots, double* xbuf, uint64_t* xbar, int W, int cr) {
+  static_assert(kStConsumers == 512 && kWcD < kWcNB, "reducer rotation assumes 16 consumer warps");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double ws = warp_sum(v);
+  double* sl = slots + (k & (kWcNB - 1)) * 16;
+  if (lane == 0) sl[warp] = ws;
+  const int bid = 2 + (k & (kWcNB - 1));
+  if (warp == (k & 15)) {
+    bar_sync(bid, kStConsumers);
+    const double t = warp_sum(lane < 16 ? sl[lane] : 0.0);
+    if (lane < W) {   // lane q serves peer q, in parallel
+      const int q = k % kWcX;
+      st_async_f64(mapa(smem_u32(xbuf + q * kWcMaxW + cr), (uint32_t)lane), t, mapa(smem_u32(&xbar[q]), (uint32_t)lane));
+    }
+  } else {
+    bar_arrive(bid, kStConsumers);
+  }
+}
+
 // Dense P_rho consumers, values KEPT in registers: row k's window values
 // are read from the stage once (dots), kept in a register slot, and applied
 // to the accumulator when row k's full dot arrives D rows later — no second
@@ -982,13 +1011,7 @@ OTB_DEV void wc_consume_keep(int cnt, const double* vsm, double (&acc)[2 * NQ], 
           stage = 0;
           phase ^= 1u;
         }
-        double dt[1] = {d0 + d1};
-        block_reduce<1, kSum>(dt, slots, rphase, kStConsumers);
-        if (threadIdx.x < W) {
-          const int q = k % kWcX;
-          st_async_f64(mapa(smem_u32(xbuf + q * kWcMaxW + cr), (uint32_t)threadIdx.x), dt[0],
-                       mapa(smem_u32(&xbar[q]), (uint32_t)threadIdx.x));
-        }
+        wc_send_partial(d0 + d1, k, slots, xbuf, xbar, W, cr);
       }
       if (ku >= 0 && ku < cnt) {   // row ku (slot (j + 1) mod (D + 1)): full dot, then the update
         const int ju = (j + 1) % (D + 1);   // static after unrolling
@@ -1039,7 +1062,7 @@ OTB_DEV void wc_consume(int cnt, const double* __restrict__ vals, const double* 
       double ar_u = 0.0;
       const bool upd = ku >= 0 && ku < cnt;
       if (upd) {
-        const WcHdr hu = hring[ku % (D + 1)];
+        const WcHdr hu = hring[warp * (D + 1) + ku % (D + 1)];   // this warp's copy (no CTA barrier per row)
         ar_u = hu.ar;
         const double* vr = vals + hu.st;
         if constexpr (DENSE) {
@@ -1107,19 +1130,14 @@ OTB_DEV void wc_consume(int cnt, const double* __restrict__ vals, const double* 
           d1 = fma(x.y, vv.y, d1);
           if (kp) pidx[j][t >> 1] = (pidx[j][t >> 1] & ~(0xffffu << (16 * (t & 1)))) | ((uint32_t)P << (16 * (t & 1)));
         }
-        if (threadIdx.x == 0) hring[k % (D + 1)] = *h;
+        if (lane == 0) hring[warp * (D + 1) + k % (D + 1)] = *h;
+        __syncwarp();
         mbar_arrive(&empty[stage]);
         if (++stage == S) {
           stage = 0;
           phase ^= 1u;
         }
-        double dt[1] = {d0 + d1};
-        block_reduce<1, kSum>(dt, slots, rphase, kStConsumers);
-        if (threadIdx.x < W) {   // thread q serves peer q, in parallel
-          const int q = k % kWcX;
-          st_async_f64(mapa(smem_u32(xbuf + q * kWcMaxW + cr), (uint32_t)threadIdx.x), dt[0],
-                       mapa(smem_u32(&xbar[q]), (uint32_t)threadIdx.x));
-        }
+        wc_send_partial(d0 + d1, k, slots, xbuf, xbar, W, cr);
       }
       // (c) row ku: the W partials in window order, then the update
       if (upd) {
@@ -1151,7 +1169,7 @@ __global__ void __launch_bounds__(kStThreads, 1) k_hv_wc(HvArgs h) {
   __shared__ double xbuf[kWcX * kWcMaxW];
   __shared__ uint64_t xbar[kWcX];
   __shared__ double slots[2 * kMaxWarps * 4];
-  __shared__ WcHdr hring[kWcD + 1];
+  __shared__ WcHdr hring[(kStConsumers / 32) * (kWcD + 1)];   // per consumer warp
   const int W = h.nwin;
   const int S = h.ng;   // ring stages (HvArgs.ng reused)
   const int cr = (int)cluster_ctarank(), cid = blockIdx.x / W, ncl = gridDim.x / W;
