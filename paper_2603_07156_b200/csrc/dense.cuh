@@ -267,10 +267,12 @@ OTB_DEV void sparsify_dense_row(DT& D, const SparsifyIO& io, int r, bool anc, do
 
 // FROMP: stream the P stored by the eval of the same gamma (one matrix, no
 // exp / division) instead of recomputing it from C and log X.
+// FROMP kernels have no producer warp (Dense<1, true>: the consumers refill
+// the ring, 128 registers).
 template <int NS, bool FROMP>
-__global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom geo, SparsifyIO io) {
+__global__ void __launch_bounds__(FROMP ? kSelfThreads : kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom geo, SparsifyIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
-  Dense<FROMP ? 1 : 2> D;
+  Dense<FROMP ? 1 : 2, FROMP> D;
   D.setup(geo, smem);
   if (D.producer) {
     D.produce();
@@ -721,6 +723,7 @@ struct TestBIO {
 template <int NS>
 __global__ void __launch_bounds__(kSelfThreads, 1) k_test_b(Geom geo, TestBIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ double rsl[2 * 8 * 16];
   Dense<2, true, 1> D;
   D.setup(geo, smem);
   const int nsl = D.nsl;
@@ -747,9 +750,7 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_b(Geom geo, TestBIO io
         acc[2 * s + 1] += f1;
       }
     }
-    double t[1] = {rs};
-    D.reduce<1, kSum>(t);
-    if (D.tid == 0) io.rowpart[(size_t)r * D.g.cl + D.cr] = t[0];
+    D.row_sum_deferred(rs, r, io.rowpart, rsl);
   }
   double* dst = io.colpart + (size_t)D.cid * D.g.n;
 #pragma unroll
@@ -791,6 +792,7 @@ template <int NS, bool METRICS>
 __global__ void __launch_bounds__(kSelfThreads, 1) k_test_c(Geom geo, TestCIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int NM = METRICS ? 2 : 1, NA = NM + (METRICS ? 3 : 2);
+  __shared__ double rsl[2 * 8 * 16];
   Dense<NA, true, NA - NM> D;
   D.setup(geo, smem);
   const int nsl = D.nsl;
@@ -826,14 +828,28 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_c(Geom geo, TestCIO io
           ex2[0] = exp(x.x);
           ex2[1] = exp(x.y);
         }
-        double f2[2];
+        double f2[2] = {(ex2[0] * z) * yy.x, (ex2[1] * z) * yy.y};   // feasibility.py:65
+        if (deficit > 0.0) {                                          // feasibility.py:67-68
+          double d0, d1;
+          DD.pair(e_r * ee.x, e_r * ee.y, d0, d1);
+          f2[0] = f2[0] + d0;
+          f2[1] = f2[1] + d1;
+        }
+        // feasibility.py:84 terms f (log f - log y) for f > 0: the logs
+        // branch-free, log() only for a pair with a zero, subnormal,
+        // negative or non-finite entry
+        bool lok = true;
+        double lg[2] = {log_core(f2[0], lok), log_core(f2[1], lok)};
+        if (!lok) {
+          lg[0] = f2[0] > 0.0 ? log(f2[0]) : 0.0;
+          lg[1] = f2[1] > 0.0 ? log(f2[1]) : 0.0;
+        }
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const double xl = e ? x.y : x.x;
-          double fv = (ex2[e] * z) * (e ? yy.y : yy.x);              // feasibility.py:65
-          if (deficit > 0.0) fv = fv + DD(e_r * (e ? ee.y : ee.x));   // feasibility.py:67-68
-          f2[e] = fv;
-          if (fv > 0.0) acc[0] += fv * (log_fast(fv) - xl);   // feasibility.py:84
+          const double fv = f2[e];
+          const double dterm = fv * (lg[e] - xl);
+          acc[0] += fv > 0.0 ? dterm : 0.0;
           acc[1] += fv;
           rs += fv;
           if constexpr (METRICS) {
@@ -844,11 +860,12 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_c(Geom geo, TestCIO io
             const double fm = fmin(fv, 0.0);
             acc[4] += fm * fm;
             const double shv = cv - gv;
+            // slack = shv - zeta >= 0 exactly (zeta is the row minimum of the
+            // same shv values, and fl(a - b) >= 0 for a >= b), so the
+            // reference's sum min(slack, 0)^2 (feasibility.py:117) is 0:
+            // acc[5] stays 0
             if constexpr (kZetaFromA) {
-              const double sl = shv - zeta_a;
-              const double sm = fmin(sl, 0.0);
-              acc[5] += sm * sm;
-              acc[6] += fv * sl;
+              acc[6] += fv * (shv - zeta_a);
             } else {
               fk[2 * s + e] = fv;
               shk[2 * s + e] = shv;
@@ -866,18 +883,11 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_c(Geom geo, TestCIO io
       for (int s = 0; s < NS; ++s) {
         if (s < nsl) {
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const double sl = shk[2 * s + e] - zeta;
-            const double sm = fmin(sl, 0.0);
-            acc[5] += sm * sm;
-            acc[6] += fk[2 * s + e] * sl;
-          }
+          for (int e = 0; e < 2; ++e) acc[6] += fk[2 * s + e] * (shk[2 * s + e] - zeta);   // slack >= 0: acc[5] = 0
         }
       }
     }
-    double t[1] = {rs};
-    D.template reduce<1, kSum>(t);
-    if (D.tid == 0) io.rowpart[(size_t)r * D.g.cl + D.cr] = t[0];
+    D.row_sum_deferred(rs, r, io.rowpart, rsl);
   }
   // CTA-level scalar partials
   double v4[4] = {acc[0], acc[1], acc[2], acc[3]};

@@ -92,9 +92,10 @@ enum DenseKind {
 // the metrics)
 const int kNmat[DK_COUNT] = {3, 2, 3, 2, 3, 5, 2, 2, 1};
 const int kNacc[DK_COUNT] = {1, 1, 1, 0, 0, 0, 1, 2, 1};   // shared accumulators (test_b, test_c: registers)
-const int kStaticSmem[DK_COUNT] = {0, (int)(kTabInts * 4 + 16), 0, 0, 0, 0, 0, 0, (int)(kTabInts * 4 + 16)};
+// static shared memory (sparsify: scan table; test_b/test_c: deferred row-sum slots)
+const int kStaticSmem[DK_COUNT] = {0, (int)(kTabInts * 4 + 16), 0, 2048, 2048, 2048, 0, 0, (int)(kTabInts * 4 + 16)};
 // kinds whose CTA has no producer warp (Dense<NMAT, true>: the consumers refill the ring)
-const bool kSelfFeed[DK_COUNT] = {true, false, true, true, true, true, false, false, false};
+const bool kSelfFeed[DK_COUNT] = {true, false, true, true, true, true, false, false, true};
 int dense_block(int kind, int nt) { return nt + (kSelfFeed[kind] ? 0 : 32); }
 constexpr int kMaxStageSelf = 16;   // ring depth cap of the self-fed kinds (misc holds their counters)
 
@@ -1510,7 +1511,7 @@ int otb_set_cg_precond(otb_ctx* c, int kind) {
   // the sparsify passes carry a second accumulator: re-size their rings
   for (int k : {(int)DK_SPARSIFY, (int)DK_SPARSP}) {
     const size_t budget = kMaxDynSmem - kStaticSmem[k] - 1024;
-    int st = 8;
+    int st = kSelfFeed[k] ? kMaxStageSelf : 8;
     while (st > 2 && dense_smem(c, k, st) > budget) --st;
     if (dense_smem(c, k, st) > budget) return fail(OTB_ERR_ARG, "PCG accumulator does not fit shared memory");
     c->nstage[k] = st;

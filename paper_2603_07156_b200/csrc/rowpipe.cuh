@@ -226,9 +226,15 @@ struct Dense {
     if (!SELF) {
       if (lane == 0) mbar_arrive(&sm.empty[stage]);
     } else {
+      // the warp whose arrival completes the stage's round refills it.  A
+      // relaxed atomic (no fence: acq_rel compiles to a MEMBAR that waits
+      // for the warp's outstanding global stores): every warp's reads of the
+      // stage are issued before its arrival, in the same in-order shared
+      // memory pipeline, and the refill's bulk copy lands a global round
+      // trip after the last arrival.
       if (lane == 0) {
         uint32_t old;
-        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+        asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;"
                      : "=r"(old)
                      : "r"(smem_u32(&sm.misc[stage]))
                      : "memory");
@@ -359,6 +365,28 @@ struct Dense {
     double s = all[0];
     for (int q = 1; q < g.cl; ++q) s = fmin(s, all[q * 4]);
     return s;
+  }
+
+  // Row sum of a per-thread value written to out[r * cl + cr] WITHOUT a
+  // barrier per row: each warp's lane sum goes to slot [row mod 8][warp]
+  // (rsl: 2 x 8 x 16 doubles, double-buffered by batch); every 8th row (and
+  // the last) one barrier, after which warp w reduces batch row w's 16 slots
+  // with block_reduce's second-level tree (the same bits as reduce<1, kSum>).
+  // Buffer b of batch k is written again by batch k + 2, after the barrier
+  // of batch k + 1 that every warp reaches only after its reads of batch k.
+  static constexpr int kRB = 8;
+  OTB_DEV void row_sum_deferred(double v, int r, double* out, double* rsl) {
+    const int i = r - r0, slot = i % kRB, buf = (i / kRB) & 1;
+    const double ws = warp_sum(v);
+    if (lane == 0) rsl[(buf * kRB + slot) * 16 + warp] = ws;
+    if (slot == kRB - 1 || r == r1 - 1) {
+      bar_sync(1, g.nt);
+      if (warp <= slot) {
+        const int nw = g.nt >> 5;
+        const double t = warp_sum(lane < nw ? rsl[(buf * kRB + warp) * 16 + lane] : 0.0);
+        if (lane == 0) out[(size_t)(r - slot + warp) * g.cl + cr] = t;
+      }
+    }
   }
 
   // Writes accumulator k to the partial row `dst` (global columns).
