@@ -96,6 +96,7 @@ SIGNATURES = {
     "otb_selftest_div": (C.c_int, [vp, i64, dbl, vp]),
     "otb_selftest_log": (C.c_int, [vp, i64, vp]),
     "otb_selftest_exp": (C.c_int, [vp, i64, vp]),
+    "otb_selftest_tab": (C.c_int, [vp, i64, vp]),
     "otb_inner_iteration": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, dbl, dbl, vp, vp, vp]),
     "otb_set_cost_norm_sq": (C.c_int, [vp, vp]),
     "otb_check_clamp_plan": (C.c_int, [vp, i64, i64, i64, dbl, vp, vp]),

@@ -48,6 +48,8 @@ constexpr int kSelfThreads = 512;
 template <int NS>
 __global__ void __launch_bounds__(kSelfThreads, 1) k_eval(Geom geo, EvalIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ double2 etab[128];
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) etab[i] = kExp2Tab[i];   // visible after setup's barrier
   Dense<3, true, 1> D;
   D.setup(geo, smem);
   const Divider DIV(io.eta);
@@ -89,10 +91,10 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_eval(Geom geo, EvalIO io) {
       if (s < nsl) {
         const double x0 = z[2 * s] - M, x1 = z[2 * s + 1] - M;
         bool ok = true;
-        double e0 = exp_fast(x0, ok), e1 = exp_fast(x1, ok);
-        if (!ok) {
-          e0 = exp(x0);
-          e1 = exp(x1);
+        double e0 = exp_tab(x0, ok, etab), e1 = exp_tab(x1, ok, etab);
+        if (!ok) {   // per element, as everywhere P is formed (exp_t)
+          e0 = exp_t(x0, etab);
+          e1 = exp_t(x1, etab);
         }
         z[2 * s] = e0;
         z[2 * s + 1] = e1;
@@ -190,13 +192,14 @@ struct SparsifyIO {
 // argmax with value 1 (sparsify.py:103-107), as in the run path.
 template <int NS, class DT>
 OTB_DEV void sparsify_dense_row(DT& D, const SparsifyIO& io, int r, bool anc, double (&P)[2 * NS], unsigned skip,
-                                unsigned keep, double ksum, int kcnt, const Divider& DS, unsigned long long& kept) {
+                                unsigned keep, double ksum, int kcnt, const Divider& DS, unsigned long long& kept,
+                                const double2* etab) {
   int jbest = -1;
   const bool fallback = !anc && kcnt == 0;
   if (fallback) {
 #pragma unroll
     for (int k = 0; k < 2 * NS; ++k)
-      if ((skip >> k) & 1u) P[k] = DS(exp(P[k]));   // skipped entries take part in the argmax
+      if ((skip >> k) & 1u) P[k] = DS(exp_t(P[k], etab));   // skipped entries take part in the argmax
     double pm = -1.0;
 #pragma unroll
     for (int k = 0; k < 2 * NS; ++k) pm = fmax(pm, P[k]);
@@ -272,6 +275,7 @@ OTB_DEV void sparsify_dense_row(DT& D, const SparsifyIO& io, int r, bool anc, do
 template <int NS, bool FROMP>
 __global__ void __launch_bounds__(FROMP ? kSelfThreads : kMaxThreads, OTB_DENSE_MINB) k_sparsify(Geom geo, SparsifyIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
+  OTB_EXP_TABLE(etab);   // (the eval's exp, for P recomputed or for the empty-row fallback)
   Dense<FROMP ? 1 : 2, FROMP> D;
   D.setup(geo, smem);
   if (D.producer) {
@@ -327,7 +331,7 @@ __global__ void __launch_bounds__(FROMP ? kSelfThreads : kMaxThreads, OTB_DENSE_
                 P[2 * s + e] = dz;
                 skip |= 1u << (2 * s + e);
               } else {
-                P[2 * s + e] = DS(exp(dz));          // semidual.py:82-83: shifted / row_sum
+                P[2 * s + e] = DS(exp_t(dz, etab));   // semidual.py:82-83: shifted / row_sum
               }
             }
           }
@@ -369,7 +373,7 @@ __global__ void __launch_bounds__(FROMP ? kSelfThreads : kMaxThreads, OTB_DENSE_
           kcnt += all[q * 4 + 1];
         }
       }
-      sparsify_dense_row<NS>(D, io, r, anc, P, skip, keep, ksum, (int)kcnt, DS, kept);
+      sparsify_dense_row<NS>(D, io, r, anc, P, skip, keep, ksum, (int)kcnt, DS, kept, etab);
       rowpar ^= 1;
       continue;
     }
@@ -427,7 +431,7 @@ __global__ void __launch_bounds__(FROMP ? kSelfThreads : kMaxThreads, OTB_DENSE_
       fallback = true;
 #pragma unroll
       for (int k = 0; k < 2 * NS; ++k)
-        if ((skip >> k) & 1u) P[k] = DS(exp(P[k]));   // skipped entries take part in the argmax
+        if ((skip >> k) & 1u) P[k] = DS(exp_t(P[k], etab));   // skipped entries take part in the argmax
       double pm = -1.0;
 #pragma unroll
       for (int k = 0; k < 2 * NS; ++k) pm = fmax(pm, P[k]);
@@ -613,6 +617,8 @@ struct TestAIO {
 template <int NS>
 __global__ void __launch_bounds__(kSelfThreads, 1) k_test_a(Geom geo, TestAIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ double2 etab[128];
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) etab[i] = kExp2Tab[i];   // visible after setup's barrier
   Dense<3, true, 1> D;
   D.setup(geo, smem);
   const int nsl = D.nsl;
@@ -658,10 +664,10 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_a(Geom geo, TestAIO io
           }
         }
         bool ok = true;   // both exps branch-free (exp() only when out of range)
-        double e0 = exp_fast(l0, ok), e1 = exp_fast(l1, ok);
-        if (!ok) {
-          e0 = exp(l0);
-          e1 = exp(l1);
+        double e0 = exp_tab(l0, ok, etab), e1 = exp_tab(l1, ok, etab);
+        if (!ok) {   // per element (exp_t), as k_materialize_rounded forms X
+          e0 = exp_t(l0, etab);
+          e1 = exp_t(l1, etab);
         }
         if (part) {
           e0 = lastv > 0 ? e0 : 0.0;
@@ -724,6 +730,8 @@ template <int NS>
 __global__ void __launch_bounds__(kSelfThreads, 1) k_test_b(Geom geo, TestBIO io) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double rsl[2 * 8 * 16];
+  __shared__ double2 etab[128];
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) etab[i] = kExp2Tab[i];   // visible after setup's barrier
   Dense<2, true, 1> D;
   D.setup(geo, smem);
   const int nsl = D.nsl;
@@ -739,10 +747,10 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_b(Geom geo, TestBIO io
         double2 v[2];   // candidate log entries, y
         D.fetchn(v);
         bool ok = true;
-        double e0 = exp_fast(v[0].x, ok), e1 = exp_fast(v[0].y, ok);
-        if (!ok) {
-          e0 = exp(v[0].x);
-          e1 = exp(v[0].y);
+        double e0 = exp_tab(v[0].x, ok, etab), e1 = exp_tab(v[0].y, ok, etab);
+        if (!ok) {   // per element (exp_t), as k_materialize_rounded forms X
+          e0 = exp_t(v[0].x, etab);
+          e1 = exp_t(v[0].y, etab);
         }
         const double f0 = (e0 * z) * v[1].x, f1 = (e1 * z) * v[1].y;   // feasibility.py:65
         rs += f0 + f1;
@@ -793,6 +801,12 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_c(Geom geo, TestCIO io
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr int NM = METRICS ? 2 : 1, NA = NM + (METRICS ? 3 : 2);
   __shared__ double rsl[2 * 8 * 16];
+  __shared__ double2 etab[128];
+  __shared__ double4 ltab[128];
+  for (int i = threadIdx.x; i < 128; i += blockDim.x) {   // visible after setup's barrier (blocks may be < 128)
+    etab[i] = kExp2Tab[i];
+    ltab[i] = kLogTab[i];
+  }
   Dense<NA, true, NA - NM> D;
   D.setup(geo, smem);
   const int nsl = D.nsl;
@@ -823,10 +837,10 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_c(Geom geo, TestCIO io
         const double2 x = v[0];
         const double2 yy = v[NM], ee = v[NM + 1];
         bool ok = true;   // both exps of the slice branch-free (exp() only when out of range)
-        double ex2[2] = {exp_fast(x.x, ok), exp_fast(x.y, ok)};
-        if (!ok) {
-          ex2[0] = exp(x.x);
-          ex2[1] = exp(x.y);
+        double ex2[2] = {exp_tab(x.x, ok, etab), exp_tab(x.y, ok, etab)};
+        if (!ok) {   // per element (exp_t), as k_materialize_rounded forms X
+          ex2[0] = exp_t(x.x, etab);
+          ex2[1] = exp_t(x.y, etab);
         }
         double f2[2] = {(ex2[0] * z) * yy.x, (ex2[1] * z) * yy.y};   // feasibility.py:65
         if (deficit > 0.0) {                                          // feasibility.py:67-68
@@ -835,14 +849,14 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_c(Geom geo, TestCIO io
           f2[0] = f2[0] + d0;
           f2[1] = f2[1] + d1;
         }
-        // feasibility.py:84 terms f (log f - log y) for f > 0: the logs
-        // branch-free, log() only for a pair with a zero, subnormal,
-        // negative or non-finite entry
+        // feasibility.py:84 terms f (log f - log y) for f > 0: table logs,
+        // branch-free; log_fast only for a pair with an entry near 1, zero,
+        // subnormal, negative or non-finite
         bool lok = true;
-        double lg[2] = {log_core(f2[0], lok), log_core(f2[1], lok)};
+        double lg[2] = {log_tab(f2[0], lok, ltab), log_tab(f2[1], lok, ltab)};
         if (!lok) {
-          lg[0] = f2[0] > 0.0 ? log(f2[0]) : 0.0;
-          lg[1] = f2[1] > 0.0 ? log(f2[1]) : 0.0;
+          lg[0] = f2[0] > 0.0 ? log_fast(f2[0]) : 0.0;
+          lg[1] = f2[1] > 0.0 ? log_fast(f2[1]) : 0.0;
         }
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
@@ -1100,12 +1114,14 @@ __global__ void __launch_bounds__(kMaxThreads, OTB_DENSE_MINB) k_warm_gamma(Geom
 __global__ void k_materialize_p(const double* C, const double* X, int64_t ld, int m_loc, int n,
                                 const double* gamma, double eta, const double* rowM, const double* rowS,
                                 double* P, int64_t ldp) {
+  OTB_EXP_TABLE(etab);
+  __syncthreads();
   const int64_t total = (int64_t)m_loc * n;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(idx / n), j = (int)(idx % n);
     const double z = X[(size_t)r * ld + j] + Divider(eta)(gamma[j] - C[(size_t)r * ld + j]);
-    P[(size_t)r * ldp + j] = div_rn(exp(z - rowM[r]), rowS[r]);
+    P[(size_t)r * ldp + j] = div_rn(exp_t(z - rowM[r], etab), rowS[r]);
   }
 }
 
@@ -1114,12 +1130,14 @@ __global__ void k_materialize_p(const double* C, const double* X, int64_t ld, in
 __global__ void k_materialize_rounded(const double* X, int64_t ld, int m_loc, int n, const double* zrow,
                                       const double* y, const double* er, const double* ec,
                                       const double* deficit_ptr, double* out, int64_t ldo) {
+  OTB_EXP_TABLE(etab);
+  __syncthreads();
   const double deficit = *deficit_ptr;
   const int64_t total = (int64_t)m_loc * n;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int r = (int)(idx / n), j = (int)(idx % n);
-    double f = (exp(X[(size_t)r * ld + j]) * zrow[r]) * y[j];
+    double f = (exp_t(X[(size_t)r * ld + j], etab) * zrow[r]) * y[j];
     if (deficit > 0.0) f = f + div_rn(er[r] * ec[j], deficit);
     out[(size_t)r * ldo + j] = f;
   }

@@ -733,6 +733,26 @@ __global__ void k_selftest_exp(const double* __restrict__ x, int64_t n, double* 
   }
 }
 
+// Test hook for the table-driven exp_tab / log_tab of the dense passes
+// (common.cuh), with the kernels' fallbacks: out[i] = exp, out[n + i] = log.
+__global__ void k_selftest_tab(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+  __shared__ double2 etab[128];
+  __shared__ double4 ltab[128];
+  if (threadIdx.x < 128) {
+    etab[threadIdx.x] = kExp2Tab[threadIdx.x];
+    ltab[threadIdx.x] = kLogTab[threadIdx.x];
+  }
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    bool ok = true;
+    const double e = exp_tab(x[i], ok, etab);
+    out[i] = ok ? e : exp(x[i]);
+    bool lok = true;
+    const double l = log_tab(x[i], lok, ltab);
+    out[n + i] = lok ? l : log_fast(x[i]);
+  }
+}
+
 // Test hook for Divider (common.cuh): out_i = x_i / y.
 __global__ void k_selftest_div(const double* __restrict__ x, int64_t n, double y, double* __restrict__ out) {
   const Divider D(y);

@@ -92,8 +92,9 @@ enum DenseKind {
 // the metrics)
 const int kNmat[DK_COUNT] = {3, 2, 3, 2, 3, 5, 2, 2, 1};
 const int kNacc[DK_COUNT] = {1, 1, 1, 0, 0, 0, 1, 2, 1};   // shared accumulators (test_b, test_c: registers)
-// static shared memory (sparsify: scan table; test_b/test_c: deferred row-sum slots)
-const int kStaticSmem[DK_COUNT] = {0, (int)(kTabInts * 4 + 16), 0, 2048, 2048, 2048, 0, 0, (int)(kTabInts * 4 + 16)};
+// static shared memory (sparsify: scan table; test_b/test_c: deferred row-sum slots; exp/log tables)
+const int kStaticSmem[DK_COUNT] = {2048, (int)(kTabInts * 4 + 16 + 2048), 2048, 4096, 8192, 8192, 0, 0,
+                                   (int)(kTabInts * 4 + 16 + 2048)};
 // kinds whose CTA has no producer warp (Dense<NMAT, true>: the consumers refill the ring)
 const bool kSelfFeed[DK_COUNT] = {true, false, true, true, true, true, false, false, true};
 int dense_block(int kind, int nt) { return nt + (kSelfFeed[kind] ? 0 : 32); }
@@ -128,6 +129,10 @@ const void* const kCgFn[kHvVariants] = HV_ROW(k_cg_fused);
         (const void*)k_hv_wc<7, D>, (const void*)k_hv_wc<8, D>                                        \
   }
 const void* const kWcFn[2][kMaxNQ + 1] = {WC_ROW(false), WC_ROW(true)};   // [dense P_rho][NQ]
+// dense P_rho without a producer warp (the one used for dense mode)
+const void* const kWcdFn[kMaxNQ + 1] = {nullptr,           (const void*)k_hv_wcd<1>, (const void*)k_hv_wcd<2>,
+                                        (const void*)k_hv_wcd<3>, (const void*)k_hv_wcd<4>, (const void*)k_hv_wcd<5>,
+                                        (const void*)k_hv_wcd<6>, (const void*)k_hv_wcd<7>, (const void*)k_hv_wcd<8>};
 int wc_stage_bytes(int nqw) {
   switch (nqw) {
     case 1: return WcGeo<1>::kStage;
@@ -207,6 +212,9 @@ struct otb_ctx {
   int hv_mode = 0, hv_grid = 0, hv_ng = 1;   // hv_mode 0 group smem, 1 global RED, 2 bitmap, 3 window clusters
   int hv_nb = 0, hv_win = 1;                   // row blocks (partial rows), CTAs per cluster (mode 3)
   int hv_var = 0, nq = 0, hv_threads = 512;   // kernel variant (sparse.cuh HvVar), bitmap words per row
+  int hv_ng_d = 0;                             // ring stages of the dense-P_rho window-cluster kernel
+  size_t hv_smem_d = 0;
+  bool hv_wcd = true;                          // OTB_HV_WCD=0: the producer-warp dense kernel (comparison)
   uint4* bm = nullptr;
   double* Pbuf = nullptr;    // P of the last eval (local rows x ld), streamed by sparsify
   unsigned long long* cg_trace = nullptr;   // OTB_CG_TRACE=1: phase stamps of the fused CG
@@ -684,13 +692,15 @@ int run_hv(otb_ctx* c, const double* v_src, const double* r, const double* p_pre
     HvArgs h{csr_view(c), c->a, n, c->hv_ng, v_src, r, p_prev, p_cur, update, st, c->colpart, c->bm, c->nq,
              c->hv_win, c->ld};
     if (c->hv_mode == 3 && c->rho_dense) h.A.vals = c->Pbuf;
+    const bool wcd = c->hv_mode == 3 && c->rho_dense && c->hv_wcd;   // dense P_rho: k_hv_wcd (no producer warp)
+    if (wcd) h.ng = c->hv_ng_d;
     TRY(prof_begin(c, &e0));
     void* args[1] = {&h};
     if (c->hv_mode == 3) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(c->hv_grid);
-      cfg.blockDim = dim3(kStThreads);
-      cfg.dynamicSmemBytes = c->hv_smem;
+      cfg.blockDim = dim3(wcd ? kStConsumers : kStThreads);
+      cfg.dynamicSmemBytes = wcd ? c->hv_smem_d : c->hv_smem;
       cfg.stream = c->stream;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -699,7 +709,7 @@ int run_hv(otb_ctx* c, const double* v_src, const double* r, const double* p_pre
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      CUDA_TRY(cudaLaunchKernelExC(&cfg, kWcFn[c->rho_dense ? 1 : 0][c->hv_var], args));
+      CUDA_TRY(cudaLaunchKernelExC(&cfg, wcd ? kWcdFn[c->hv_var] : kWcFn[c->rho_dense ? 1 : 0][c->hv_var], args));
     } else {
       CUDA_TRY(cudaLaunchKernel(kHvFn[c->hv_var], dim3(c->hv_grid), dim3(c->hv_threads), args, c->hv_smem,
                                 c->stream));
@@ -1297,6 +1307,37 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
       c->hv_smem = wc_smem_bytes(best_nq, wc_stage_bytes(best_nq), best_s);
       c->hv_nb = best_ncl;
       c->hv_grid = best_ncl * best_w;
+      const char* env_wcd = std::getenv("OTB_HV_WCD");
+      c->hv_wcd = !(env_wcd && std::atoi(env_wcd) == 0);
+      // the dense-P_rho kernel: no v window in shared memory, as many stages as fit
+      const int stage = wc_stage_bytes(best_nq);
+      c->hv_ng_d = (int)std::min<int64_t>(kWcMaxStages, (int64_t)(kMaxDynSmem - 8192) / (stage + 16));
+      c->hv_smem_d = (size_t)c->hv_ng_d * stage + 2 * (size_t)c->hv_ng_d * 8;
+      const void* fd = kWcdFn[best_nq];
+      cudaError_t e = allow_max_smem(fd, device);
+      if (e == cudaSuccess && best_w > 8) e = cudaFuncSetAttribute(fd, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      int ncd = 0;
+      if (e == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)c->hv_grid);
+        cfg.blockDim = dim3(kStConsumers);
+        cfg.dynamicSmemBytes = c->hv_smem_d;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)best_w;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        e = cudaOccupancyMaxActiveClusters(&ncd, fd, &cfg);
+      }
+      cudaGetLastError();
+      if (e != cudaSuccess || ncd < best_ncl) {   // keep the producer-warp dense kernel
+        if (std::getenv("OTB_DEBUG_GEOM"))
+          std::fprintf(stderr, "otb: k_hv_wcd<%d> W=%d: %d co-resident clusters (< %d, %s); producer-warp kernel kept\n",
+                       best_nq, best_w, ncd, best_ncl, cudaGetErrorString(e));
+        c->hv_wcd = false;
+      }
     }
   }
   if (c->hv_mode == 0 || c->hv_mode == 2) {
@@ -2077,6 +2118,15 @@ int otb_selftest_exp(const double* x, int64_t n, double* out) {
   if ((!x || !out) && n > 0) return fail(OTB_ERR_ARG, "null");
   if (n <= 0) return OTB_OK;
   k_selftest_exp<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256>>>(x, n, out);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaDeviceSynchronize());
+  return OTB_OK;
+}
+
+int otb_selftest_tab(const double* x, int64_t n, double* out) {
+  if ((!x || !out) && n > 0) return fail(OTB_ERR_ARG, "null");
+  if (n <= 0) return OTB_OK;
+  k_selftest_tab<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256>>>(x, n, out);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaDeviceSynchronize());
   return OTB_OK;

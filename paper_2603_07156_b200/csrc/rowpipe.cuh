@@ -204,8 +204,11 @@ struct Dense {
     const size_t off = (size_t)r * g.ld + c0 + (size_t)s * slice;
     bulk_g2s(stage_buf(st, 0), g.mat0 + off, bytes, &sm.full[st]);
     if (NM > 1) bulk_g2s(stage_buf(st, 1), g.mat1 + off, bytes, &sm.full[st]);
+    if constexpr (NV > 0) {
 #pragma unroll
-    for (int v = 0; v < NV; ++v) bulk_g2s(stage_buf(st, NM + v), g.vec[v] + c0 + (size_t)s * slice, vbytes, &sm.full[st]);
+      for (int v = 0; v < NV; ++v)
+        bulk_g2s(stage_buf(st, NM + v), g.vec[v] + c0 + (size_t)s * slice, vbytes, &sm.full[st]);
+    }
   }
 
   // Producer: stream every (row, slice) of this CTA's window.
@@ -232,6 +235,10 @@ struct Dense {
       // stage are issued before its arrival, in the same in-order shared
       // memory pipeline, and the refill's bulk copy lands a global round
       // trip after the last arrival.
+      // The count is checked at once: deferring the check (and the refill)
+      // by even one slice's arithmetic was measured slower (config 5: eval
+      // 17.6 -> 20.0 ms, test_c 28.1 -> 35.2 ms) — the ring is shallow and
+      // the refill latency matters more than the atomic's round trip.
       if (lane == 0) {
         uint32_t old;
         asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;"

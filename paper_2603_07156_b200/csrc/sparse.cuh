@@ -858,6 +858,7 @@ constexpr double kDenseRhoMin = 0.5;   // kept density above which sparsify writ
 constexpr int kWcD = 4;                  // exchange lookahead (rows)
 constexpr int kWcX = 2 * kWcD + 2;       // exchange buffers (>= 2 D + 1: see the note in wc_consume)
 constexpr int kWcMaxW = 16;
+constexpr int kWcMaxStages = 16;   // ring stages of the window-cluster kernels
 constexpr int kWcHdr = 32;
 
 template <int NQ>
@@ -982,7 +983,7 @@ OTB_DEV void wc_consume_keep(int cnt, const double* vsm, double (&acc)[2 * NQ], 
   using G = WcGeo<NQ>;
   constexpr int D = 1;
   const int lane = threadIdx.x & 31;
-  int stage = 0, rphase = 0;
+  int stage = 0;
   uint32_t phase = 0;
   double kv[D + 1][2 * NQ];
   double kar[D + 1];
@@ -1046,7 +1047,7 @@ OTB_DEV void wc_consume(int cnt, const double* __restrict__ vals, const double* 
   constexpr int NI = (NQ + 1) / 2;   // uint32 words of packed uint16 pair positions per row
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lb = 1u << lane, lt = lb - 1u;
-  int stage = 0, rphase = 0;
+  int stage = 0;
   uint32_t phase = 0;
   uint32_t pidx[D][NI];
 #pragma unroll
@@ -1160,6 +1161,146 @@ OTB_DEV void wc_consume(int cnt, const double* __restrict__ vals, const double* 
       }
     }
   }
+}
+
+// Dense-P_rho window-cluster hess_apply without a producer warp: 16
+// consumer warps (128 registers), the window of v in REGISTERS (no second
+// shared-memory read per value: the stage values are the only LDS traffic),
+// the ring refilled by the warp whose arrival completes a stage's round (as
+// in rowpipe.cuh Dense<.., true>).  Same per-thread sums, row order, row
+// reduction tree and exchange as wc_consume_keep: the same bits.
+template <int NQ>
+__global__ void __launch_bounds__(kStConsumers, 1) k_hv_wcd(HvArgs h) {
+  using G = WcGeo<NQ>;
+  extern __shared__ __align__(16) unsigned char wsm[];
+  __shared__ double xbuf[kWcX * kWcMaxW];
+  __shared__ uint64_t xbar[kWcX];
+  __shared__ double slots[2 * kMaxWarps * 4];
+  __shared__ uint32_t arrivals[kWcMaxStages];
+  const int W = h.nwin;
+  const int S = h.ng;   // ring stages
+  const int cr = (int)cluster_ctarank(), cid = blockIdx.x / W, ncl = gridDim.x / W;
+  const int lane = threadIdx.x & 31;
+  unsigned char* ring = wsm;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)S * G::kStage);
+  const int cb = 1024 * NQ * cr;                              // first column of this window
+  const int wcols = min(1024 * NQ, (int)(h.ld - cb));         // columns of the window inside the matrix
+  int rb, re;
+  cta_rows(h.A, cid, ncl, rb, re);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    for (int q = 0; q < kWcX; ++q) mbar_init(&xbar[q], 1);
+    fence_mbar_init();
+    for (int q = 0; q < kWcX; ++q) mbar_arrive_expect_tx(&xbar[q], 8u * (uint32_t)W);
+  }
+  if (threadIdx.x < kWcMaxStages) arrivals[threadIdx.x] = 0u;
+  if (wcols < 1024 * NQ)   // the last window's stage tail (past the matrix) reads as 0.0
+    for (int i = threadIdx.x; i < S * (1024 * NQ - wcols); i += blockDim.x) {
+      const int st = i / (1024 * NQ - wcols), col = wcols + i % (1024 * NQ - wcols);
+      reinterpret_cast<double*>(ring + (size_t)st * G::kStage + G::WW * 16 + kWcHdr)[col] = 0.0;
+    }
+  fence_proxy_async();
+  __syncwarp();
+  cluster_sync_all();
+  // bulk copy of local row r's window into stage st
+  auto issue = [&](int st, int r) {
+    unsigned char* sp = ring + (size_t)st * G::kStage;
+    mbar_arrive_expect_tx(&full[st], (uint32_t)wcols * 8u);
+    bulk_g2s(sp + G::WW * 16 + kWcHdr, h.A.vals + (size_t)r * h.ld + cb, (uint32_t)wcols * 8u, &full[st]);
+  };
+  if (h.st == nullptr || h.st->status == CG_RUN) {   // same decision in every CTA
+    if (threadIdx.x == 0)
+      for (int s = 0; s < S && rb + s < re; ++s) issue(s, rb + s);
+    // the window of v in registers; p = r + beta p by the column's owner (krylov.py:83)
+    const double beta = h.update ? h.st->beta : 0.0;
+    double vr[2 * NQ], acc[2 * NQ];
+#pragma unroll
+    for (int i = 0; i < 2 * NQ; ++i) {
+      const int j = cb + bm_col<16>(i >> 1, i & 1);
+      double v = 0.0;
+      if (j < h.n) {
+        if (h.update) {
+          v = h.r[j] + beta * h.p_prev[j];
+          if (cid == 0) h.p_cur[j] = v;
+        } else {
+          v = h.v_src[j];
+        }
+      }
+      vr[i] = v;
+      acc[i] = 0.0;
+    }
+    const int cnt = re - rb;
+    const uint32_t nwarps = kStConsumers / 32;
+    int stage = 0, fill = S;   // fill: local index of the row the next refill of `stage` loads
+    uint32_t phase = 0, rounds = 1;
+    constexpr int D = 1;
+    double kv[D + 1][2 * NQ];
+    double kar[D + 1];
+    for (int k0 = 0; k0 < cnt + D; k0 += D + 1) {
+#pragma unroll
+      for (int j = 0; j <= D; ++j) {
+        const int k = k0 + j, ku = k - D;
+        if (k < cnt) {   // dots of row k; its values stay in slot j
+          mbar_wait(&full[stage], phase);
+          kar[j] = __ldg(h.a + h.A.row0 + rb + k);   // a_r, used by the update one row later
+          const unsigned char* sp = ring + (size_t)stage * G::kStage;
+          const double* sv = reinterpret_cast<const double*>(sp + G::WW * 16 + kWcHdr);
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int t = 0; t < NQ; ++t) {
+            const double2 x = *reinterpret_cast<const double2*>(sv + bm_col<16>(t, 0));
+            kv[j][2 * t] = x.x;
+            kv[j][2 * t + 1] = x.y;
+            d0 = fma(x.x, vr[2 * t], d0);
+            d1 = fma(x.y, vr[2 * t + 1], d1);
+          }
+          __syncwarp();
+          // the arrival that completes the stage's round refills it; its
+          // count is checked after the row's partial went out (the atomic's
+          // round trip overlaps the reduction)
+          uint32_t old = 0u;
+          if (lane == 0)
+            asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;"
+                         : "=r"(old)
+                         : "r"(smem_u32(&arrivals[stage]))
+                         : "memory");
+          const int rst = stage, rfill = fill;
+          const uint32_t tgt = rounds * nwarps - 1u;
+          ++fill;
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1u;
+            ++rounds;
+          }
+          wc_send_partial(d0 + d1, k, slots, xbuf, xbar, W, cr);
+          if (lane == 0 && old == tgt && rfill < cnt) {
+            fence_proxy_async();
+            issue(rst, rb + rfill);
+          }
+        }
+        if (ku >= 0 && ku < cnt) {   // row ku: full dot, then the update
+          const int ju = (j + 1) % (D + 1);
+          const int q = ku % kWcX;
+          mbar_wait(&xbar[q], (uint32_t)((ku / kWcX) & 1));
+          double dot = (lane < W) ? xbuf[q * kWcMaxW + lane] : 0.0;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+          if (threadIdx.x == 0) mbar_arrive_expect_tx(&xbar[q], 8u * (uint32_t)W);
+          const double w = kar[ju] * dot;   // sparsify.py:153: weights * pv
+#pragma unroll
+          for (int i = 0; i < 2 * NQ; ++i) acc[i] = fma(kv[ju][i], w, acc[i]);
+        }
+      }
+    }
+    double* dst = h.colpart + (size_t)cid * h.n;
+#pragma unroll
+    for (int i = 0; i < 2 * NQ; ++i) {
+      const int jj = cb + bm_col<16>(i >> 1, i & 1);
+      if (jj < h.n) dst[jj] = acc[i];
+    }
+  }
+  __syncwarp();
+  cluster_sync_all();   // no CTA leaves while a peer may still address its shared memory
 }
 
 template <int NQ, bool DENSE>

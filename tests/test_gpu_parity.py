@@ -614,6 +614,41 @@ def test_fast_exp_is_cuda_exp(cuda):
         assert np.max(np.abs(ref[fin] - np.exp(x[fin])) / np.spacing(np.exp(x[fin]))) <= 2.0
 
 
+def test_table_exp_log_accuracy(cuda):
+    """The streaming passes' table-driven exp (<= 0.51 ulp by construction)
+    and log (<= 1.5 ulp) with their fallbacks (exp() for |x| >= 707 and NaN,
+    log_fast near 1 and for special inputs), against numpy on the range
+    edges, subnormal results, special values and the near-1 switch."""
+    import torch
+
+    from paper_2603_07156_b200 import _lib
+
+    rng = np.random.default_rng(23)
+    x = np.concatenate([rng.uniform(-750, 710, 400_000), rng.standard_normal(200_000) * 30,
+                        rng.uniform(-1e-3, 1e-3, 100_000), np.linspace(-708.0, -706.0, 20_001),
+                        np.linspace(706.0, 708.0, 20_001), -(2.0 ** np.arange(-1074, 11, dtype=np.float64)),
+                        np.exp(rng.uniform(-700, 700, 200_000)), 1.0 + rng.uniform(-0.05, 0.05, 100_000),
+                        2.0 ** rng.integers(-1070, 1020, 20_000) * rng.uniform(1, 2, 20_000),
+                        np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, 1.0, 0.984375, 1.015625,
+                                  709.782712893384, -745.1332191019412, -1e6])])
+    xd = torch.from_numpy(x).cuda()
+    out = torch.empty(2 * x.size, dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib.otb_selftest_tab(xd.data_ptr(), x.size, out.data_ptr()))
+    got = out.cpu().numpy()
+    e, lg = got[: x.size], got[x.size:]
+    with np.errstate(all="ignore"):
+        we, wl = np.exp(x), np.log(x)
+    fin = np.isfinite(we) & (we > 0)
+    ulp_e = np.abs(e[fin] - we[fin]) / np.spacing(we[fin])
+    assert ulp_e.max() <= 1.0, (ulp_e.max(), x[fin][np.argmax(ulp_e)])
+    assert np.array_equal(np.isnan(e), np.isnan(we)) and np.array_equal(e[~fin & ~np.isnan(we)], we[~fin & ~np.isnan(we)])
+    finl = np.isfinite(wl) & (wl != 0)
+    ulp_l = np.abs(lg[finl] - wl[finl]) / np.spacing(np.abs(wl[finl]))
+    assert ulp_l.max() <= 2.0, (ulp_l.max(), x[finl][np.argmax(ulp_l)])
+    assert lg[x == 1.0][0] == 0.0
+    assert np.isneginf(lg[x == 0.0]).all() and np.isnan(lg[x == -1.0]).all() and np.isposinf(lg[x == np.inf]).all()
+
+
 def test_host_tensor_log_plan_check_and_clamp_on_device(cuda):
     """A LogPlan given as a host torch tensor is checked and clamped on the
     device in one pass (otb_check_clamp_plan, core.py:141-145): NaN or +inf
