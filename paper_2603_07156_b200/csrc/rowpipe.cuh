@@ -213,7 +213,8 @@ struct Dense {
 
   // Producer: stream every (row, slice) of this CTA's window.
   OTB_DEV void produce() {
-    if (SELF || lane != 0) return;
+    if constexpr (SELF) return;
+    if (lane != 0) return;
     for (int r = r0; r < r1; ++r) {
       for (int s = 0; s < nsl; ++s) {
         mbar_wait(&sm.empty[stage], phase ^ 1u);
