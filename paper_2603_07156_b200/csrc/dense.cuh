@@ -593,6 +593,140 @@ __global__ void __launch_bounds__(FROMP ? kSelfThreads : kMaxThreads, OTB_DENSE_
   D.finish();
 }
 
+// Dense P_rho from the stored P, lean (sparsify's dense mode when P is
+// valid): the same kept set, kept sum, values and d (and PCG diagonal)
+// bits as k_sparsify<NS, true> with io.dense, with the keep decision
+// recomputed from P in the write loop instead of per-row bit masks, no
+// run/bitmap machinery, and the masked columns of a partial last slice
+// handled by one uniform branch.
+template <int NS>
+__global__ void __launch_bounds__(kSelfThreads, 1) k_sparsify_dense(Geom geo, SparsifyIO io) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  Dense<1, true> D;
+  D.setup(geo, smem);
+  const double rho = io.gnorm != nullptr ? (io.eta * *io.gnorm) / io.mn : io.rho;   // inner_newton.py:112-114
+  const int nsl = D.nsl;
+  const bool tail = D.tail;
+  const int lastv = D.c1 - (D.c0 + (nsl - 1) * D.slice) - 2 * D.tid;   // valid columns of the last pair
+  const bool pcg = io.colpart2 != nullptr;
+  unsigned long long kept = 0;
+  for (int r = D.r0; r < D.r1; ++r) {
+    const bool anc = (r == io.anchor_local);
+    double P[2 * NS];
+    double ks = 0.0;
+    int kc = 0;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      if (s < nsl) {
+        double2 v[1];
+        D.fetchn(v);
+        P[2 * s] = v[0].x;
+        P[2 * s + 1] = v[0].y;
+        if (tail && s == nsl - 1) {   // masked columns: -1 (never kept, never the argmax)
+          P[2 * s] = lastv > 0 ? P[2 * s] : -1.0;
+          P[2 * s + 1] = lastv > 1 ? P[2 * s + 1] : -1.0;
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {   // sparsify.py:96-101
+          const double p = P[2 * s + e];
+          const bool k = anc ? p >= 0.0 : (p >= rho && p > 0.0);
+          if (k) {
+            ks += p;
+            ++kc;
+          }
+        }
+      }
+    }
+    // kept sum and kept count of the row: one block reduction of both, one
+    // cluster exchange (the trees of k_sparsify's dense mode)
+    double t2[2] = {ks, (double)kc};
+    D.template reduce<2, kSum>(t2);
+    double ksum = t2[0], kcnt = t2[1];
+    if (D.g.cl > 1) {
+      const double* all = D.template exchange<2>(t2);
+      ksum = 0.0;
+      kcnt = 0.0;
+      for (int q = 0; q < D.g.cl; ++q) {
+        ksum += all[q * 4];
+        kcnt += all[q * 4 + 1];
+      }
+    }
+    int jbest = -1;
+    const bool fallback = !anc && kcnt == 0.0;
+    if (fallback) {   // sparsify.py:103-107: keep the first argmax of the row with value 1
+      double pm = -1.0;
+#pragma unroll
+      for (int k = 0; k < 2 * NS; ++k)
+        if ((k >> 1) < nsl) pm = fmax(pm, P[k]);
+      double u[1] = {pm};
+      D.template reduce<1, kMax>(u);
+      const double pmax = u[0];
+      double jm = 1e300;
+#pragma unroll
+      for (int k = 0; k < 2 * NS; ++k)
+        if ((k >> 1) < nsl && P[k] >= 0.0 && P[k] == pmax) jm = fmin(jm, (double)D.col(k >> 1, k & 1));
+      u[0] = jm;
+      D.template reduce<1, kMin>(u);
+      jm = u[0];
+      if (D.g.cl > 1) {
+        double v2[2] = {pmax, jm};
+        const double* all = D.template exchange<2>(v2);
+        double bp = all[0], bj = all[1];
+        for (int q = 1; q < D.g.cl; ++q) {
+          if (all[q * 4] > bp || (all[q * 4] == bp && all[q * 4 + 1] < bj)) {
+            bp = all[q * 4];
+            bj = all[q * 4 + 1];
+          }
+        }
+        jm = bj;
+      }
+      jbest = (int)jm;
+    }
+    const double ai = __ldg(io.a + D.g.row0 + r);
+    double* drow = io.dense + (size_t)r * D.g.ld + D.col(0, 0);
+    const Divider DK(ksum);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      if (s < nsl) {
+        const double p0 = P[2 * s], p1 = P[2 * s + 1];
+        double v0, v1;
+        if (fallback) {
+          const int j = D.col(s, 0);
+          v0 = (j == jbest && p0 >= 0.0) ? 1.0 : 0.0;
+          v1 = (j + 1 == jbest && p1 >= 0.0) ? 1.0 : 0.0;
+        } else {   // sparsify.py:109-110: kept / kept_sum (the anchor row unnormalised)
+          const bool k0 = anc ? p0 >= 0.0 : (p0 >= rho && p0 > 0.0);
+          const bool k1 = anc ? p1 >= 0.0 : (p1 >= rho && p1 > 0.0);
+          double n0 = p0, n1 = p1;
+          if (!anc) DK.pair(p0, p1, n0, n1);
+          v0 = k0 ? n0 : 0.0;
+          v1 = k1 ? n1 : 0.0;
+        }
+        double* dst = drow + s * D.slice;
+        if (!(tail && s == nsl - 1) || lastv > 1) {
+          *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+        } else if (lastv > 0) {
+          dst[0] = v0;
+        }
+        double2* a2 = D.acc2(0, s);   // d += a_i v (0 where dropped: the same bits as adding only kept)
+        a2->x += ai * v0;
+        a2->y += ai * v1;
+        if (pcg) {   // Jacobi diagonal of P_rho^T diag(a) P_rho
+          double2* q2 = D.acc2(1, s);
+          q2->x += ai * (v0 * v0);
+          q2->y += ai * (v1 * v1);
+        }
+      }
+    }
+    if (D.tid == 0 && D.cr == 0) kept += fallback ? 1ull : (unsigned long long)kcnt;
+  }
+  if (D.tid == 0 && D.cr == 0 && kept) atomicAdd(io.nnzc, kept);
+  bar_sync(1, D.g.nt);
+  D.store_acc(0, io.colpart + (size_t)D.cid * D.g.n);
+  if (pcg) D.store_acc(1, io.colpart2 + (size_t)D.cid * D.g.n);
+  D.finish();
+}
+
 // ------------------------------------------------- inexact test, pass A (K7/K8)
 // inner_newton.py:160-167 + core.py:141-145 (candidate log plan, NaN/+inf
 // check, floor clamp) fused with feasibility.py:56-60 (row sums, z, column
@@ -693,8 +827,8 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_a(Geom geo, TestAIO io
       if (s < nsl) {
         double2* a2 = D.acc2(0, s);
         double2 v = *a2;
-        v.x = v.x + xv[2 * s] * z;
-        v.y = v.y + xv[2 * s + 1] * z;
+        v.x = fma(xv[2 * s], z, v.x);   // column sums: a reduction, fused multiply-add
+        v.y = fma(xv[2 * s + 1], z, v.y);
         *a2 = v;
       }
     }
@@ -862,24 +996,25 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_c(Geom geo, TestCIO io
         for (int e = 0; e < 2; ++e) {
           const double xl = e ? x.y : x.x;
           const double fv = f2[e];
-          const double dterm = fv * (lg[e] - xl);
-          acc[0] += fv > 0.0 ? dterm : 0.0;
+          // the sums below are reductions (their order differs from numpy's
+          // anyway): fused multiply-adds
+          acc[0] = fma(fv > 0.0 ? fv : 0.0, lg[e] - xl, acc[0]);
           acc[1] += fv;
           rs += fv;
           if constexpr (METRICS) {
             const double cv = e ? v[1].y : v[1].x;
             const double gv = e ? v[NM + 2].y : v[NM + 2].x;
-            acc[2] += cv * fv;
-            acc[3] += fv * fv;
+            acc[2] = fma(cv, fv, acc[2]);
+            acc[3] = fma(fv, fv, acc[3]);
             const double fm = fmin(fv, 0.0);
-            acc[4] += fm * fm;
+            acc[4] = fma(fm, fm, acc[4]);
             const double shv = cv - gv;
             // slack = shv - zeta >= 0 exactly (zeta is the row minimum of the
             // same shv values, and fl(a - b) >= 0 for a >= b), so the
             // reference's sum min(slack, 0)^2 (feasibility.py:117) is 0:
             // acc[5] stays 0
             if constexpr (kZetaFromA) {
-              acc[6] += fv * (shv - zeta_a);
+              acc[6] = fma(fv, shv - zeta_a, acc[6]);
             } else {
               fk[2 * s + e] = fv;
               shk[2 * s + e] = shv;
@@ -897,7 +1032,7 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_c(Geom geo, TestCIO io
       for (int s = 0; s < NS; ++s) {
         if (s < nsl) {
 #pragma unroll
-          for (int e = 0; e < 2; ++e) acc[6] += fk[2 * s + e] * (shk[2 * s + e] - zeta);   // slack >= 0: acc[5] = 0
+          for (int e = 0; e < 2; ++e) acc[6] = fma(fk[2 * s + e], shk[2 * s + e] - zeta, acc[6]);   // slack >= 0: acc[5] = 0
         }
       }
     }

@@ -86,17 +86,18 @@ int load_nccl(const char* path, Nccl& api) {
 
 // ------------------------------------------------------------- kernels
 enum DenseKind {
-  DK_EVAL = 0, DK_SPARSIFY, DK_TESTA, DK_TESTB, DK_TESTC0, DK_TESTC1, DK_WARMZ, DK_WARMG, DK_SPARSP, DK_COUNT
+  DK_EVAL = 0, DK_SPARSIFY, DK_TESTA, DK_TESTB, DK_TESTC0, DK_TESTC1, DK_WARMZ, DK_WARMG, DK_SPARSP, DK_SPDENSE,
+  DK_COUNT
 };
 // streamed arrays: eval and test_a C, log X, gamma; test_b X, y; test_c X, y, e_c (+ C, gamma with
 // the metrics)
-const int kNmat[DK_COUNT] = {3, 2, 3, 2, 3, 5, 2, 2, 1};
-const int kNacc[DK_COUNT] = {1, 1, 1, 0, 0, 0, 1, 2, 1};   // shared accumulators (test_b, test_c: registers)
+const int kNmat[DK_COUNT] = {3, 2, 3, 2, 3, 5, 2, 2, 1, 1};
+const int kNacc[DK_COUNT] = {1, 1, 1, 0, 0, 0, 1, 2, 1, 1};   // shared accumulators (test_b, test_c: registers)
 // static shared memory (sparsify: scan table; test_b/test_c: deferred row-sum slots; exp/log tables)
 const int kStaticSmem[DK_COUNT] = {2048, (int)(kTabInts * 4 + 16 + 2048), 2048, 4096, 8192, 8192, 0, 0,
-                                   (int)(kTabInts * 4 + 16 + 2048)};
+                                   (int)(kTabInts * 4 + 16 + 2048), 0};
 // kinds whose CTA has no producer warp (Dense<NMAT, true>: the consumers refill the ring)
-const bool kSelfFeed[DK_COUNT] = {true, false, true, true, true, true, false, false, true};
+const bool kSelfFeed[DK_COUNT] = {true, false, true, true, true, true, false, false, true, true};
 int dense_block(int kind, int nt) { return nt + (kSelfFeed[kind] ? 0 : 32); }
 constexpr int kMaxStageSelf = 16;   // ring depth cap of the self-fed kinds (misc holds their counters)
 
@@ -112,7 +113,7 @@ static_assert(kMaxNS == 10, "kDenseFn rows list NS = 1..10");
 const void* const kDenseFn[DK_COUNT][kMaxNS + 1] = {
     NS_ROW(k_eval),          NS_ROW2(k_sparsify, false), NS_ROW(k_test_a),    NS_ROW(k_test_b),
     NS_ROW2(k_test_c, false), NS_ROW2(k_test_c, true),   NS_ROW(k_warm_zeta), NS_ROW(k_warm_gamma),
-    NS_ROW2(k_sparsify, true)};
+    NS_ROW2(k_sparsify, true), NS_ROW(k_sparsify_dense)};
 
 #define HV_ROW(K)                                                                                    \
   {                                                                                                  \
@@ -323,7 +324,7 @@ cudaError_t allow_max_smem(const void* fn, int device) {
 
 // Jacobi PCG: sparsify also accumulates q = (P_rho o P_rho)^T a (accumulator 1)
 int nacc_of(const otb_ctx* c, int kind) {
-  return ((kind == DK_SPARSIFY || kind == DK_SPARSP) && c->precond) ? 2 : kNacc[kind];
+  return ((kind == DK_SPARSIFY || kind == DK_SPARSP || kind == DK_SPDENSE) && c->precond) ? 2 : kNacc[kind];
 }
 
 size_t dense_smem(const otb_ctx* c, int kind, int nstage) {
@@ -570,7 +571,6 @@ int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho
   // alloc, nnzc, flags are adjacent in DevScalars
   CUDA_TRY(cudaMemsetAsync(&c->ds->alloc, 0, 2 * sizeof(unsigned long long) + sizeof(int), c->stream));
   const int kind = c->p_valid ? DK_SPARSP : DK_SPARSIFY;
-  Geom geo = c->p_valid ? make_geom(c, DK_SPARSP, c->Pbuf, nullptr) : make_geom(c, DK_SPARSIFY, c->C, X);
   const bool bitmap = c->hv_mode == 2 || c->hv_mode == 3;   // hess_apply reads the bitmap, not the columns
   // window-cluster hess_apply: dense P_rho (written over the stored P) when
   // most pairs are kept — a fixed position per value instead of bitmap
@@ -580,6 +580,9 @@ int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho
   c->dense_policy = env_hd ? (std::atoi(env_hd) > 0 ? 1 : 0) : -1;
   const bool dense = c->hv_mode == 3 && c->Pbuf != nullptr &&
                      (c->dense_policy == 1 || (c->dense_policy < 0 && c->last_density >= kDenseRhoMin));
+  // dense P_rho from the stored P: the lean kernel (same bits as k_sparsify's dense mode)
+  const int launch_kind = (dense && c->p_valid) ? (int)DK_SPDENSE : kind;
+  Geom geo = c->p_valid ? make_geom(c, launch_kind, c->Pbuf, nullptr) : make_geom(c, DK_SPARSIFY, c->C, X);
   SparsifyIO io{gamma, c->a, c->eta, rho, anchor_local, c->rowM, c->rowS, c->lse, bitmap ? nullptr : c->cols,
                 c->vals, c->cap,
                 c->row_start, c->row_len, &c->ds->alloc, &c->ds->nnzc, c->chunk, c->colpart, &c->ds->flags,
@@ -588,7 +591,7 @@ int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho
   c->rho_dense = dense;
   cudaEvent_t e0 = nullptr;
   TRY(prof_begin(c, &e0));
-  TRY(launch_dense(c, kind, geo, &io));
+  TRY(launch_dense(c, launch_kind, geo, &io));
   if (dense) c->p_valid = false;   // Pbuf now holds P_rho
   *rec = c->prof ? (int64_t)c->recs.size() : -1;
   TRY(prof_end(c, PC_SPARSIFY, e0, 0.0));
@@ -1550,7 +1553,7 @@ int otb_set_cg_precond(otb_ctx* c, int kind) {
   }
   c->precond = kind;
   // the sparsify passes carry a second accumulator: re-size their rings
-  for (int k : {(int)DK_SPARSIFY, (int)DK_SPARSP}) {
+  for (int k : {(int)DK_SPARSIFY, (int)DK_SPARSP, (int)DK_SPDENSE}) {
     const size_t budget = kMaxDynSmem - kStaticSmem[k] - 1024;
     int st = kSelfFeed[k] ? kMaxStageSelf : 8;
     while (st > 2 && dense_smem(c, k, st) > budget) --st;
