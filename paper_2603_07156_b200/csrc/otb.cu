@@ -206,7 +206,7 @@ struct otb_ctx {
   int64_t m_glob = 0, n = 0, row0 = 0, row1 = 0, m_loc = 0, ld = 0;
   int num_sms = 148;
   // dense geometry
-  int nt = 0, ns = 0, cl = 1, colw = 0, ncl = 0, grid = 0;
+  int nt = 0, ns = 0, cl = 1, colw = 0, ncl = 0, grid = 0, per_sm = 1;
   int nstage[DK_COUNT] = {};
   size_t smem[DK_COUNT] = {};
   // hess_apply
@@ -329,7 +329,8 @@ int nacc_of(const otb_ctx* c, int kind) {
 
 size_t dense_smem(const otb_ctx* c, int kind, int nstage) {
   const size_t slice = 2 * (size_t)c->nt;
-  const size_t dbl = (size_t)nstage * kNmat[kind] * slice + (size_t)nacc_of(c, kind) * c->ns * slice + 2 * kMaxWarps * 4 + kXb * 8 * 4;
+  const size_t dbl = (size_t)nstage * kNmat[kind] * slice + (size_t)nacc_of(c, kind) * c->ns * slice + 2 * kMaxWarps * 4 +
+                     kXb * kMaxCluster * 4;
   return dbl * 8 + (2 * (size_t)nstage + kXb) * 8 + 64 * 4;
 }
 
@@ -1085,13 +1086,19 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   c->num_sms = sms;
-  // dense geometry: cluster size, column window, slices, threads
-  // Cluster size: any cl <= 8 whose window fits one CTA (<= kMaxNS slices),
+  // dense geometry: CTAs per SM, cluster size, column window, slices, threads
+  // Cluster size: any cl <= 16 whose window fits one CTA (<= kMaxNS slices),
   // chosen for the least time per row block: rows per co-resident cluster x
   // (slices per CTA + the cost of the row exchanges, ~2 slices).  Clusters
   // must fit in a GPC, so the co-resident count is queried: e.g. n = 50000
   // gets cl = 5 (26 clusters, 130 SMs) instead of cl = 8 (15 clusters,
-  // 120 SMs).  OTB_DENSE_CL forces the size.
+  // 120 SMs).  OTB_DENSE_CL forces the size.  OTB_DENSE_CTAS_PER_SM=2: two
+  // CTAs of at most 256 threads per SM (512-column slices, half the shared
+  // memory each), so that one CTA's row synchronisation overlaps the other's
+  // arithmetic.
+  const char* env_cps = std::getenv("OTB_DENSE_CTAS_PER_SM");
+  const int per_sm = env_cps ? std::max(1, std::min(2, std::atoi(env_cps))) : 1;
+  const int slice_cols = 1024 / per_sm;   // 2 x the most threads per CTA
   int cl = 1;
   {
     const char* env_cl = std::getenv("OTB_DENSE_CL");
@@ -1100,20 +1107,22 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
     for (int q = 1; q <= kMaxCluster; ++q) {
       if (force_cl > 0 && q != force_cl) continue;
       const int64_t colw_q = rup(cdiv(n, q), q > 1 ? 64 : 2);
-      if (cdiv(colw_q, 1024) > kMaxNS) continue;
-      const int ns_q = (int)std::max<int64_t>(1, cdiv(colw_q, 1024));
+      if (cdiv(colw_q, slice_cols) > kMaxNS) continue;
+      const int ns_q = (int)std::max<int64_t>(1, cdiv(colw_q, slice_cols));
       const int nt_q = (int)std::max<int64_t>(32, rup(cdiv(colw_q, 2 * ns_q), 32));
-      int fit = sms / q;
+      int fit = sms * per_sm / q;
       if (q > 1) {
         c->nt = nt_q;
         c->ns = ns_q;
         int st = 8;
-        while (st > 2 && dense_smem(c, DK_EVAL, st) > kMaxDynSmem - 1024) --st;
+        while (st > 2 && dense_smem(c, DK_EVAL, st) > kMaxDynSmem / per_sm - kStaticSmem[DK_EVAL] - 1024) --st;
         const void* fn = kDenseFn[DK_EVAL][ns_q];
         int nclus = 0;
-        if (allow_max_smem(fn, device) == cudaSuccess) {
+        cudaError_t e = allow_max_smem(fn, device);
+        if (e == cudaSuccess && q > 8) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e == cudaSuccess) {
           cudaLaunchConfig_t cfg = {};
-          cfg.gridDim = dim3((unsigned)(q * (sms / q)));
+          cfg.gridDim = dim3((unsigned)(q * (sms * per_sm / q)));
           cfg.blockDim = dim3((unsigned)dense_block(DK_EVAL, nt_q));
           cfg.dynamicSmemBytes = dense_smem(c, DK_EVAL, st);
           cudaLaunchAttribute attr[1];
@@ -1142,13 +1151,14 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
     }
   }
   c->cl = cl;
+  c->per_sm = per_sm;
   c->colw = (int)rup(cdiv(n, cl), cl > 1 ? 64 : 2);   // cluster windows start on 64-column words
-  int ns = (int)std::min<int64_t>(kMaxNS, std::max<int64_t>(1, cdiv(c->colw, 1024)));
+  int ns = (int)std::min<int64_t>(kMaxNS, std::max<int64_t>(1, cdiv(c->colw, slice_cols)));
   int nt = (int)rup(cdiv(c->colw, 2 * ns), 32);
   const char* env_nt = std::getenv("OTB_DENSE_NT");
   if (env_nt) {
     const int want = std::atoi(env_nt);
-    if (want >= 32 && want <= 512 && want % 32 == 0) {
+    if (want >= 32 && want <= slice_cols / 2 && want % 32 == 0) {
       nt = want;
       ns = (int)cdiv(c->colw, 2 * nt);
       if (ns > kMaxNS) {
@@ -1163,9 +1173,6 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   // can end on a partial slice (whose masked columns lie past n, where the
   // eval's gamma stream is -inf)
   if (cl > 1) c->colw = 2 * c->nt * c->ns;
-  int per_sm = 1;
-  const char* env_cps = std::getenv("OTB_DENSE_CTAS_PER_SM");
-  if (env_cps) per_sm = std::max(1, std::min(4, std::atoi(env_cps)));
   c->ncl = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)(sms * per_sm) / cl, c->m_loc));
   c->grid = c->ncl * cl;
   // ring depth: 8 stages unless OTB_DENSE_NSTAGE caps it (a shallower ring
@@ -1180,10 +1187,15 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
     c->nstage[k] = st;
     c->smem[k] = dense_smem(c, k, st);
     if (c->smem[k] > budget) {
+      if (std::getenv("OTB_DEBUG_GEOM"))
+        std::fprintf(stderr, "otb: dense kind %d: %zu B of shared memory > %zu (nt %d, ns %d, cl %d, %d per SM)\n", k,
+                     c->smem[k], budget, c->nt, c->ns, cl, per_sm);
       delete c;
       return fail(OTB_ERR_ARG, "dense geometry does not fit shared memory");
     }
     cudaError_t e = allow_max_smem(kDenseFn[k][c->ns], device);
+    if (e == cudaSuccess && cl > 8)
+      e = cudaFuncSetAttribute(kDenseFn[k][c->ns], cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e == cudaSuccess && env_ns) {   // carve only what the ring needs: the rest is L1
       const int pct = (int)std::min<int64_t>(100, cdiv(100 * (int64_t)(c->smem[k] + kStaticSmem[k] + 1024), 233472));
       e = cudaFuncSetAttribute(kDenseFn[k][c->ns], cudaFuncAttributePreferredSharedMemoryCarveout, pct);
@@ -1554,7 +1566,7 @@ int otb_set_cg_precond(otb_ctx* c, int kind) {
   c->precond = kind;
   // the sparsify passes carry a second accumulator: re-size their rings
   for (int k : {(int)DK_SPARSIFY, (int)DK_SPARSP, (int)DK_SPDENSE}) {
-    const size_t budget = kMaxDynSmem - kStaticSmem[k] - 1024;
+    const size_t budget = kMaxDynSmem / c->per_sm - kStaticSmem[k] - 1024;
     int st = kSelfFeed[k] ? kMaxStageSelf : 8;
     while (st > 2 && dense_smem(c, k, st) > budget) --st;
     if (dense_smem(c, k, st) > budget) return fail(OTB_ERR_ARG, "PCG accumulator does not fit shared memory");

@@ -25,7 +25,7 @@
 
 namespace otb {
 
-constexpr int kMaxCluster = 8;
+constexpr int kMaxCluster = 16;   // > 8: non-portable cluster sizes
 constexpr int kXb = 4;       // cluster exchange buffers (rotating; >= 3 needed, see exchange())
 constexpr int kMaxNS = 10;   // 1024-column slices per CTA: one CTA per row up to n = 10240
 
@@ -52,7 +52,7 @@ struct SmemMap {
   double* ring;      // nstage * nmat * 2nt
   double* acc;       // nacc * ns * 2nt
   double* slots;     // 2 * kMaxWarps * 4
-  double* xbuf;      // kXb * 8 * 4
+  double* xbuf;      // kXb * kMaxCluster * 4
   uint64_t* full;    // nstage
   uint64_t* empty;   // nstage
   uint64_t* xbar;    // kXb
@@ -61,7 +61,7 @@ struct SmemMap {
 
 OTB_DEV size_t smem_bytes_for(const Geom& g, int nmat) {
   size_t slice = 2 * (size_t)g.nt;
-  size_t d = (size_t)g.nstage * nmat * slice + (size_t)g.nacc * g.ns * slice + 2 * kMaxWarps * 4 + kXb * 8 * 4;
+  size_t d = (size_t)g.nstage * nmat * slice + (size_t)g.nacc * g.ns * slice + 2 * kMaxWarps * 4 + kXb * kMaxCluster * 4;
   return d * 8 + (2 * (size_t)g.nstage + kXb) * 8 + 64 * 4;
 }
 
@@ -76,7 +76,7 @@ OTB_DEV SmemMap carve(const Geom& g, int nmat, unsigned char* base) {
   s.slots = p;
   p += 2 * kMaxWarps * 4;
   s.xbuf = p;
-  p += kXb * 8 * 4;
+  p += kXb * kMaxCluster * 4;
   uint64_t* b = reinterpret_cast<uint64_t*>(p);
   s.full = b;
   s.empty = b + g.nstage;

@@ -19,7 +19,8 @@ import os
 import subprocess
 import sys
 
-CLASS = {"k_cg_fused": "cg_fused", "k_eval": "eval", "k_sparsify": "sparsify", "k_test_a": "test_a",
+CLASS = {"k_cg_fused": "cg_fused", "k_eval": "eval", "k_sparsify_dense": "sparsify", "k_sparsify": "sparsify",
+         "k_test_a": "test_a", "k_hv_wcd": "hess_apply",
          "k_test_b": "test_b", "k_test_c": "test_c", "k_hv_grp": "hess_apply", "k_hv_wc": "hess_apply", "k_warm_zeta": "warm_zeta",
          "k_warm_gamma": "warm_gamma"}
 
