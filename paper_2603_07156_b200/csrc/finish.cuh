@@ -517,6 +517,26 @@ __global__ void k_warm_gamma_post(int n, const double* M, const double* S, const
 
 // zeta_i = eta (log a_i - lse_i): the row potential of the accepted dual
 // (bregman_outer.py:123-126 -> sinkhorn.py:47-51 on the cached lse).
+// Kept-density estimate before a context's first sparsify (no history to
+// choose dense P_rho or the bitmap runs from): the fraction of P >= rho
+// (P > 0) over every `stride`-th local row of the stored P.  One count in
+// *out (relaxed atomic: only compared against a threshold).
+__global__ void k_density_sample(const double* __restrict__ P, int64_t ld, int m_loc, int n, int stride,
+                                 const double* gnorm, double eta, double mn, double rho_host,
+                                 unsigned long long* out) {
+  const double rho = gnorm != nullptr ? (eta * *gnorm) / mn : rho_host;   // inner_newton.py:112-114
+  unsigned long long cnt = 0;
+  const int rows = (m_loc + stride - 1) / stride;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < (int64_t)rows * n;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(idx / n) * stride, j = (int)(idx % n);
+    const double p = P[(size_t)r * ld + j];
+    cnt += (p >= rho && p > 0.0) ? 1ull : 0ull;
+  }
+  cnt = (unsigned long long)warp_sum_i((int)cnt);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(out, cnt);
+}
+
 __global__ void k_zeta_from_lse(int m_loc, const double* log_a, int64_t row0, const double* lse, double eta,
                                 double* zeta) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m_loc; i += gridDim.x * blockDim.x)

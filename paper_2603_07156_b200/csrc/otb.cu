@@ -223,6 +223,7 @@ struct otb_ctx {
   bool rho_dense = false;    // the last sparsify wrote P_rho dense into Pbuf (window-cluster hess_apply)
   int dense_policy = -1;     // OTB_HV_DENSE: 0 never, 1 always, -1 by the last kept density
   double last_density = 0.0; // kept entries / (m_loc n) of the last sparsify
+  bool have_density = false; // last_density is from a sparsify of this context (else sampled)
   int precond = 0;           // CG preconditioner: 0 none (the reference's plain CG), 1 Jacobi
   bool force_post = false;   // OTB_FORCE_EVAL_POST=1 (tests): the multi-rank eval finish on one rank
   // CUDA graphs of a 16-iteration CG batch (per-iteration path): [0] the
@@ -579,8 +580,24 @@ int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho
   // every thread sums the same columns in the same order)
   const char* env_hd = std::getenv("OTB_HV_DENSE");   // read per call: an experiment / test knob
   c->dense_policy = env_hd ? (std::atoi(env_hd) > 0 ? 1 : 0) : -1;
+  double density = c->last_density;
+  if (c->hv_mode == 3 && c->Pbuf != nullptr && c->p_valid && c->dense_policy < 0 && !c->have_density) {
+    // no kept density yet on this context: estimate it from every 64th row
+    // of the stored P (one host synchronisation, first sparsify only)
+    const int stride = 64;
+    const int64_t rows = (c->m_loc + stride - 1) / stride;
+    CUDA_TRY(cudaMemsetAsync(&c->ds->scratch[3], 0, sizeof(double), c->stream));
+    k_density_sample<<<c->num_sms * 4, 256, 0, c->stream>>>(c->Pbuf, c->ld, (int)c->m_loc, n, stride, gnorm_dev,
+                                                            c->eta, (double)c->m_glob * (double)c->n, rho,
+                                                            reinterpret_cast<unsigned long long*>(&c->ds->scratch[3]));
+    LAUNCH_CHECK();
+    TRY(sync_scalars(c));
+    unsigned long long cnt = 0;
+    std::memcpy(&cnt, &c->hs->scratch[3], sizeof cnt);
+    density = (double)cnt / std::max(1.0, (double)rows * (double)n);
+  }
   const bool dense = c->hv_mode == 3 && c->Pbuf != nullptr &&
-                     (c->dense_policy == 1 || (c->dense_policy < 0 && c->last_density >= kDenseRhoMin));
+                     (c->dense_policy == 1 || (c->dense_policy < 0 && density >= kDenseRhoMin));
   // dense P_rho from the stored P: the lean kernel (same bits as k_sparsify's dense mode)
   const int launch_kind = (dense && c->p_valid) ? (int)DK_SPDENSE : kind;
   Geom geo = c->p_valid ? make_geom(c, launch_kind, c->Pbuf, nullptr) : make_geom(c, DK_SPARSIFY, c->C, X);
@@ -645,6 +662,7 @@ int sparsify_finish(otb_ctx* c, int64_t rec, bool* redo) {
   c->nnz = nnz;
   c->nnz_glob = c->nranks > 1 ? (int64_t)c->hs->sp_glob[1] : nnz;
   c->last_density = (double)nnz / std::max(1.0, (double)c->m_loc * (double)c->n);
+  c->have_density = true;
   return OTB_OK;
 }
 
@@ -1962,12 +1980,25 @@ int otb_materialize_rounded(otb_ctx* c, double* out, int64_t ldo) {
 int sweep_zeta(otb_ctx* c, const double* logX, const double* gamma, double* zeta, double* err) {
   const int n = (int)c->n;
   const double mn = (double)c->m_loc * n;
-  Geom geo = make_geom(c, DK_WARMZ, c->C, logX);
-  WarmZIO io{gamma, c->log_a, c->eta, zeta, c->colpart};
+  // sinkhorn.py:47-51 is the eval's row log-sum-exp of logX + (gamma - C)/eta
+  // (global row max first, as _lse): the eval kernel without the P store;
+  // zeta = eta (log a - lse).  The column sums of the error check
+  // (sinkhorn.py:61-65, exp(logX + (zeta + gamma - C)/eta) summed over rows)
+  // are then sum_i a_i P_ij, which the eval accumulates anyway (w e_ij with
+  // w = a_i / S_i): one pass instead of k_warm_zeta's three divisions and two
+  // exps per element; the sums differ from the reference's expression in the
+  // last bits and only decide warm_tol.
+  if (gamma != c->gev)
+    CUDA_TRY(cudaMemcpyAsync(c->gev, gamma, sizeof(double) * n, cudaMemcpyDeviceToDevice, c->stream));
+  Geom geo = make_geom(c, DK_EVAL, c->C, logX);
+  geo.vec[0] = c->gev;
+  EvalIO io{c->gev, c->a, c->eta, c->rowM, c->rowS, c->lse, c->colpart, c->vpart, nullptr};
   cudaEvent_t e0 = nullptr;
   TRY(prof_begin(c, &e0));
-  TRY(launch_dense(c, DK_WARMZ, geo, &io));
+  TRY(launch_dense(c, DK_EVAL, geo, &io));
   TRY(prof_end(c, PC_WARMZ, e0, 16.0 * mn));
+  k_zeta_from_lse<<<c->colgrid, 256, 0, c->stream>>>((int)c->m_loc, c->log_a, c->row0, c->lse, c->eta, zeta);
+  LAUNCH_CHECK();
   TRY(colreduce(c, c->ncl, nullptr, 0, 0, 0));
   TRY(allreduce(c, c->sendbuf, (size_t)n, kNcclSum));
   k_vec_post<<<c->colgrid, 256, 0, c->stream>>>(POST_WARMERR, n, c->sendbuf, c->b, nullptr, c->ds, c->bpart,
