@@ -854,7 +854,10 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_hv_grp(HvArgs h) {
 // re-read is an L2 hit; HBM sees each value once.  The ring holds only the
 // rows in flight (loads + dots); the exchange waits hold no stage.  Rows are
 // applied in order, partials summed in window order: deterministic.
-constexpr double kDenseRhoMin = 0.5;   // kept density above which sparsify writes P_rho dense (OTB_HV_DENSE)
+// kept density above which sparsify writes P_rho dense (OTB_HV_DENSE forces either): with the
+// producer-free dense kernel, config 4 (37% kept) measured hess_apply 2.22 -> 1.78 ms and sparsify
+// 7.15 -> 5.06 ms dense against the bitmap runs
+constexpr double kDenseRhoMin = 0.25;
 constexpr int kWcD = 4;                  // exchange lookahead (rows)
 constexpr int kWcX = 2 * kWcD + 2;       // exchange buffers (>= 2 D + 1: see the note in wc_consume)
 constexpr int kWcMaxW = 16;
