@@ -126,6 +126,28 @@ def test_trajectory_csv_roundtrip_and_clock():
         t.record(TrajectoryRecord(2, 3, 30, 0.1, 0.1, 0.1, 0.1))
 
 
+def test_trajectory_csv_bytes_match_reference_text():
+    """The CSV text the reference's Trajectory.to_csv wrote for these records
+    (generated in the build container from pkg/src/otibsn/trajectory.py)."""
+    import math
+
+    from paper_2603_07156_b200.trajectory import Trajectory, TrajectoryRecord
+
+    expected = ("outer_k,inner_total,cg_total,wall_seconds,objective,kkt,grad_norm,gap\n"
+                "0,1,5,0.10000000000000001,1.2345678901234567,0.001,2.4999999999999999e-07,\n"
+                "1,3,17,0.25,1.2,9.9999999999999995e-07,1.0000000000000001e-09,0.00123\n")
+    t = Trajectory()
+    t.record(TrajectoryRecord(0, 1, 5, 0.1, 1.2345678901234567, 1e-3, 2.5e-7, None))
+    t.record(TrajectoryRecord(1, 3, 17, 0.25, 1.2, 1e-6, 1e-9, 0.00123))
+    assert t.to_csv() == expected
+    assert Trajectory.from_csv(expected).to_csv() == expected
+    for bad, exc, msg in [((2, 3, 17, 0.3, math.nan, 1e-6, 1e-9), ValueError, "non-finite objective"),
+                          ((0, 3, 17, 0.3, 1.0, 1e-6, 1e-9), ValueError, "outer iteration index went backwards"),
+                          ((2, 3, 17, 0.3, 1.0, 1e-6, 1e-9, math.inf), ValueError, "non-finite gap")]:
+        with pytest.raises(exc, match=msg):
+            t.record(TrajectoryRecord(*bad))
+
+
 def test_row_partition():
     from paper_2603_07156_b200.distributed import anchor_owner, row_range
 
