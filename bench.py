@@ -214,7 +214,7 @@ class Resident:
         # C on the GPU: this rank's rows only, bit-identical to the host recipe
         local = instances.device_cost(pts, dev, rows=(self.r0, self.r1), ld=ld, comm=comm)
         self.cost_local = local
-        cost = RowShardCost(local, self.r0, m) if world > 1 else local
+        cost = RowShardCost(local, self.r0, m) if comm is not None else local
         self.prob = OtProblem(cost, pts.a, pts.b)
         self.cfg = SolverConfig(eta=pts.eta, kkt_tol=pts.kkt_tol, max_inner=1)
         self.s = s = session_for(self.prob, pts.eta, comm)
@@ -341,7 +341,7 @@ def e2e_measure(res, steps, world, dev, comm):
 
     def one():
         # a sharded host cost is wrapped like the device one: rows of this rank
-        cost = C_pin if world == 1 else RowShardCost(C_pin, res.r0, m)
+        cost = C_pin if comm is None else RowShardCost(C_pin, res.r0, m)
         hprob = OtProblem(cost, a, b)
         gs, cand, rep = inner_solve(LogPlan(lx_pin), DualState(g_pin), hprob, cfg, mu_k=1e3, outer_k=0, comm=comm)
         return np.asarray(gs.gamma).sum() + rep.objective + rep.kkt
@@ -417,7 +417,9 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     comm = None
-    if world > 1:
+    # OTB_NCCL_SELFTEST=1 (under torchrun --nproc-per-node 1): the multi-rank set-up and the NCCL
+    # all-reduce call sites with a one-rank communicator, for a one-GPU box
+    if world > 1 or os.environ.get("OTB_NCCL_SELFTEST") == "1":
         dist.init_process_group("nccl", device_id=dev)
         from paper_2603_07156_b200.distributed import RowComm
 
@@ -473,7 +475,7 @@ def run_ours(args):
             "secondary": sec or None,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

@@ -62,8 +62,23 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_eval(Geom geo, EvalIO io) {
     double z[2 * NS];
     double mx = -INFINITY;
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      if (s < nsl) {
+    for (int s = 0; s < NS; s += 2) {
+      if (s + 1 < NS && s + 1 < nsl) {   // two slices at once: four interleaved chains
+        double2 v[2][3];                 // [slice][C, log X, gamma]
+        D.fetchn2(v);
+        const double dq[4] = {v[0][2].x - v[0][0].x, v[0][2].y - v[0][0].y, v[1][2].x - v[1][0].x,
+                              v[1][2].y - v[1][0].y};
+        double q[4];
+        DIV.quad(dq, q);   // semidual.py:52
+        z[2 * s] = v[0][1].x + q[0];
+        z[2 * s + 1] = v[0][1].y + q[1];
+        z[2 * s + 2] = v[1][1].x + q[2];
+        z[2 * s + 3] = v[1][1].y + q[3];
+        const double zm0 = z[2 * s] > z[2 * s + 1] ? z[2 * s] : z[2 * s + 1];
+        const double zm1 = z[2 * s + 2] > z[2 * s + 3] ? z[2 * s + 2] : z[2 * s + 3];
+        mx = zm0 > mx ? zm0 : mx;
+        mx = zm1 > mx ? zm1 : mx;
+      } else if (s < nsl) {
         double2 c, x, gm;
         D.fetch3(c, x, gm);
         double q0, q1;
@@ -87,8 +102,24 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_eval(Geom geo, EvalIO io) {
     // semidual.py:81: exp(logits - row_max)
     double se = 0.0;
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      if (s < nsl) {
+    for (int s = 0; s < NS; s += 2) {
+      if (s + 1 < NS && s + 1 < nsl) {   // four exps, one range check (se in column order, as below)
+        double x[4], e[4];
+        bool ok = true;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = z[2 * s + i] - M;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) e[i] = exp_tab(x[i], ok, etab);
+        if (!ok) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) e[i] = exp_t(x[i], etab);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          z[2 * s + i] = e[i];
+          se += e[i];
+        }
+      } else if (s < nsl) {
         const double x0 = z[2 * s] - M, x1 = z[2 * s + 1] - M;
         bool ok = true;
         double e0 = exp_tab(x0, ok, etab), e1 = exp_tab(x1, ok, etab);
@@ -108,8 +139,31 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_eval(Geom geo, EvalIO io) {
     const Divider DS(S);
     double* Prow = io.P != nullptr ? io.P + (size_t)r * D.g.ld + D.col(0, 0) : nullptr;
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      if (s < nsl) {
+    for (int s = 0; s < NS; s += 2) {
+      if (s + 1 < NS && s + 1 < nsl) {   // two slices at once
+        double2* a0 = D.acc2(0, s);
+        double2* a1 = D.acc2(0, s + 1);
+        double2 v0 = *a0, v1 = *a1;
+        v0.x = fma(w, z[2 * s], v0.x);
+        v0.y = fma(w, z[2 * s + 1], v0.y);
+        v1.x = fma(w, z[2 * s + 2], v1.x);
+        v1.y = fma(w, z[2 * s + 3], v1.y);
+        *a0 = v0;
+        *a1 = v1;
+        if (Prow != nullptr) {                    // semidual.py:82-83: shifted / row_sum
+          const double e4[4] = {z[2 * s], z[2 * s + 1], z[2 * s + 2], z[2 * s + 3]};
+          double p[4];
+          DS.quad(e4, p);
+          double* dst = Prow + s * D.slice;
+          *reinterpret_cast<double2*>(dst) = make_double2(p[0], p[1]);   // slice s is not the last
+          dst += D.slice;
+          if (s + 1 < nsl - 1 || !tail || lastv > 1) {
+            *reinterpret_cast<double2*>(dst) = make_double2(p[2], p[3]);
+          } else if (lastv > 0) {
+            dst[0] = p[2];
+          }
+        }
+      } else if (s < nsl) {
         double2* a2 = D.acc2(0, s);
         double2 v = *a2;
         v.x = fma(w, z[2 * s], v.x);
@@ -773,8 +827,56 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_a(Geom geo, TestAIO io
     double rs = 0.0;
     double shmin = INFINITY;
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      if (s < nsl) {
+    for (int s = 0; s < NS; s += 2) {
+      if (s + 1 < NS && s + 1 < nsl) {   // two slices at once: four interleaved chains, one range check each
+        double2 v[2][3];                 // [slice][C, log X, gamma]
+        D.fetchn2(v);
+        const bool part = tail && s + 1 == nsl - 1;   // only the second slice can be the partial one
+        const double cc[4] = {v[0][0].x, v[0][0].y, v[1][0].x, v[1][0].y};
+        const double xx[4] = {v[0][1].x, v[0][1].y, v[1][1].x, v[1][1].y};
+        const double gg[4] = {v[0][2].x, v[0][2].y, v[1][2].x, v[1][2].y};
+        if (kCtr && ctr) {   // the slack's c-transform for pass C's KKT metrics
+#pragma unroll
+          for (int i = 0; i < 4; ++i) shmin = fmin(shmin, cc[i] - gg[i]);
+        }
+        double l4[4] = {xx[0], xx[1], xx[2], xx[3]};   // log entries (candidate, or the plan as given)
+        if (io.recover) {                               // inner_newton.py:160-167, core.py:141-145
+          double dq[4], q[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dq[i] = gg[i] - cc[i];
+          DIV.quad(dq, q);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const double raw = ((la + xx[i]) + q[i]) - l;
+            bad |= isnan(raw) || raw == INFINITY;
+            l4[i] = fmax(raw, kLogFloor);
+          }
+          double* dst = Xrow + s * D.slice;
+          *reinterpret_cast<double2*>(dst) = make_double2(l4[0], l4[1]);   // slice s is not the last
+          dst += D.slice;
+          if (!part || lastv > 1) {
+            *reinterpret_cast<double2*>(dst) = make_double2(l4[2], l4[3]);
+          } else if (lastv > 0) {
+            dst[0] = l4[2];
+          }
+        }
+        bool ok = true;   // four exps branch-free (exp() only when out of range)
+        double e[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) e[i] = exp_tab(l4[i], ok, etab);
+        if (!ok) {   // per element (exp_t), as k_materialize_rounded forms X
+#pragma unroll
+          for (int i = 0; i < 4; ++i) e[i] = exp_t(l4[i], etab);
+        }
+        if (part) {
+          e[2] = lastv > 0 ? e[2] : 0.0;
+          e[3] = lastv > 1 ? e[3] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xv[2 * s + i] = e[i];
+        rs += e[0] + e[1];
+        rs += e[2] + e[3];
+      } else if (s < nsl) {
         double2 c, x, gm;
         D.fetch3(c, x, gm);
         const bool part = tail && s == nsl - 1;
@@ -876,8 +978,27 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_b(Geom geo, TestBIO io
     const double z = io.zrow[r];
     double rs = 0.0;
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      if (s < nsl) {
+    for (int s = 0; s < NS; s += 2) {
+      if (s + 1 < NS && s + 1 < nsl) {   // two slices at once: four interleaved chains, one range check
+        double2 v[2][2];                 // [slice][candidate log entries, y]
+        D.fetchn2(v);
+        const double x[4] = {v[0][0].x, v[0][0].y, v[1][0].x, v[1][0].y};
+        const double yv[4] = {v[0][1].x, v[0][1].y, v[1][1].x, v[1][1].y};
+        double e[4], f[4];
+        bool ok = true;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) e[i] = exp_tab(x[i], ok, etab);
+        if (!ok) {   // per element (exp_t), as k_materialize_rounded forms X
+#pragma unroll
+          for (int i = 0; i < 4; ++i) e[i] = exp_t(x[i], etab);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) f[i] = (e[i] * z) * yv[i];   // feasibility.py:65
+        rs += f[0] + f[1];
+        rs += f[2] + f[3];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[2 * s + i] += f[i];
+      } else if (s < nsl) {
         double2 v[2];   // candidate log entries, y
         D.fetchn(v);
         bool ok = true;

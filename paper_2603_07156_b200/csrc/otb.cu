@@ -1552,7 +1552,14 @@ int otb_nccl_get_unique_id(const char* nccl_path, void* id128) {
 
 int otb_attach_nccl(otb_ctx* c, const char* nccl_path, const void* id128, int nranks, int rank) {
   if (!c) return fail(OTB_ERR_ARG, "null context");
-  if (nranks <= 1) {
+  // OTB_NCCL_SELFTEST=1: a ONE-rank communicator driven through every
+  // multi-rank code path (the context behaves as rank 0 of 2: per-iteration
+  // CG, fallback reductions, every ncclAllReduce call site, their graph
+  // capture), so that a one-GPU box exercises the NCCL binding; the results
+  // equal the single-rank ones.
+  const char* st = std::getenv("OTB_NCCL_SELFTEST");
+  const bool selftest = nranks == 1 && st && st[0] == '1';
+  if (nranks <= 1 && !selftest) {
     c->nranks = 1;
     c->rank = 0;
     return OTB_OK;
@@ -1563,7 +1570,7 @@ int otb_attach_nccl(otb_ctx* c, const char* nccl_path, const void* id128, int nr
   CUDA_TRY(cudaSetDevice(c->device));
   const int r = c->nccl.commInitRank(&c->comm, nranks, id, rank);
   if (r != 0) return fail(OTB_ERR_NCCL, "ncclCommInitRank failed");
-  c->nranks = nranks;
+  c->nranks = selftest ? 2 : nranks;
   c->rank = rank;
   c->cg_fused = false;   // the persistent CG has no H v all-reduce (krylov.py:68-84 needs the global H v)
   c->have_eval = false;

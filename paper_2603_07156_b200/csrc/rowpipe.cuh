@@ -292,6 +292,62 @@ struct Dense {
     release();
     advance();
   }
+  // TWO consecutive slices of the current row at once (SELF only): both
+  // stages are waited for, read and released together, so the arithmetic of
+  // the four elements forms one basic block and their dependent fp64 chains
+  // interleave.  With one slice per fetch a warp has two elements in flight
+  // and every slice costs the full latency of its chain (the wait loop and
+  // the release are block boundaries the scheduler does not move code
+  // across): the dense passes ran latency bound at ~45% issue-active.  The
+  // two arrival atomics go out back to back (one round trip, not two).
+  OTB_DEV void fetchn2(double2 (&v)[2][NMAT]) {
+    static_assert(SELF, "fetchn2 is for the self-fed ring");
+    const int st0 = stage;
+    const uint32_t ph0 = phase, rd0 = rounds;
+    advance();
+    const int st1 = stage;
+    const uint32_t ph1 = phase, rd1 = rounds;
+    advance();
+    mbar_wait(&sm.full[st0], ph0);
+    mbar_wait(&sm.full[st1], ph1);
+#pragma unroll
+    for (int k = 0; k < NMAT; ++k) {
+      v[0][k] = reinterpret_cast<const double2*>(stage_buf(st0, k))[tid];
+      v[1][k] = reinterpret_cast<const double2*>(stage_buf(st1, k))[tid];
+    }
+    __syncwarp();
+    // refill cursor of the second slice
+    int fr1 = fr, fs1 = fs + 1;
+    if (fs1 == nsl) {
+      fs1 = 0;
+      ++fr1;
+    }
+    if (lane == 0) {
+      uint32_t old0, old1;
+      asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;"
+                   : "=r"(old0)
+                   : "r"(smem_u32(&sm.misc[st0]))
+                   : "memory");
+      asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;"
+                   : "=r"(old1)
+                   : "r"(smem_u32(&sm.misc[st1]))
+                   : "memory");
+      const uint32_t nw = (uint32_t)(g.nt >> 5);
+      const bool f0 = old0 == rd0 * nw - 1u && fr < r1, f1 = old1 == rd1 * nw - 1u && fr1 < r1;
+      if (f0 || f1) {
+        fence_proxy_async();
+        if (f0) issue(st0, fr, fs);
+        if (f1) issue(st1, fr1, fs1);
+      }
+    }
+    fr = fr1;
+    fs = fs1 + 1;
+    if (fs == nsl) {
+      fs = 0;
+      ++fr;
+    }
+  }
+
   OTB_DEV void fetch3(double2& v0, double2& v1, double2& v2) {
     static_assert(NMAT == 3, "fetch3 needs three streamed arrays");
     double2 v[3];

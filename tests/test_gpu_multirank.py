@@ -239,3 +239,58 @@ def test_row_shard_cost_bench_step_two_ranks(cuda):
         assert np.max(np.abs(g2 - g1)) <= 1e-9 * max(1.0, np.abs(g1).max())
         assert r2.objective == pytest.approx(r1.objective, rel=1e-10)
         assert r2.kkt == pytest.approx(r1.kkt, rel=1e-6)
+
+
+_NCCL_SELFTEST = r"""
+import json, os, sys
+import numpy as np
+import torch
+import torch.distributed as dist
+sys.path.insert(0, os.environ["OTB_REPO"])
+import paper_2603_07156_b200 as P
+from paper_2603_07156_b200 import instances
+from paper_2603_07156_b200.distributed import RowComm
+
+torch.cuda.set_device(0)
+inst = instances.config(int(os.environ["OTB_TEST_CONFIG"]), 0)
+cfg = P.SolverConfig(eta=inst.eta, kkt_tol=inst.kkt_tol)
+one = P.ibsn_solve(P.OtProblem(inst.cost, inst.a, inst.b), cfg)
+dist.init_process_group("gloo", rank=0, world_size=1)
+os.environ["OTB_NCCL_SELFTEST"] = "1"
+res = P.ibsn_solve(P.OtProblem(inst.cost, inst.a, inst.b), cfg, comm=RowComm())
+info = res._session.info()
+torch.cuda.synchronize()
+print(json.dumps({"one": [one.outer_iters, one.newton_iters, one.cg_iters, one.objective, one.kkt],
+                  "nccl": [res.outer_iters, res.newton_iters, res.cg_iters, res.objective, res.kkt],
+                  "nranks": info["nranks"], "cg_fused": info["cg_fused"],
+                  "dgamma": float(np.max(np.abs(np.asarray(res.gamma) - np.asarray(one.gamma))))}))
+dist.destroy_process_group()
+"""
+
+
+@pytest.mark.parametrize("config", [1, 2])
+def test_nccl_binding_one_rank_selftest(cuda, config):
+    """The NCCL transport on a one-GPU box: OTB_NCCL_SELFTEST=1 attaches a
+    ONE-rank NCCL communicator (dlopen of the torch-bundled libnccl, unique
+    id, ncclCommInitRank) and runs the context through every multi-rank code
+    path — per-iteration CG, fallback reductions, every ncclAllReduce call
+    site and their CUDA-graph capture.  The solve must equal the one-rank
+    solve (same reduction order on one rank: counts equal, objective 1e-8)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, OTB_REPO=root, OTB_TEST_CONFIG=str(config), MASTER_ADDR="127.0.0.1",
+               MASTER_PORT=str(29600 + config))
+    env.pop("OTB_NCCL_SELFTEST", None)
+    out = subprocess.run([sys.executable, "-c", _NCCL_SELFTEST], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert r["nranks"] == 2 and r["cg_fused"] == 0      # the context took the multi-rank paths
+    assert r["nccl"][0] == r["one"][0] and r["nccl"][1] == r["one"][1]
+    assert abs(r["nccl"][2] - r["one"][2]) <= 0.05 * r["one"][2]
+    assert abs(r["nccl"][3] - r["one"][3]) <= 1e-8 * abs(r["one"][3])
+    assert r["nccl"][4] < (1e-6 if config < 3 else 1e-7)
