@@ -14,6 +14,11 @@ constexpr int kMaxThreads = OTB_DENSE_MAXT;   // 512 consumers + 1 producer warp
 #define OTB_DENSE_MINB 1           // CTAs per SM the register allocation is sized for
 #endif
 constexpr int kTabInts = 2 * kMaxNS * 32;
+// test_c with two slices per fetch (as eval, test_a, test_b): measured SLOWER at config 5 (29.8 ->
+// 32.5 ms: the pass sits at the 128-register cap and the paired form spills), so off.
+#ifndef OTB_TESTC_PAIRS
+#define OTB_TESTC_PAIRS 0
+#endif
 #ifndef OTB_ZETA_A_NS
 #define OTB_ZETA_A_NS 6   // rows of more than this many slices take the KKT c-transform from pass A
 #endif
@@ -78,6 +83,7 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_eval(Geom geo, EvalIO io) {
         const double zm1 = z[2 * s + 2] > z[2 * s + 3] ? z[2 * s + 2] : z[2 * s + 3];
         mx = zm0 > mx ? zm0 : mx;
         mx = zm1 > mx ? zm1 : mx;
+        D.refill2_deferred();
       } else if (s < nsl) {
         double2 c, x, gm;
         D.fetch3(c, x, gm);
@@ -876,6 +882,7 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_a(Geom geo, TestAIO io
         for (int i = 0; i < 4; ++i) xv[2 * s + i] = e[i];
         rs += e[0] + e[1];
         rs += e[2] + e[3];
+        D.refill2_deferred();
       } else if (s < nsl) {
         double2 c, x, gm;
         D.fetch3(c, x, gm);
@@ -998,6 +1005,7 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_b(Geom geo, TestBIO io
         rs += f[2] + f[3];
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[2 * s + i] += f[i];
+        D.refill2_deferred();
       } else if (s < nsl) {
         double2 v[2];   // candidate log entries, y
         D.fetchn(v);
@@ -1085,8 +1093,75 @@ __global__ void __launch_bounds__(kSelfThreads, 1) k_test_c(Geom geo, TestCIO io
     double shmin = INFINITY;
     double rs = 0.0;
 #pragma unroll
-    for (int s = 0; s < NS; ++s) {
-      if (s < nsl) {
+    for (int s = 0; s < NS; s += (OTB_TESTC_PAIRS ? 2 : 1)) {
+      if (OTB_TESTC_PAIRS && s + 1 < NS && s + 1 < nsl) {   // two slices at once (off: see OTB_TESTC_PAIRS)
+        double2 v[2][NA];
+        D.fetchn2(v);
+        const double xl[4] = {v[0][0].x, v[0][0].y, v[1][0].x, v[1][0].y};
+        const double yv[4] = {v[0][NM].x, v[0][NM].y, v[1][NM].x, v[1][NM].y};
+        double ex[4], f[4], lg[4];
+        bool ok = true;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ex[i] = exp_tab(xl[i], ok, etab);
+        if (!ok) {   // per element (exp_t), as k_materialize_rounded forms X
+#pragma unroll
+          for (int i = 0; i < 4; ++i) ex[i] = exp_t(xl[i], etab);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) f[i] = (ex[i] * z) * yv[i];   // feasibility.py:65
+        if (deficit > 0.0) {                                         // feasibility.py:67-68
+          const double ev[4] = {e_r * v[0][NM + 1].x, e_r * v[0][NM + 1].y, e_r * v[1][NM + 1].x,
+                                e_r * v[1][NM + 1].y};
+          double d[4];
+          DD.quad(ev, d);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) f[i] = f[i] + d[i];
+        }
+        // feasibility.py:84 terms: table logs, branch-free; log_fast per PAIR with an entry near 1,
+        // zero, subnormal, negative or non-finite (the same pairs, the same bits as the single-slice path)
+        bool lok0 = true, lok1 = true;
+        lg[0] = log_tab(f[0], lok0, ltab);
+        lg[1] = log_tab(f[1], lok0, ltab);
+        lg[2] = log_tab(f[2], lok1, ltab);
+        lg[3] = log_tab(f[3], lok1, ltab);
+        if (!(lok0 && lok1)) {
+          if (!lok0) {
+            lg[0] = f[0] > 0.0 ? log_fast(f[0]) : 0.0;
+            lg[1] = f[1] > 0.0 ? log_fast(f[1]) : 0.0;
+          }
+          if (!lok1) {
+            lg[2] = f[2] > 0.0 ? log_fast(f[2]) : 0.0;
+            lg[3] = f[3] > 0.0 ? log_fast(f[3]) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double fv = f[i];
+          acc[0] = fma(fv > 0.0 ? fv : 0.0, lg[i] - xl[i], acc[0]);
+          acc[1] += fv;
+          rs += fv;
+          if constexpr (METRICS) {
+            const double2 c2 = v[i >> 1][1], g2 = v[i >> 1][NM + 2];
+            const double cv = (i & 1) ? c2.y : c2.x;
+            const double gv = (i & 1) ? g2.y : g2.x;
+            acc[2] = fma(cv, fv, acc[2]);
+            acc[3] = fma(fv, fv, acc[3]);
+            const double fm = fmin(fv, 0.0);
+            acc[4] = fma(fm, fm, acc[4]);
+            const double shv = cv - gv;
+            if constexpr (kZetaFromA) {   // slack >= 0: acc[5] stays 0 (see the single-slice path)
+              acc[6] = fma(fv, shv - zeta_a, acc[6]);
+            } else {
+              fk[2 * s + i] = fv;
+              shk[2 * s + i] = shv;
+              shmin = fmin(shmin, shv);
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cacc[2 * s + i] += f[i];
+        D.refill2_deferred();
+      } else if (s < nsl) {
         double2 v[NA];
         D.fetchn(v);
         const double2 x = v[0];

@@ -1322,7 +1322,14 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
       cudaGetLastError();
       if (e != cudaSuccess || nclusters < 1) continue;
       nclusters = std::min(nclusters, sms / W);
-      const double cost = (double)nqw / nclusters;   // rows per cluster x window width
+      // rows per cluster x the measured time per row of the dense-P_rho kernel (config 4, n =
+      // 16384, profiles/r2/hv_nq_sweep_cfg4.txt): 0.42 us of per-row reduction and exchange plus
+      // 0.09 us per 1024 columns (NQ = 2: 0.66, 3: 0.68, 4: 0.75, 6: 0.96 us).  The kernel holds
+      // 6 NQ doubles per thread (two rows' values, v, the accumulator) and spills from NQ = 7 on
+      // (ptxas: 108 B at 7, 404 B at 8): NQ = 8 measured 2.07 us per row.  So W = 3 x 6144 on 135
+      // SMs (1.40 ms per product) beats W = 2 x 8192 on 148 SMs (1.83 ms).
+      const double spill = nqw >= 8 ? 1.8 : (nqw == 7 ? 1.3 : 1.0);
+      const double cost = (0.42 + 0.09 * nqw) * spill / nclusters;
       if (cost < best * (1.0 - 1e-9)) {
         best = cost;
         best_nq = nqw;

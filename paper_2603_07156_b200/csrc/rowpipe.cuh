@@ -28,6 +28,9 @@ namespace otb {
 constexpr int kMaxCluster = 16;   // > 8: non-portable cluster sizes
 constexpr int kXb = 4;       // cluster exchange buffers (rotating; >= 3 needed, see exchange())
 constexpr int kMaxNS = 10;   // 1024-column slices per CTA: one CTA per row up to n = 10240
+#ifndef OTB_F2_DEFER
+#define OTB_F2_DEFER 0   // fetchn2's refill decision after the slices' arithmetic (refill2_deferred)
+#endif
 
 struct Geom {
   const double* mat0;   // first streamed matrix (row-major, ld)
@@ -316,28 +319,41 @@ struct Dense {
       v[1][k] = reinterpret_cast<const double2*>(stage_buf(st1, k))[tid];
     }
     __syncwarp();
-    // refill cursor of the second slice
+    if (lane == 0) {
+      asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;"
+                   : "=r"(pend_old[0])
+                   : "r"(smem_u32(&sm.misc[st0]))
+                   : "memory");
+      asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;"
+                   : "=r"(pend_old[1])
+                   : "r"(smem_u32(&sm.misc[st1]))
+                   : "memory");
+    }
+    pend_st[0] = st0;
+    pend_st[1] = st1;
+    pend_tgt[0] = rd0 * (uint32_t)(g.nt >> 5) - 1u;
+    pend_tgt[1] = rd1 * (uint32_t)(g.nt >> 5) - 1u;
+#if !OTB_F2_DEFER
+    refill2();
+#endif
+  }
+  // The refill decision of the last fetchn2 (lane 0: did this warp's arrival
+  // complete a stage's round?).  With OTB_F2_DEFER the kernel calls it after
+  // the slices' arithmetic, so the atomics' round trip is not waited for.
+  uint32_t pend_old[2], pend_tgt[2];
+  int pend_st[2];
+  OTB_DEV void refill2() {
     int fr1 = fr, fs1 = fs + 1;
     if (fs1 == nsl) {
       fs1 = 0;
       ++fr1;
     }
     if (lane == 0) {
-      uint32_t old0, old1;
-      asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;"
-                   : "=r"(old0)
-                   : "r"(smem_u32(&sm.misc[st0]))
-                   : "memory");
-      asm volatile("atom.relaxed.cta.shared::cta.add.u32 %0, [%1], 1;"
-                   : "=r"(old1)
-                   : "r"(smem_u32(&sm.misc[st1]))
-                   : "memory");
-      const uint32_t nw = (uint32_t)(g.nt >> 5);
-      const bool f0 = old0 == rd0 * nw - 1u && fr < r1, f1 = old1 == rd1 * nw - 1u && fr1 < r1;
+      const bool f0 = pend_old[0] == pend_tgt[0] && fr < r1, f1 = pend_old[1] == pend_tgt[1] && fr1 < r1;
       if (f0 || f1) {
         fence_proxy_async();
-        if (f0) issue(st0, fr, fs);
-        if (f1) issue(st1, fr1, fs1);
+        if (f0) issue(pend_st[0], fr, fs);
+        if (f1) issue(pend_st[1], fr1, fs1);
       }
     }
     fr = fr1;
@@ -346,6 +362,11 @@ struct Dense {
       fs = 0;
       ++fr;
     }
+  }
+  OTB_DEV void refill2_deferred() {
+#if OTB_F2_DEFER
+    refill2();
+#endif
   }
 
   OTB_DEV void fetch3(double2& v0, double2& v1, double2& v2) {
