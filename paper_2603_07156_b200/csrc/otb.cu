@@ -216,6 +216,13 @@ struct otb_ctx {
   int hv_ng_d = 0;                             // ring stages of the dense-P_rho window-cluster kernel
   size_t hv_smem_d = 0;
   bool hv_wcd = true;                          // OTB_HV_WCD=0: the producer-warp dense kernel (comparison)
+  // dense-P_rho overlay of a group-kernel context (hv_mode 0, n > 8192, e.g. config 3): while the
+  // kept density is >= kDenseRhoMin sparsify writes P_rho dense over the stored P and hess_apply
+  // is k_hv_wcd<ov_nq> on ov_ncl clusters of ov_win CTAs; below it the CSR group kernel runs
+  bool ov_ok = false;
+  int ov_nq = 0, ov_win = 0, ov_ncl = 0, ov_stages = 0;
+  size_t ov_smem = 0;
+  int* ov_rb = nullptr;                        // [ov_ncl + 1] equal row counts per cluster
   uint4* bm = nullptr;
   double* Pbuf = nullptr;    // P of the last eval (local rows x ld), streamed by sparsify
   unsigned long long* cg_trace = nullptr;   // OTB_CG_TRACE=1: phase stamps of the fused CG
@@ -581,7 +588,8 @@ int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho
   const char* env_hd = std::getenv("OTB_HV_DENSE");   // read per call: an experiment / test knob
   c->dense_policy = env_hd ? (std::atoi(env_hd) > 0 ? 1 : 0) : -1;
   double density = c->last_density;
-  if (c->hv_mode == 3 && c->Pbuf != nullptr && c->p_valid && c->dense_policy < 0 && !c->have_density) {
+  const bool dense_cap = c->hv_mode == 3 || c->ov_ok;
+  if (dense_cap && c->Pbuf != nullptr && c->p_valid && c->dense_policy < 0 && !c->have_density) {
     // no kept density yet on this context: estimate it from every 64th row
     // of the stored P (one host synchronisation, first sparsify only)
     const int stride = 64;
@@ -596,7 +604,9 @@ int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho
     std::memcpy(&cnt, &c->hs->scratch[3], sizeof cnt);
     density = (double)cnt / std::max(1.0, (double)rows * (double)n);
   }
-  const bool dense = c->hv_mode == 3 && c->Pbuf != nullptr &&
+  // (a group-kernel context can write the dense P_rho only from the stored P: its recomputing
+  // sparsify writes the CSR columns)
+  const bool dense = dense_cap && c->Pbuf != nullptr && (c->hv_mode == 3 || c->p_valid) &&
                      (c->dense_policy == 1 || (c->dense_policy < 0 && density >= kDenseRhoMin));
   // dense P_rho from the stored P: the lean kernel (same bits as k_sparsify's dense mode)
   const int launch_kind = (dense && c->p_valid) ? (int)DK_SPDENSE : kind;
@@ -614,7 +624,7 @@ int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho
   *rec = c->prof ? (int64_t)c->recs.size() : -1;
   TRY(prof_end(c, PC_SPARSIFY, e0, 0.0));
   // the row prefix (CSR export, nnz-balanced bounds) only where it is used
-  if (!bitmap) {
+  if (!bitmap && !dense) {
     TRY(row_prefix(c));
     // nnz-balanced row bounds of the hess_apply CTAs, once per sparsify
     // (the bitmap kernels use fixed equal row counts, set at creation)
@@ -623,7 +633,7 @@ int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho
     k_cta_bounds<<<(int)cdiv(c->hv_nb + 1, 256), 256, 0, c->stream>>>(A, c->hv_nb, c->cta_rb, 0);
     LAUNCH_CHECK();
   }
-  c->rowpre_valid = !bitmap;
+  c->rowpre_valid = !bitmap && !dense;
   if (c->precond) {   // q = (P_rho o P_rho)^T a for the Jacobi diagonal, summed over ranks
     k_colreduce<<<c->col32, 256, 0, c->stream>>>(c->colpart2, c->ncl, n, c->jq, nullptr, 0, 0, 0,
                                                    &c->ds->cnt[CNT_COLRED], ColPost{-1, nullptr, nullptr, {nullptr, nullptr}});
@@ -710,28 +720,36 @@ int run_hv(otb_ctx* c, const double* v_src, const double* r, const double* p_pre
            const CgState* st, HvResult* res) {
   const int n = (int)c->n;
   cudaEvent_t e0 = nullptr;
+  int hv_parts = c->hv_nb;
   if (c->hv_mode != 1) {
     HvArgs h{csr_view(c), c->a, n, c->hv_ng, v_src, r, p_prev, p_cur, update, st, c->colpart, c->bm, c->nq,
              c->hv_win, c->ld};
-    if (c->hv_mode == 3 && c->rho_dense) h.A.vals = c->Pbuf;
-    const bool wcd = c->hv_mode == 3 && c->rho_dense && c->hv_wcd;   // dense P_rho: k_hv_wcd (no producer warp)
-    if (wcd) h.ng = c->hv_ng_d;
+    if (c->rho_dense) h.A.vals = c->Pbuf;
+    const bool ov = c->hv_mode != 3 && c->rho_dense;                  // dense overlay of a group-kernel context
+    const bool wcd = ov || (c->hv_mode == 3 && c->rho_dense && c->hv_wcd);   // dense P_rho: k_hv_wcd (no producer warp)
+    if (wcd) h.ng = ov ? c->ov_stages : c->hv_ng_d;
+    if (ov) {
+      h.A.cta_rb = c->ov_rb;
+      h.nwin = c->ov_win;
+    }
+    hv_parts = ov ? c->ov_ncl : c->hv_nb;
     TRY(prof_begin(c, &e0));
     void* args[1] = {&h};
-    if (c->hv_mode == 3) {
+    if (c->hv_mode == 3 || ov) {
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(c->hv_grid);
+      cfg.gridDim = dim3(ov ? c->ov_ncl * c->ov_win : c->hv_grid);
       cfg.blockDim = dim3(wcd ? kStConsumers : kStThreads);
-      cfg.dynamicSmemBytes = wcd ? c->hv_smem_d : c->hv_smem;
+      cfg.dynamicSmemBytes = ov ? c->ov_smem : (wcd ? c->hv_smem_d : c->hv_smem);
       cfg.stream = c->stream;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = (unsigned)c->hv_win;
+      attr[0].val.clusterDim.x = (unsigned)(ov ? c->ov_win : c->hv_win);
       attr[0].val.clusterDim.y = 1;
       attr[0].val.clusterDim.z = 1;
       cfg.attrs = attr;
       cfg.numAttrs = 1;
-      CUDA_TRY(cudaLaunchKernelExC(&cfg, wcd ? kWcdFn[c->hv_var] : kWcFn[c->rho_dense ? 1 : 0][c->hv_var], args));
+      const void* fn = ov ? kWcdFn[c->ov_nq] : (wcd ? kWcdFn[c->hv_var] : kWcFn[c->rho_dense ? 1 : 0][c->hv_var]);
+      CUDA_TRY(cudaLaunchKernelExC(&cfg, fn, args));
     } else {
       CUDA_TRY(cudaLaunchKernel(kHvFn[c->hv_var], dim3(c->hv_grid), dim3(c->hv_threads), args, c->hv_smem,
                                 c->stream));
@@ -739,11 +757,11 @@ int run_hv(otb_ctx* c, const double* v_src, const double* r, const double* p_pre
     LAUNCH_CHECK();
     TRY(prof_end(c, PC_HV, e0, hv_bytes(c)));
     if (c->nranks > 1) {
-      TRY(colreduce(c, c->hv_nb, nullptr, 0, 0, 0));
+      TRY(colreduce(c, hv_parts, nullptr, 0, 0, 0));
       TRY(allreduce(c, c->sendbuf, (size_t)n, kNcclSum));
       *res = {nullptr, 0, nullptr, c->sendbuf};
     } else {
-      *res = {c->colpart, c->hv_nb, nullptr, nullptr};
+      *res = {c->colpart, hv_parts, nullptr, nullptr};
     }
   } else {
     const double* v = update ? p_cur : v_src;
@@ -1407,6 +1425,57 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
     c->hv_grid = sms * 8;
     c->hv_nb = 1;
   }
+  // Dense-P_rho overlay of a group-kernel context (8192 < n, e.g. config 3: n = 10000): the
+  // dense window-cluster kernel streams P_rho at ~6 TB/s whatever the row's nnz, the CSR group
+  // kernel moves 10 B per kept entry at ~2.3 TB/s, so dense wins while a quarter or more is kept
+  // (config 3's first Newton steps keep 49%: 212 -> 135 us per product).  Geometry as for the
+  // window clusters: the measured time per row x rows per co-resident cluster.
+  {
+    const char* env_ov = std::getenv("OTB_HV_OVERLAY");
+    if (c->hv_mode == 0 && n > 8192 && !(env_ov && std::atoi(env_ov) == 0)) {
+      double best = 1e300;
+      for (int nqw = 1; nqw <= kMaxNQ; ++nqw) {
+        const int W = (int)cdiv(n, 1024 * nqw);
+        if (W < 2 || W > kWcMaxW) continue;
+        const void* fd = kWcdFn[nqw];
+        const int stage = wc_stage_bytes(nqw);
+        const int S = (int)std::min<int64_t>(kWcMaxStages, (int64_t)(kMaxDynSmem - 8192) / (stage + 16));
+        if (S < 2) continue;
+        const size_t smem = (size_t)S * stage + 2 * (size_t)S * 8;
+        cudaError_t e = allow_max_smem(fd, device);
+        if (e == cudaSuccess && W > 8) e = cudaFuncSetAttribute(fd, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        int ncd = 0;
+        if (e == cudaSuccess) {
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3((unsigned)(W * (sms / W)));
+          cfg.blockDim = dim3(kStConsumers);
+          cfg.dynamicSmemBytes = smem;
+          cudaLaunchAttribute attr[1];
+          attr[0].id = cudaLaunchAttributeClusterDimension;
+          attr[0].val.clusterDim.x = (unsigned)W;
+          attr[0].val.clusterDim.y = 1;
+          attr[0].val.clusterDim.z = 1;
+          cfg.attrs = attr;
+          cfg.numAttrs = 1;
+          e = cudaOccupancyMaxActiveClusters(&ncd, fd, &cfg);
+        }
+        cudaGetLastError();
+        if (e != cudaSuccess || ncd < 1) continue;
+        ncd = (int)std::min<int64_t>(std::min(ncd, sms / W), c->m_loc);
+        const double spill = nqw >= 8 ? 1.8 : (nqw == 7 ? 1.3 : 1.0);
+        const double cost = (0.42 + 0.09 * nqw) * spill / ncd;
+        if (cost < best * (1.0 - 1e-9)) {
+          best = cost;
+          c->ov_ok = true;
+          c->ov_nq = nqw;
+          c->ov_win = W;
+          c->ov_ncl = ncd;
+          c->ov_stages = S;
+          c->ov_smem = smem;
+        }
+      }
+    }
+  }
   c->colgrid = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 2 * sms));
   c->col32 = (int)cdiv(n, 32);
   // buffers
@@ -1423,7 +1492,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   A(&c->czeta, m_loc);
   A(&c->er, m_loc);
   A(&c->rowpart, (size_t)m_loc * cl);
-  const int64_t parts = std::max<int64_t>(2 * c->ncl, c->hv_nb);
+  const int64_t parts = std::max<int64_t>(std::max<int64_t>(2 * c->ncl, c->hv_nb), c->ov_ncl);
   A(&c->colpart, (size_t)parts * n);
   A(&c->vpart, (size_t)std::max(c->grid, c->ncl) * 8 + 8);
   A(&c->sendbuf, nv);
@@ -1439,6 +1508,7 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   if (st == OTB_OK) st = dalloc(&c->rowpre, m_loc + 1);
   if (st == OTB_OK) st = dalloc(&c->row_len, m_loc);
   if (st == OTB_OK) st = dalloc(&c->cta_rb, (size_t)c->hv_grid + 2);
+  if (st == OTB_OK && c->ov_ok) st = dalloc(&c->ov_rb, (size_t)c->ov_ncl + 2);
   if (st == OTB_OK) st = dalloc(&c->ds, 1);
   if (st == OTB_OK) st = dalloc(&c->cg, 1);
   if (st == OTB_OK && (c->hv_mode == 2 || c->hv_mode == 3)) st = dalloc(&c->bm, (size_t)m_loc * c->nq);
@@ -1489,6 +1559,11 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
     A.cta_rb = nullptr;
     k_cta_bounds<<<(int)cdiv(c->hv_nb + 1, 256), 256>>>(A, c->hv_nb, c->cta_rb, 1);
   }
+  if (c->ov_ok) {   // the overlay's clusters: equal row counts
+    Csr A = csr_view(c);
+    A.cta_rb = nullptr;
+    k_cta_bounds<<<(int)cdiv(c->ov_ncl + 1, 256), 256>>>(A, c->ov_ncl, c->ov_rb, 1);
+  }
   cudaMemset(c->cg, 0, sizeof(CgState));
   cudaMemset(c->cg_y, 0, sizeof(double) * nv);
   cudaMemset(c->row_len, 0, sizeof(int) * m_loc);
@@ -1522,7 +1597,7 @@ int otb_destroy(otb_ctx* c) {
                   (void*)c->cg_ap, (void*)c->cg_y, (void*)c->gtrial, (void*)c->yv, (void*)c->ec, (void*)c->Mloc,
                   (void*)c->Mglob, (void*)c->Sloc, (void*)c->gev, (void*)c->row_start, (void*)c->rowpre, (void*)c->row_len, (void*)c->row_nnz,
                   (void*)c->cols, (void*)c->vals, (void*)c->ds, (void*)c->cg, (void*)c->scal, (void*)c->cta_rb,
-                  (void*)c->bm, (void*)c->Pbuf, (void*)c->cg_trace, (void*)c->lg_tmp, (void*)c->jq,
+                  (void*)c->ov_rb, (void*)c->bm, (void*)c->Pbuf, (void*)c->cg_trace, (void*)c->lg_tmp, (void*)c->jq,
                   (void*)c->minv, (void*)c->zv, (void*)c->colpart2})
     if (p) cudaFree(p);
   if (c->hs) cudaFreeHost(c->hs);
@@ -1709,7 +1784,7 @@ int otb_sparsify(otb_ctx* c, const double* logX, const double* gamma, double rho
 int otb_csr_export(otb_ctx* c, int64_t* row_ptr, int32_t* cols, double* vals, double* d) {
   TRY(require_bound(c));
   const bool bitmap = c->hv_mode == 2 || c->hv_mode == 3;   // pair-layout runs, columns in the bitmap words
-  if (c->hv_mode == 3 && c->rho_dense) {   // dense P_rho: nonzeros per row (every entry of the anchor row)
+  if (c->rho_dense) {   // dense P_rho: nonzeros per row (every entry of the anchor row)
     const int64_t anchor_local = (c->anchor >= c->row0 && c->anchor < c->row1) ? c->anchor - c->row0 : -1;
     if (!c->row_nnz) TRY(dalloc(&c->row_nnz, c->m_loc));
     k_dense_rownnz<<<c->num_sms * 8, 256, 0, c->stream>>>(c->Pbuf, c->ld, (int)c->m_loc, (int)c->n, anchor_local,
@@ -2147,9 +2222,11 @@ int otb_materialize_p(otb_ctx* c, const double* logX, const double* gamma, doubl
 
 int otb_info(otb_ctx* c, int64_t* o) {
   if (!c || !o) return fail(OTB_ERR_ARG, "null");
-  const int64_t v[20] = {c->nt,     c->ns,  c->cl,  c->colw,  c->nstage[DK_EVAL], c->ncl,    c->grid,
+  const int64_t v[24] = {c->nt,     c->ns,  c->cl,  c->colw,  c->nstage[DK_EVAL], c->ncl,    c->grid,
                          c->hv_mode, c->hv_grid, c->nnz, c->cap, c->m_loc, c->n, c->ld, c->nranks, c->rank,
-                         c->hv_ng,   c->cg_fused ? 1 : 0, (int64_t)c->hv_smem, c->launches};
+                         c->hv_ng,   c->cg_fused ? 1 : 0, (int64_t)c->hv_smem, c->launches,
+                         c->rho_dense ? 1 : 0, c->hv_mode == 3 ? c->hv_var : c->ov_nq,
+                         c->hv_mode == 3 ? c->hv_win : c->ov_win, c->hv_mode == 3 ? c->hv_nb : c->ov_ncl};
   std::memcpy(o, v, sizeof v);
   return OTB_OK;
 }

@@ -229,10 +229,11 @@ class Session:
         return t
 
     def info(self) -> dict:
-        out = (C.c_int64 * 20)()
+        out = (C.c_int64 * 24)()
         _lib.check(_lib.lib.otb_info(self.ctx, out))
         keys = ("nt", "ns", "cl", "colw", "nstage", "ncl", "grid", "hv_mode", "hv_grid", "nnz", "capacity",
-                "m_loc", "n", "ld", "nranks", "rank", "hv_groups", "cg_fused", "hv_smem_bytes", "launches")
+                "m_loc", "n", "ld", "nranks", "rank", "hv_groups", "cg_fused", "hv_smem_bytes", "launches",
+                "rho_dense", "wc_nq", "wc_win", "wc_ncl")
         return dict(zip(keys, list(out)))
 
     def launches(self) -> int:

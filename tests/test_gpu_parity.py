@@ -775,6 +775,74 @@ def test_dense_rho_equals_bitmap_rho(cuda, monkeypatch, m, n):
     assert out["0"][3:5] == out["1"][3:5]
 
 
+def _drop_pooled_contexts():
+    """Destroy the idle libotb contexts (geometry knobs are read at creation)."""
+    from paper_2603_07156_b200 import _lib, session
+
+    for pool in session._CTX_POOL.values():
+        while pool:
+            _lib.lib.otb_destroy(pool.pop())
+
+
+@pytest.mark.parametrize("m,n", [(150, 9000), (80, 10000)])
+def test_dense_overlay_equals_group_kernel(cuda, monkeypatch, m, n):
+    """8192 < n with shared-memory accumulators (the CSR group kernel, config
+    3's geometry): while a quarter or more of P is kept, sparsify writes P_rho
+    dense and hess_apply is the dense window-cluster kernel (the overlay);
+    OTB_HV_OVERLAY=0 keeps the CSR group kernel.  The same CSR (bitwise), H v
+    to reduction-order accuracy, the same CG counts and objective in a 2-step
+    inner solve, and below the density threshold the overlay context goes back
+    to the group kernel."""
+    P = _api()
+    from paper_2603_07156_b200 import instances
+    from paper_2603_07156_b200.inner_newton import inner_solve
+
+    C, a, b = instances.small_uniform(m, n, 5 + n)
+    lx = O.product_log_plan(a, b)
+    rng = np.random.default_rng(n)
+    gam = rng.standard_normal(n) * 1e-3
+    v = rng.standard_normal(n)
+    eta = 1e-2
+    out = {}
+    for mode in ("0", "1"):
+        _drop_pooled_contexts()
+        monkeypatch.setenv("OTB_HV_OVERLAY", mode)
+        monkeypatch.setenv("OTB_HV_DENSE", "1")   # dense wherever the context can (whatever the kept density)
+        prob = P.OtProblem(C, a, b)
+        cache = P.compute_p(P.LogPlan(lx), P.DualState(gam), prob, eta)
+        rho = eta * float(np.linalg.norm(P.semidual_gradient(cache, prob))) / (m * n)
+        sp = P.sparsify_p(cache, rho, int(np.argmax(a)))
+        info = cache.session.info()
+        hv = P.SparseHessianOp(sp).matvec(v)
+        # by density (the default policy) with a threshold that keeps almost nothing: the overlay
+        # context takes the group kernel again
+        monkeypatch.delenv("OTB_HV_DENSE")
+        cache2 = P.compute_p(P.LogPlan(lx), P.DualState(gam), prob, eta)
+        sp2 = P.sparsify_p(cache2, 0.05, int(np.argmax(a)))
+        info2 = cache2.session.info()
+        hv2 = P.SparseHessianOp(sp2).matvec(v)
+        monkeypatch.setenv("OTB_HV_DENSE", "1")
+        cfg = P.SolverConfig(eta=eta, kkt_tol=1e-9, max_inner=2)
+        gs, cand, rep = inner_solve(P.LogPlan(lx), P.DualState(np.zeros(n)), P.OtProblem(C, a, b), cfg,
+                                    mu_k=1e-3, outer_k=0)
+        out[mode] = (sp, hv, np.asarray(gs.gamma).copy(), rep.cg_iters_total, rep.objective, info, info2, sp2, hv2)
+    i0, i1 = out["0"][5], out["1"][5]
+    assert i0["hv_mode"] == 0 and i1["hv_mode"] == 0
+    assert i0["rho_dense"] == 0 and i1["rho_dense"] == 1 and i1["wc_win"] >= 2     # the overlay ran
+    assert out["1"][6]["rho_dense"] == 0                                            # ... and was left
+    s0, s1 = out["0"][0], out["1"][0]
+    assert np.array_equal(s0.row_offsets, s1.row_offsets) and np.array_equal(s0.col_indices, s1.col_indices)
+    assert np.array_equal(s0.values, s1.values) and np.array_equal(s0.anchor_row, s1.anchor_row)
+    assert np.max(np.abs(out["0"][1] - out["1"][1])) <= 1e-13 * np.max(np.abs(out["0"][1]))
+    assert np.array_equal(out["0"][7].values, out["1"][7].values)
+    assert np.array_equal(out["0"][8].view(np.uint64), out["1"][8].view(np.uint64))   # both: the group kernel
+    assert np.max(np.abs(out["0"][2] - out["1"][2])) <= 1e-9 * max(1.0, np.max(np.abs(out["0"][2])))
+    assert abs(out["0"][3] - out["1"][3]) <= 1
+    assert abs(out["0"][4] - out["1"][4]) <= 1e-10 * abs(out["0"][4])
+    monkeypatch.delenv("OTB_HV_DENSE")
+    _drop_pooled_contexts()
+
+
 @pytest.mark.parametrize("m,n", [(90, 70), (300, 4100), (64, 16400)])
 def test_jacobi_pcg_matches_oracle(cuda, m, n):
     """cg_solve(preconditioner="jacobi") (extension; the reference's CG is

@@ -9,7 +9,7 @@ for n in (4096, 10000, 16384, 50000):
     st = _lib.lib.otb_create(C.byref(ctx), n, n, 0, n, ld, 0, None)
     print(n, st, _lib.lib.otb_last_error().decode() if st else "ok", flush=True)
     if st == 0:
-        o = (C.c_int64 * 20)()
+        o = (C.c_int64 * 24)()
         _lib.lib.otb_info(ctx, o)
         print("  nt ns cl colw nstage ncl grid:", list(o)[:7], flush=True)
         _lib.lib.otb_destroy(ctx)
