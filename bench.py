@@ -373,18 +373,20 @@ def solve_measure(prob, pts, comm, world, warm):
     from paper_2603_07156_b200.core import SolverConfig
 
     full = SolverConfig(eta=pts.eta, kkt_tol=pts.kkt_tol)
-    if warm:
-        ibsn_solve(prob, full, comm=comm)   # session + CSR capacity growth
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    r = ibsn_solve(prob, full, comm=comm)
-    e1.record()
-    torch.cuda.synchronize()
-    sec = e0.elapsed_time(e1) / 1e3
-    return {"time_s": sec, "outer": r.outer_iters, "newton": r.newton_iters, "cg": r.cg_iters,
+    first = None
+    for _ in range(2 if warm else 1):   # the first call grows the CSR capacity and captures the CG graphs
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = ibsn_solve(prob, full, comm=comm)
+        e1.record()
+        torch.cuda.synchronize()
+        sec = e0.elapsed_time(e1) / 1e3
+        if first is None:
+            first = sec
+    return {"time_s": sec, "first_call_s": first, "outer": r.outer_iters, "newton": r.newton_iters, "cg": r.cg_iters,
             "warm_sweeps": r.warm_sweeps, "objective": r.objective, "kkt": r.kkt,
             "newton_it_per_s": r.newton_iters / sec if sec > 0 else None,
             "from": "device-resident C; ibsn_solve(OtProblem, SolverConfig(eta, kkt_tol)) to kkt < tol"}
@@ -437,7 +439,7 @@ def run_ours(args):
 
     solve = None
     if not args.no_solve:
-        solve = solve_measure(res.prob, res.pts, comm, world, warm=m * n < 5e8)
+        solve = solve_measure(res.prob, res.pts, comm, world, warm=True)
     e2e = e2e_measure(res, args.e2e_steps, world, dev, comm) if args.e2e_steps > 0 else None
 
     sec = {}
