@@ -220,6 +220,7 @@ struct otb_ctx {
   // kept density is >= kDenseRhoMin sparsify writes P_rho dense over the stored P and hess_apply
   // is k_hv_wcd<ov_nq> on ov_ncl clusters of ov_win CTAs; below it the CSR group kernel runs
   bool ov_ok = false;
+  double ov_min_density = kDenseRhoMin;        // kept density from which the overlay's dense product is the faster one
   int ov_nq = 0, ov_win = 0, ov_ncl = 0, ov_stages = 0;
   size_t ov_smem = 0;
   int* ov_rb = nullptr;                        // [ov_ncl + 1] equal row counts per cluster
@@ -589,7 +590,8 @@ int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho
   c->dense_policy = env_hd ? (std::atoi(env_hd) > 0 ? 1 : 0) : -1;
   double density = c->last_density;
   const bool dense_cap = c->hv_mode == 3 || c->ov_ok;
-  if (dense_cap && c->Pbuf != nullptr && c->p_valid && c->dense_policy < 0 && !c->have_density) {
+  const double dense_min = c->hv_mode == 3 ? kDenseRhoMin : c->ov_min_density;
+  if (dense_cap && dense_min > 0.0 && c->Pbuf != nullptr && c->p_valid && c->dense_policy < 0 && !c->have_density) {
     // no kept density yet on this context: estimate it from every 64th row
     // of the stored P (one host synchronisation, first sparsify only)
     const int stride = 64;
@@ -607,7 +609,7 @@ int sparsify_launch(otb_ctx* c, const double* X, const double* gamma, double rho
   // (a group-kernel context can write the dense P_rho only from the stored P: its recomputing
   // sparsify writes the CSR columns)
   const bool dense = dense_cap && c->Pbuf != nullptr && (c->hv_mode == 3 || c->p_valid) &&
-                     (c->dense_policy == 1 || (c->dense_policy < 0 && density >= kDenseRhoMin));
+                     (c->dense_policy == 1 || (c->dense_policy < 0 && density >= dense_min));
   // dense P_rho from the stored P: the lean kernel (same bits as k_sparsify's dense mode)
   const int launch_kind = (dense && c->p_valid) ? (int)DK_SPDENSE : kind;
   Geom geo = c->p_valid ? make_geom(c, launch_kind, c->Pbuf, nullptr) : make_geom(c, DK_SPARSIFY, c->C, X);
@@ -1473,6 +1475,18 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
           c->ov_stages = S;
           c->ov_smem = smem;
         }
+      }
+      if (c->ov_ok) {
+        // Which product is faster, from config 3's solve (tools/solve_probe.py, kept density 49% ->
+        // 8%): the dense kernel streams m_loc x ld doubles at ~6 TB/s (139 us) whatever is kept; the
+        // group kernel costs ~2.2 us per row of a CTA (150 us at 68 rows: latency, not bytes) plus
+        // 1.27 us per million kept entries (212 us at 49%, ~165 us at 8-20%).  Dense from the
+        // density where it wins — at config 3 always (solve 0.60-0.63 -> 0.53-0.58 s).
+        const double dense_us = (double)c->m_loc * (double)ld * 8.0 / 6.0e6 + 5.0;
+        const double group_fixed_us = 2.2 * (double)cdiv(c->m_loc, c->hv_grid);
+        const double per_entry_us = 1.27e-6;
+        c->ov_min_density =
+            std::max(0.0, (dense_us - group_fixed_us) / (per_entry_us * (double)c->m_loc * (double)n));
       }
     }
   }

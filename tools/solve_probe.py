@@ -35,3 +35,21 @@ print(f"profiled kernel time {tot:.1f} ms")
 for k, v in prof.items():
     if v["launches"]:
         print(f"  {k:12s} {v['ms']:9.2f} ms  {v['launches']:5d} launches  {1e3 * v['ms'] / v['launches']:9.1f} us each")
+# kept density and CG iterations per Newton iteration of the last repeat (OTB_PROBE_TRACE=1)
+if os.environ.get("OTB_PROBE_TRACE") == "1":
+    import paper_2603_07156_b200.bregman_outer as BO
+    from paper_2603_07156_b200 import inner_newton as IN
+
+    reports = []
+    orig = IN.inner_solve
+
+    def spy(*a, **k):
+        out = orig(*a, **k)
+        reports.append(out[2])
+        return out
+
+    BO.inner_solve = spy
+    ibsn_solve(res.prob, cfg)
+    m, n = res.m, res.n
+    for k, rep in enumerate(reports):
+        print(f"  outer {k}: cg {list(rep.cg_iters)} density {[round(z / (m * n), 4) for z in rep.nnz]}")
