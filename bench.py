@@ -303,7 +303,7 @@ def roofline(res, idx, steps):
            "dram_frac": d["dram_frac"], "per_kernel": per}
     if dom == "hess_apply":
         out["note"] = ("achieved uses SURVEY 8(d)'s CSR bytes 12 nnz + 8(m+1) + 16n; in the dense-P_rho mode "
-                       "(kept density >= 0.25) hess_apply reads 8 B per matrix entry and no column indices, so "
+                       "hess_apply reads 8 B per matrix entry and no column indices, so "
                        "achieved can exceed the bytes moved: dram_GB/s (ncu DRAM bytes per launch / the same "
                        "time) is the physical rate")
     return out

@@ -217,10 +217,10 @@ struct otb_ctx {
   size_t hv_smem_d = 0;
   bool hv_wcd = true;                          // OTB_HV_WCD=0: the producer-warp dense kernel (comparison)
   // dense-P_rho overlay of a group-kernel context (hv_mode 0, n > 8192, e.g. config 3): while the
-  // kept density is >= kDenseRhoMin sparsify writes P_rho dense over the stored P and hess_apply
+  // kept density is >= ov_min_density sparsify writes P_rho dense over the stored P and hess_apply
   // is k_hv_wcd<ov_nq> on ov_ncl clusters of ov_win CTAs; below it the CSR group kernel runs
   bool ov_ok = false;
-  double ov_min_density = kDenseRhoMin;        // kept density from which the overlay's dense product is the faster one
+  double ov_min_density = 0.25;                // kept density from which the overlay's dense product is the faster one
   int ov_nq = 0, ov_win = 0, ov_ncl = 0, ov_stages = 0;
   size_t ov_smem = 0;
   int* ov_rb = nullptr;                        // [ov_ncl + 1] equal row counts per cluster

@@ -854,10 +854,13 @@ __global__ void __launch_bounds__(HvVar<V>::kThreads, 1) k_hv_grp(HvArgs h) {
 // re-read is an L2 hit; HBM sees each value once.  The ring holds only the
 // rows in flight (loads + dots); the exchange waits hold no stage.  Rows are
 // applied in order, partials summed in window order: deterministic.
-// kept density above which sparsify writes P_rho dense (OTB_HV_DENSE forces either): with the
-// producer-free dense kernel, config 4 (37% kept) measured hess_apply 2.22 -> 1.78 ms and sparsify
-// 7.15 -> 5.06 ms dense against the bitmap runs
-constexpr double kDenseRhoMin = 0.25;
+// kept density from which sparsify writes P_rho dense (OTB_HV_DENSE forces either).  0: always.
+// The bitmap kernel visits every column slot of a row whatever is kept, so its time does not fall
+// with the density (tools/hv_density_sweep.py: config 4, 37% -> 18% kept: 2.37 ms flat, config 5
+// 76% -> 46%: 5.6 -> 5.5 ms) and the dense kernel's 1.37 ms / 3.13 ms wins at every density
+// (sparsify too: 5.1 against 7.2 ms at config 4).  The bitmap runs remain the format when the
+// eval's P is not stored (OTB_STORE_P=0) and the comparison format of the tests.
+constexpr double kDenseRhoMin = 0.0;
 constexpr int kWcD = 4;                  // exchange lookahead (rows)
 constexpr int kWcX = 2 * kWcD + 2;       // exchange buffers (>= 2 D + 1: see the note in wc_consume)
 constexpr int kWcMaxW = 16;
