@@ -302,10 +302,10 @@ def roofline(res, idx, steps):
            "us_per_launch": d["us_per_launch"], "time_share": d["share"], "dram_GB/s": d["dram_GB/s"],
            "dram_frac": d["dram_frac"], "per_kernel": per}
     if dom == "hess_apply":
-        out["note"] = ("achieved uses SURVEY 8(d)'s CSR bytes 12 nnz + 8(m+1) + 16n; in the dense-P_rho mode "
-                       "hess_apply reads 8 B per matrix entry and no column indices, so "
-                       "achieved can exceed the bytes moved: dram_GB/s (ncu DRAM bytes per launch / the same "
-                       "time) is the physical rate")
+        out["note"] = ("hess_apply streams the dense P_rho (sparsify's dense mode): algorithmic bytes per launch = "
+                       "8 m n + 8 (m + 1) + 16 n, one pass over the matrix and no column indices (SURVEY 8(d)'s CSR "
+                       "figure 12 nnz + 8(m+1) + 16n applies to the CSR/bitmap formats); dram_GB/s is the ncu DRAM "
+                       "bytes per launch over the same time")
     return out
 
 

@@ -706,7 +706,12 @@ Csr csr_view(const otb_ctx* c) {
 // Algorithmic bytes of one hess_apply, SURVEY §8(d) / DESIGN.md: CSR with
 // int32 columns, 12 nnz + 8 (m + 1) + 16 n, whatever the stored format
 // (the bitmap index moves 8 nnz + m nq 16 bytes; ncu traffic shows it).
-double hv_bytes(const otb_ctx* c) { return 12.0 * c->nnz + 8.0 * (c->m_loc + 1) + 16.0 * c->n; }
+// With the dense P_rho the product streams every matrix entry once and no column indices:
+// 8 m n + 8 (m + 1) + 16 n (fewer than the CSR figure from 2/3 kept on, more below it).
+double hv_bytes(const otb_ctx* c) {
+  if (c->rho_dense) return 8.0 * (double)c->m_loc * (double)c->n + 8.0 * (c->m_loc + 1) + 16.0 * c->n;
+  return 12.0 * c->nnz + 8.0 * (c->m_loc + 1) + 16.0 * c->n;
+}
 
 // y = P_rho^T (a * (P_rho v)) reduced to: (mode smem) colpart[hv_grid][n] or
 // sendbuf (multi-rank), (mode atomic) cg_y or sendbuf.  Returns via
