@@ -1559,6 +1559,12 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   // first Newton steps keep 50-70% of P: start at 3/4
   int64_t init_cap =
       std::max<int64_t>((int64_t)1 << 20, m_loc * (rup(n, kCsrAlign)) * 3 / 4) + (int64_t)c->ncl * c->chunk;
+  // Contexts whose sparsify writes the dense P_rho at every density (window clusters, an overlay that
+  // always wins: configs 3-5) never touch the CSR runs: start them at the minimum (config 5: 19 GB of
+  // values + columns not allocated); a sparsify in the sparse format (OTB_HV_DENSE=0, OTB_STORE_P=0)
+  // grows it through the overflow-and-redo path.
+  if (c->Pbuf != nullptr && ((c->hv_mode == 3 && kDenseRhoMin <= 0.0) || (c->ov_ok && c->ov_min_density <= 0.0)))
+    init_cap = ((int64_t)1 << 20) + (int64_t)c->ncl * c->chunk;
   const char* env_cap = std::getenv("OTB_CSR_CAP0");   // tests: start small to exercise the overflow path
   if (env_cap && std::atoll(env_cap) > 0) init_cap = std::atoll(env_cap);
   st = grow_csr(c, init_cap);
