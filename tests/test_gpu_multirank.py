@@ -241,6 +241,79 @@ def test_row_shard_cost_bench_step_two_ranks(cuda):
         assert r2.kkt == pytest.approx(r1.kkt, rel=1e-6)
 
 
+def _host(x):
+    return x.cpu().numpy() if hasattr(x, "cpu") else np.asarray(x)
+
+
+def _free_device_memory():
+    """Destroy the pooled libotb contexts and return torch's cached blocks (the full-size tests
+    hold tens of GB each)."""
+    import gc
+
+    import torch
+
+    from paper_2603_07156_b200 import _lib, session
+
+    gc.collect()
+    for pool in session._CTX_POOL.values():
+        while pool:
+            _lib.lib.otb_destroy(pool.pop())
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("idx,world", [(4, 2), (4, 4), (5, 2)])
+def test_full_size_solve_sharded(cuda, idx, world):
+    """BASELINE configs 4 and 5 at FULL size (65536 x 16384 and 50000^2, the configurations BASELINE
+    shards over 1/2/4/8 GPUs), rows sharded over a local group: each rank builds only its rows of C on the
+    device, the window-cluster hess_apply and the cluster-split dense passes run on the shards,
+    every length-n all-reduce goes through the group.  ibsn_solve to tol must match the one-rank
+    solve: <C,X> to 1e-8, equal outer and Newton counts, CG within 5%, the same dual on every
+    rank."""
+    import torch
+
+    P = _api()
+    from paper_2603_07156_b200 import instances
+    from paper_2603_07156_b200.core import RowShardCost
+    from paper_2603_07156_b200.distributed import LocalGroup
+
+    pts = instances.config_points(idx, 0)
+    m, n = len(pts.a), len(pts.b)
+    ld = (n + 31) // 32 * 32
+    dev = torch.device("cuda", 0)
+    cfg = P.SolverConfig(eta=pts.eta, kkt_tol=pts.kkt_tol)
+    _free_device_memory()
+    one = P.ibsn_solve(P.OtProblem(instances.device_cost(pts, dev, ld=ld), pts.a, pts.b), cfg)
+    ref = (one.outer_iters, one.newton_iters, one.cg_iters, one.objective, one.kkt)
+    g1 = _host(one.gamma)[:n].copy()
+    one._session.close()
+    del one
+    _free_device_memory()
+    grp = LocalGroup(world)
+    try:
+        def body(r, comm):
+            r0, r1 = comm.row_range(m)
+            local = instances.device_cost(pts, dev, rows=(r0, r1), ld=ld, comm=comm)
+            res = P.ibsn_solve(P.OtProblem(RowShardCost(local, r0, m), pts.a, pts.b), cfg, comm=comm)
+            info = res._session.info()
+            out = (res.outer_iters, res.newton_iters, res.cg_iters, res.objective, res.kkt,
+                   _host(res.gamma)[:n].copy(), info["nranks"], info["m_loc"], info["hv_mode"])
+            res._session.close()
+            return out
+
+        outs = grp.run(body, timeout=900)
+    finally:
+        grp.close()
+        _free_device_memory()
+    for r, o in enumerate(outs):
+        assert o[6] == world and o[7] in (m // world, m // world + 1) and o[8] == 3
+        assert (o[0], o[1]) == ref[:2]
+        assert abs(o[2] - ref[2]) <= 0.05 * ref[2]
+        assert abs(o[3] - ref[3]) <= 1e-8 * abs(ref[3])
+        assert o[4] < pts.kkt_tol
+        assert np.array_equal(o[5], outs[0][5])
+        assert np.max(np.abs(o[5] - g1)) <= 1e-8 * max(1.0, np.abs(g1).max())
+
+
 _NCCL_SELFTEST = r"""
 import json, os, sys
 import numpy as np
