@@ -1113,7 +1113,10 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
   if (!out) return fail(OTB_ERR_ARG, "out is null");
   *out = nullptr;
   if (m_global <= 0 || n <= 0) return fail(OTB_ERR_ARG, "empty problem");
-  if (n > 65536) return fail(OTB_ERR_ARG, "n > 65536 is not supported (16-bit CSR column indices)");
+  // n <= 65536 where the CSR stores uint16 columns; the window-cluster formats (bitmap words, dense
+  // P_rho) store none and go to 16 windows of 8192 columns (checked once the variant is known)
+  if (n > (int64_t)kWcMaxW * 1024 * kMaxNQ)
+    return fail(OTB_ERR_ARG, "n > 131072 is not supported (16 hess_apply windows of 8192 columns)");
   if (row_begin < 0 || row_end > m_global || row_end <= row_begin) return fail(OTB_ERR_ARG, "bad row range");
   if (ld < n || ld % 32 != 0) return fail(OTB_ERR_ARG, "ld must be >= n and a multiple of 32");
   CUDA_TRY(cudaSetDevice(device));
@@ -1404,6 +1407,10 @@ int otb_create(otb_ctx** out, int64_t m_global, int64_t n, int64_t row_begin, in
         c->hv_wcd = false;
       }
     }
+  }
+  if (n > 65536 && c->hv_mode != 3) {
+    delete c;
+    return fail(OTB_ERR_ARG, "n > 65536 needs the window-cluster hess_apply (16-bit CSR column indices otherwise)");
   }
   if (c->hv_mode == 0 || c->hv_mode == 2) {
     c->hv_grid = sms;

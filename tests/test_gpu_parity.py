@@ -217,11 +217,13 @@ def test_baseline_config_end_to_end(cuda, idx):
 
 # ------------------------------------------------- oracle-checked seeded cases
 @pytest.mark.parametrize("m,n,eta", [(1, 5, 1e-2), (7, 1, 1e-2), (37, 29, 5e-2), (257, 131, 1e-2),
-                                     (64, 9000, 1e-2), (40, 16400, 1e-2), (9, 50001, 1e-2), (24, 60000, 1e-2)])
+                                     (64, 9000, 1e-2), (40, 16400, 1e-2), (9, 50001, 1e-2), (24, 60000, 1e-2),
+                                     (12, 70000, 1e-2), (6, 131072, 1e-2)])
 def test_step_pipeline_vs_oracle(cuda, m, n, eta):
     """Ragged / odd / cluster-split (n > 10240; 60000 columns = clusters of 8)
     / window-cluster geometries: eval, one Newton step and the inexact test
-    vs the oracle."""
+    vs the oracle.  n > 65536 (up to 131072 = 16 windows of 8192 columns) runs
+    on the window-cluster formats, which store no 16-bit column indices."""
     P = _api()
     from paper_2603_07156_b200 import instances
 
@@ -324,7 +326,7 @@ def test_fast_division_is_correctly_rounded(cuda, y):
 
 @pytest.mark.parametrize("m,n,env", [(300, 4100, None), (200, 9000, None), (120, 16400, None),
                                      (310, 4000, "OTB_HV_STAGED"), (190, 9000, "OTB_HV_WC"),
-                                     (70, 50001, None)])
+                                     (70, 50001, None), (20, 70000, None)])
 def test_hess_apply_deterministic_and_matches_oracle(cuda, monkeypatch, m, n, env):
     """hess_apply (cp.async bitmap, TMA-staged bitmap, warp-group and
     window-cluster variants) is bitwise reproducible run to run and matches
